@@ -1,0 +1,191 @@
+/*
+ * include/mclahe_gpu.h -- C ABI of the B200-native MCLAHE hot path.
+ *
+ * Plain pointers and sizes only (no C++/torch types), so it binds from C++,
+ * ctypes, cgo or JNI alike.  Every entry point cites the reference interface
+ * it replaces (paths relative to /root/reference/proj/core/).
+ *
+ * Status codes: MCLAHE_OK (0), MCLAHE_ERR_VALIDATION (1; message = the
+ * reference ValidationError text), MCLAHE_ERR_CUDA (2), MCLAHE_ERR_COMM (3),
+ * MCLAHE_ERR_OOM (4), MCLAHE_ERR_UNSUPPORTED (5).  No function throws across
+ * the ABI; mclahe_last_error() returns the message of the calling thread's
+ * last failure.
+ *
+ * Two ways in:
+ *   1. mclahe_gpu_run()        one-shot, HOST buffers: the drop-in for
+ *                              mclahe::mclahe (include/mclahe/pipeline.hpp:30).
+ *   2. mclahe_plan_* + passes  device-resident, stream-ordered, caller-owned
+ *                              workspace; the slab (multi-GPU) layer inserts
+ *                              its collectives between the passes.
+ */
+#ifndef MCLAHE_GPU_H
+#define MCLAHE_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MCLAHE_MAX_RANK 8
+
+enum {
+  MCLAHE_OK = 0,
+  MCLAHE_ERR_VALIDATION = 1,
+  MCLAHE_ERR_CUDA = 2,
+  MCLAHE_ERR_COMM = 3,
+  MCLAHE_ERR_OOM = 4,
+  MCLAHE_ERR_UNSUPPORTED = 5
+};
+
+enum { MCLAHE_F32 = 0, MCLAHE_F64 = 1 };
+
+/* McLaheRequest (include/mclahe/pipeline.hpp:12-17) + EnhanceParams
+ * (include/mclahe/histogram.hpp:17-21) flattened to POD.  `adaptive` is
+ * RangeMode (histogram.hpp:13): 0 = Global, 1 = Adaptive.  `dtype` is the
+ * element type of both the input and the output buffer. */
+typedef struct {
+  int32_t rank;
+  int32_t adaptive;
+  int32_t dtype;
+  int32_t reserved;
+  int64_t shape[MCLAHE_MAX_RANK];
+  int64_t kernel[MCLAHE_MAX_RANK];
+  int64_t n_bins;
+  double clip_limit;
+} mclahe_params_t;
+
+/* PhaseTimings (include/mclahe/pipeline.hpp:20-24), filled from CUDA events:
+ * pad = 0 (padding is virtual), histograms = range + counts + mappings,
+ * interpolation = blend.  Accumulates (+=) like the reference. */
+typedef struct {
+  double pad_s;
+  double histograms_s;
+  double interpolation_s;
+} mclahe_timings_t;
+
+/* Geometry and workspace layout of a plan, for the slab exchange layer. */
+typedef struct {
+  int32_t rank;
+  int32_t fast_hist;      /* 1 if the pencil histogram kernel is used */
+  int32_t fast_interp;    /* 1 if the pencil interpolation kernel is used */
+  int32_t trailing_dims;  /* k: trailing dims covered by one pencil */
+  int64_t before[MCLAHE_MAX_RANK];
+  int64_t after[MCLAHE_MAX_RANK];
+  int64_t grid[MCLAHE_MAX_RANK];
+  int64_t tiles;          /* all tiles of the full volume */
+  int64_t row_begin, row_end;           /* slab rows along dim 0 (original) */
+  int64_t tile_row_begin, tile_row_end; /* tile-row window held in workspace */
+  int64_t count_row_begin, count_row_end; /* tile rows this slab counts into */
+  int64_t need_row_begin, need_row_end;   /* tile rows the slab's voxels blend */
+  int64_t tiles_per_row;  /* prod_{j>=1} grid[j] */
+  int64_t n_bins;
+  /* workspace byte offsets */
+  int64_t off_range;      /* int64[4]: ~key(lo), key(hi), nonfinite, 0 (MAX-reducible) */
+  int64_t off_tile_range; /* int64[window tiles][2]: ~key(lo), key(hi)   (MAX-reducible) */
+  int64_t off_counts;     /* int32[window tiles][n_bins]                 (SUM-reducible) */
+  int64_t off_tparams;    /* per-tile binning parameters */
+  int64_t off_lut;        /* float32[window tiles][n_bins] */
+  int64_t workspace_bytes;
+  int64_t hist_units, interp_units;
+} mclahe_plan_info_t;
+
+typedef struct mclahe_plan_s* mclahe_plan_t;
+
+/* Optional per-tile intermediates (device pointers, any may be NULL), tile
+ * index = window tile (tile-row window of the plan).  Mirrors what
+ * build_mappings (src/histogram.cpp:72-106) produces per KernelMapping plus
+ * the compute_histogram / clip_histogram arrays. */
+typedef struct {
+  double* lo;            /* [tiles]  IntensityRange.lo */
+  double* hi;            /* [tiles]  IntensityRange.hi */
+  uint32_t* counts;      /* [tiles][n_bins] raw counts (compute_histogram) */
+  double* clipped;       /* [tiles][n_bins] clip_histogram output */
+  double* lut;           /* [tiles][n_bins] normalized_cdf values (f64) */
+  uint8_t* degenerate;   /* [tiles]  KernelMapping.degenerate */
+} mclahe_debug_t;
+
+/* ---- one-shot drop-in ------------------------------------------------- */
+
+/* Replaces mclahe::mclahe(const McLaheRequest&, PhaseTimings*)
+ * (include/mclahe/pipeline.hpp:30, src/pipeline.cpp:73-129).  `in` and `out`
+ * are HOST buffers of prod(shape) elements of `dtype`; validation
+ * (src/pipeline.cpp:19-34) happens first, with the reference messages.
+ * Pinned host buffers are copied asynchronously; pageable ones through the
+ * driver's staging path.  timings may be NULL. */
+int mclahe_gpu_run(const mclahe_params_t* params, const void* in, void* out,
+                   mclahe_timings_t* timings);
+
+/* Same, with DEVICE buffers on `stream` (cudaStream_t; NULL = legacy).  The
+ * library allocates (and caches) its workspace.  Synchronises `stream` before
+ * returning so the non-finite check can be reported. */
+int mclahe_gpu_run_device(const mclahe_params_t* params, const void* in_dev, void* out_dev,
+                          void* stream, mclahe_timings_t* timings);
+
+/* ---- plans and passes (device-resident) --------------------------------- */
+
+/* Plans one slab: original rows [row_begin, row_end) along dim 0 of the
+ * volume described by params (the whole volume: 0, shape[0]).  The input and
+ * output buffers given to the passes hold exactly those rows.  Validates
+ * like src/pipeline.cpp:19-33 (the non-finite check runs on the device). */
+int mclahe_plan_create(const mclahe_params_t* params, int64_t row_begin, int64_t row_end,
+                       mclahe_plan_t* plan);
+int mclahe_plan_destroy(mclahe_plan_t plan);
+int mclahe_plan_get_info(mclahe_plan_t plan, mclahe_plan_info_t* info);
+
+/* Resets the workspace (ranges, counts) -- first pass of every run. */
+int mclahe_pass_reset(mclahe_plan_t plan, void* workspace, void* stream);
+
+/* Pass 1.  Global mode: min/max + finiteness of the slab
+ * (NdImage::min_max / all_finite, src/nd_image.cpp:70-83).  Adaptive mode:
+ * per-tile min/max over the padded tiles this slab touches
+ * (src/histogram.cpp:86-94).  Results land MAX-reducible at off_range /
+ * off_tile_range for the exchange layer. */
+int mclahe_pass_range(mclahe_plan_t plan, const void* in_dev, void* workspace, void* stream);
+
+/* Turns the (exchanged) ranges into per-tile binning parameters. */
+int mclahe_pass_params(mclahe_plan_t plan, void* workspace, void* stream);
+
+/* Pass 2.  Per-tile counts over the virtually padded kernel grid
+ * (kernelize + compute_histogram + bin_index, src/nd_image.cpp:146-187,
+ * src/histogram.cpp:24-40).  Partial (SUM-reducible) for slabs. */
+int mclahe_pass_histograms(mclahe_plan_t plan, const void* in_dev, void* workspace,
+                           void* stream);
+
+/* Pass 3.  clip_histogram + normalized_cdf per tile (src/histogram.cpp:42-70),
+ * bit-exact f64, LUT stored as f32.  debug may be NULL. */
+int mclahe_pass_mappings(mclahe_plan_t plan, void* workspace, const mclahe_debug_t* debug,
+                         void* stream);
+
+/* Pass 4.  Per-voxel multilinear blend of the 2^D neighbour LUTs
+ * (src/pipeline.cpp:94-127, src/interpolation.cpp:7-86).  Writes nothing if
+ * pass 1 saw a non-finite value. */
+int mclahe_pass_interpolate(mclahe_plan_t plan, const void* in_dev, void* out_dev,
+                            void* workspace, void* stream);
+
+/* All passes for a single-slab plan, stream-ordered, no host sync. */
+int mclahe_plan_enqueue(mclahe_plan_t plan, const void* in_dev, void* out_dev,
+                        void* workspace, void* stream);
+
+/* Synchronises `stream` and reports MCLAHE_ERR_VALIDATION ("image contains
+ * non-finite values") if pass 1 flagged the input. */
+int mclahe_plan_check(mclahe_plan_t plan, const void* workspace, void* stream);
+
+/* Exact bin_index (src/histogram.cpp:24-32) of n device values through the
+ * same fast-guarded routine the kernels use; out is int32[n].  For testing
+ * the binning on adversarial values. */
+int mclahe_debug_bin_index(int32_t dtype, const void* values_dev, int64_t n, double lo,
+                           double hi, int64_t n_bins, int32_t* out_dev, void* stream);
+
+/* Number of kernel launches the last pass call on this thread issued. */
+int64_t mclahe_launch_count(void);
+
+const char* mclahe_last_error(void);
+const char* mclahe_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MCLAHE_GPU_H */

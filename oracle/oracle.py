@@ -1,0 +1,238 @@
+"""TEST INFRASTRUCTURE ONLY -- ctypes front end of the CPU oracle.
+
+Two checkers live behind one interface (``impl=``):
+
+* ``"c"``   -- ``oracle/liboracle.so``, the plain-C restatement
+              (``oracle/mclahe_oracle.c``) of the reference algorithm.
+* ``"ref"`` -- ``oracle/_ref/libmclahe_ref.so``, the reference library compiled
+              from its own sources (``oracle/Makefile``) behind a C shim
+              (``oracle/ref_shim.cpp``).
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s CPU-baseline /
+reference legs may import this module.  The product never does.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+_LIBS: dict[str, C.CDLL] = {}
+
+_i64p = C.POINTER(C.c_int64)
+_f64p = C.POINTER(C.c_double)
+_u8p = C.POINTER(C.c_uint8)
+
+
+def build(quiet: bool = True) -> None:
+    """Compile liboracle.so (and _ref/ when /root/reference is present)."""
+    kw = dict(stdout=subprocess.DEVNULL, stderr=subprocess.STDOUT) if quiet else {}
+    subprocess.run(["make", "-s", "-C", HERE], check=True, **kw)
+
+
+def _lib(impl: str) -> C.CDLL:
+    if impl in _LIBS:
+        return _LIBS[impl]
+    if impl == "c":
+        path = os.path.join(HERE, "liboracle.so")
+    elif impl == "ref":
+        path = os.path.join(HERE, "_ref", "libmclahe_ref.so")
+    else:
+        raise ValueError(f"unknown oracle impl {impl!r}")
+    if not os.path.exists(path):
+        build()
+    if not os.path.exists(path):
+        raise FileNotFoundError(path)
+    lib = C.CDLL(path)
+    if impl == "c":
+        lib.orc_bin_index.restype = C.c_int64
+        lib.orc_bin_index.argtypes = [C.c_double, C.c_double, C.c_double, C.c_int64]
+        lib.orc_mirror_index.restype = C.c_int64
+        lib.orc_mirror_index.argtypes = [C.c_int64, C.c_int64]
+        lib.orc_pad_plan.argtypes = [C.c_int, _i64p, _i64p, _i64p, _i64p]
+        lib.orc_clip_histogram.argtypes = [_f64p, C.c_int64, C.c_double, _f64p]
+        lib.orc_normalized_cdf.argtypes = [_f64p, C.c_int64, _f64p]
+        lib.orc_tile_stats.argtypes = [_f64p, C.c_int, _i64p, _i64p, C.c_int64, C.c_double,
+                                       C.c_int, _f64p, _f64p, _f64p, _f64p, _f64p, _u8p]
+        lib.orc_neighbor_1d.argtypes = [C.c_int64, C.c_int64, C.c_int64, _i64p, _f64p, _f64p]
+        lib.orc_interp_coefficients.argtypes = [C.c_int, _f64p, _f64p, _i64p, _f64p]
+        lib.orc_blend.restype = C.c_double
+        lib.orc_blend.argtypes = [C.c_int, _f64p, _f64p]
+        lib.orc_mclahe.argtypes = [_f64p, C.c_int, _i64p, _i64p, C.c_int64, C.c_double,
+                                   C.c_int, _f64p, C.c_char_p, C.c_int]
+    else:
+        lib.ref_mclahe.argtypes = [_f64p, C.c_int, _i64p, _i64p, C.c_int64, C.c_double,
+                                   C.c_int, C.c_uint, _f64p, _f64p, C.c_char_p, C.c_int]
+        lib.ref_tile_stats.argtypes = [_f64p, C.c_int, _i64p, _i64p, C.c_int64, C.c_double,
+                                       C.c_int, _f64p, _f64p, _f64p, _f64p, _f64p, _u8p,
+                                       C.c_char_p, C.c_int]
+        lib.ref_bin_index.restype = C.c_int64
+        lib.ref_bin_index.argtypes = [C.c_double, C.c_double, C.c_double, C.c_int64]
+        lib.ref_clip_histogram.argtypes = [_f64p, C.c_int64, C.c_double, _f64p]
+        lib.ref_normalized_cdf.argtypes = [_f64p, C.c_int64, _f64p]
+        lib.ref_neighbors.argtypes = [C.c_int, _i64p, _i64p, _i64p, _i64p, _f64p, _f64p, _f64p]
+        lib.ref_transform_pixel.restype = C.c_double
+        lib.ref_transform_pixel.argtypes = [C.c_double, C.c_int, _f64p, C.c_int64, _f64p,
+                                            _f64p, _u8p, _f64p]
+    _LIBS[impl] = lib
+    return lib
+
+
+def have_ref() -> bool:
+    try:
+        _lib("ref")
+        return True
+    except (FileNotFoundError, OSError, subprocess.CalledProcessError):
+        return False
+
+
+def _p(a: np.ndarray, t):
+    return a.ctypes.data_as(t)
+
+
+def _i64(seq) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(seq, dtype=np.int64))
+
+
+class OracleValidationError(ValueError):
+    """The reference rejected the request (ValidationError)."""
+
+
+def mclahe(data: np.ndarray, kernel, n_bins: int = 256, clip_limit: float = 1.0,
+           adaptive: bool = False, impl: str = "c", threads: int = 0,
+           timings: list | None = None) -> np.ndarray:
+    """Full pipeline; returns float64 of data's shape (mclahe, pipeline.cpp:73)."""
+    x = np.ascontiguousarray(data, dtype=np.float64)
+    shape, ker = _i64(x.shape), _i64(kernel)
+    out = np.empty(x.shape, dtype=np.float64)
+    err = C.create_string_buffer(256)
+    lib = _lib(impl)
+    if impl == "c":
+        rc = lib.orc_mclahe(_p(x, _f64p), x.ndim, _p(shape, _i64p), _p(ker, _i64p), int(n_bins),
+                            float(clip_limit), int(bool(adaptive)), _p(out, _f64p), err, 256)
+    else:
+        t = np.zeros(3)
+        rc = lib.ref_mclahe(_p(x, _f64p), x.ndim, _p(shape, _i64p), _p(ker, _i64p), int(n_bins),
+                            float(clip_limit), int(bool(adaptive)), int(threads), _p(out, _f64p),
+                            _p(t, _f64p), err, 256)
+        if timings is not None:
+            timings[:] = list(t)
+    if rc == 1:
+        raise OracleValidationError(err.value.decode())
+    if rc != 0:
+        raise RuntimeError(err.value.decode())
+    return out
+
+
+def geometry(shape, kernel):
+    """(before, after, grid) per dimension (compute_pad_plan, nd_image.cpp:85-102)."""
+    shape, kernel = _i64(shape), _i64(kernel)
+    before, after = np.zeros_like(shape), np.zeros_like(shape)
+    if _lib("c").orc_pad_plan(len(shape), _p(shape, _i64p), _p(kernel, _i64p),
+                              _p(before, _i64p), _p(after, _i64p)):
+        raise OracleValidationError("invalid kernel")
+    grid = (shape + before + after) // kernel
+    return before, after, grid
+
+
+def tile_stats(data: np.ndarray, kernel, n_bins: int, clip_limit: float, adaptive: bool,
+               impl: str = "c") -> dict:
+    """Per-tile lo/hi/counts/clipped/lut/degenerate (build_mappings internals)."""
+    x = np.ascontiguousarray(data, dtype=np.float64)
+    shape, ker = _i64(x.shape), _i64(kernel)
+    _, _, grid = geometry(x.shape, kernel)
+    T = int(np.prod(grid))
+    lo, hi = np.zeros(T), np.zeros(T)
+    counts, clipped, lut = (np.zeros((T, n_bins)) for _ in range(3))
+    degen = np.zeros(T, dtype=np.uint8)
+    args = [_p(x, _f64p), x.ndim, _p(shape, _i64p), _p(ker, _i64p), int(n_bins),
+            float(clip_limit), int(bool(adaptive)), _p(lo, _f64p), _p(hi, _f64p),
+            _p(counts, _f64p), _p(clipped, _f64p), _p(lut, _f64p), _p(degen, _u8p)]
+    if impl == "c":
+        rc = _lib("c").orc_tile_stats(*args)
+    else:
+        err = C.create_string_buffer(256)
+        rc = _lib("ref").ref_tile_stats(*args, err, 256)
+    if rc:
+        raise OracleValidationError("tile_stats rejected the request")
+    return dict(lo=lo, hi=hi, counts=counts, clipped=clipped, lut=lut,
+                degenerate=degen.astype(bool), grid=tuple(int(g) for g in grid))
+
+
+def bin_index(value: float, lo: float, hi: float, n_bins: int, impl: str = "c") -> int:
+    if impl == "c":
+        return int(_lib("c").orc_bin_index(value, lo, hi, n_bins))
+    return int(_lib("ref").ref_bin_index(value, lo, hi, n_bins))
+
+
+def bin_index_array(values: np.ndarray, lo: float, hi: float, n_bins: int) -> np.ndarray:
+    """Vectorised restatement of bin_index (histogram.cpp:24-32) in numpy
+    float64 (IEEE round-to-nearest, no FMA): floor((v-lo)/(hi-lo)*n), clamped."""
+    v = np.asarray(values, dtype=np.float64)
+    with np.errstate(invalid="ignore", divide="ignore"):
+        scaled = np.floor((v - np.float64(lo)) / (np.float64(hi) - np.float64(lo))
+                          * np.float64(n_bins))
+    out = np.where(scaled > 0.0, scaled, 0.0)
+    out = np.where(out >= n_bins, n_bins - 1, out)
+    return out.astype(np.int64)
+
+
+def clip_histogram(counts, clip_limit: float, impl: str = "c") -> np.ndarray:
+    c = np.ascontiguousarray(counts, dtype=np.float64)
+    out = np.empty_like(c)
+    getattr(_lib(impl), "orc_clip_histogram" if impl == "c" else "ref_clip_histogram")(
+        _p(c, _f64p), c.size, float(clip_limit), _p(out, _f64p))
+    return out
+
+
+def normalized_cdf(clipped, impl: str = "c"):
+    c = np.ascontiguousarray(clipped, dtype=np.float64)
+    out = np.empty_like(c)
+    d = getattr(_lib(impl), "orc_normalized_cdf" if impl == "c" else "ref_normalized_cdf")(
+        _p(c, _f64p), c.size, _p(out, _f64p))
+    return out, bool(d)
+
+
+def neighbors(pixel, kernel, grid, impl: str = "c"):
+    """(lower, dist_lo, dist_hi, coefficients) for one padded pixel."""
+    rank = len(pixel)
+    px, ker, gr = _i64(pixel), _i64(kernel), _i64(grid)
+    lower = np.zeros(rank, dtype=np.int64)
+    dlo, dhi = np.zeros(rank), np.zeros(rank)
+    coeff = np.zeros(1 << rank)
+    if impl == "c":
+        lib = _lib("c")
+        for j in range(rank):
+            lj = C.c_int64()
+            a, b = C.c_double(), C.c_double()
+            if lib.orc_neighbor_1d(int(px[j]), int(ker[j]), int(gr[j]), C.byref(lj),
+                                   C.byref(a), C.byref(b)):
+                raise OracleValidationError("pixel outside the valid interpolation region")
+            lower[j], dlo[j], dhi[j] = lj.value, a.value, b.value
+        lib.orc_interp_coefficients(rank, _p(dlo, _f64p), _p(dhi, _f64p), _p(ker, _i64p),
+                                    _p(coeff, _f64p))
+    else:
+        if _lib("ref").ref_neighbors(rank, _p(px, _i64p), _p(ker, _i64p), _p(gr, _i64p),
+                                     _p(lower, _i64p), _p(dlo, _f64p), _p(dhi, _f64p),
+                                     _p(coeff, _f64p)):
+            raise OracleValidationError("pixel outside the valid interpolation region")
+    return lower, dlo, dhi, coeff
+
+
+def blend(coeff, mapped) -> float:
+    """transform_pixel's ascending-order sum and clamp (interpolation.cpp:68-86)."""
+    c = np.ascontiguousarray(coeff, dtype=np.float64)
+    m = np.ascontiguousarray(mapped, dtype=np.float64)
+    return float(_lib("c").orc_blend(c.size, _p(c, _f64p), _p(m, _f64p)))
+
+
+def transform_pixel_ref(value, luts, lo, hi, degenerate, coeff) -> float:
+    luts = np.ascontiguousarray(luts, dtype=np.float64)
+    lo, hi, coeff = (np.ascontiguousarray(a, dtype=np.float64) for a in (lo, hi, coeff))
+    dg = np.ascontiguousarray(degenerate, dtype=np.uint8)
+    return float(_lib("ref").ref_transform_pixel(float(value), coeff.size, _p(luts, _f64p),
+                                                 luts.shape[1], _p(lo, _f64p), _p(hi, _f64p),
+                                                 _p(dg, _u8p), _p(coeff, _f64p)))

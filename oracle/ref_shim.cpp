@@ -1,0 +1,178 @@
+// oracle/ref_shim.cpp -- TEST INFRASTRUCTURE ONLY.
+//
+// A C-ABI shim over the reference library compiled from its own sources under
+// /root/reference/proj/core (oracle/Makefile builds both into
+// oracle/_ref/libmclahe_ref.so).  It lets the Python tests and bench.py's
+// reference arm drive the UNMODIFIED reference code through its public API:
+// mclahe::mclahe (pipeline.hpp:30), build_mappings / compute_histogram /
+// clip_histogram / normalized_cdf / bin_index / apply_mapping
+// (histogram.hpp:51-80), neighbor_kernels / interp_coefficients /
+// transform_pixel (interpolation.hpp:28-45).
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <string>
+#include <vector>
+
+#include "mclahe/histogram.hpp"
+#include "mclahe/interpolation.hpp"
+#include "mclahe/nd_image.hpp"
+#include "mclahe/pipeline.hpp"
+
+namespace {
+
+void put_err(char* err, int len, const char* what) {
+  if (err && len > 0) {
+    std::strncpy(err, what, static_cast<size_t>(len) - 1);
+    err[len - 1] = '\0';
+  }
+}
+
+mclahe::NdImage make_image(const double* data, int rank, const int64_t* shape) {
+  mclahe::Shape s(shape, shape + rank);
+  size_t n = 1;
+  for (int i = 0; i < rank; ++i) n *= static_cast<size_t>(shape[i]);
+  return mclahe::NdImage(std::move(s), std::vector<double>(data, data + n));
+}
+
+}  // namespace
+
+extern "C" {
+
+// Runs mclahe::mclahe end to end.  timings (nullable) receives
+// {pad_s, histograms_s, interpolation_s}.  Returns 0, 1 (ValidationError) or
+// 2 (other exception) with the message in err.
+int ref_mclahe(const double* data, int rank, const int64_t* shape, const int64_t* kernel,
+               int64_t n_bins, double clip_limit, int adaptive, unsigned threads,
+               double* out, double* timings, char* err, int err_len) {
+  try {
+    mclahe::McLaheRequest req{make_image(data, rank, shape),
+                              mclahe::KernelSpec{std::vector<size_t>(kernel, kernel + rank)},
+                              mclahe::EnhanceParams{}, threads};
+    req.params.clip_limit = clip_limit;
+    req.params.n_bins = static_cast<size_t>(n_bins);
+    req.params.range_mode = adaptive ? mclahe::RangeMode::Adaptive : mclahe::RangeMode::Global;
+    mclahe::PhaseTimings pt;
+    const mclahe::NdImage res = mclahe::mclahe(req, &pt);
+    std::memcpy(out, res.values().data(), res.size() * sizeof(double));
+    if (timings) {
+      timings[0] = pt.pad_s;
+      timings[1] = pt.histograms_s;
+      timings[2] = pt.interpolation_s;
+    }
+    return 0;
+  } catch (const mclahe::ValidationError& e) {
+    put_err(err, err_len, e.what());
+    return 1;
+  } catch (const std::exception& e) {
+    put_err(err, err_len, e.what());
+    return 2;
+  }
+}
+
+// Per-tile intermediates through the reference's public API: pad plan,
+// symmetric_pad, kernelize, then build_mappings for ranges / LUTs and
+// compute_histogram + clip_histogram per block for counts and clipped counts
+// (zero for degenerate-range tiles, which build_mappings never bins).
+int ref_tile_stats(const double* data, int rank, const int64_t* shape, const int64_t* kernel,
+                   int64_t n_bins, double clip_limit, int adaptive, double* lo, double* hi,
+                   double* counts, double* clipped, double* lut, uint8_t* degenerate,
+                   char* err, int err_len) {
+  try {
+    const mclahe::NdImage image = make_image(data, rank, shape);
+    const mclahe::KernelSpec ks{std::vector<size_t>(kernel, kernel + rank)};
+    const mclahe::PadPlan plan = mclahe::compute_pad_plan(image.shape(), ks);
+    const mclahe::NdImage padded = mclahe::symmetric_pad(image, plan);
+    const mclahe::KernelGrid grid = mclahe::kernelize(padded, ks);
+    mclahe::EnhanceParams params;
+    params.clip_limit = clip_limit;
+    params.n_bins = static_cast<size_t>(n_bins);
+    params.range_mode = adaptive ? mclahe::RangeMode::Adaptive : mclahe::RangeMode::Global;
+    mclahe::IntensityRange global;
+    image.min_max(global.lo, global.hi);
+    const mclahe::MappingGrid maps = mclahe::build_mappings(grid, params, global, 1);
+    const size_t nb = static_cast<size_t>(n_bins);
+    for (size_t k = 0; k < grid.block_count(); ++k) {
+      const mclahe::KernelMapping& m = maps.at(k);
+      if (lo) lo[k] = m.range.lo;
+      if (hi) hi[k] = m.range.hi;
+      if (degenerate) degenerate[k] = m.degenerate ? 1 : 0;
+      if (lut) std::memcpy(lut + k * nb, m.values.data(), nb * sizeof(double));
+      std::vector<double> c(nb, 0.0), cl(nb, 0.0);
+      if (!m.range.degenerate()) {
+        c = mclahe::compute_histogram(grid.block(k), m.range, nb);
+        cl = mclahe::clip_histogram(c, clip_limit);
+      }
+      if (counts) std::memcpy(counts + k * nb, c.data(), nb * sizeof(double));
+      if (clipped) std::memcpy(clipped + k * nb, cl.data(), nb * sizeof(double));
+    }
+    return 0;
+  } catch (const mclahe::ValidationError& e) {
+    put_err(err, err_len, e.what());
+    return 1;
+  } catch (const std::exception& e) {
+    put_err(err, err_len, e.what());
+    return 2;
+  }
+}
+
+int64_t ref_bin_index(double value, double lo, double hi, int64_t n_bins) {
+  try {
+    return static_cast<int64_t>(
+        mclahe::bin_index(value, mclahe::IntensityRange{lo, hi}, static_cast<size_t>(n_bins)));
+  } catch (...) {
+    return -1;
+  }
+}
+
+void ref_clip_histogram(const double* counts, int64_t n, double clip_limit, double* out) {
+  const std::vector<double> r =
+      mclahe::clip_histogram(std::span<const double>(counts, static_cast<size_t>(n)), clip_limit);
+  std::memcpy(out, r.data(), r.size() * sizeof(double));
+}
+
+int ref_normalized_cdf(const double* clipped, int64_t n, double* out) {
+  const mclahe::NormalizedCdf r =
+      mclahe::normalized_cdf(std::span<const double>(clipped, static_cast<size_t>(n)));
+  std::memcpy(out, r.values.data(), r.values.size() * sizeof(double));
+  return r.degenerate ? 1 : 0;
+}
+
+// neighbor_kernels + interp_coefficients for one padded pixel.  Returns 0 or
+// 1 (ValidationError).
+int ref_neighbors(int rank, const int64_t* pixel, const int64_t* kernel, const int64_t* grid,
+                  int64_t* lower, double* dist_lo, double* dist_hi, double* coeff) {
+  try {
+    std::vector<size_t> px(pixel, pixel + rank), gs(grid, grid + rank);
+    const mclahe::KernelSpec ks{std::vector<size_t>(kernel, kernel + rank)};
+    const mclahe::NeighborSet ns = mclahe::neighbor_kernels(px, ks, gs);
+    for (int j = 0; j < rank; ++j) {
+      lower[j] = static_cast<int64_t>(ns.lower[j]);
+      dist_lo[j] = ns.dist_lo[j];
+      dist_hi[j] = ns.dist_hi[j];
+    }
+    mclahe::interp_coefficients(ns, ks, std::span<double>(coeff, size_t{1} << rank));
+    return 0;
+  } catch (const mclahe::ValidationError&) {
+    return 1;
+  }
+}
+
+// transform_pixel over explicit per-corner LUTs (n_bins each, ranges lo/hi,
+// degenerate flags).
+double ref_transform_pixel(double value, int corners, const double* luts, int64_t n_bins,
+                           const double* lo, const double* hi, const uint8_t* degenerate,
+                           const double* coeff) {
+  std::vector<mclahe::KernelMapping> maps(static_cast<size_t>(corners));
+  std::vector<const mclahe::KernelMapping*> ptrs;
+  for (int c = 0; c < corners; ++c) {
+    maps[c].range = {lo[c], hi[c]};
+    maps[c].values.assign(luts + c * n_bins, luts + (c + 1) * n_bins);
+    maps[c].degenerate = degenerate[c] != 0;
+    ptrs.push_back(&maps[c]);
+  }
+  return mclahe::transform_pixel(value, ptrs,
+                                 std::span<const double>(coeff, static_cast<size_t>(corners)));
+}
+
+}  // extern "C"

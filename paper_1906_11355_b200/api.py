@@ -1,0 +1,312 @@
+"""Python host mirror of the reference's MCLAHE interface, over the C ABI.
+
+Reference interface (paths relative to /root/reference/proj/core/):
+
+* ``RangeMode`` / ``EnhanceParams``     include/mclahe/histogram.hpp:13-21
+* ``KernelSpec``                        include/mclahe/nd_image.hpp:81-83
+* ``McLaheRequest`` / ``PhaseTimings``  include/mclahe/pipeline.hpp:12-24
+* ``mclahe(request, timings)``          include/mclahe/pipeline.hpp:30
+* ``ValidationError``                   include/mclahe/nd_image.hpp:19-22
+
+Same names, argument meaning and error behaviour; the compute is the sm_100a
+library (``libmclahe_gpu.so``).  Host ``numpy`` images go through the
+one-shot ``mclahe_gpu_run`` (H2D, four passes, D2H); CUDA ``torch`` tensors go
+through a cached device-resident :class:`Plan` on the current stream.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as N
+from ._native import ValidationError  # noqa: F401  (re-export)
+
+
+class RangeMode(enum.IntEnum):
+    Global = 0
+    Adaptive = 1
+
+
+@dataclass
+class EnhanceParams:
+    clip_limit: float = 1.0
+    n_bins: int = 256
+    range_mode: RangeMode = RangeMode.Global
+
+
+@dataclass
+class KernelSpec:
+    sizes: tuple = ()
+
+
+@dataclass
+class McLaheRequest:
+    image: object = None
+    kernel: KernelSpec = field(default_factory=KernelSpec)
+    params: EnhanceParams = field(default_factory=EnhanceParams)
+    threads: int = 0  # accepted for interface parity; the GPU path ignores it
+
+
+@dataclass
+class PhaseTimings:
+    pad_s: float = 0.0
+    histograms_s: float = 0.0
+    interpolation_s: float = 0.0
+
+
+def _is_torch(x) -> bool:
+    try:
+        import torch
+    except ImportError:  # pragma: no cover
+        return False
+    return isinstance(x, torch.Tensor)
+
+
+def _dtype_code(dt) -> int:
+    if _is_torch_dtype(dt):
+        import torch
+        return N.F64 if dt == torch.float64 else N.F32
+    return N.F64 if np.dtype(dt) == np.float64 else N.F32
+
+
+def _is_torch_dtype(dt) -> bool:
+    try:
+        import torch
+    except ImportError:  # pragma: no cover
+        return False
+    return isinstance(dt, torch.dtype)
+
+
+def _stream_handle(stream=None) -> int:
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+class Plan:
+    """A device-resident plan for one slab (rows [row_begin, row_end) along
+    dim 0) of a volume.  Wraps mclahe_plan_* and the pass entry points."""
+
+    def __init__(self, shape, kernel, n_bins=256, clip_limit=1.0, adaptive=False,
+                 dtype=N.F32, row_begin: int = 0, row_end: int | None = None):
+        self.params = N.make_params(shape, kernel, n_bins, clip_limit, adaptive, dtype)
+        self.shape = tuple(int(s) for s in shape)
+        self.kernel = tuple(int(k) for k in kernel)
+        self.n_bins, self.clip_limit, self.adaptive, self.dtype = int(n_bins), float(clip_limit), \
+            bool(adaptive), dtype
+        row_end = self.shape[0] if row_end is None else int(row_end)
+        L = N.lib()
+        h = C.c_void_p()
+        N.check(L.mclahe_plan_create(C.byref(self.params), int(row_begin), row_end, C.byref(h)))
+        self._h = h
+        info = N.PlanInfo()
+        N.check(L.mclahe_plan_get_info(h, C.byref(info)))
+        self.info = info
+        self.row_begin, self.row_end = int(row_begin), row_end
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                N.lib().mclahe_plan_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+    # ---- geometry ----
+    @property
+    def workspace_bytes(self) -> int:
+        return int(self.info.workspace_bytes)
+
+    @property
+    def window_tiles(self) -> int:
+        i = self.info
+        return int((i.tile_row_end - i.tile_row_begin) * i.tiles_per_row)
+
+    @property
+    def local_shape(self) -> tuple:
+        return (self.row_end - self.row_begin,) + self.shape[1:]
+
+    def new_workspace(self, device=None):
+        import torch
+        return torch.empty(self.workspace_bytes, dtype=torch.uint8, device=device or "cuda")
+
+    # workspace views (torch), for the slab exchange layer
+    def range_view(self, ws):
+        import torch
+        o = self.info.off_range
+        return ws[o:o + 32].view(torch.int64)
+
+    def tile_range_view(self, ws):
+        import torch
+        o = self.info.off_tile_range
+        return ws[o:o + 16 * self.window_tiles].view(torch.int64).view(-1, 2)
+
+    def counts_view(self, ws):
+        import torch
+        o = self.info.off_counts
+        n = self.window_tiles * self.n_bins
+        return ws[o:o + 4 * n].view(torch.int32).view(self.window_tiles, self.n_bins)
+
+    def lut_view(self, ws):
+        import torch
+        o = self.info.off_lut
+        n = self.window_tiles * self.n_bins
+        return ws[o:o + 4 * n].view(torch.float32).view(self.window_tiles, self.n_bins)
+
+    # ---- passes ----
+    def _ptr(self, t) -> int:
+        return int(t.data_ptr())
+
+    def reset(self, ws, stream=None):
+        N.check(N.lib().mclahe_pass_reset(self._h, self._ptr(ws), _stream_handle(stream)))
+
+    def range(self, x, ws, stream=None):
+        N.check(N.lib().mclahe_pass_range(self._h, self._ptr(x), self._ptr(ws),
+                                          _stream_handle(stream)))
+
+    def make_params(self, ws, stream=None):
+        N.check(N.lib().mclahe_pass_params(self._h, self._ptr(ws), _stream_handle(stream)))
+
+    def histograms(self, x, ws, stream=None):
+        N.check(N.lib().mclahe_pass_histograms(self._h, self._ptr(x), self._ptr(ws),
+                                               _stream_handle(stream)))
+
+    def mappings(self, ws, stream=None, debug: dict | None = None):
+        dbg = None
+        if debug is not None:
+            dbg = N.Debug()
+            for k in ("lo", "hi", "counts", "clipped", "lut", "degenerate"):
+                t = debug.get(k)
+                setattr(dbg, k, self._ptr(t) if t is not None else None)
+        N.check(N.lib().mclahe_pass_mappings(self._h, self._ptr(ws),
+                                             C.byref(dbg) if dbg is not None else None,
+                                             _stream_handle(stream)))
+
+    def interpolate(self, x, out, ws, stream=None):
+        N.check(N.lib().mclahe_pass_interpolate(self._h, self._ptr(x), self._ptr(out),
+                                                self._ptr(ws), _stream_handle(stream)))
+
+    def enqueue(self, x, out, ws, stream=None):
+        N.check(N.lib().mclahe_plan_enqueue(self._h, self._ptr(x), self._ptr(out), self._ptr(ws),
+                                            _stream_handle(stream)))
+
+    def check(self, ws, stream=None):
+        N.check(N.lib().mclahe_plan_check(self._h, self._ptr(ws), _stream_handle(stream)))
+
+    def tile_stats(self, x, stream=None) -> dict:
+        """Runs passes 1-3 and returns the per-tile intermediates of the
+        workspace window (debug arrays of build_mappings, histogram.cpp:72-106)."""
+        import torch
+        ws = self.new_workspace(x.device)
+        T, n = self.window_tiles, self.n_bins
+        dev = x.device
+        dbg = dict(lo=torch.empty(T, dtype=torch.float64, device=dev),
+                   hi=torch.empty(T, dtype=torch.float64, device=dev),
+                   counts=torch.empty(T, n, dtype=torch.int32, device=dev),
+                   clipped=torch.empty(T, n, dtype=torch.float64, device=dev),
+                   lut=torch.empty(T, n, dtype=torch.float64, device=dev),
+                   degenerate=torch.empty(T, dtype=torch.uint8, device=dev))
+        self.reset(ws, stream)
+        self.range(x, ws, stream)
+        self.make_params(ws, stream)
+        self.histograms(x, ws, stream)
+        self.mappings(ws, stream, debug=dbg)
+        self.check(ws, stream)
+        out = {k: v.cpu().numpy() for k, v in dbg.items()}
+        out["degenerate"] = out["degenerate"].astype(bool)
+        out["lut32"] = self.lut_view(ws).cpu().numpy()
+        return out
+
+
+_PLAN_CACHE: dict = {}
+
+
+def _cached_plan(shape, kernel, n_bins, clip_limit, adaptive, dtype) -> Plan:
+    import torch
+    key = (tuple(shape), tuple(kernel), int(n_bins), float(clip_limit), bool(adaptive), dtype,
+           torch.cuda.current_device())
+    p = _PLAN_CACHE.get(key)
+    if p is None:
+        if len(_PLAN_CACHE) > 32:
+            _PLAN_CACHE.clear()
+        p = _PLAN_CACHE[key] = Plan(shape, kernel, n_bins, clip_limit, adaptive, dtype)
+    return p
+
+
+def _request_parts(request: McLaheRequest):
+    sizes = request.kernel.sizes if isinstance(request.kernel, KernelSpec) else request.kernel
+    p = request.params
+    return (tuple(int(s) for s in sizes), int(p.n_bins), float(p.clip_limit),
+            RangeMode(p.range_mode) == RangeMode.Adaptive)
+
+
+def mclahe(request: McLaheRequest, timings: PhaseTimings | None = None):
+    """mclahe::mclahe (include/mclahe/pipeline.hpp:30, src/pipeline.cpp:73-129).
+
+    numpy image -> numpy result (float32 for float32 input, float64 for every
+    other real dtype, as the reference computes on doubles); CUDA torch
+    tensor -> CUDA torch tensor on the current stream.  Raises
+    ValidationError with the reference's messages."""
+    kernel, n_bins, clip, adaptive = _request_parts(request)
+    img = request.image
+    if _is_torch(img):
+        return _mclahe_device(img, kernel, n_bins, clip, adaptive, timings)
+    x = np.asarray(img)
+    if x.dtype != np.float32:
+        x = x.astype(np.float64)
+    x = np.ascontiguousarray(x)
+    params = N.make_params(x.shape, kernel, n_bins, clip, adaptive, _dtype_code(x.dtype))
+    out = np.empty_like(x)
+    t = N.Timings()
+    N.check(N.lib().mclahe_gpu_run(C.byref(params), x.ctypes.data, out.ctypes.data, C.byref(t)))
+    if timings is not None:
+        timings.pad_s += t.pad_s
+        timings.histograms_s += t.histograms_s
+        timings.interpolation_s += t.interpolation_s
+    return out
+
+
+def _mclahe_device(x, kernel, n_bins, clip, adaptive, timings=None):
+    import torch
+    if not x.is_cuda:
+        raise ValidationError("torch input must be a CUDA tensor (use numpy for host data)")
+    if x.dtype not in (torch.float32, torch.float64):
+        x = x.to(torch.float64)
+    x = x.contiguous()
+    plan = _cached_plan(x.shape, kernel, n_bins, clip, adaptive, _dtype_code(x.dtype))
+    ws = plan.new_workspace(x.device)
+    out = torch.empty_like(x)
+    plan.enqueue(x, out, ws)
+    plan.check(ws)
+    return out
+
+
+def enhance(image, kernel_size, n_bins: int = 256, clip_limit: float = 1.0,
+            adaptive_hist_range: bool = False):
+    """Convenience form with the paper's argument names (data, kernel_size,
+    n_bins, clip_limit, adaptive_hist_range)."""
+    req = McLaheRequest(image=image, kernel=KernelSpec(tuple(kernel_size)),
+                        params=EnhanceParams(clip_limit, n_bins,
+                                             RangeMode.Adaptive if adaptive_hist_range
+                                             else RangeMode.Global))
+    return mclahe(req)
+
+
+def bin_index_device(values, lo: float, hi: float, n_bins: int):
+    """bin_index (src/histogram.cpp:24-32) of a CUDA tensor through the kernels'
+    guarded fast routine; int32 result (-1 for a degenerate range)."""
+    import torch
+    v = values.contiguous()
+    out = torch.empty(v.shape, dtype=torch.int32, device=v.device)
+    code = N.F64 if v.dtype == torch.float64 else N.F32
+    N.check(N.lib().mclahe_debug_bin_index(code, v.data_ptr(), v.numel(), float(lo), float(hi),
+                                           int(n_bins), out.data_ptr(), _stream_handle()))
+    return out
+
+
+def launch_count() -> int:
+    return int(N.lib().mclahe_launch_count())

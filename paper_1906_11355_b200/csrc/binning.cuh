@@ -1,0 +1,121 @@
+// binning.cuh -- bit-exact bin_index (src/histogram.cpp:24-32) at FP32 speed.
+//
+// The reference computes  floor(((double)v - lo) / (hi - lo) * n)  in IEEE
+// double (divide, then multiply; no FMA) and clamps into [0, n-1].  A double
+// divide per voxel per corner does not fit the issue budget of the blend pass,
+// and a plain FP32 fused estimate misbins values that sit on (or within a few
+// ulp of) a bin edge -- which quantised data does constantly.  So:
+//
+//   y  = fl32(fl32(v - lo) * c),  c = fl32(n / (hi - lo))
+//
+// differs from the reference's f64 value q by at most |y| * 1.81e-7 (three
+// f32 roundings + O(2^-50)), i.e. by less than tol = 2.5e-7 * n on the only
+// interval that matters, y in [0.5, n - 0.5] (outside it the clamp decides the
+// bin whatever the rounding).  If frac(y) is further than tol from an integer
+// then floor(y) == floor(q) and the fast answer is exact; otherwise (rare) the
+// lane recomputes q exactly as the reference does, with __ddiv_rn.  Ranges the
+// bound does not cover (c not a normal float, hi - lo overflowing f32, huge n)
+// set lim < 0 and always take the exact path.  For f64 data the same scheme
+// runs in f64 with tol = 1e-15 * n.
+#pragma once
+
+#include <cfloat>
+#include <cmath>
+#include <cstdint>
+
+#include "geometry.h"
+
+namespace mg {
+
+// Per-tile binning parameters.  lim in (0, 0.5): guarded fast path;
+// lim < 0: exact path only; lim > 1: degenerate range (no histogram, the
+// mapping is the constant 0.5 -- histogram.cpp:95-98).
+template <typename T>
+struct alignas(4 * sizeof(T)) TileParam {
+  T lo, hi, c, lim;
+};
+
+MG_HD bool tp_degenerate(float lim) { return lim > 1.0f; }
+MG_HD bool tp_degenerate(double lim) { return lim > 1.0; }
+
+// Builds the parameters for range [lo, hi] (exact values of the data type).
+MG_HD TileParam<float> make_tile_param_f32(double lo, double hi, int64_t n) {
+  TileParam<float> tp;
+  tp.lo = static_cast<float>(lo);
+  tp.hi = static_cast<float>(hi);
+  if (!(lo < hi)) {
+    tp.c = 0.0f;
+    tp.lim = 2.0f;
+    return tp;
+  }
+  const double c64 = static_cast<double>(n) / (hi - lo);
+  const float c = static_cast<float>(c64);
+  const float span = tp.hi - tp.lo;  // plain f32 subtraction, no contraction possible
+  const bool ok = std::isfinite(c) && c >= FLT_MIN && std::isfinite(span) &&
+                  std::isfinite(tp.lo) && std::isfinite(tp.hi) && n <= (int64_t{1} << 20);
+  tp.c = ok ? c : 0.0f;
+  tp.lim = ok ? 0.5f - static_cast<float>(n) * 2.5e-7f : -1.0f;
+  return tp;
+}
+
+MG_HD TileParam<double> make_tile_param_f64(double lo, double hi, int64_t n) {
+  TileParam<double> tp;
+  tp.lo = lo;
+  tp.hi = hi;
+  if (!(lo < hi)) {
+    tp.c = 0.0;
+    tp.lim = 2.0;
+    return tp;
+  }
+  const double c = static_cast<double>(n) / (hi - lo);
+  const bool ok = std::isfinite(c) && c >= DBL_MIN && n <= (int64_t{1} << 40);
+  tp.c = ok ? c : 0.0;
+  tp.lim = ok ? 0.5 - static_cast<double>(n) * 1e-15 : -1.0;
+  return tp;
+}
+
+template <typename T>
+MG_HD TileParam<T> make_tile_param(double lo, double hi, int64_t n);
+template <>
+MG_HD TileParam<float> make_tile_param<float>(double lo, double hi, int64_t n) {
+  return make_tile_param_f32(lo, hi, n);
+}
+template <>
+MG_HD TileParam<double> make_tile_param<double>(double lo, double hi, int64_t n) {
+  return make_tile_param_f64(lo, hi, n);
+}
+
+#ifdef __CUDACC__
+
+// The reference arithmetic, operation for operation (histogram.cpp:27-31).
+__device__ __forceinline__ int bin_exact(double v, double lo, double hi, int n) {
+  const double scaled = floor(__dmul_rn(__ddiv_rn(__dsub_rn(v, lo), __dsub_rn(hi, lo)),
+                                        static_cast<double>(n)));
+  if (!(scaled > 0.0)) return 0;
+  if (scaled >= static_cast<double>(n)) return n - 1;
+  return static_cast<int>(scaled);
+}
+
+// nm05 = n - 0.5 (exact in f32 for n < 2^23).
+__device__ __forceinline__ int bin_of(float v, const TileParam<float>& tp, int n, float nm05) {
+  float y = __fmul_rn(__fsub_rn(v, tp.lo), tp.c);
+  y = fminf(fmaxf(y, 0.5f), nm05);
+  const float t = __fadd_rd(y, 12582912.0f);  // 1.5 * 2^23: t = floor(y) + M exactly
+  const float fr = __fsub_rn(y, __fsub_rn(t, 12582912.0f));
+  if (fabsf(__fsub_rn(fr, 0.5f)) < tp.lim) return __float_as_int(t) - 0x4B400000;
+  return bin_exact(static_cast<double>(v), static_cast<double>(tp.lo),
+                   static_cast<double>(tp.hi), n);
+}
+
+__device__ __forceinline__ int bin_of(double v, const TileParam<double>& tp, int n, double nm05) {
+  double y = __dmul_rn(__dsub_rn(v, tp.lo), tp.c);
+  y = fmin(fmax(y, 0.5), nm05);
+  const double fl = floor(y);
+  const double fr = __dsub_rn(y, fl);
+  if (fabs(__dsub_rn(fr, 0.5)) < tp.lim) return static_cast<int>(fl);
+  return bin_exact(v, tp.lo, tp.hi, n);
+}
+
+#endif  // __CUDACC__
+
+}  // namespace mg

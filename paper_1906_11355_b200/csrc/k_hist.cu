@@ -1,0 +1,32 @@
+// k_hist.cu -- instantiations of the K2a/K2b pencil kernels (own translation
+// unit so the build compiles kernel families in parallel).
+#include "k_pencil.cuh"
+
+namespace mg {
+
+PencilRangeFn get_range_pencil(int ko) {
+  switch (ko) {
+    case 1: return k_range_pencil<1>;
+    case 2: return k_range_pencil<2>;
+    case 3: return k_range_pencil<3>;
+    case 4: return k_range_pencil<4>;
+    default: return k_range_pencil<5>;
+  }
+}
+
+template <bool A>
+static PencilHistFn hist_t(int ko) {
+  switch (ko) {
+    case 1: return k_hist_pencil<1, A>;
+    case 2: return k_hist_pencil<2, A>;
+    case 3: return k_hist_pencil<3, A>;
+    case 4: return k_hist_pencil<4, A>;
+    default: return k_hist_pencil<5, A>;
+  }
+}
+
+PencilHistFn get_hist_pencil(int ko, bool adaptive) {
+  return adaptive ? hist_t<true>(ko) : hist_t<false>(ko);
+}
+
+}  // namespace mg

@@ -1,0 +1,290 @@
+// k_misc.cuh -- the non-pencil kernels: workspace reset, K1 global range,
+// binning parameters, K3 mappings, and the generic (any-shape, f32/f64)
+// fallbacks of K2 and K4 that run one voxel per thread with global atomics.
+#pragma once
+
+#include "common.cuh"
+
+namespace mg {
+
+__device__ __forceinline__ int64_t window_tile(const KGeom& G, const int64_t* t) {
+  int64_t f = (t[0] - G.trow0) * G.tstride[0];
+  for (int j = 1; j < G.rank; ++j) f += t[j] * G.tstride[j];
+  return f;
+}
+
+__device__ __forceinline__ void decode_local(const KGeom& G, int64_t idx, int64_t* x) {
+  for (int j = G.rank - 1; j >= 0; --j) {
+    const int64_t ext = j == 0 ? (G.local_voxels / G.vstride[0]) : G.d[j].s;
+    x[j] = idx % ext;
+    idx /= ext;
+  }
+  x[0] += G.row0;
+}
+
+// ---------------------------------------------------------------- reset ---
+__global__ void k_reset(int64_t* range, int64_t* trange, int64_t n_trange) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < 4) range[i] = i < 2 ? INT64_MIN : 0;
+  for (int64_t k = i; k < n_trange; k += (int64_t)gridDim.x * blockDim.x) trange[k] = INT64_MIN;
+}
+
+// ------------------------------------------------------------------ K1 ----
+// Global min/max + finiteness over the slab (NdImage::min_max / all_finite,
+// src/nd_image.cpp:70-83).  Grid-stride, 16-byte loads, one atomic per CTA.
+template <typename T>
+__global__ void __launch_bounds__(256) k_global_range(const T* __restrict__ in, int64_t n,
+                                                      int64_t* __restrict__ range) {
+  constexpr int V = 16 / sizeof(T);
+  T lo = INFINITY, hi = -INFINITY;
+  int bad = 0;
+  const int64_t nv = ((reinterpret_cast<uintptr_t>(in) & 15) == 0) ? n / V : 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nv; i += stride) {
+    T v[V];
+    if constexpr (V == 4) {
+      const float4 q = __ldcs(reinterpret_cast<const float4*>(in) + i);
+      v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+    } else {
+      const double2 q = __ldcs(reinterpret_cast<const double2*>(in) + i);
+      v[0] = q.x; v[1] = q.y;
+    }
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      bad |= !isfinite(v[k]);
+      lo = fmin(lo, v[k]);
+      hi = fmax(hi, v[k]);
+    }
+  }
+  for (int64_t i = nv * V + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    const T v = in[i];
+    bad |= !isfinite(v);
+    lo = fmin(lo, v);
+    hi = fmax(hi, v);
+  }
+  // warp + block reduction
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+  }
+  __shared__ T slo[8], shi[8];
+  __shared__ int sbad[8];
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) {
+    slo[w] = lo;
+    shi[w] = hi;
+    sbad[w] = bad;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int k = 1; k < (int)(blockDim.x >> 5); ++k) {
+      lo = fmin(lo, slo[k]);
+      hi = fmax(hi, shi[k]);
+      bad |= sbad[k];
+    }
+    if (lo <= hi) {  // skip CTAs that saw no finite value
+      atomicMax(reinterpret_cast<long long*>(&range[0]), (long long)~okey((double)lo));
+      atomicMax(reinterpret_cast<long long*>(&range[1]), (long long)okey((double)hi));
+    }
+    if (bad) atomicMax(reinterpret_cast<long long*>(&range[2]), 1LL);
+  }
+}
+
+// --------------------------------------------------------------- params ---
+template <typename T>
+__global__ void k_params(const KGeom G, WS W) {
+  TileParam<T>* tp = reinterpret_cast<TileParam<T>*>(W.tparams);
+  const int64_t n = G.adaptive ? G.win_tiles : 1;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t* r = G.adaptive ? W.trange + 2 * t : W.range;
+    const double lo = okey_decode(~r[0]);
+    const double hi = okey_decode(r[1]);
+    tp[t] = make_tile_param<T>(lo, hi, G.n_bins);
+  }
+}
+
+// ------------------------------------------------------ K2 generic -------
+// One voxel per thread; enumerates the (<= 3^D) tiles a voxel's padded copies
+// fall in.  MODE 0: per-tile min/max (adaptive ranges); MODE 1: counts.
+template <typename T, int MODE, bool ADAPT>
+__global__ void __launch_bounds__(256) k_tiles_generic(const KGeom G, const T* __restrict__ in,
+                                                       WS W) {
+  const int n = G.n_bins;
+  const T nm05 = (T)n - (T)0.5;
+  const TileParam<T>* tparams = reinterpret_cast<const TileParam<T>*>(W.tparams);
+  int bad = 0;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < G.local_voxels;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    int64_t x[kMaxRank];
+    decode_local(G, idx, x);
+    const T v = in[idx];
+    if (MODE == 0) bad |= !isfinite(v);
+    int64_t tl[kMaxRank][3];
+    int wl[kMaxRank][3], nl[kMaxRank], ci[kMaxRank];
+    for (int j = 0; j < G.rank; ++j) {
+      nl[j] = voxel_tiles(G.d[j], x[j], tl[j], wl[j]);
+      ci[j] = 0;
+    }
+    while (true) {
+      int64_t t[kMaxRank];
+      int w = 1;
+      for (int j = 0; j < G.rank; ++j) {
+        t[j] = tl[j][ci[j]];
+        w *= wl[j][ci[j]];
+      }
+      const int64_t f = window_tile(G, t);
+      if (MODE == 0) {
+        atomicMax(reinterpret_cast<long long*>(W.trange + 2 * f), (long long)~okey((double)v));
+        atomicMax(reinterpret_cast<long long*>(W.trange + 2 * f + 1), (long long)okey((double)v));
+      } else {
+        const TileParam<T> tp = tparams[ADAPT ? f : 0];
+        if (!tp_degenerate(tp.lim)) atomicAdd(W.counts + f * n + bin_of(v, tp, n, nm05), (uint32_t)w);
+      }
+      int j = G.rank - 1;
+      while (j >= 0 && ++ci[j] == nl[j]) ci[j--] = 0;
+      if (j < 0) break;
+    }
+  }
+  if (MODE == 0 && bad) atomicMax(reinterpret_cast<long long*>(&W.range[2]), 1LL);
+}
+
+// ------------------------------------------------------------------ K3 ----
+// One warp per tile.  The two order-sensitive f64 sums of the reference run in
+// bin order exactly as written there: the clip excess (histogram.cpp:47-48;
+// only clipped bins add non-zero terms, found by ballot, summed in order) and
+// the CDF prefix (histogram.cpp:59-63, one lane, sequential).  Everything else
+// is bin-parallel.  Output: f32 LUT (+ optional f64 debug arrays).
+template <typename T>
+__global__ void __launch_bounds__(128) k_mappings(const KGeom G, WS W, Debug Dbg) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int n = G.n_bins;
+  const int warps = blockDim.x >> 5, wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* cdf = reinterpret_cast<double*>(smem) + (int64_t)wid * n;
+  const TileParam<T>* tparams = reinterpret_cast<const TileParam<T>*>(W.tparams);
+  for (int64_t tile = (int64_t)blockIdx.x * warps + wid; tile < G.win_tiles;
+       tile += (int64_t)gridDim.x * warps) {
+    const TileParam<T> tp = tparams[G.adaptive ? tile : 0];
+    const uint32_t* cnt = W.counts + tile * n;
+    float* lut = W.lut + tile * n;
+    if (Dbg.lo && lane == 0) {
+      Dbg.lo[tile] = (double)tp.lo;
+      Dbg.hi[tile] = (double)tp.hi;
+    }
+    if (Dbg.counts)
+      for (int b = lane; b < n; b += 32) Dbg.counts[tile * n + b] = cnt[b];
+    if (tp_degenerate(tp.lim)) {  // histogram.cpp:95-98
+      for (int b = lane; b < n; b += 32) {
+        lut[b] = 0.5f;
+        if (Dbg.clipped) Dbg.clipped[tile * n + b] = 0.0;
+        if (Dbg.lut) Dbg.lut[tile * n + b] = 0.5;
+      }
+      if (Dbg.degenerate && lane == 0) Dbg.degenerate[tile] = 1;
+      continue;
+    }
+    // total = sum of counts (integers: exact in any order)
+    unsigned long long tot = 0;
+    for (int b = lane; b < n; b += 32) tot += cnt[b];
+    for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+    const double threshold = __dmul_rn(G.clip, (double)tot);
+    double excess = 0.0;
+    for (int base = 0; base < n; base += 32) {
+      const int b = base + lane;
+      const double over = b < n ? __dsub_rn((double)cnt[b], threshold) : 0.0;
+      unsigned m = __ballot_sync(0xffffffffu, over > 0.0);
+      while (m) {
+        const int src = __ffs(m) - 1;
+        excess = __dadd_rn(excess, __shfl_sync(0xffffffffu, over, src));
+        m &= m - 1;
+      }
+    }
+    const double share = __ddiv_rn(excess, (double)n);
+    for (int b = lane; b < n; b += 32) {
+      const double c = (double)cnt[b];
+      const double cl = __dadd_rn(c < threshold ? c : threshold, share);
+      cdf[b] = cl;
+      if (Dbg.clipped) Dbg.clipped[tile * n + b] = cl;
+    }
+    __syncwarp();
+    if (lane == 0) {
+      double run = 0.0;
+      int b = 0;
+      for (; b + 8 <= n; b += 8) {
+        double v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = cdf[b + k];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          run = __dadd_rn(run, v[k]);
+          cdf[b + k] = run;
+        }
+      }
+      for (; b < n; ++b) {
+        run = __dadd_rn(run, cdf[b]);
+        cdf[b] = run;
+      }
+    }
+    __syncwarp();
+    const double first = cdf[0];
+    const double span = __dsub_rn(cdf[n - 1], first);
+    const bool degen = !(span > 0.0);
+    for (int b = lane; b < n; b += 32) {
+      const double m = degen ? 0.5 : __ddiv_rn(__dsub_rn(cdf[b], first), span);
+      lut[b] = (float)m;
+      if (Dbg.lut) Dbg.lut[tile * n + b] = m;
+    }
+    if (Dbg.degenerate && lane == 0) Dbg.degenerate[tile] = degen ? 1 : 0;
+    __syncwarp();
+  }
+}
+
+// -------------------------------------------------------- K4 generic -----
+template <typename T, bool ADAPT>
+__global__ void __launch_bounds__(256) k_interp_generic(const KGeom G, const T* __restrict__ in,
+                                                        T* __restrict__ out, WS W) {
+  if (W.range[2] != 0) return;
+  const int n = G.n_bins;
+  const T nm05 = (T)n - (T)0.5;
+  const TileParam<T>* tparams = reinterpret_cast<const TileParam<T>*>(W.tparams);
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < G.local_voxels;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    int64_t x[kMaxRank], c[kMaxRank];
+    double f1[kMaxRank];
+    decode_local(G, idx, x);
+    const T v = in[idx];
+    for (int j = 0; j < G.rank; ++j) {
+      c[j] = cell_of(G.d[j], x[j]);
+      f1[j] = (double)twice_dlo(G.d[j], x[j], c[j]) / (double)(2 * G.d[j].b);
+    }
+    const int corners = 1 << G.rank;
+    const int bg = ADAPT ? 0 : bin_of(v, tparams[0], n, nm05);
+    double acc = 0.0;
+    for (int co = 0; co < corners; ++co) {
+      int64_t t[kMaxRank];
+      double w = 1.0;
+      for (int j = 0; j < G.rank; ++j) {
+        const int bit = (co >> (G.rank - 1 - j)) & 1;
+        t[j] = c[j] + bit;
+        w *= bit ? f1[j] : 1.0 - f1[j];
+      }
+      const int64_t f = window_tile(G, t);
+      const int b = ADAPT ? bin_of(v, tparams[f], n, nm05) : bg;
+      acc += w * (double)W.lut[f * n + b];
+    }
+    out[idx] = (T)fmin(fmax(acc, 0.0), 1.0);
+  }
+}
+
+// ------------------------------------------------------- debug binning ---
+template <typename T>
+__global__ void k_debug_bins(const T* __restrict__ v, int64_t count, double lo, double hi, int n,
+                             int32_t* __restrict__ out) {
+  const TileParam<T> tp = make_tile_param<T>(lo, hi, n);
+  const T nm05 = (T)n - (T)0.5;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = tp_degenerate(tp.lim) ? -1 : bin_of(v[i], tp, n, nm05);
+}
+
+}  // namespace mg

@@ -1,0 +1,396 @@
+// k_pencil.cuh -- the HBM-rate pencil kernels (consumers of the bulk-copy
+// stage pipeline in common.cuh).
+//
+//   k_range_pencil  K2a  per-tile min/max            (src/histogram.cpp:86-94)
+//   k_hist_pencil   K2b  per-tile counts             (src/histogram.cpp:24-40 over
+//                                                     src/nd_image.cpp:104-187)
+//   k_interp_pencil K4   2^D-corner blend            (src/pipeline.cpp:94-127,
+//                                                     src/interpolation.cpp:7-86)
+#pragma once
+
+#include "common.cuh"
+
+namespace mg {
+
+struct PencilSmem {
+  Pipe* pipe;
+  float* bufs;
+  unsigned char* tail;
+};
+
+__device__ __forceinline__ PencilSmem pencil_smem(const KGeom& G, unsigned char* smem) {
+  PencilSmem s;
+  s.pipe = reinterpret_cast<Pipe*>(smem);
+  s.bufs = reinterpret_cast<float*>(smem + pipe_bytes());
+  s.tail = smem + pipe_bytes() + (size_t)G.nst * G.stage_rows * G.P * 4;
+  return s;
+}
+
+// Trailing-block tile (primary; pencil kernels require merged mirror copies
+// along trailing dims) and multiplicity of the element at offset e.
+__device__ __forceinline__ void trailing_tile(const KGeom& G, int64_t e, int* tile, int* w) {
+  int64_t t = 0;
+  int wt = 1;
+  for (int j = G.rank - 1; j >= G.rank - G.kt; --j) {
+    const int64_t x = e % G.d[j].s;
+    e /= G.d[j].s;
+    const int64_t tj = (x + G.d[j].before) / G.d[j].b;
+    wt *= tile_parts(G.d[j], tj).weight(x);
+    t += tj * G.tstride[j];
+  }
+  *tile = (int)t;
+  *w = wt;
+}
+
+// --------------------------------------------------------------- K2a -----
+template <int KO>
+__global__ void __launch_bounds__(kPencilThreads, 3)
+    k_range_pencil(const __grid_constant__ KGeom G, const float* __restrict__ in, const int32_t* __restrict__ units,
+                   const int32_t* __restrict__ cta_units, WS W) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const PencilSmem P = pencil_smem(G, smem);
+  int32_t* smin = reinterpret_cast<int32_t*>(P.tail);  // [gtr] ~key32(lo)
+  int32_t* smax = smin + G.gtr;                         // [gtr] key32(hi)
+  pipe_init(*P.pipe, G.nst);
+  __syncthreads();
+  const int u0 = cta_units[blockIdx.x], u1 = cta_units[blockIdx.x + 1];
+  if (threadIdx.x >= kConsumers) {
+    if (threadIdx.x == kConsumers) pipe_produce<KO, false>(G, in, units, u0, u1, *P.pipe, P.bufs);
+    return;
+  }
+  const int tid = threadIdx.x;
+  const int slot = tid / G.tpr;
+  const int64_t e0 = (int64_t)(tid % G.tpr) * 4;
+  const bool lane_on = slot < G.rpi;
+  int trt[4], dummy;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) trailing_tile(G, e0 + i, &trt[i], &dummy);
+  float mn[4], mx[4];
+  int bad = 0;
+  int64_t cur = -1;
+  const int64_t stage_elems = (int64_t)G.stage_rows * G.P;
+
+  auto flush = [&]() {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (lane_on && mn[i] <= mx[i]) {
+        atomicMax(&smin[trt[i]], ~key32(mn[i]));
+        atomicMax(&smax[trt[i]], key32(mx[i]));
+      }
+    consumers_sync();
+    for (int64_t t = tid; t < G.gtr; t += kConsumers) {
+      if (smax[t] != INT32_MIN) {
+        long long* r = reinterpret_cast<long long*>(W.trange + 2 * (cur + t));
+        atomicMax(r, (long long)~okey((double)key32_decode(~smin[t])));
+        atomicMax(r + 1, (long long)okey((double)key32_decode(smax[t])));
+      }
+    }
+  };
+
+  uint32_t it = 0;
+  while (true) {
+    const int s = it % G.nst;
+    mbar_wait(&P.pipe->full[s], (it / G.nst) & 1);
+    const Stage& S = P.pipe->st[s];
+    if (S.unit < 0) break;
+    const int64_t key = S.key;
+    if (key != cur) {
+      if (cur >= 0) flush();
+      consumers_sync();
+      for (int64_t t = tid; t < G.gtr; t += kConsumers) smin[t] = smax[t] = INT32_MIN;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        mn[i] = INFINITY;
+        mx[i] = -INFINITY;
+      }
+      consumers_sync();
+      cur = key;
+    }
+    const int rows = S.nruns * S.nr;
+    const float* buf = P.bufs + s * stage_elems;
+    if (lane_on) {
+      for (int q = slot; q < rows; q += G.rpi) {
+        const float4 v = *reinterpret_cast<const float4*>(buf + q * G.P + e0);
+        const float a[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          bad |= !isfinite(a[i]);
+          mn[i] = fminf(mn[i], a[i]);
+          mx[i] = fmaxf(mx[i], a[i]);
+        }
+      }
+    }
+    __syncwarp();
+    if ((tid & 31) == 0) mbar_arrive(&P.pipe->empty[s]);
+    ++it;
+  }
+  if (cur >= 0) flush();
+  if (bad) atomicMax(reinterpret_cast<long long*>(&W.range[2]), 1LL);
+}
+
+// --------------------------------------------------------------- K2b -----
+// A voxel's multiplicity in a tile is the product of its per-dimension
+// multiplicities, so counting the support box with those weights equals
+// kernelize + compute_histogram while reading each input byte once.  Lanes
+// with equal (tile, bin, weight) merge via __match_any_sync: one shared
+// atomic carries the whole run.
+template <int KO, bool ADAPT>
+__global__ void __launch_bounds__(kPencilThreads, 3)
+    k_hist_pencil(const __grid_constant__ KGeom G, const float* __restrict__ in, const int32_t* __restrict__ units,
+                  const int32_t* __restrict__ cta_units, WS W) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const PencilSmem P = pencil_smem(G, smem);
+  const int n = G.n_bins;
+  uint32_t* hist = reinterpret_cast<uint32_t*>(P.tail);  // [gtr][n]
+  TileParam<float>* rng =
+      reinterpret_cast<TileParam<float>*>(P.tail + ((G.gtr * n * 4 + 15) & ~15LL));
+  const TileParam<float>* tparams = reinterpret_cast<const TileParam<float>*>(W.tparams);
+  const TileParam<float> g0 = tparams[0];
+  if (!ADAPT && tp_degenerate(g0.lim)) return;  // constant image: every mapping is 0.5
+  pipe_init(*P.pipe, G.nst);
+  __syncthreads();
+  const int u0 = cta_units[blockIdx.x], u1 = cta_units[blockIdx.x + 1];
+  if (threadIdx.x >= kConsumers) {
+    if (threadIdx.x == kConsumers) pipe_produce<KO, false>(G, in, units, u0, u1, *P.pipe, P.bufs);
+    return;
+  }
+  const float nm05 = (float)n - 0.5f;
+  const int tid = threadIdx.x;
+  const int slot = tid / G.tpr;
+  const int64_t e0 = (int64_t)(tid % G.tpr) * 4;
+  const bool lane_on = slot < G.rpi;
+  int trt[4], trw[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) trailing_tile(G, e0 + i, &trt[i], &trw[i]);
+  const int64_t stage_elems = (int64_t)G.stage_rows * G.P;
+  int64_t cur = -1;
+
+  uint32_t it = 0;
+  while (true) {
+    const int s = it % G.nst;
+    mbar_wait(&P.pipe->full[s], (it / G.nst) & 1);
+    const Stage& S = P.pipe->st[s];
+    if (S.unit < 0) break;
+    const int64_t key = S.key;
+    if (key != cur) {
+      consumers_sync();
+      if (cur >= 0) {
+        uint32_t* dst = W.counts + cur * n;
+        for (int64_t k = tid; k < G.gtr * n; k += kConsumers) {
+          const uint32_t c = hist[k];
+          if (c) atomicAdd(dst + k, c);
+        }
+        consumers_sync();
+      }
+      for (int64_t k = tid; k < G.gtr * n; k += kConsumers) hist[k] = 0;
+      if (ADAPT)
+        for (int64_t t = tid; t < G.gtr; t += kConsumers) rng[t] = tparams[key + t];
+      consumers_sync();
+      cur = key;
+    }
+    const int rows = S.nruns * S.nr;
+    const int nr = S.nr;
+    const float* buf = P.bufs + s * stage_elems;
+    for (int q0 = 0; q0 < rows; q0 += G.rpi) {  // trip count uniform over the warp
+      const int q = q0 + slot;
+      const bool ok = lane_on && q < rows;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      uint32_t wrow = 0;
+      if (ok) {
+        const int run = q / nr;
+        const int r = S.r0 + (q - run * nr);
+        wrow = (uint32_t)(S.run_w[run] * S.pl.weight(S.a_last + r));
+        v = *reinterpret_cast<const float4*>(buf + q * G.P + e0);
+      }
+      const float a[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        unsigned long long k64 = ~0ull - tid;  // unique: never merges
+        int cell = -1;
+        uint32_t wgt = 0;
+        if (ok) {
+          const TileParam<float> tp = ADAPT ? rng[trt[i]] : g0;
+          if (!tp_degenerate(tp.lim)) {
+            cell = trt[i] * n + bin_of(a[i], tp, n, nm05);
+            wgt = wrow * (uint32_t)trw[i];
+            k64 = ((unsigned long long)cell << 16) | wgt;
+          }
+        }
+        const unsigned peers = __match_any_sync(0xffffffffu, k64);
+        if (cell >= 0 && (__ffs(peers) - 1) == (tid & 31))
+          atomicAdd(&hist[cell], wgt * (uint32_t)__popc(peers));
+      }
+    }
+    __syncwarp();
+    if ((tid & 31) == 0) mbar_arrive(&P.pipe->empty[s]);
+    ++it;
+  }
+  consumers_sync();
+  if (cur >= 0) {
+    uint32_t* dst = W.counts + cur * n;
+    for (int64_t k = tid; k < G.gtr * n; k += kConsumers) {
+      const uint32_t c = hist[k];
+      if (c) atomicAdd(dst + k, c);
+    }
+  }
+}
+
+// ---------------------------------------------------------------- K4 -----
+// The pencil's 2^KO x gtr LUTs (and ranges) are staged in shared memory once
+// per cell.  Each thread owns a fixed 4-voxel column, so its 2^KT trailing
+// corner tiles and weights are registers; outer weights come per row from
+// the exact half-integer distances (d_lo = twice_dlo / 2).  FP32 sum.
+template <int KO, int KT, bool ADAPT>
+__global__ void __launch_bounds__(kPencilThreads, 2)
+    k_interp_pencil(const __grid_constant__ KGeom G, const float* __restrict__ in, float* __restrict__ out,
+                    const int32_t* __restrict__ units, const int32_t* __restrict__ cta_units, WS W) {
+  constexpr int NCO = 1 << KO, NCT = 1 << KT;
+  if (W.range[2] != 0) return;  // non-finite input: write nothing
+  extern __shared__ __align__(128) unsigned char smem[];
+  const PencilSmem P = pencil_smem(G, smem);
+  const int n = G.n_bins;
+  const int64_t gtr = G.gtr;
+  float* lutS = reinterpret_cast<float*>(P.tail);  // [NCO][gtr][n]
+  TileParam<float>* rngS =
+      reinterpret_cast<TileParam<float>*>(P.tail + ((NCO * gtr * n * 4 + 15) & ~15LL));
+  pipe_init(*P.pipe, G.nst);
+  __syncthreads();
+  const int u0 = cta_units[blockIdx.x], u1 = cta_units[blockIdx.x + 1];
+  if (threadIdx.x >= kConsumers) {
+    if (threadIdx.x == kConsumers) pipe_produce<KO, true>(G, in, units, u0, u1, *P.pipe, P.bufs);
+    return;
+  }
+  const TileParam<float>* tparams = reinterpret_cast<const TileParam<float>*>(W.tparams);
+  const TileParam<float> g0 = tparams[0];
+  const float nm05 = (float)n - 0.5f;
+  const int tid = threadIdx.x;
+  const int slot = tid / G.tpr;
+  const int64_t e0 = (int64_t)(tid % G.tpr) * 4;
+  const bool lane_on = slot < G.rpi;
+
+  // The plan only picks this kernel when a thread's 4 columns share their
+  // trailing cell (cell boundaries along the last dim are multiples of 4), so
+  // corner tiles are per thread and only the weights are per column.
+  int tt[NCT];
+  float tw[4][NCT];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    int64_t e = e0 + i;
+    int64_t c[KT];
+    float f1[KT];
+#pragma unroll
+    for (int q = KT - 1; q >= 0; --q) {
+      const int j = G.rank - KT + q;
+      const int64_t x = e % G.d[j].s;
+      e /= G.d[j].s;
+      c[q] = cell_of(G.d[j], x);
+      f1[q] = (float)twice_dlo(G.d[j], x, c[q]) / (float)(2 * G.d[j].b);
+    }
+#pragma unroll
+    for (int ct = 0; ct < NCT; ++ct) {
+      int64_t t = 0;
+      float w = 1.0f;
+#pragma unroll
+      for (int q = 0; q < KT; ++q) {
+        const int bit = (ct >> (KT - 1 - q)) & 1;
+        t += (c[q] + bit) * G.tstride[G.rank - KT + q];
+        w *= bit ? f1[q] : (1.0f - f1[q]);
+      }
+      if (i == 0) tt[ct] = (int)t;
+      tw[i][ct] = w;
+    }
+  }
+  float inv2b[KO];
+#pragma unroll
+  for (int j = 0; j < KO; ++j) inv2b[j] = 1.0f / (float)(2 * G.d[j].b);
+
+  const int64_t stage_elems = (int64_t)G.stage_rows * G.P;
+  int64_t cur = -1;
+  uint32_t it = 0;
+  while (true) {
+    const int s = it % G.nst;
+    mbar_wait(&P.pipe->full[s], (it / G.nst) & 1);
+    const Stage& S = P.pipe->st[s];
+    if (S.unit < 0) break;
+    const int64_t key = S.key;
+    if (key != cur) {
+      consumers_sync();
+      for (int co = 0; co < NCO; ++co) {
+        int64_t of = (S.cell[0] + ((co >> (KO - 1)) & 1) - G.trow0) * G.tstride[0];
+        for (int j = 1; j < KO; ++j) of += (S.cell[j] + ((co >> (KO - 1 - j)) & 1)) * G.tstride[j];
+        const float4* src = reinterpret_cast<const float4*>(W.lut + of * n);
+        float4* dst = reinterpret_cast<float4*>(lutS + co * gtr * n);
+        for (int64_t k = tid; k < gtr * n / 4; k += kConsumers) dst[k] = __ldg(src + k);
+        if (ADAPT)
+          for (int64_t t = tid; t < gtr; t += kConsumers) rngS[co * gtr + t] = tparams[of + t];
+      }
+      consumers_sync();
+      cur = key;
+    }
+    const int rows = S.nruns * S.nr;
+    const int nr = S.nr;
+    const float* buf = P.bufs + s * stage_elems;
+    if (lane_on) {
+      int cellv[KO];
+#pragma unroll
+      for (int j = 0; j < KO; ++j) cellv[j] = S.cell[j];
+      for (int q = slot; q < rows; q += G.rpi) {
+        const int run = q / nr;
+        const int rr = q - run * nr;
+        float fo[KO];
+#pragma unroll
+        for (int j = 0; j < KO; ++j) {
+          const int64_t xj = (j == KO - 1) ? S.a_last + S.r0 + rr : (int64_t)S.run_x[run][j];
+          fo[j] = (float)twice_dlo(G.d[j], xj, cellv[j]) * inv2b[j];
+        }
+        const float4 v4 = *reinterpret_cast<const float4*>(buf + q * G.P + e0);
+        const float v[4] = {v4.x, v4.y, v4.z, v4.w};
+        float acc[4] = {0.f, 0.f, 0.f, 0.f};
+        int bg[4];
+        if (!ADAPT) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) bg[i] = bin_of(v[i], g0, n, nm05);
+        }
+#pragma unroll
+        for (int co = 0; co < NCO; ++co) {
+          float wo = 1.0f;
+#pragma unroll
+          for (int j = 0; j < KO; ++j) wo *= ((co >> (KO - 1 - j)) & 1) ? fo[j] : (1.0f - fo[j]);
+#pragma unroll
+          for (int ct = 0; ct < NCT; ++ct) {
+            const float* L = lutS + (co * gtr + tt[ct]) * n;
+            if (ADAPT) {
+              const TileParam<float> tp = rngS[co * gtr + tt[ct]];
+#pragma unroll
+              for (int i = 0; i < 4; ++i)
+                acc[i] = fmaf(wo * tw[i][ct], L[bin_of(v[i], tp, n, nm05)], acc[i]);
+            } else {
+#pragma unroll
+              for (int i = 0; i < 4; ++i) acc[i] = fmaf(wo * tw[i][ct], L[bg[i]], acc[i]);
+            }
+          }
+        }
+        float4 r;
+        r.x = fminf(fmaxf(acc[0], 0.f), 1.f);
+        r.y = fminf(fmaxf(acc[1], 0.f), 1.f);
+        r.z = fminf(fmaxf(acc[2], 0.f), 1.f);
+        r.w = fminf(fmaxf(acc[3], 0.f), 1.f);
+        __stcs(reinterpret_cast<float4*>(out + S.run_off[run] + (int64_t)rr * G.P + e0), r);
+      }
+    }
+    __syncwarp();
+    if ((tid & 31) == 0) mbar_arrive(&P.pipe->empty[s]);
+    ++it;
+  }
+}
+
+// Host-side accessors (defined in the k_*.cu translation units).
+using PencilRangeFn = void (*)(const KGeom, const float*, const int32_t*, const int32_t*, WS);
+using PencilHistFn = void (*)(const KGeom, const float*, const int32_t*, const int32_t*, WS);
+using PencilInterpFn = void (*)(const KGeom, const float*, float*, const int32_t*, const int32_t*,
+                                WS);
+PencilRangeFn get_range_pencil(int ko);
+PencilHistFn get_hist_pencil(int ko, bool adaptive);
+PencilInterpFn get_interp_pencil(int ko, int kt, bool adaptive);
+
+}  // namespace mg

@@ -1,0 +1,853 @@
+// mclahe_gpu.cu -- host side of the C ABI (include/mclahe_gpu.h): request
+// validation, slab planning (tile windows, pencil units, CTA balancing),
+// pass launches and the one-shot drop-in.  Kernels live in kernels.cuh.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/mclahe_gpu.h"
+#include "k_misc.cuh"
+#include "k_pencil.cuh"
+
+namespace {
+
+using namespace mg;
+
+thread_local std::string g_last_error;
+std::atomic<int64_t> g_launches{0};
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(e == cudaErrorMemoryAllocation ? MCLAHE_ERR_OOM : MCLAHE_ERR_CUDA,
+              std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define MG_CUDA(call)                                 \
+  do {                                                \
+    cudaError_t e_ = (call);                          \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
+  } while (0)
+
+#define MG_LAUNCHED()                                         \
+  do {                                                        \
+    ++g_launches;                                             \
+    cudaError_t e_ = cudaGetLastError();                      \
+    if (e_ != cudaSuccess) return cuda_fail(e_, "kernel launch"); \
+  } while (0)
+
+int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+// validate_request (src/pipeline.cpp:19-34) minus the finiteness scan, which
+// runs on the device; plus the NdImage invariants (src/nd_image.cpp:52-58).
+int validate(const mclahe_params_t* p) {
+  if (!p) return fail(MCLAHE_ERR_VALIDATION, "null params");
+  if (p->rank < 1 || p->rank > MCLAHE_MAX_RANK)
+    return fail(MCLAHE_ERR_VALIDATION, "rank must be in [1, 8]");
+  for (int i = 0; i < p->rank; ++i)
+    if (p->shape[i] <= 0) return fail(MCLAHE_ERR_VALIDATION, "shape extents must be positive");
+  for (int i = 0; i < p->rank; ++i) {
+    if (p->kernel[i] <= 0 || p->kernel[i] > p->shape[i])
+      return fail(MCLAHE_ERR_VALIDATION,
+                  "kernel size must be in [1, extent] along dimension " + std::to_string(i));
+  }
+  if (!(p->clip_limit > 0.0) || !(p->clip_limit <= 1.0))
+    return fail(MCLAHE_ERR_VALIDATION, "clip_limit must be in (0, 1]");
+  if (p->n_bins < 2) return fail(MCLAHE_ERR_VALIDATION, "n_bins must be at least 2");
+  if (p->n_bins > 16384)
+    return fail(MCLAHE_ERR_UNSUPPORTED, "n_bins above 16384 is not supported on the GPU path");
+  if (p->dtype != MCLAHE_F32 && p->dtype != MCLAHE_F64)
+    return fail(MCLAHE_ERR_VALIDATION, "dtype must be MCLAHE_F32 or MCLAHE_F64");
+  int64_t tile = 1;
+  for (int i = 0; i < p->rank; ++i) tile *= p->kernel[i];
+  if (tile >= (int64_t{1} << 31))
+    return fail(MCLAHE_ERR_UNSUPPORTED, "kernel volume too large for 32-bit tile counts");
+  if (p->shape[0] >= (int64_t{1} << 31))
+    return fail(MCLAHE_ERR_UNSUPPORTED, "dim-0 extent must be below 2^31");
+  return MCLAHE_OK;
+}
+
+// Pencil configuration for one kernel family.
+struct Pencil {
+  bool on = false;
+  int kt = 0, ko = 0;
+  int64_t P = 0, gtr = 0;
+  int tpr = 0, rpi = 0;
+  int nst = 0, stage_rows = 0;
+  int64_t smem = 0;
+};
+
+constexpr int64_t kPipeBytes = (sizeof(mg::Pipe) + 127) & ~int64_t(127);
+constexpr int64_t kStageBytes = 8192;
+
+}  // namespace
+
+struct mclahe_plan_s {
+  mclahe_params_t p{};
+  mclahe_plan_info_t info{};
+  Dim d[kMaxRank];
+  KGeom G{};  // base geometry (kt/tpr/rpi/P/gtr filled per kernel)
+  Pencil hist, interp;
+  std::vector<int32_t> hist_units, interp_units;
+  std::vector<int64_t> hist_vox, interp_vox;  // voxels per unit (balancing)
+  // device state (lazy)
+  int device = -1;
+  int sms = 0;
+  int32_t* d_tables = nullptr;
+  int64_t off_hist_units = 0, off_hist_cta = 0, off_interp_units = 0, off_interp_cta = 0;
+  int hist_grid = 0, interp_grid = 0, range_grid = 0, map_grid = 0, map_block = 128;
+  int64_t map_smem = 0;
+  bool f32() const { return p.dtype == MCLAHE_F32; }
+};
+
+namespace {
+
+KGeom pencil_geom(const mclahe_plan_s& pl, const Pencil& pc) {
+  KGeom G = pl.G;
+  G.kt = pc.kt;
+  G.P = pc.P;
+  G.gtr = pc.gtr;
+  G.tpr = pc.tpr;
+  G.rpi = pc.rpi;
+  G.nst = pc.nst;
+  G.stage_rows = pc.stage_rows;
+  return G;
+}
+
+bool trailing_merged(const Dim& d) {
+  for (int64_t x = 0; x < d.before && x < d.s; ++x)
+    if ((d.before - 1 - x) / d.b != (x + d.before) / d.b) return false;
+  for (int64_t x = std::max<int64_t>(0, d.s - d.after); x < d.s; ++x)
+    if ((d.before + 2 * d.s - 1 - x) / d.b != (x + d.before) / d.b) return false;
+  return true;
+}
+
+// Chooses how many trailing dims one pencil covers for a kernel family.
+Pencil choose_pencil(const mclahe_plan_s& pl, bool for_hist) {
+  Pencil best;
+  const int D = pl.p.rank;
+  const int64_t n = pl.p.n_bins;
+  if (!pl.f32() || D < 2) return best;
+  std::vector<Pencil> ok;
+  for (int kt = 1; kt <= D - 1; ++kt) {
+    const int ko = D - kt;
+    if (ko > kMaxOuterDims) continue;
+    if (!for_hist && kt > 2) continue;
+    Pencil c;
+    c.kt = kt;
+    c.ko = ko;
+    c.P = 1;
+    c.gtr = 1;
+    bool merged = true;
+    for (int j = D - kt; j < D; ++j) {
+      c.P *= pl.d[j].s;
+      c.gtr *= pl.d[j].g;
+      merged = merged && trailing_merged(pl.d[j]);
+    }
+    if (c.P % 4 != 0) continue;
+    c.tpr = (int)std::min<int64_t>(c.P / 4, 1 << 20);
+    if (c.P / 4 > 256) continue;
+    c.rpi = 256 / c.tpr;
+    c.stage_rows = (int)std::max<int64_t>(1, kStageBytes / (c.P * 4));
+    const int64_t stage = c.stage_rows * c.P * 4;
+    int64_t tail;
+    if (for_hist) {
+      if (!merged) continue;
+      if (c.gtr * n >= (int64_t{1} << 31) / 2) continue;
+      tail = align_up(c.gtr * n * 4, 16) + c.gtr * 16;
+      if (tail > 64 * 1024) continue;
+      c.nst = 4;
+    } else {
+      if (ko > 4 || n % 4 != 0) continue;
+      // a thread's 4 columns must share their trailing cell
+      const Dim& dl = pl.d[D - 1];
+      if (dl.s % 4 != 0) continue;
+      bool shared = true;
+      for (int64_t c = 1; c <= dl.g - 2 && shared; ++c) {
+        int64_t ca, ce;
+        cell_range(dl, c, &ca, &ce);
+        shared = (ca % 4) == 0;
+      }
+      if (!shared) continue;
+      tail = align_up((int64_t{1} << ko) * c.gtr * n * 4, 16) + (int64_t{1} << ko) * c.gtr * 16;
+      // two CTAs per SM when the LUTs allow it, else one with a deeper pipeline
+      const int64_t two = 113 * 1024 - kPipeBytes - tail;
+      if (two >= 2 * stage) c.nst = (int)std::min<int64_t>(4, two / stage);
+      else if (224 * 1024 - kPipeBytes - tail >= 2 * stage)
+        c.nst = (int)std::min<int64_t>(kMaxStages, (224 * 1024 - kPipeBytes - tail) / stage);
+      else continue;
+    }
+    c.smem = kPipeBytes + c.nst * stage + tail;
+    c.on = true;
+    ok.push_back(c);
+  }
+  for (const Pencil& c : ok)
+    if (c.P >= 32) return c;
+  if (!ok.empty()) return ok.back();
+  return best;
+}
+
+void push_unit(std::vector<int32_t>& units, std::vector<int64_t>& vox, const int64_t* idx, int ko,
+               int64_t ra, int64_t re, int64_t vox_per_row, int64_t target) {
+  const int64_t rows = std::max<int64_t>(1, target / std::max<int64_t>(1, vox_per_row));
+  for (int64_t a = ra; a < re; a += rows) {
+    const int64_t e = std::min(re, a + rows);
+    int32_t rec[kUnitInts] = {0};
+    for (int j = 0; j < ko; ++j) rec[j] = (int32_t)idx[j];
+    rec[8] = (int32_t)a;
+    rec[9] = (int32_t)e;
+    units.insert(units.end(), rec, rec + kUnitInts);
+    vox.push_back((e - a) * vox_per_row);
+  }
+}
+
+void build_units(mclahe_plan_s& pl) {
+  const int D = pl.p.rank;
+  const int64_t local = pl.G.local_voxels;
+  const int64_t target = std::min<int64_t>(std::max<int64_t>(local / (148 * 16), 4096), 1 << 18);
+  if (pl.hist.on) {
+    const int ko = pl.hist.ko;
+    int64_t idx[kMaxRank] = {0};
+    idx[0] = pl.info.count_row_begin;
+    for (int j = 1; j < ko; ++j) idx[j] = 0;
+    while (true) {
+      int64_t per_row = pl.hist.P;
+      for (int j = 1; j < ko; ++j) {
+        const TileParts tp = tile_parts(pl.d[j], idx[j]);
+        per_row *= tp.support_end() - tp.support_begin();
+      }
+      const TileParts t0 = tile_parts(pl.d[0], idx[0]);
+      const int64_t ra = std::max(t0.support_begin(), pl.info.row_begin);
+      const int64_t re = std::min(t0.support_end(), pl.info.row_end);
+      if (re > ra) push_unit(pl.hist_units, pl.hist_vox, idx, ko, ra, re, per_row, target);
+      int j = ko - 1;
+      while (j >= 1 && ++idx[j] == pl.d[j].g) idx[j--] = 0;
+      if (j == 0 && ++idx[0] == pl.info.count_row_end) break;
+    }
+  }
+  if (pl.interp.on) {
+    const int ko = pl.interp.ko;
+    int64_t idx[kMaxRank] = {0};
+    const int64_t c0 = cell_of(pl.d[0], pl.info.row_begin);
+    const int64_t c1 = cell_of(pl.d[0], pl.info.row_end - 1) + 1;
+    idx[0] = c0;
+    while (true) {
+      int64_t per_row = pl.interp.P;
+      bool empty = false;
+      for (int j = 1; j < ko; ++j) {
+        int64_t a, e;
+        cell_range(pl.d[j], idx[j], &a, &e);
+        per_row *= e - a;
+        empty = empty || e <= a;
+      }
+      int64_t a0, e0;
+      cell_range(pl.d[0], idx[0], &a0, &e0);
+      const int64_t ra = std::max(a0, pl.info.row_begin), re = std::min(e0, pl.info.row_end);
+      if (!empty && re > ra) push_unit(pl.interp_units, pl.interp_vox, idx, ko, ra, re, per_row, target);
+      int j = ko - 1;
+      while (j >= 1 && ++idx[j] == pl.d[j].g - 1) idx[j--] = 0;
+      if (j == 0 && ++idx[0] == c1) break;
+    }
+  }
+  (void)D;
+}
+
+// Contiguous, voxel-balanced unit ranges per CTA.
+std::vector<int32_t> balance(const std::vector<int64_t>& vox, int grid) {
+  std::vector<int32_t> cta(grid + 1, 0);
+  int64_t total = 0;
+  for (int64_t v : vox) total += v;
+  int64_t acc = 0;
+  int c = 1;
+  for (size_t u = 0; u < vox.size() && c < grid; ++u) {
+    acc += vox[u];
+    while (c < grid && acc * grid >= total * c) cta[c++] = (int32_t)(u + 1);
+  }
+  while (c <= grid) cta[c++] = (int32_t)vox.size();
+  cta[grid] = (int32_t)vox.size();
+  return cta;
+}
+
+int plan_describe(const mclahe_params_t* params, int64_t row_begin, int64_t row_end,
+                  mclahe_plan_s* pl) {
+  int rc = validate(params);
+  if (rc) return rc;
+  if (row_begin < 0 || row_end > params->shape[0] || row_begin >= row_end)
+    return fail(MCLAHE_ERR_VALIDATION, "slab rows must satisfy 0 <= begin < end <= shape[0]");
+  pl->p = *params;
+  const int D = params->rank;
+  mclahe_plan_info_t& I = pl->info;
+  std::memset(&I, 0, sizeof I);
+  I.rank = D;
+  I.tiles = 1;
+  for (int j = 0; j < D; ++j) {
+    pl->d[j] = make_dim(params->shape[j], params->kernel[j]);
+    I.before[j] = pl->d[j].before;
+    I.after[j] = pl->d[j].after;
+    I.grid[j] = pl->d[j].g;
+    I.tiles *= pl->d[j].g;
+  }
+  I.row_begin = row_begin;
+  I.row_end = row_end;
+  I.n_bins = params->n_bins;
+  // tile rows whose support meets the slab
+  int64_t cb = INT64_MAX, ce = INT64_MIN;
+  for (int64_t t = 0; t < pl->d[0].g; ++t) {
+    const TileParts tp = tile_parts(pl->d[0], t);
+    if (tp.support_begin() < row_end && tp.support_end() > row_begin) {
+      cb = std::min(cb, t);
+      ce = std::max(ce, t + 1);
+    }
+  }
+  I.count_row_begin = cb;
+  I.count_row_end = ce;
+  I.need_row_begin = cell_of(pl->d[0], row_begin);
+  I.need_row_end = cell_of(pl->d[0], row_end - 1) + 2;
+  I.tile_row_begin = std::min(I.count_row_begin, I.need_row_begin);
+  I.tile_row_end = std::max(I.count_row_end, I.need_row_end);
+  I.tiles_per_row = I.tiles / pl->d[0].g;
+  const int64_t win_tiles = (I.tile_row_end - I.tile_row_begin) * I.tiles_per_row;
+  const int64_t n = params->n_bins;
+  const int64_t tp_size = pl->f32() ? sizeof(TileParam<float>) : sizeof(TileParam<double>);
+  I.off_range = 0;
+  I.off_tile_range = 256;
+  I.off_counts = align_up(I.off_tile_range + (params->adaptive ? win_tiles * 16 : 16), 256);
+  I.off_tparams = align_up(I.off_counts + win_tiles * n * 4, 256);
+  I.off_lut = align_up(I.off_tparams + (params->adaptive ? win_tiles : 1) * tp_size, 256);
+  I.workspace_bytes = align_up(I.off_lut + win_tiles * n * 4, 256);
+
+  KGeom& G = pl->G;
+  std::memset(&G, 0, sizeof G);
+  G.rank = D;
+  G.n_bins = (int)n;
+  G.adaptive = params->adaptive ? 1 : 0;
+  for (int j = 0; j < D; ++j) G.d[j] = pl->d[j];
+  G.vstride[D - 1] = 1;
+  G.tstride[D - 1] = 1;
+  for (int j = D - 1; j > 0; --j) {
+    G.vstride[j - 1] = G.vstride[j] * params->shape[j];
+    G.tstride[j - 1] = G.tstride[j] * pl->d[j].g;
+  }
+  G.row0 = row_begin;
+  G.trow0 = I.tile_row_begin;
+  G.win_tiles = win_tiles;
+  G.local_voxels = (row_end - row_begin) * G.vstride[0];
+  G.clip = params->clip_limit;
+
+  pl->hist = choose_pencil(*pl, true);
+  pl->interp = choose_pencil(*pl, false);
+  I.fast_hist = pl->hist.on;
+  I.fast_interp = pl->interp.on;
+  I.trailing_dims = pl->interp.on ? pl->interp.kt : pl->hist.kt;
+  build_units(*pl);
+  I.hist_units = (int64_t)pl->hist_vox.size();
+  I.interp_units = (int64_t)pl->interp_vox.size();
+  return MCLAHE_OK;
+}
+
+using RangeFn = PencilRangeFn;
+using HistFn = PencilHistFn;
+using InterpFn = PencilInterpFn;
+RangeFn range_fn(int ko) { return get_range_pencil(ko); }
+HistFn hist_fn(int ko, bool a) { return get_hist_pencil(ko, a); }
+InterpFn interp_fn(int ko, int kt, bool a) { return get_interp_pencil(ko, kt, a); }
+
+WS ws_view(const mclahe_plan_s* pl, void* ws) {
+  char* b = static_cast<char*>(ws);
+  WS W;
+  W.range = reinterpret_cast<int64_t*>(b + pl->info.off_range);
+  W.trange = reinterpret_cast<int64_t*>(b + pl->info.off_tile_range);
+  W.counts = reinterpret_cast<uint32_t*>(b + pl->info.off_counts);
+  W.tparams = b + pl->info.off_tparams;
+  W.lut = reinterpret_cast<float*>(b + pl->info.off_lut);
+  return W;
+}
+
+int64_t range_smem(const mclahe_plan_s* pl) {
+  return kPipeBytes + pl->hist.nst * pl->hist.stage_rows * pl->hist.P * 4 + pl->hist.gtr * 8;
+}
+
+int device_init(mclahe_plan_s* pl) {
+  int dev;
+  MG_CUDA(cudaGetDevice(&dev));
+  if (pl->device == dev) return MCLAHE_OK;
+  if (pl->device >= 0) return fail(MCLAHE_ERR_CUDA, "plan used on a different device");
+  MG_CUDA(cudaDeviceGetAttribute(&pl->sms, cudaDevAttrMultiProcessorCount, dev));
+  const bool A = pl->p.adaptive != 0;
+  std::vector<int32_t> hist_cta, interp_cta;
+  if (pl->hist.on) {
+    int occ = 0;
+    HistFn f = hist_fn(pl->hist.ko, A);
+    MG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl->hist.smem));
+    MG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f, kPencilThreads, pl->hist.smem));
+    if (A) {
+      RangeFn r = range_fn(pl->hist.ko);
+      MG_CUDA(cudaFuncSetAttribute(r, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)range_smem(pl)));
+    }
+    pl->hist_grid = (int)std::max<int64_t>(
+        1, std::min<int64_t>((int64_t)pl->hist_vox.size(), (int64_t)std::max(occ, 1) * pl->sms));
+    hist_cta = balance(pl->hist_vox, pl->hist_grid);
+  }
+  if (pl->interp.on) {
+    int occ = 0;
+    InterpFn f = interp_fn(pl->interp.ko, pl->interp.kt, A);
+    MG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl->interp.smem));
+    MG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f, kPencilThreads, pl->interp.smem));
+    pl->interp_grid = (int)std::max<int64_t>(
+        1, std::min<int64_t>((int64_t)pl->interp_vox.size(), (int64_t)std::max(occ, 1) * pl->sms));
+    interp_cta = balance(pl->interp_vox, pl->interp_grid);
+  }
+  const size_t total = pl->hist_units.size() + hist_cta.size() + pl->interp_units.size() +
+                       interp_cta.size() + 4;
+  MG_CUDA(cudaMalloc(&pl->d_tables, total * sizeof(int32_t)));
+  std::vector<int32_t> host;
+  host.reserve(total);
+  pl->off_hist_units = (int64_t)host.size();
+  host.insert(host.end(), pl->hist_units.begin(), pl->hist_units.end());
+  pl->off_hist_cta = (int64_t)host.size();
+  host.insert(host.end(), hist_cta.begin(), hist_cta.end());
+  pl->off_interp_units = (int64_t)host.size();
+  host.insert(host.end(), pl->interp_units.begin(), pl->interp_units.end());
+  pl->off_interp_cta = (int64_t)host.size();
+  host.insert(host.end(), interp_cta.begin(), interp_cta.end());
+  host.resize(total, 0);
+  MG_CUDA(cudaMemcpy(pl->d_tables, host.data(), total * sizeof(int32_t), cudaMemcpyHostToDevice));
+  pl->range_grid = pl->sms * 4;
+  // mappings: one warp per tile, f64 scratch of n_bins per warp
+  const int64_t n = pl->p.n_bins;
+  int warps = (int)std::max<int64_t>(1, std::min<int64_t>(4, (96 * 1024) / (n * 8)));
+  pl->map_block = warps * 32;
+  pl->map_smem = (int64_t)warps * n * 8;
+  if (pl->f32())
+    MG_CUDA(cudaFuncSetAttribute(k_mappings<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)pl->map_smem));
+  else
+    MG_CUDA(cudaFuncSetAttribute(k_mappings<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)pl->map_smem));
+  const int64_t tiles = pl->G.win_tiles;
+  pl->map_grid = (int)std::max<int64_t>(1, std::min<int64_t>((tiles + warps - 1) / warps, 1 << 20));
+  pl->device = dev;
+  return MCLAHE_OK;
+}
+
+int generic_grid(const mclahe_plan_s* pl) {
+  return (int)std::max<int64_t>(
+      1, std::min<int64_t>((pl->G.local_voxels + 255) / 256, (int64_t)pl->sms * 32));
+}
+
+int do_reset(mclahe_plan_s* pl, void* ws, cudaStream_t st) {
+  WS W = ws_view(pl, ws);
+  const int64_t ntr = pl->p.adaptive ? pl->G.win_tiles * 2 : 0;
+  MG_CUDA(cudaMemsetAsync(W.counts, 0, (size_t)pl->G.win_tiles * pl->p.n_bins * 4, st));
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((ntr + 255) / 256, 1024));
+  k_reset<<<grid, 256, 0, st>>>(W.range, W.trange, ntr);
+  MG_LAUNCHED();
+  return MCLAHE_OK;
+}
+
+int do_range(mclahe_plan_s* pl, const void* in, void* ws, cudaStream_t st) {
+  WS W = ws_view(pl, ws);
+  if (!pl->p.adaptive) {
+    if (pl->f32())
+      k_global_range<float><<<pl->range_grid, 256, 0, st>>>(static_cast<const float*>(in),
+                                                            pl->G.local_voxels, W.range);
+    else
+      k_global_range<double><<<pl->range_grid, 256, 0, st>>>(static_cast<const double*>(in),
+                                                             pl->G.local_voxels, W.range);
+    MG_LAUNCHED();
+    return MCLAHE_OK;
+  }
+  if (pl->hist.on) {
+    const KGeom G = pencil_geom(*pl, pl->hist);
+    RangeFn f = range_fn(pl->hist.ko);
+    f<<<pl->hist_grid, kPencilThreads, range_smem(pl), st>>>(G, static_cast<const float*>(in),
+                                                    pl->d_tables + pl->off_hist_units,
+                                                    pl->d_tables + pl->off_hist_cta, W);
+    MG_LAUNCHED();
+    return MCLAHE_OK;
+  }
+  const int grid = generic_grid(pl);
+  if (pl->f32())
+    k_tiles_generic<float, 0, true><<<grid, 256, 0, st>>>(pl->G, static_cast<const float*>(in), W);
+  else
+    k_tiles_generic<double, 0, true><<<grid, 256, 0, st>>>(pl->G, static_cast<const double*>(in), W);
+  MG_LAUNCHED();
+  return MCLAHE_OK;
+}
+
+int do_params(mclahe_plan_s* pl, void* ws, cudaStream_t st) {
+  WS W = ws_view(pl, ws);
+  const int64_t n = pl->p.adaptive ? pl->G.win_tiles : 1;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + 127) / 128, 4096));
+  if (pl->f32()) k_params<float><<<grid, 128, 0, st>>>(pl->G, W);
+  else k_params<double><<<grid, 128, 0, st>>>(pl->G, W);
+  MG_LAUNCHED();
+  return MCLAHE_OK;
+}
+
+int do_hist(mclahe_plan_s* pl, const void* in, void* ws, cudaStream_t st) {
+  WS W = ws_view(pl, ws);
+  const bool A = pl->p.adaptive != 0;
+  if (pl->hist.on) {
+    const KGeom G = pencil_geom(*pl, pl->hist);
+    HistFn f = hist_fn(pl->hist.ko, A);
+    f<<<pl->hist_grid, kPencilThreads, pl->hist.smem, st>>>(G, static_cast<const float*>(in),
+                                                 pl->d_tables + pl->off_hist_units,
+                                                 pl->d_tables + pl->off_hist_cta, W);
+    MG_LAUNCHED();
+    return MCLAHE_OK;
+  }
+  const int grid = generic_grid(pl);
+  if (pl->f32()) {
+    if (A) k_tiles_generic<float, 1, true><<<grid, 256, 0, st>>>(pl->G, static_cast<const float*>(in), W);
+    else k_tiles_generic<float, 1, false><<<grid, 256, 0, st>>>(pl->G, static_cast<const float*>(in), W);
+  } else {
+    if (A) k_tiles_generic<double, 1, true><<<grid, 256, 0, st>>>(pl->G, static_cast<const double*>(in), W);
+    else k_tiles_generic<double, 1, false><<<grid, 256, 0, st>>>(pl->G, static_cast<const double*>(in), W);
+  }
+  MG_LAUNCHED();
+  return MCLAHE_OK;
+}
+
+int do_map(mclahe_plan_s* pl, void* ws, const mclahe_debug_t* dbg, cudaStream_t st) {
+  WS W = ws_view(pl, ws);
+  Debug D{};
+  if (dbg) {
+    D.lo = dbg->lo;
+    D.hi = dbg->hi;
+    D.counts = dbg->counts;
+    D.clipped = dbg->clipped;
+    D.lut = dbg->lut;
+    D.degenerate = dbg->degenerate;
+    if ((D.lo == nullptr) != (D.hi == nullptr))
+      return fail(MCLAHE_ERR_VALIDATION, "debug lo and hi must both be set or both NULL");
+  }
+  if (pl->f32()) k_mappings<float><<<pl->map_grid, pl->map_block, pl->map_smem, st>>>(pl->G, W, D);
+  else k_mappings<double><<<pl->map_grid, pl->map_block, pl->map_smem, st>>>(pl->G, W, D);
+  MG_LAUNCHED();
+  return MCLAHE_OK;
+}
+
+int do_interp(mclahe_plan_s* pl, const void* in, void* out, void* ws, cudaStream_t st) {
+  WS W = ws_view(pl, ws);
+  const bool A = pl->p.adaptive != 0;
+  if (pl->interp.on) {
+    const KGeom G = pencil_geom(*pl, pl->interp);
+    InterpFn f = interp_fn(pl->interp.ko, pl->interp.kt, A);
+    f<<<pl->interp_grid, kPencilThreads, pl->interp.smem, st>>>(G, static_cast<const float*>(in),
+                                                     static_cast<float*>(out),
+                                                     pl->d_tables + pl->off_interp_units,
+                                                     pl->d_tables + pl->off_interp_cta, W);
+    MG_LAUNCHED();
+    return MCLAHE_OK;
+  }
+  const int grid = generic_grid(pl);
+  if (pl->f32()) {
+    if (A) k_interp_generic<float, true><<<grid, 256, 0, st>>>(pl->G, static_cast<const float*>(in), static_cast<float*>(out), W);
+    else k_interp_generic<float, false><<<grid, 256, 0, st>>>(pl->G, static_cast<const float*>(in), static_cast<float*>(out), W);
+  } else {
+    if (A) k_interp_generic<double, true><<<grid, 256, 0, st>>>(pl->G, static_cast<const double*>(in), static_cast<double*>(out), W);
+    else k_interp_generic<double, false><<<grid, 256, 0, st>>>(pl->G, static_cast<const double*>(in), static_cast<double*>(out), W);
+  }
+  MG_LAUNCHED();
+  return MCLAHE_OK;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+int check_ptrs(const mclahe_plan_s* pl, const void* in, const void* out) {
+  if (!in) return fail(MCLAHE_ERR_VALIDATION, "null input buffer");
+  if ((pl->hist.on || pl->interp.on) && (!aligned16(in) || (out && !aligned16(out))))
+    return fail(MCLAHE_ERR_VALIDATION, "device buffers must be 16-byte aligned");
+  return MCLAHE_OK;
+}
+
+// ---- one-shot context: cached plan + buffers ----
+struct OneShot {
+  std::mutex mu;
+  std::map<std::string, std::unique_ptr<mclahe_plan_s>> plans;
+  void* buf = nullptr;
+  size_t buf_bytes = 0;
+  int buf_dev = -1;
+  cudaStream_t stream = nullptr;
+  int stream_dev = -1;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+};
+OneShot& oneshot() {
+  static OneShot* o = new OneShot();  // intentionally leaked (process lifetime)
+  return *o;
+}
+
+std::string plan_key(const mclahe_params_t* p, int dev) {
+  std::string k(reinterpret_cast<const char*>(p), sizeof *p);
+  k.append(reinterpret_cast<const char*>(&dev), sizeof dev);
+  return k;
+}
+
+mclahe_plan_s* cached_plan(OneShot& o, const mclahe_params_t* p, int* rc) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) {
+    *rc = cuda_fail(e, "cudaGetDevice");
+    return nullptr;
+  }
+  mclahe_params_t q = *p;
+  q.reserved = 0;
+  for (int i = q.rank; i < MCLAHE_MAX_RANK; ++i) q.shape[i] = q.kernel[i] = 0;
+  const std::string key = plan_key(&q, dev);
+  auto it = o.plans.find(key);
+  if (it != o.plans.end()) return it->second.get();
+  auto pl = std::make_unique<mclahe_plan_s>();
+  *rc = plan_describe(&q, 0, q.shape[0], pl.get());
+  if (*rc) return nullptr;
+  *rc = device_init(pl.get());
+  if (*rc) return nullptr;
+  if (o.plans.size() > 32) o.plans.clear();
+  mclahe_plan_s* raw = pl.get();
+  o.plans[key] = std::move(pl);
+  return raw;
+}
+
+int ensure_buf(OneShot& o, size_t bytes) {
+  int dev;
+  MG_CUDA(cudaGetDevice(&dev));
+  if (o.buf && o.buf_bytes >= bytes && o.buf_dev == dev) return MCLAHE_OK;
+  if (o.buf) {
+    cudaFree(o.buf);
+    o.buf = nullptr;
+  }
+  MG_CUDA(cudaMalloc(&o.buf, bytes));
+  o.buf_bytes = bytes;
+  o.buf_dev = dev;
+  return MCLAHE_OK;
+}
+
+int ensure_stream(OneShot& o) {
+  int dev;
+  MG_CUDA(cudaGetDevice(&dev));
+  if (o.stream && o.stream_dev == dev) return MCLAHE_OK;
+  MG_CUDA(cudaStreamCreateWithFlags(&o.stream, cudaStreamNonBlocking));
+  for (auto& e : o.ev) MG_CUDA(cudaEventCreate(&e));
+  o.stream_dev = dev;
+  return MCLAHE_OK;
+}
+
+int enqueue_all(mclahe_plan_s* pl, const void* in, void* out, void* ws, cudaStream_t st,
+                cudaEvent_t* ev) {
+  int rc;
+  if (ev) MG_CUDA(cudaEventRecord(ev[0], st));
+  if ((rc = do_reset(pl, ws, st))) return rc;
+  if ((rc = do_range(pl, in, ws, st))) return rc;
+  if ((rc = do_params(pl, ws, st))) return rc;
+  if ((rc = do_hist(pl, in, ws, st))) return rc;
+  if ((rc = do_map(pl, ws, nullptr, st))) return rc;
+  if (ev) MG_CUDA(cudaEventRecord(ev[1], st));
+  if ((rc = do_interp(pl, in, out, ws, st))) return rc;
+  if (ev) MG_CUDA(cudaEventRecord(ev[2], st));
+  return MCLAHE_OK;
+}
+
+int read_status(const mclahe_plan_s* pl, const void* ws, cudaStream_t st) {
+  int64_t flag = 0;
+  MG_CUDA(cudaMemcpyAsync(&flag, static_cast<const char*>(ws) + pl->info.off_range + 16,
+                          sizeof flag, cudaMemcpyDeviceToHost, st));
+  MG_CUDA(cudaStreamSynchronize(st));
+  if (flag) return fail(MCLAHE_ERR_VALIDATION, "image contains non-finite values");
+  return MCLAHE_OK;
+}
+
+int64_t elem_size(const mclahe_params_t* p) { return p->dtype == MCLAHE_F64 ? 8 : 4; }
+
+int64_t volume(const mclahe_params_t* p) {
+  int64_t n = 1;
+  for (int i = 0; i < p->rank; ++i) n *= p->shape[i];
+  return n;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* mclahe_last_error(void) { return g_last_error.c_str(); }
+const char* mclahe_version(void) { return "mclahe-b200 0.1 (sm_100a)"; }
+int64_t mclahe_launch_count(void) { return g_launches.load(); }
+
+int mclahe_plan_create(const mclahe_params_t* params, int64_t row_begin, int64_t row_end,
+                       mclahe_plan_t* plan) {
+  if (!plan) return fail(MCLAHE_ERR_VALIDATION, "null plan pointer");
+  *plan = nullptr;
+  try {
+    auto pl = std::make_unique<mclahe_plan_s>();
+    const int rc = plan_describe(params, row_begin, row_end, pl.get());
+    if (rc) return rc;
+    *plan = pl.release();
+    return MCLAHE_OK;
+  } catch (const std::bad_alloc&) {
+    return fail(MCLAHE_ERR_OOM, "host allocation failed");
+  }
+}
+
+int mclahe_plan_destroy(mclahe_plan_t plan) {
+  if (!plan) return MCLAHE_OK;
+  if (plan->d_tables) cudaFree(plan->d_tables);
+  delete plan;
+  return MCLAHE_OK;
+}
+
+int mclahe_plan_get_info(mclahe_plan_t plan, mclahe_plan_info_t* info) {
+  if (!plan || !info) return fail(MCLAHE_ERR_VALIDATION, "null plan or info");
+  *info = plan->info;
+  return MCLAHE_OK;
+}
+
+#define MG_PLAN_INIT(pl)                       \
+  do {                                         \
+    if (!(pl)) return fail(MCLAHE_ERR_VALIDATION, "null plan"); \
+    int rc_ = device_init(pl);                 \
+    if (rc_) return rc_;                       \
+  } while (0)
+
+int mclahe_pass_reset(mclahe_plan_t plan, void* ws, void* stream) {
+  MG_PLAN_INIT(plan);
+  return do_reset(plan, ws, static_cast<cudaStream_t>(stream));
+}
+
+int mclahe_pass_range(mclahe_plan_t plan, const void* in, void* ws, void* stream) {
+  MG_PLAN_INIT(plan);
+  int rc = check_ptrs(plan, in, nullptr);
+  if (rc) return rc;
+  return do_range(plan, in, ws, static_cast<cudaStream_t>(stream));
+}
+
+int mclahe_pass_params(mclahe_plan_t plan, void* ws, void* stream) {
+  MG_PLAN_INIT(plan);
+  return do_params(plan, ws, static_cast<cudaStream_t>(stream));
+}
+
+int mclahe_pass_histograms(mclahe_plan_t plan, const void* in, void* ws, void* stream) {
+  MG_PLAN_INIT(plan);
+  int rc = check_ptrs(plan, in, nullptr);
+  if (rc) return rc;
+  return do_hist(plan, in, ws, static_cast<cudaStream_t>(stream));
+}
+
+int mclahe_pass_mappings(mclahe_plan_t plan, void* ws, const mclahe_debug_t* debug, void* stream) {
+  MG_PLAN_INIT(plan);
+  return do_map(plan, ws, debug, static_cast<cudaStream_t>(stream));
+}
+
+int mclahe_pass_interpolate(mclahe_plan_t plan, const void* in, void* out, void* ws, void* stream) {
+  MG_PLAN_INIT(plan);
+  int rc = check_ptrs(plan, in, out);
+  if (rc) return rc;
+  if (!out) return fail(MCLAHE_ERR_VALIDATION, "null output buffer");
+  return do_interp(plan, in, out, ws, static_cast<cudaStream_t>(stream));
+}
+
+int mclahe_plan_enqueue(mclahe_plan_t plan, const void* in, void* out, void* ws, void* stream) {
+  MG_PLAN_INIT(plan);
+  if (plan->info.row_begin != 0 || plan->info.row_end != plan->p.shape[0])
+    return fail(MCLAHE_ERR_VALIDATION, "mclahe_plan_enqueue needs a whole-volume plan");
+  int rc = check_ptrs(plan, in, out);
+  if (rc) return rc;
+  if (!out) return fail(MCLAHE_ERR_VALIDATION, "null output buffer");
+  return enqueue_all(plan, in, out, ws, static_cast<cudaStream_t>(stream), nullptr);
+}
+
+int mclahe_plan_check(mclahe_plan_t plan, const void* ws, void* stream) {
+  if (!plan) return fail(MCLAHE_ERR_VALIDATION, "null plan");
+  return read_status(plan, ws, static_cast<cudaStream_t>(stream));
+}
+
+int mclahe_gpu_run_device(const mclahe_params_t* params, const void* in, void* out, void* stream,
+                          mclahe_timings_t* timings) {
+  int rc = validate(params);
+  if (rc) return rc;
+  OneShot& o = oneshot();
+  std::lock_guard<std::mutex> lock(o.mu);
+  mclahe_plan_s* pl = cached_plan(o, params, &rc);
+  if (!pl) return rc;
+  if ((rc = check_ptrs(pl, in, out))) return rc;
+  if ((rc = ensure_buf(o, (size_t)pl->info.workspace_bytes))) return rc;
+  if ((rc = ensure_stream(o))) return rc;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if ((rc = enqueue_all(pl, in, out, o.buf, st, timings ? o.ev : nullptr))) return rc;
+  if ((rc = read_status(pl, o.buf, st))) return rc;
+  if (timings) {
+    float a = 0, b = 0;
+    MG_CUDA(cudaEventElapsedTime(&a, o.ev[0], o.ev[1]));
+    MG_CUDA(cudaEventElapsedTime(&b, o.ev[1], o.ev[2]));
+    timings->histograms_s += a * 1e-3;
+    timings->interpolation_s += b * 1e-3;
+  }
+  return MCLAHE_OK;
+}
+
+int mclahe_gpu_run(const mclahe_params_t* params, const void* in, void* out,
+                   mclahe_timings_t* timings) {
+  int rc = validate(params);
+  if (rc) return rc;
+  if (!in || !out) return fail(MCLAHE_ERR_VALIDATION, "null host buffer");
+  OneShot& o = oneshot();
+  std::lock_guard<std::mutex> lock(o.mu);
+  mclahe_plan_s* pl = cached_plan(o, params, &rc);
+  if (!pl) return rc;
+  const size_t bytes = (size_t)(volume(params) * elem_size(params));
+  const size_t io = (size_t)align_up((int64_t)bytes, 256);
+  if ((rc = ensure_buf(o, 2 * io + (size_t)pl->info.workspace_bytes))) return rc;
+  if ((rc = ensure_stream(o))) return rc;
+  char* base = static_cast<char*>(o.buf);
+  void* d_in = base;
+  void* d_out = base + io;
+  void* ws = base + 2 * io;
+  cudaStream_t st = o.stream;
+  MG_CUDA(cudaMemcpyAsync(d_in, in, bytes, cudaMemcpyHostToDevice, st));
+  if ((rc = enqueue_all(pl, d_in, d_out, ws, st, timings ? o.ev : nullptr))) return rc;
+  int64_t flag = 0;
+  MG_CUDA(cudaMemcpyAsync(&flag, static_cast<char*>(ws) + pl->info.off_range + 16, sizeof flag,
+                          cudaMemcpyDeviceToHost, st));
+  MG_CUDA(cudaStreamSynchronize(st));
+  if (flag) return fail(MCLAHE_ERR_VALIDATION, "image contains non-finite values");
+  MG_CUDA(cudaMemcpyAsync(out, d_out, bytes, cudaMemcpyDeviceToHost, st));
+  MG_CUDA(cudaStreamSynchronize(st));
+  if (timings) {
+    float a = 0, b = 0;
+    MG_CUDA(cudaEventElapsedTime(&a, o.ev[0], o.ev[1]));
+    MG_CUDA(cudaEventElapsedTime(&b, o.ev[1], o.ev[2]));
+    timings->histograms_s += a * 1e-3;
+    timings->interpolation_s += b * 1e-3;
+  }
+  return MCLAHE_OK;
+}
+
+int mclahe_debug_bin_index(int32_t dtype, const void* values, int64_t n, double lo, double hi,
+                           int64_t n_bins, int32_t* out, void* stream) {
+  if (n_bins < 2 || n_bins > 16384) return fail(MCLAHE_ERR_VALIDATION, "n_bins out of range");
+  if (n <= 0) return MCLAHE_OK;
+  const int grid = (int)std::min<int64_t>((n + 255) / 256, 4096);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (dtype == MCLAHE_F32)
+    k_debug_bins<float><<<grid, 256, 0, st>>>(static_cast<const float*>(values), n, lo, hi,
+                                              (int)n_bins, out);
+  else
+    k_debug_bins<double><<<grid, 256, 0, st>>>(static_cast<const double*>(values), n, lo, hi,
+                                               (int)n_bins, out);
+  MG_LAUNCHED();
+  return MCLAHE_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,293 @@
+"""GPU parity: the sm_100a path against the oracle (oracle/) and the golden
+fixtures the reference generated (tests/golden).
+
+Bars (BASELINE.json north_star): bin indices, raw counts and clipped
+histograms bit-exact; the f64 CDF/LUT is also bit-exact here (sequential f64
+sums in bin order); the float32 output within 1e-5 absolute of the reference
+float64 output (OUT_TOL).  Full-size configs are checked through
+size-independent properties plus exact spot checks of sampled tiles/voxels.
+"""
+import glob
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import oracle as O  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+OUT_TOL = 1e-5
+GOLDEN = sorted(glob.glob(os.path.join(os.path.dirname(__file__), "golden", "*.npz")))
+
+
+@pytest.fixture(scope="module")
+def M():
+    import paper_1906_11355_b200 as M
+    from paper_1906_11355_b200 import _native
+    _native.lib()  # fails loudly if the CUDA library is missing
+    return M
+
+
+def gpu_stats(M, x, kernel, nb, clip, ad):
+    xt = torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    code = 1 if xt.dtype == torch.float64 else 0
+    plan = M.Plan(x.shape, kernel, nb, clip, ad, code)
+    st = plan.tile_stats(xt)
+    return st, plan
+
+
+def assert_stats_equal(st, ref, ctx=""):
+    assert np.array_equal(st["degenerate"], ref["degenerate"]), ctx
+    assert np.array_equal(st["lo"], ref["lo"]), ctx
+    assert np.array_equal(st["hi"], ref["hi"]), ctx
+    assert np.array_equal(st["counts"].astype(np.float64), ref["counts"]), ctx + " counts"
+    assert np.array_equal(st["clipped"], ref["clipped"]), ctx + " clipped"
+    assert np.array_equal(st["lut"], ref["lut"]), ctx + " lut"
+
+
+@pytest.mark.parametrize("path", GOLDEN, ids=[os.path.basename(p) for p in GOLDEN])
+def test_golden(M, path):
+    g = np.load(path)
+    kernel = tuple(int(k) for k in g["kernel"])
+    nb, clip, ad = int(g["n_bins"]), float(g["clip_limit"]), bool(g["adaptive"])
+    st, _ = gpu_stats(M, g["x"], kernel, nb, clip, ad)
+    assert_stats_equal(st, {k: g[k] for k in ("lo", "hi", "counts", "clipped", "lut",
+                                               "degenerate")}, os.path.basename(path))
+    out = M.enhance(g["x"], kernel, nb, clip, ad)
+    assert out.dtype == np.float32
+    assert np.max(np.abs(out.astype(np.float64) - g["out"])) <= OUT_TOL
+
+
+def random_case(seed):
+    rng = np.random.default_rng(1000 + seed)
+    rank = 1 + seed % 5
+    hi = {1: 300, 2: 70, 3: 24, 4: 12, 5: 8}[rank]
+    shape = tuple(int(v) for v in rng.integers(2, hi, rank))
+    kernel = tuple(int(rng.integers(1, s + 1)) for s in shape)
+    nb = int(rng.choice([2, 3, 16, 64, 256]))
+    clip = float(rng.choice([0.005, 0.05, 0.3, 1.0]))
+    ad = bool(rng.integers(0, 2))
+    kind = seed % 4
+    if kind == 0:
+        x = rng.random(shape)
+    elif kind == 1:
+        x = np.round(rng.random(shape) * 9) / 9          # values on bin edges
+    elif kind == 2:
+        x = rng.poisson(2.0, shape) / 7.0                # quantised, many zeros
+    else:
+        x = rng.normal(0, 3, shape)                      # signed
+    return x.astype(np.float32), kernel, nb, clip, ad
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_random_shapes_vs_oracle(M, seed):
+    x, kernel, nb, clip, ad = random_case(seed)
+    st, _ = gpu_stats(M, x, kernel, nb, clip, ad)
+    ref = O.tile_stats(x, kernel, nb, clip, ad, "c")
+    assert_stats_equal(st, ref, f"seed {seed} {x.shape} {kernel} nb={nb} ad={ad}")
+    out = M.enhance(x, kernel, nb, clip, ad)
+    want = O.mclahe(x, kernel, nb, clip, ad, "c")
+    assert np.max(np.abs(out.astype(np.float64) - want)) <= OUT_TOL
+
+
+# the five BASELINE configs at oracle-sized scale (same structure, every extent / 4)
+SCALED = {
+    "2d": dict(shape=(256, 256), kernel=(16, 16), n_bins=256, clip_limit=0.01, adaptive=False),
+    "3d": dict(shape=(64, 64, 64), kernel=(8, 8, 8), n_bins=256, clip_limit=0.02, adaptive=False),
+    "4d": dict(shape=(64, 64, 32, 32), kernel=(8, 8, 4, 4), n_bins=256, clip_limit=0.02,
+               adaptive=True),
+    "l4d": dict(shape=(64, 64, 32, 32), kernel=(8, 8, 4, 8), n_bins=512, clip_limit=0.01,
+                adaptive=False),
+    "5d": dict(shape=(32, 32, 16, 16, 16), kernel=(4, 4, 2, 4, 4), n_bins=128, clip_limit=0.03,
+               adaptive=True),
+}
+
+
+@pytest.mark.parametrize("name", list(SCALED))
+def test_scaled_configs_vs_oracle(M, name):
+    from paper_1906_11355_b200 import datasets
+    c = SCALED[name]
+    x = datasets.make(name, seed=1, shape=c["shape"]).numpy()
+    args = (c["kernel"], c["n_bins"], c["clip_limit"], c["adaptive"])
+    st, plan = gpu_stats(M, x, *args)
+    assert plan.info.fast_hist and plan.info.fast_interp, "pencil kernels expected"
+    assert_stats_equal(st, O.tile_stats(x, *args, "c"), name)
+    out = M.enhance(x, *args)
+    want = O.mclahe(x, *args, "c")
+    assert np.max(np.abs(out.astype(np.float64) - want)) <= OUT_TOL
+
+
+def test_bin_index_adversarial(M):
+    # values exactly on and one ulp around every bin edge of quantised data
+    vals = []
+    for m in (7, 12, 200, 500, 255, 1000):
+        k = np.arange(0, m + 1, dtype=np.float64) / m
+        vals.append(k)
+    base = np.concatenate(vals).astype(np.float32)
+    up = np.nextafter(base, np.float32(2))
+    dn = np.nextafter(base, np.float32(-1))
+    rng = np.random.default_rng(5)
+    v = np.concatenate([base, up, dn, rng.random(200000).astype(np.float32),
+                        np.array([-1e30, 1e30, 0.0, -0.0], np.float32)])
+    vt = torch.from_numpy(v).cuda()
+    for lo, hi, n in [(0.0, 1.0, 256), (0.0, 1.0, 512), (0.02, 0.98, 128), (1 / 7, 6 / 7, 256),
+                      (0.0, 3.0 / 500, 256), (-2.5, 1.0, 7), (0.3, 0.30000003, 64)]:
+        lo32, hi32 = float(np.float32(lo)), float(np.float32(hi))
+        got = M.bin_index_device(vt, lo32, hi32, n).cpu().numpy()
+        want = O.bin_index_array(v.astype(np.float64), lo32, hi32, n)
+        assert np.array_equal(got, want), (lo, hi, n, np.flatnonzero(got != want)[:5])
+    # f64 values that are not float32-representable
+    v64 = np.concatenate([np.arange(0, 3001) / 3000.0, rng.random(100000)])
+    got = M.bin_index_device(torch.from_numpy(v64).cuda(), 0.0, 1.0, 256).cpu().numpy()
+    assert np.array_equal(got, O.bin_index_array(v64, 0.0, 1.0, 256))
+
+
+def test_float64_input(M):
+    rng = np.random.default_rng(11)
+    x = np.round(rng.random((40, 36, 12)) * 1000) / 1000  # f64 values off the f32 grid
+    args = ((8, 6, 4), 64, 0.05, True)
+    st, _ = gpu_stats(M, x, *args)
+    assert_stats_equal(st, O.tile_stats(x, *args, "c"), "f64")
+    out = M.enhance(x, *args)
+    assert out.dtype == np.float64
+    assert np.max(np.abs(out - O.mclahe(x, *args, "c"))) <= OUT_TOL
+
+
+@pytest.mark.parametrize("bad", [np.nan, np.inf, -np.inf])
+@pytest.mark.parametrize("adaptive", [False, True])
+def test_nonfinite_rejected(M, bad, adaptive):
+    x = np.random.default_rng(0).random((32, 32)).astype(np.float32)
+    x[5, 7] = bad
+    with pytest.raises(M.ValidationError, match="non-finite"):
+        M.enhance(x, (8, 8), 16, 0.1, adaptive)
+    xt = torch.from_numpy(x).cuda()
+    with pytest.raises(M.ValidationError, match="non-finite"):
+        M.mclahe(M.McLaheRequest(xt, M.KernelSpec((8, 8)), M.EnhanceParams(0.1, 16)))
+
+
+def test_constant_image(M):
+    for ad in (False, True):
+        out = M.enhance(np.full((40, 30, 8), 0.25, np.float32), (8, 8, 4), 32, 0.1, ad)
+        assert np.all(out == 0.5)
+
+
+def test_determinism_and_device_api(M):
+    from paper_1906_11355_b200 import datasets
+    c = SCALED["4d"]
+    x = datasets.make("4d", seed=2, shape=c["shape"]).cuda()
+    req = M.McLaheRequest(x, M.KernelSpec(c["kernel"]),
+                          M.EnhanceParams(c["clip_limit"], c["n_bins"], M.RangeMode.Adaptive))
+    a = M.mclahe(req)
+    b = M.mclahe(req)
+    assert torch.equal(a, b)
+    host = M.mclahe(M.McLaheRequest(x.cpu().numpy(), req.kernel, req.params))
+    assert np.array_equal(a.cpu().numpy(), host)
+
+
+@pytest.mark.parametrize("name,slabs", [("2d", 2), ("3d", 3), ("4d", 4), ("l4d", 2), ("5d", 4),
+                                        ("4d", 8)])
+def test_fake_slabs_bit_identical(M, name, slabs):
+    """The multi-GPU slab path (windows, partial counts, neighbour combine)
+    emulated on one device must reproduce the single-GPU output bit for bit."""
+    from paper_1906_11355_b200 import datasets, slabs as S
+    c = SCALED[name]
+    x = datasets.make(name, seed=3, shape=c["shape"]).cuda()
+    args = (c["kernel"], c["n_bins"], c["clip_limit"], c["adaptive"])
+    whole = M.enhance(x, *args)
+    parts = S.run_local(x, *args, slabs=slabs)
+    assert torch.equal(whole, parts)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_fake_slabs_ragged(M, seed):
+    from paper_1906_11355_b200 import slabs as S
+    rng = np.random.default_rng(77 + seed)
+    shape = (int(rng.integers(20, 60)), int(rng.integers(5, 30)), int(rng.integers(4, 12)))
+    kernel = (int(rng.integers(2, 9)), int(rng.integers(1, shape[1] + 1)),
+              int(rng.integers(1, shape[2] + 1)))
+    x = torch.from_numpy(rng.random(shape).astype(np.float32)).cuda()
+    ncell = len(S.cell_ranges(shape[0], kernel[0]))
+    for g in sorted({2, min(3, ncell), ncell}):
+        if g < 2:
+            continue
+        whole = M.enhance(x, kernel, 32, 0.1, bool(seed % 2))
+        assert torch.equal(whole, S.run_local(x, kernel, 32, 0.1, bool(seed % 2), slabs=g))
+
+
+FULL = ["2d", "3d", "4d", "5d", "l4d"]
+
+
+@pytest.mark.parametrize("name", FULL)
+def test_full_size_properties(M, name):
+    """BASELINE sizes: tile mass = prod(kernel) for every binned tile, LUTs
+    monotone ending at 1, output in [0, 1], run-to-run bit-identical, and
+    exact spot checks of sampled tiles (counts by numpy from the padded
+    block) and voxels (f64 blend from the GPU's f64 LUTs)."""
+    from paper_1906_11355_b200 import datasets
+    c = datasets.CONFIGS[name]
+    x = datasets.make(name, seed=0, device="cuda")
+    plan = M.Plan(x.shape, c["kernel"], c["n_bins"], c["clip_limit"], c["adaptive"])
+    assert plan.info.fast_hist and plan.info.fast_interp
+    st = plan.tile_stats(x)
+    nb = c["n_bins"]
+    binned = ~((st["lo"] >= st["hi"]))
+    tile_len = int(np.prod(c["kernel"]))
+    assert np.all(st["counts"][binned].sum(1) == tile_len)
+    lut = st["lut"][~st["degenerate"]]
+    assert np.all(np.diff(lut, axis=1) >= 0) and np.all(lut[:, -1] == 1.0)
+    ws = plan.new_workspace()
+    out = torch.empty_like(x)
+    plan.enqueue(x, out, ws)
+    plan.check(ws)
+    out2 = torch.empty_like(x)
+    plan.enqueue(x, out2, ws)
+    plan.check(ws)
+    assert torch.equal(out, out2)
+    assert float(out.min()) >= 0.0 and float(out.max()) <= 1.0
+    # spot check: padded tiles rebuilt on the host from the data
+    rng = np.random.default_rng(9)
+    grid = np.array(st_grid(plan))
+    before = np.array(plan.info.before[:x.dim()])
+    D = x.dim()
+    for t in rng.choice(len(st["lo"]), 24, replace=False):
+        tc = np.unravel_index(t, grid)
+        idx = []
+        for d in range(D):
+            o = np.arange(tc[d] * c["kernel"][d], (tc[d] + 1) * c["kernel"][d]) - before[d]
+            s = x.shape[d]
+            m = np.mod(o, 2 * s)
+            m = np.where(m >= s, 2 * s - 1 - m, m)
+            idx.append(torch.from_numpy(m).cuda())
+        blk = x.index_select(0, idx[0])
+        for d in range(1, D):
+            blk = blk.index_select(d, idx[d])
+        blk = blk.double().cpu().numpy().ravel()
+        lo, hi = (st["lo"][t], st["hi"][t])
+        if not lo < hi:
+            continue
+        cnt = np.bincount(O.bin_index_array(blk, lo, hi, nb), minlength=nb)
+        assert np.array_equal(cnt, st["counts"][t]), f"tile {t}"
+    # spot check voxels: f64 blend with the GPU's f64 LUTs
+    flat = rng.choice(x.numel(), 4000, replace=False)
+    xs = x.view(-1)[torch.from_numpy(flat).cuda()].double().cpu().numpy()
+    got = out.view(-1)[torch.from_numpy(flat).cuda()].double().cpu().numpy()
+    gstride = np.cumprod((list(grid[1:]) + [1])[::-1])[::-1]
+    shape = np.array(x.shape)
+    for f, v, y in zip(flat, xs, got):
+        coord = np.array(np.unravel_index(f, shape))
+        lower, dlo, dhi, coeff = O.neighbors(coord + before, c["kernel"], grid, "c")
+        mapped = []
+        for cidx in range(1 << D):
+            bits = [(cidx >> (D - 1 - j)) & 1 for j in range(D)]
+            t = int(sum((lower[j] + bits[j]) * gstride[j] for j in range(D)))
+            if st["degenerate"][t]:
+                mapped.append(0.5)
+            else:
+                mapped.append(st["lut"][t][O.bin_index(float(v), st["lo"][t], st["hi"][t], nb)])
+        assert abs(O.blend(coeff, mapped) - y) <= OUT_TOL
+
+
+def st_grid(plan):
+    return [int(plan.info.grid[j]) for j in range(plan.info.rank)]
