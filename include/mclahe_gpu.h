@@ -87,6 +87,7 @@ typedef struct {
   int64_t off_counts;     /* int32[window tiles][n_bins]                 (SUM-reducible) */
   int64_t off_tparams;    /* per-tile binning parameters */
   int64_t off_lut;        /* float32[window tiles][n_bins] */
+  int64_t off_thr;        /* float32[adaptive ? window tiles : 1][n_bins] bin-edge tables */
   int64_t workspace_bytes;
   int64_t hist_units, interp_units;
 } mclahe_plan_info_t;

@@ -57,7 +57,7 @@ class PlanInfo(C.Structure):
                 ("tiles_per_row", C.c_int64), ("n_bins", C.c_int64),
                 ("off_range", C.c_int64), ("off_tile_range", C.c_int64),
                 ("off_counts", C.c_int64), ("off_tparams", C.c_int64), ("off_lut", C.c_int64),
-                ("workspace_bytes", C.c_int64), ("hist_units", C.c_int64),
+                ("off_thr", C.c_int64), ("workspace_bytes", C.c_int64), ("hist_units", C.c_int64),
                 ("interp_units", C.c_int64)]
 
 

@@ -96,24 +96,63 @@ __device__ __forceinline__ int bin_exact(double v, double lo, double hi, int n) 
   return static_cast<int>(scaled);
 }
 
-// nm05 = n - 0.5 (exact in f32 for n < 2^23).
-__device__ __forceinline__ int bin_of(float v, const TileParam<float>& tp, int n, float nm05) {
+// nm05 = n - 0.5 (exact in f32 for n < 2^23).  thr = the tile's bin-edge
+// table: thr[k] = smallest float whose reference bin is >= k (k in [1, n-1]).
+// When y is within tol of an integer k the reference bin is k or k-1 and the
+// table decides it with one (L2-resident) load instead of an f64 divide.
+__device__ __forceinline__ int bin_of(float v, const TileParam<float>& tp, const float* thr,
+                                      int n, float nm05) {
   float y = __fmul_rn(__fsub_rn(v, tp.lo), tp.c);
   y = fminf(fmaxf(y, 0.5f), nm05);
   const float t = __fadd_rd(y, 12582912.0f);  // 1.5 * 2^23: t = floor(y) + M exactly
   const float fr = __fsub_rn(y, __fsub_rn(t, 12582912.0f));
   if (fabsf(__fsub_rn(fr, 0.5f)) < tp.lim) return __float_as_int(t) - 0x4B400000;
-  return bin_exact(static_cast<double>(v), static_cast<double>(tp.lo),
-                   static_cast<double>(tp.hi), n);
+  if (tp.lim < 0.0f)
+    return bin_exact(static_cast<double>(v), static_cast<double>(tp.lo),
+                     static_cast<double>(tp.hi), n);
+  const int k = __float2int_rn(y);
+  return v >= __ldg(thr + k) ? k : k - 1;
 }
 
-__device__ __forceinline__ int bin_of(double v, const TileParam<double>& tp, int n, double nm05) {
+__device__ __forceinline__ int bin_of(double v, const TileParam<double>& tp, const double*, int n,
+                                      double nm05) {
   double y = __dmul_rn(__dsub_rn(v, tp.lo), tp.c);
   y = fmin(fmax(y, 0.5), nm05);
   const double fl = floor(y);
   const double fr = __dsub_rn(y, fl);
   if (fabs(__dsub_rn(fr, 0.5)) < tp.lim) return static_cast<int>(fl);
   return bin_exact(v, tp.lo, tp.hi, n);
+}
+
+// Smallest float whose reference bin is >= k (1 <= k <= n-1) for a
+// non-degenerate, non-pathological range: guess, walk a few ulps, and fall
+// back to bisection over the ordered float keys if the walk is long.
+__device__ inline float bin_threshold(double lo, double hi, int n, int k) {
+  float v = static_cast<float>(lo + (hi - lo) * static_cast<double>(k) / n);
+  v = fminf(fmaxf(v, static_cast<float>(lo)), static_cast<float>(hi));
+  int steps = 0;
+  if (bin_exact(v, lo, hi, n) >= k) {
+    while (steps++ < 16) {
+      const float w = nextafterf(v, -INFINITY);
+      if (bin_exact(w, lo, hi, n) >= k) v = w;
+      else return v;
+    }
+  } else {
+    while (steps++ < 16) {
+      v = nextafterf(v, INFINITY);
+      if (bin_exact(v, lo, hi, n) >= k) return v;
+    }
+  }
+  // bisection on monotone int keys: bin(lo) = 0 < k <= n-1 = bin(hi)
+  auto key = [](float f) { int i = __float_as_int(f); return i >= 0 ? i : (i ^ 0x7FFFFFFF); };
+  auto unkey = [](int i) { return __int_as_float(i >= 0 ? i : (i ^ 0x7FFFFFFF)); };
+  int a = key(static_cast<float>(lo)), b = key(static_cast<float>(hi));  // bin(a) < k <= bin(b)
+  while (b - a > 1) {
+    const int m = a + (b - a) / 2;
+    if (bin_exact(unkey(m), lo, hi, n) >= k) b = m;
+    else a = m;
+  }
+  return unkey(b);
 }
 
 #endif  // __CUDACC__

@@ -6,12 +6,15 @@
 // trailing dimensions, and a chunk of dim-0 rows.  A unit's voxels are
 // "runs": for every coordinate of the outer dims except the last, the
 // ext[KO-1] consecutive rows of P = prod(trailing extents) floats are one
-// contiguous span of the input.  A producer warp streams runs into shared
-// memory stages with cp.async.bulk (TMA bulk copy, completion on an
+// contiguous span of the input.  The input is described to the TMA engine
+// as a (KO + 1 or 2)-D tensor (outer dims, trailing block split into <=256
+// wide rows); one producer thread walks each unit in R2 x R1 row boxes and
+// issues ONE cp.async.bulk.tensor per pipeline stage (completion counted on an
 // mbarrier); eight consumer warps read each stage with conflict-free 16-byte
 // LDS, every thread owning a fixed 4-voxel column of the trailing block.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -37,7 +40,11 @@ struct KGeom {
   int rpi;          // trailing blocks (rows) per consumer iteration
   int adaptive;
   int nst;          // pipeline stages
-  int stage_rows;   // rows of P floats per stage
+  int stage_rows;   // rows of P floats per stage (= R1 * R2)
+  int r1, lg_r1;    // box rows along outer dim KO-1 (power of two) and log2
+  int r2;           // box rows along outer dim KO-2 (1 if KO == 1)
+  int tma_rank;     // rank of the TMA tensor view of the input
+  int64_t stage_stride;  // floats between stage buffers (128-byte multiple)
   int64_t P;        // elements of one trailing block
   int64_t gtr;      // tiles of one trailing block
   Dim d[kMaxRank];
@@ -57,6 +64,7 @@ struct WS {
   uint32_t* counts;     // [win_tiles][n_bins]
   void* tparams;        // TileParam<T>[adaptive ? win_tiles : 1]
   float* lut;           // [win_tiles][n_bins]
+  float* thr;           // [adaptive ? win_tiles : 1][n_bins] bin-edge tables (f32 data)
 };
 
 struct Debug {
@@ -115,19 +123,16 @@ __device__ __forceinline__ void consumers_sync() {
   asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory");
 }
 
-// One pipeline stage: up to kMaxRuns runs (or one chunk of one run) of one unit.
+// One pipeline stage = one TMA box of one unit: R2 x R1 rows of P floats.
 struct Stage {
   int32_t unit;   // -1: end of stream
-  int32_t nruns;  // runs in the stage
-  int32_t nr;     // rows per run in the stage
-  int32_t r0;     // first row (relative to the box) of each run
+  int32_t wuni;   // K2: 1 if the multiplicity is uniform over the box (= wfix)
+  int32_t wfix;   // K2: multiplicity over dims < KO-2 (or over the whole box if wuni)
+  int32_t pad_;
   int64_t key;    // tile window offset (K2) or cell key (K4) of the unit
-  int64_t a_last; // box start along outer dim KO-1
-  TileParts pl;   // K2: tile parts along outer dim KO-1
-  int32_t cell[kMaxOuterDims];           // K4: cells of the unit
-  int64_t run_off[kMaxRuns];             // local element offset of (run, row r0)
-  int32_t run_w[kMaxRuns];               // K2: multiplicity over dims 0..KO-2
-  int32_t run_x[kMaxRuns][kMaxOuterDims];  // K4: absolute coords of dims 0..KO-2
+  int32_t x[kMaxOuterDims];     // absolute coordinates of the box origin (dim 0 global)
+  int32_t cell[kMaxOuterDims];  // K4: cells of the unit (K2: tiles)
+  TileParts p1, p2;             // K2: tile parts along dims KO-1 and KO-2
 };
 
 // Producer-private per-unit box (kept in shared memory, not registers, so
@@ -159,16 +164,54 @@ __device__ __forceinline__ void pipe_init(Pipe& pp, int nst) {
   }
 }
 
-// Producer (one thread): walks the CTA's units, cuts their runs into stages
-// and issues the bulk copies.  CELLS selects interpolation-cell boxes (K4)
+// TMA tensor load of one box; coordinates innermost first.
+__device__ __forceinline__ void tma_load(void* dst, const CUtensorMap* map, int rank, const int* c,
+                                         uint64_t* bar) {
+  const uint64_t m = reinterpret_cast<uint64_t>(map);
+  const uint32_t d = smem_u32(dst), b = smem_u32(bar);
+  switch (rank) {
+    case 2:
+      asm volatile(
+          "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+          " [%0], [%1, {%2, %3}], [%4];" ::"r"(d), "l"(m), "r"(c[0]), "r"(c[1]), "r"(b)
+          : "memory");
+      break;
+    case 3:
+      asm volatile(
+          "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+          " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(d), "l"(m), "r"(c[0]), "r"(c[1]), "r"(c[2]),
+          "r"(b)
+          : "memory");
+      break;
+    case 4:
+      asm volatile(
+          "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+          " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(d), "l"(m), "r"(c[0]), "r"(c[1]),
+          "r"(c[2]), "r"(c[3]), "r"(b)
+          : "memory");
+      break;
+    default:
+      asm volatile(
+          "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+          " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(d), "l"(m), "r"(c[0]), "r"(c[1]),
+          "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(b)
+          : "memory");
+      break;
+  }
+}
+
+// Producer (one thread): walks the CTA's units box by box (the plan makes
+// every unit extent along dims KO-1 / KO-2 a multiple of R1 / R2) and issues
+// one TMA box load per stage.  CELLS selects interpolation-cell boxes (K4)
 // instead of tile-support boxes (K2).
 template <int KO, bool CELLS>
-__device__ __noinline__ void pipe_produce(const KGeom& G, const float* __restrict__ in,
+__device__ __noinline__ void pipe_produce(const KGeom& G, const CUtensorMap* map,
                                           const int32_t* __restrict__ units, int u0, int u1,
                                           Pipe& pp, float* bufs) {
   const int nst = G.nst;
-  const int srows = G.stage_rows;
-  const int64_t stage_elems = (int64_t)srows * G.P;
+  const int64_t stage_elems = G.stage_stride;
+  const uint32_t box_bytes = (uint32_t)((int64_t)G.stage_rows * G.P * 4);
+  const int R1 = G.r1, R2 = G.r2;
   ProdBox& B = pp.box;
   uint32_t it = 0;
 #pragma unroll 1
@@ -177,7 +220,7 @@ __device__ __noinline__ void pipe_produce(const KGeom& G, const float* __restric
     int64_t key = 0;
     B.a[0] = U[8];
     B.ext[0] = U[9] - U[8];
-    if (!CELLS) B.parts[0] = tile_parts(G.d[0], U[0]);
+    B.parts[0] = tile_parts(G.d[0], U[0]);
 #pragma unroll 1
     for (int j = 1; j < KO; ++j) {
       if (CELLS) {
@@ -199,51 +242,77 @@ __device__ __noinline__ void pipe_produce(const KGeom& G, const float* __restric
 #pragma unroll 1
       for (int j = 1; j < KO; ++j) key += (int64_t)U[j] * G.tstride[j];
     }
-    const int32_t el = B.ext[KO - 1];
-    int64_t nrun = 1;
+    // boxes: dims < KO-2 one coordinate each, dim KO-2 in steps of R2, dim KO-1 of R1
+    int64_t nfix = 1;
 #pragma unroll 1
-    for (int j = 0; j < KO - 1; ++j) nrun *= B.ext[j];
-    const bool chunked = el >= srows;
-    const int32_t m = chunked ? 1 : min(kMaxRuns, srows / el);
+    for (int j = 0; j < KO - 2; ++j) nfix *= B.ext[j];
+    const int n1 = B.ext[KO - 1] / R1;
+    const int n2 = KO >= 2 ? B.ext[KO - 2] / R2 : 1;
 #pragma unroll 1
-    for (int64_t run = 0; run < nrun; run += m) {
-      const int32_t nruns = (int32_t)min((int64_t)m, nrun - run);
+    for (int64_t f = 0; f < nfix; ++f) {
+      int32_t xf[kMaxOuterDims];
+      int32_t wfix = 1;
+      int64_t rem = f;
 #pragma unroll 1
-      for (int32_t r0 = 0; r0 < el; r0 += (chunked ? srows : el)) {
-        const int32_t nr = chunked ? min(srows, el - r0) : el;
-        const int slot = it % nst;
-        mbar_wait(&pp.empty[slot], ((it / nst) & 1) ^ 1);
-        Stage& S = pp.st[slot];
-        S.unit = u;
-        S.nruns = nruns;
-        S.nr = nr;
-        S.r0 = r0;
-        S.key = key;
-        S.a_last = B.a[KO - 1];
-        if (!CELLS) S.pl = B.parts[KO - 1];
+      for (int j = KO - 3; j >= 0; --j) {
+        xf[j] = (int32_t)(B.a[j] + rem % B.ext[j]);
+        rem /= B.ext[j];
+        if (!CELLS) wfix *= B.parts[j].weight(xf[j]);
+      }
 #pragma unroll 1
-        for (int j = 0; j < KO; ++j) S.cell[j] = U[j];
-        const uint32_t run_bytes = (uint32_t)(nr * G.P * 4);
-        mbar_expect_tx(&pp.full[slot], run_bytes * nruns);
-        float* dst = bufs + slot * stage_elems;
+      for (int i2 = 0; i2 < n2; ++i2) {
 #pragma unroll 1
-        for (int k = 0; k < nruns; ++k) {
-          int64_t rem = run + k;
-          int64_t off = (KO == 1 ? B.a[0] + r0 - G.row0 : B.a[KO - 1] + r0) * G.vstride[KO - 1];
-          int32_t w = 1;
+        for (int i1 = 0; i1 < n1; ++i1) {
+          const int slot = it % nst;
+          mbar_wait(&pp.empty[slot], ((it / nst) & 1) ^ 1);
+          Stage& S = pp.st[slot];
+          S.unit = u;
+          S.key = key;
 #pragma unroll 1
-          for (int j = KO - 2; j >= 0; --j) {
-            const int64_t x = B.a[j] + rem % B.ext[j];
-            rem /= B.ext[j];
-            off += (j == 0 ? x - G.row0 : x) * G.vstride[j];
-            if (!CELLS) w *= B.parts[j].weight(x);
-            S.run_x[k][j] = (int32_t)x;
+          for (int j = 0; j < KO - 2; ++j) S.x[j] = xf[j];
+          const int32_t x1 = (int32_t)(B.a[KO - 1] + i1 * R1);
+          S.x[KO - 1] = x1;
+          int32_t x2 = 0;
+          if (KO >= 2) {
+            x2 = (int32_t)(B.a[KO - 2] + i2 * R2);
+            S.x[KO - 2] = x2;
           }
-          S.run_off[k] = off;
-          S.run_w[k] = w;
-          bulk_g2s(dst + (int64_t)k * nr * G.P, in + off, run_bytes, &pp.full[slot]);
+#pragma unroll 1
+          for (int j = 0; j < KO; ++j) S.cell[j] = U[j];
+          if (!CELLS) {
+            S.p1 = B.parts[KO - 1];
+            if (KO >= 2) S.p2 = B.parts[KO - 2];
+            // uniform multiplicity over the box?  (ends of each box range)
+            const int w1a = S.p1.weight(x1), w1b = S.p1.weight(x1 + R1 - 1);
+            int w2a = 1, w2b = 1;
+            if (KO >= 2) {
+              w2a = S.p2.weight(x2);
+              w2b = S.p2.weight(x2 + R2 - 1);
+            }
+            bool uni = w1a == w1b && w2a == w2b;
+            if (uni) {  // a range of equal end weights can still dip in between: check all
+#pragma unroll 1
+              for (int r = 1; r < R1 - 1 && uni; ++r) uni = S.p1.weight(x1 + r) == w1a;
+#pragma unroll 1
+              for (int r = 1; r < R2 - 1 && uni; ++r) uni = S.p2.weight(x2 + r) == w2a;
+            }
+            S.wuni = uni ? 1 : 0;
+            S.wfix = uni ? wfix * w1a * w2a : wfix;
+          }
+          // TMA coordinates, innermost first: trailing block, then dims KO-1 .. 0
+          int c[6];
+          int r = 0;
+          c[r++] = 0;
+          if (G.tma_rank - KO == 2) c[r++] = 0;
+#pragma unroll 1
+          for (int j = KO - 1; j >= 0; --j) {
+            const int32_t xj = j == KO - 1 ? x1 : (j == KO - 2 ? x2 : xf[j]);
+            c[r++] = j == 0 ? (int)(xj - G.row0) : xj;
+          }
+          mbar_expect_tx(&pp.full[slot], box_bytes);
+          tma_load(bufs + slot * stage_elems, map, G.tma_rank, c, &pp.full[slot]);
+          ++it;
         }
-        ++it;
       }
     }
   }

@@ -13,6 +13,17 @@ __device__ __forceinline__ int64_t window_tile(const KGeom& G, const int64_t* t)
   return f;
 }
 
+template <typename T>
+__device__ __forceinline__ const T* thr_row(const WS& W, int64_t idx, int n);
+template <>
+__device__ __forceinline__ const float* thr_row<float>(const WS& W, int64_t idx, int n) {
+  return W.thr + idx * n;
+}
+template <>
+__device__ __forceinline__ const double* thr_row<double>(const WS&, int64_t, int) {
+  return nullptr;  // f64 data takes the exact path near bin edges
+}
+
 __device__ __forceinline__ void decode_local(const KGeom& G, int64_t idx, int64_t* x) {
   for (int j = G.rank - 1; j >= 0; --j) {
     const int64_t ext = j == 0 ? (G.local_voxels / G.vstride[0]) : G.d[j].s;
@@ -140,7 +151,9 @@ __global__ void __launch_bounds__(256) k_tiles_generic(const KGeom G, const T* _
         atomicMax(reinterpret_cast<long long*>(W.trange + 2 * f + 1), (long long)okey((double)v));
       } else {
         const TileParam<T> tp = tparams[ADAPT ? f : 0];
-        if (!tp_degenerate(tp.lim)) atomicAdd(W.counts + f * n + bin_of(v, tp, n, nm05), (uint32_t)w);
+        if (!tp_degenerate(tp.lim))
+          atomicAdd(W.counts + f * n + bin_of(v, tp, thr_row<T>(W, ADAPT ? f : 0, n), n, nm05),
+                    (uint32_t)w);
       }
       int j = G.rank - 1;
       while (j >= 0 && ++ci[j] == nl[j]) ci[j--] = 0;
@@ -258,7 +271,7 @@ __global__ void __launch_bounds__(256) k_interp_generic(const KGeom G, const T* 
       f1[j] = (double)twice_dlo(G.d[j], x[j], c[j]) / (double)(2 * G.d[j].b);
     }
     const int corners = 1 << G.rank;
-    const int bg = ADAPT ? 0 : bin_of(v, tparams[0], n, nm05);
+    const int bg = ADAPT ? 0 : bin_of(v, tparams[0], thr_row<T>(W, 0, n), n, nm05);
     double acc = 0.0;
     for (int co = 0; co < corners; ++co) {
       int64_t t[kMaxRank];
@@ -269,7 +282,7 @@ __global__ void __launch_bounds__(256) k_interp_generic(const KGeom G, const T* 
         w *= bit ? f1[j] : 1.0 - f1[j];
       }
       const int64_t f = window_tile(G, t);
-      const int b = ADAPT ? bin_of(v, tparams[f], n, nm05) : bg;
+      const int b = ADAPT ? bin_of(v, tparams[f], thr_row<T>(W, f, n), n, nm05) : bg;
       acc += w * (double)W.lut[f * n + b];
     }
     out[idx] = (T)fmin(fmax(acc, 0.0), 1.0);
@@ -277,14 +290,39 @@ __global__ void __launch_bounds__(256) k_interp_generic(const KGeom G, const T* 
 }
 
 // ------------------------------------------------------- debug binning ---
+// Bin-edge tables for every binning range (f32 data): thr[t][k] = smallest
+// float whose reference bin is >= k; thr[t][0] = -inf.
+__global__ void k_thresholds(const KGeom G, WS W) {
+  const TileParam<float>* tp = reinterpret_cast<const TileParam<float>*>(W.tparams);
+  const int n = G.n_bins;
+  const int64_t total = (G.adaptive ? G.win_tiles : 1) * (int64_t)n;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = i / n;
+    const int k = (int)(i - t * n);
+    const TileParam<float> p = tp[t];
+    W.thr[i] = (k == 0 || tp_degenerate(p.lim) || p.lim < 0.0f)
+                   ? -INFINITY
+                   : bin_threshold((double)p.lo, (double)p.hi, n, k);
+  }
+}
+
+__global__ void k_debug_thresholds(double lo, double hi, int n, float* thr) {
+  const TileParam<float> p = make_tile_param<float>(lo, hi, n);
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x)
+    thr[k] = (k == 0 || tp_degenerate(p.lim) || p.lim < 0.0f)
+                 ? -INFINITY
+                 : bin_threshold((double)p.lo, (double)p.hi, n, k);
+}
+
 template <typename T>
 __global__ void k_debug_bins(const T* __restrict__ v, int64_t count, double lo, double hi, int n,
-                             int32_t* __restrict__ out) {
+                             const T* thr, int32_t* __restrict__ out) {
   const TileParam<T> tp = make_tile_param<T>(lo, hi, n);
   const T nm05 = (T)n - (T)0.5;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
        i += (int64_t)gridDim.x * blockDim.x)
-    out[i] = tp_degenerate(tp.lim) ? -1 : bin_of(v[i], tp, n, nm05);
+    out[i] = tp_degenerate(tp.lim) ? -1 : bin_of(v[i], tp, thr, n, nm05);
 }
 
 }  // namespace mg

@@ -22,7 +22,7 @@ __device__ __forceinline__ PencilSmem pencil_smem(const KGeom& G, unsigned char*
   PencilSmem s;
   s.pipe = reinterpret_cast<Pipe*>(smem);
   s.bufs = reinterpret_cast<float*>(smem + pipe_bytes());
-  s.tail = smem + pipe_bytes() + (size_t)G.nst * G.stage_rows * G.P * 4;
+  s.tail = smem + pipe_bytes() + (size_t)G.nst * G.stage_stride * 4;
   return s;
 }
 
@@ -45,7 +45,8 @@ __device__ __forceinline__ void trailing_tile(const KGeom& G, int64_t e, int* ti
 // --------------------------------------------------------------- K2a -----
 template <int KO>
 __global__ void __launch_bounds__(kPencilThreads, 3)
-    k_range_pencil(const __grid_constant__ KGeom G, const float* __restrict__ in, const int32_t* __restrict__ units,
+    k_range_pencil(const __grid_constant__ KGeom G, const __grid_constant__ CUtensorMap tmap,
+                   const float* __restrict__ in, const int32_t* __restrict__ units,
                    const int32_t* __restrict__ cta_units, WS W) {
   extern __shared__ __align__(128) unsigned char smem[];
   const PencilSmem P = pencil_smem(G, smem);
@@ -55,7 +56,7 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
   __syncthreads();
   const int u0 = cta_units[blockIdx.x], u1 = cta_units[blockIdx.x + 1];
   if (threadIdx.x >= kConsumers) {
-    if (threadIdx.x == kConsumers) pipe_produce<KO, false>(G, in, units, u0, u1, *P.pipe, P.bufs);
+    if (threadIdx.x == kConsumers) pipe_produce<KO, false>(G, &tmap, units, u0, u1, *P.pipe, P.bufs);
     return;
   }
   const int tid = threadIdx.x;
@@ -68,7 +69,7 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
   float mn[4], mx[4];
   int bad = 0;
   int64_t cur = -1;
-  const int64_t stage_elems = (int64_t)G.stage_rows * G.P;
+  const int64_t stage_elems = G.stage_stride;
 
   auto flush = [&]() {
 #pragma unroll
@@ -106,7 +107,7 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
       consumers_sync();
       cur = key;
     }
-    const int rows = S.nruns * S.nr;
+    const int rows = G.stage_rows;
     const float* buf = P.bufs + s * stage_elems;
     if (lane_on) {
       for (int q = slot; q < rows; q += G.rpi) {
@@ -136,7 +137,8 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
 // atomic carries the whole run.
 template <int KO, bool ADAPT>
 __global__ void __launch_bounds__(kPencilThreads, 3)
-    k_hist_pencil(const __grid_constant__ KGeom G, const float* __restrict__ in, const int32_t* __restrict__ units,
+    k_hist_pencil(const __grid_constant__ KGeom G, const __grid_constant__ CUtensorMap tmap,
+                   const float* __restrict__ in, const int32_t* __restrict__ units,
                   const int32_t* __restrict__ cta_units, WS W) {
   extern __shared__ __align__(128) unsigned char smem[];
   const PencilSmem P = pencil_smem(G, smem);
@@ -151,7 +153,7 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
   __syncthreads();
   const int u0 = cta_units[blockIdx.x], u1 = cta_units[blockIdx.x + 1];
   if (threadIdx.x >= kConsumers) {
-    if (threadIdx.x == kConsumers) pipe_produce<KO, false>(G, in, units, u0, u1, *P.pipe, P.bufs);
+    if (threadIdx.x == kConsumers) pipe_produce<KO, false>(G, &tmap, units, u0, u1, *P.pipe, P.bufs);
     return;
   }
   const float nm05 = (float)n - 0.5f;
@@ -162,7 +164,7 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
   int trt[4], trw[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) trailing_tile(G, e0 + i, &trt[i], &trw[i]);
-  const int64_t stage_elems = (int64_t)G.stage_rows * G.P;
+  const int64_t stage_elems = G.stage_stride;
   int64_t cur = -1;
 
   uint32_t it = 0;
@@ -188,18 +190,24 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
       consumers_sync();
       cur = key;
     }
-    const int rows = S.nruns * S.nr;
-    const int nr = S.nr;
+    const int rows = G.stage_rows;
     const float* buf = P.bufs + s * stage_elems;
+    const bool wuni = S.wuni != 0;
+    const int32_t wfix = S.wfix;
     for (int q0 = 0; q0 < rows; q0 += G.rpi) {  // trip count uniform over the warp
       const int q = q0 + slot;
       const bool ok = lane_on && q < rows;
       float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
       uint32_t wrow = 0;
       if (ok) {
-        const int run = q / nr;
-        const int r = S.r0 + (q - run * nr);
-        wrow = (uint32_t)(S.run_w[run] * S.pl.weight(S.a_last + r));
+        if (wuni) {
+          wrow = (uint32_t)wfix;
+        } else {
+          const int r1 = q & (G.r1 - 1), r2 = q >> G.lg_r1;
+          int32_t w = wfix * S.p1.weight(S.x[KO - 1] + r1);
+          if (KO >= 2) w *= S.p2.weight(S.x[KO >= 2 ? KO - 2 : 0] + r2);
+          wrow = (uint32_t)w;
+        }
         v = *reinterpret_cast<const float4*>(buf + q * G.P + e0);
       }
       const float a[4] = {v.x, v.y, v.z, v.w};
@@ -211,7 +219,7 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
         if (ok) {
           const TileParam<float> tp = ADAPT ? rng[trt[i]] : g0;
           if (!tp_degenerate(tp.lim)) {
-            cell = trt[i] * n + bin_of(a[i], tp, n, nm05);
+            cell = trt[i] * n + bin_of(a[i], tp, W.thr + (ADAPT ? (cur + trt[i]) * n : 0), n, nm05);
             wgt = wrow * (uint32_t)trw[i];
             k64 = ((unsigned long long)cell << 16) | wgt;
           }
@@ -242,7 +250,8 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
 // the exact half-integer distances (d_lo = twice_dlo / 2).  FP32 sum.
 template <int KO, int KT, bool ADAPT>
 __global__ void __launch_bounds__(kPencilThreads, 2)
-    k_interp_pencil(const __grid_constant__ KGeom G, const float* __restrict__ in, float* __restrict__ out,
+    k_interp_pencil(const __grid_constant__ KGeom G, const __grid_constant__ CUtensorMap tmap,
+                    const float* __restrict__ in, float* __restrict__ out,
                     const int32_t* __restrict__ units, const int32_t* __restrict__ cta_units, WS W) {
   constexpr int NCO = 1 << KO, NCT = 1 << KT;
   if (W.range[2] != 0) return;  // non-finite input: write nothing
@@ -257,7 +266,7 @@ __global__ void __launch_bounds__(kPencilThreads, 2)
   __syncthreads();
   const int u0 = cta_units[blockIdx.x], u1 = cta_units[blockIdx.x + 1];
   if (threadIdx.x >= kConsumers) {
-    if (threadIdx.x == kConsumers) pipe_produce<KO, true>(G, in, units, u0, u1, *P.pipe, P.bufs);
+    if (threadIdx.x == kConsumers) pipe_produce<KO, true>(G, &tmap, units, u0, u1, *P.pipe, P.bufs);
     return;
   }
   const TileParam<float>* tparams = reinterpret_cast<const TileParam<float>*>(W.tparams);
@@ -304,7 +313,8 @@ __global__ void __launch_bounds__(kPencilThreads, 2)
 #pragma unroll
   for (int j = 0; j < KO; ++j) inv2b[j] = 1.0f / (float)(2 * G.d[j].b);
 
-  const int64_t stage_elems = (int64_t)G.stage_rows * G.P;
+  const int64_t stage_elems = G.stage_stride;
+  __shared__ int64_t s_of[NCO];  // window tile offset of each outer corner
   int64_t cur = -1;
   uint32_t it = 0;
   while (true) {
@@ -318,6 +328,7 @@ __global__ void __launch_bounds__(kPencilThreads, 2)
       for (int co = 0; co < NCO; ++co) {
         int64_t of = (S.cell[0] + ((co >> (KO - 1)) & 1) - G.trow0) * G.tstride[0];
         for (int j = 1; j < KO; ++j) of += (S.cell[j] + ((co >> (KO - 1 - j)) & 1)) * G.tstride[j];
+        if (tid == 0) s_of[co] = of;
         const float4* src = reinterpret_cast<const float4*>(W.lut + of * n);
         float4* dst = reinterpret_cast<float4*>(lutS + co * gtr * n);
         for (int64_t k = tid; k < gtr * n / 4; k += kConsumers) dst[k] = __ldg(src + k);
@@ -327,21 +338,29 @@ __global__ void __launch_bounds__(kPencilThreads, 2)
       consumers_sync();
       cur = key;
     }
-    const int rows = S.nruns * S.nr;
-    const int nr = S.nr;
+    const int rows = G.stage_rows;
     const float* buf = P.bufs + s * stage_elems;
     if (lane_on) {
-      int cellv[KO];
+      int cellv[KO], xb[KO];
 #pragma unroll
-      for (int j = 0; j < KO; ++j) cellv[j] = S.cell[j];
+      for (int j = 0; j < KO; ++j) {
+        cellv[j] = S.cell[j];
+        xb[j] = S.x[j];
+      }
+      // outer factors and output offset of the fixed dims (< KO-2)
+      int64_t obase = e0;
+#pragma unroll
+      for (int j = 0; j < KO; ++j)
+        if (j < KO - 2) obase += (int64_t)(j == 0 ? xb[j] - G.row0 : xb[j]) * G.vstride[j];
       for (int q = slot; q < rows; q += G.rpi) {
-        const int run = q / nr;
-        const int rr = q - run * nr;
+        const int r1 = q & (G.r1 - 1), r2 = q >> G.lg_r1;
         float fo[KO];
+        int64_t ooff = obase;
 #pragma unroll
         for (int j = 0; j < KO; ++j) {
-          const int64_t xj = (j == KO - 1) ? S.a_last + S.r0 + rr : (int64_t)S.run_x[run][j];
+          const int64_t xj = xb[j] + (j == KO - 1 ? r1 : (j == KO - 2 ? r2 : 0));
           fo[j] = (float)twice_dlo(G.d[j], xj, cellv[j]) * inv2b[j];
+          if (j >= KO - 2) ooff += (j == 0 ? xj - G.row0 : xj) * G.vstride[j];
         }
         const float4 v4 = *reinterpret_cast<const float4*>(buf + q * G.P + e0);
         const float v[4] = {v4.x, v4.y, v4.z, v4.w};
@@ -349,7 +368,7 @@ __global__ void __launch_bounds__(kPencilThreads, 2)
         int bg[4];
         if (!ADAPT) {
 #pragma unroll
-          for (int i = 0; i < 4; ++i) bg[i] = bin_of(v[i], g0, n, nm05);
+          for (int i = 0; i < 4; ++i) bg[i] = bin_of(v[i], g0, W.thr, n, nm05);
         }
 #pragma unroll
         for (int co = 0; co < NCO; ++co) {
@@ -361,9 +380,10 @@ __global__ void __launch_bounds__(kPencilThreads, 2)
             const float* L = lutS + (co * gtr + tt[ct]) * n;
             if (ADAPT) {
               const TileParam<float> tp = rngS[co * gtr + tt[ct]];
+              const float* thr_co = W.thr + (s_of[co] + tt[ct]) * n;
 #pragma unroll
               for (int i = 0; i < 4; ++i)
-                acc[i] = fmaf(wo * tw[i][ct], L[bin_of(v[i], tp, n, nm05)], acc[i]);
+                acc[i] = fmaf(wo * tw[i][ct], L[bin_of(v[i], tp, thr_co, n, nm05)], acc[i]);
             } else {
 #pragma unroll
               for (int i = 0; i < 4; ++i) acc[i] = fmaf(wo * tw[i][ct], L[bg[i]], acc[i]);
@@ -375,7 +395,7 @@ __global__ void __launch_bounds__(kPencilThreads, 2)
         r.y = fminf(fmaxf(acc[1], 0.f), 1.f);
         r.z = fminf(fmaxf(acc[2], 0.f), 1.f);
         r.w = fminf(fmaxf(acc[3], 0.f), 1.f);
-        __stcs(reinterpret_cast<float4*>(out + S.run_off[run] + (int64_t)rr * G.P + e0), r);
+        __stcs(reinterpret_cast<float4*>(out + ooff), r);
       }
     }
     __syncwarp();
@@ -385,10 +405,11 @@ __global__ void __launch_bounds__(kPencilThreads, 2)
 }
 
 // Host-side accessors (defined in the k_*.cu translation units).
-using PencilRangeFn = void (*)(const KGeom, const float*, const int32_t*, const int32_t*, WS);
-using PencilHistFn = void (*)(const KGeom, const float*, const int32_t*, const int32_t*, WS);
-using PencilInterpFn = void (*)(const KGeom, const float*, float*, const int32_t*, const int32_t*,
-                                WS);
+using PencilRangeFn = void (*)(const KGeom, const CUtensorMap, const float*, const int32_t*,
+                               const int32_t*, WS);
+using PencilHistFn = PencilRangeFn;
+using PencilInterpFn = void (*)(const KGeom, const CUtensorMap, const float*, float*,
+                                const int32_t*, const int32_t*, WS);
 PencilRangeFn get_range_pencil(int ko);
 PencilHistFn get_hist_pencil(int ko, bool adaptive);
 PencilInterpFn get_interp_pencil(int ko, int kt, bool adaptive);

@@ -87,11 +87,16 @@ struct Pencil {
   int64_t P = 0, gtr = 0;
   int tpr = 0, rpi = 0;
   int nst = 0, stage_rows = 0;
+  int r1 = 1, lg_r1 = 0, r2 = 1;  // TMA box rows along outer dims KO-1, KO-2
+  int tma_rank = 0, width = 0;    // TMA view: [outer dims..., P/width, width]
+  int64_t stage_stride = 0;       // floats per stage buffer
+  int64_t tail = 0;               // kernel-specific shared memory (hist / LUTs)
+  int64_t stage_budget = 0;
   int64_t smem = 0;
 };
 
 constexpr int64_t kPipeBytes = (sizeof(mg::Pipe) + 127) & ~int64_t(127);
-constexpr int64_t kStageBytes = 8192;
+constexpr int64_t kStageBytes = 16384;
 
 }  // namespace
 
@@ -110,6 +115,9 @@ struct mclahe_plan_s {
   int64_t off_hist_units = 0, off_hist_cta = 0, off_interp_units = 0, off_interp_cta = 0;
   int hist_grid = 0, interp_grid = 0, range_grid = 0, map_grid = 0, map_block = 128;
   int64_t map_smem = 0;
+  // TMA views of the last input buffer (re-encoded when the pointer changes)
+  const void* map_ptr[2] = {nullptr, nullptr};
+  CUtensorMap map[2];
   bool f32() const { return p.dtype == MCLAHE_F32; }
 };
 
@@ -124,6 +132,11 @@ KGeom pencil_geom(const mclahe_plan_s& pl, const Pencil& pc) {
   G.rpi = pc.rpi;
   G.nst = pc.nst;
   G.stage_rows = pc.stage_rows;
+  G.r1 = pc.r1;
+  G.lg_r1 = pc.lg_r1;
+  G.r2 = pc.r2;
+  G.tma_rank = pc.tma_rank;
+  G.stage_stride = pc.stage_stride;
   return G;
 }
 
@@ -135,7 +148,8 @@ bool trailing_merged(const Dim& d) {
   return true;
 }
 
-// Chooses how many trailing dims one pencil covers for a kernel family.
+// Chooses how many trailing dims one pencil covers for a kernel family
+// (box rows and pipeline depth are fixed later, once the units are known).
 Pencil choose_pencil(const mclahe_plan_s& pl, bool for_hist) {
   Pencil best;
   const int D = pl.p.rank;
@@ -145,7 +159,7 @@ Pencil choose_pencil(const mclahe_plan_s& pl, bool for_hist) {
   for (int kt = 1; kt <= D - 1; ++kt) {
     const int ko = D - kt;
     if (ko > kMaxOuterDims) continue;
-    if (!for_hist && kt > 2) continue;
+    if (!for_hist && (kt > 2 || ko > 4)) continue;
     Pencil c;
     c.kt = kt;
     c.ko = ko;
@@ -157,40 +171,40 @@ Pencil choose_pencil(const mclahe_plan_s& pl, bool for_hist) {
       c.gtr *= pl.d[j].g;
       merged = merged && trailing_merged(pl.d[j]);
     }
-    if (c.P % 4 != 0) continue;
-    c.tpr = (int)std::min<int64_t>(c.P / 4, 1 << 20);
-    if (c.P / 4 > 256) continue;
+    if (c.P % 4 != 0 || c.P / 4 > 256) continue;
+    c.width = (int)std::min<int64_t>(c.P, 256);
+    if (c.P % c.width != 0) continue;
+    c.tma_rank = ko + (c.P > 256 ? 2 : 1);
+    if (c.tma_rank > 5) continue;
+    c.tpr = (int)(c.P / 4);
     c.rpi = 256 / c.tpr;
-    c.stage_rows = (int)std::max<int64_t>(1, kStageBytes / (c.P * 4));
-    const int64_t stage = c.stage_rows * c.P * 4;
-    int64_t tail;
     if (for_hist) {
       if (!merged) continue;
       if (c.gtr * n >= (int64_t{1} << 31) / 2) continue;
-      tail = align_up(c.gtr * n * 4, 16) + c.gtr * 16;
-      if (tail > 64 * 1024) continue;
-      c.nst = 4;
+      c.tail = align_up(c.gtr * n * 4, 16) + c.gtr * 16;
+      if (c.tail > 64 * 1024) continue;
+      c.stage_budget = kStageBytes;  // 3 stages, ~3 CTAs per SM
     } else {
-      if (ko > 4 || n % 4 != 0) continue;
+      if (n % 4 != 0) continue;
       // a thread's 4 columns must share their trailing cell
       const Dim& dl = pl.d[D - 1];
       if (dl.s % 4 != 0) continue;
       bool shared = true;
-      for (int64_t c = 1; c <= dl.g - 2 && shared; ++c) {
+      for (int64_t cc = 1; cc <= dl.g - 2 && shared; ++cc) {
         int64_t ca, ce;
-        cell_range(dl, c, &ca, &ce);
+        cell_range(dl, cc, &ca, &ce);
         shared = (ca % 4) == 0;
       }
       if (!shared) continue;
-      tail = align_up((int64_t{1} << ko) * c.gtr * n * 4, 16) + (int64_t{1} << ko) * c.gtr * 16;
-      // two CTAs per SM when the LUTs allow it, else one with a deeper pipeline
-      const int64_t two = 113 * 1024 - kPipeBytes - tail;
-      if (two >= 2 * stage) c.nst = (int)std::min<int64_t>(4, two / stage);
-      else if (224 * 1024 - kPipeBytes - tail >= 2 * stage)
-        c.nst = (int)std::min<int64_t>(kMaxStages, (224 * 1024 - kPipeBytes - tail) / stage);
+      c.tail = align_up((int64_t{1} << ko) * c.gtr * n * 4, 16) + (int64_t{1} << ko) * c.gtr * 16;
+      // two CTAs per SM when the LUTs allow >= 3 stages of >= 4 KB, else one
+      const int64_t two = 113 * 1024 - kPipeBytes - c.tail;
+      if (two >= 3 * 4096) c.stage_budget = std::min<int64_t>(kStageBytes, two / 3);
+      else if (224 * 1024 - kPipeBytes - c.tail >= 3 * 4096)
+        c.stage_budget = std::min<int64_t>(kStageBytes, (224 * 1024 - kPipeBytes - c.tail) / 4);
       else continue;
     }
-    c.smem = kPipeBytes + c.nst * stage + tail;
+    if (c.stage_budget < c.P * 4) continue;
     c.on = true;
     ok.push_back(c);
   }
@@ -200,9 +214,78 @@ Pencil choose_pencil(const mclahe_plan_s& pl, bool for_hist) {
   return best;
 }
 
+int64_t gcd64(int64_t a, int64_t b) {
+  while (b) {
+    const int64_t t = a % b;
+    a = b;
+    b = t;
+  }
+  return a;
+}
+
+int64_t pow2_divisor(int64_t g, int64_t cap) {
+  int64_t r = 1;
+  while (r * 2 <= cap && g % (r * 2) == 0) r *= 2;
+  return r;
+}
+
+// Natural per-unit extents along an outer dim: tile supports (K2) or
+// interpolation-cell ranges (K4), dim 0 clipped to the slab.
+void extents(const mclahe_plan_s& pl, bool cells, int j, std::vector<std::pair<int64_t, int64_t>>& out) {
+  const Dim& d = pl.d[j];
+  out.clear();
+  const int64_t n = cells ? d.g - 1 : d.g;
+  for (int64_t t = 0; t < n; ++t) {
+    int64_t a, e;
+    if (cells) {
+      cell_range(d, t, &a, &e);
+    } else {
+      const TileParts tp = tile_parts(d, t);
+      a = tp.support_begin();
+      e = tp.support_end();
+    }
+    if (j == 0) {
+      a = std::max(a, pl.info.row_begin);
+      e = std::min(e, pl.info.row_end);
+    }
+    if (e > a) out.push_back({a, e});
+  }
+}
+
+// Box rows (powers of two dividing every unit extent, so boxes never cross a
+// unit), pipeline depth and shared memory of a pencil family.
+void size_boxes(const mclahe_plan_s& pl, Pencil& c, bool cells) {
+  const int64_t rows_cap = std::max<int64_t>(1, std::min<int64_t>(c.stage_budget / (c.P * 4), 256));
+  std::vector<std::pair<int64_t, int64_t>> ex;
+  int64_t g1 = 0, g2 = 0;
+  extents(pl, cells, c.ko - 1, ex);
+  for (auto& p : ex) g1 = gcd64(g1, p.second - p.first);
+  c.r1 = (int)pow2_divisor(g1, std::min<int64_t>(rows_cap, 256));
+  c.r2 = 1;
+  if (c.ko >= 2) {
+    extents(pl, cells, c.ko - 2, ex);
+    for (auto& p : ex) g2 = gcd64(g2, p.second - p.first);
+    c.r2 = (int)pow2_divisor(g2, std::min<int64_t>(rows_cap / c.r1, 256));
+  }
+  c.lg_r1 = 0;
+  while ((1 << c.lg_r1) < c.r1) ++c.lg_r1;
+  c.stage_rows = c.r1 * c.r2;
+  c.stage_stride = align_up(c.stage_rows * c.P * 4, 128) / 4;
+  const int64_t stage = c.stage_stride * 4;
+  if (!cells) {
+    c.nst = 3;
+  } else {
+    const int64_t two = 113 * 1024 - kPipeBytes - c.tail;
+    c.nst = (int)std::max<int64_t>(2, std::min<int64_t>(4, (two >= 3 * stage ? two : 224 * 1024 -
+                                                             kPipeBytes - c.tail) / stage));
+  }
+  c.smem = kPipeBytes + c.nst * stage + c.tail;
+}
+
 void push_unit(std::vector<int32_t>& units, std::vector<int64_t>& vox, const int64_t* idx, int ko,
-               int64_t ra, int64_t re, int64_t vox_per_row, int64_t target) {
-  const int64_t rows = std::max<int64_t>(1, target / std::max<int64_t>(1, vox_per_row));
+               int64_t ra, int64_t re, int64_t vox_per_row, int64_t target, int64_t quantum) {
+  int64_t rows = std::max<int64_t>(1, target / std::max<int64_t>(1, vox_per_row));
+  rows = std::max<int64_t>(quantum, rows / quantum * quantum);
   for (int64_t a = ra; a < re; a += rows) {
     const int64_t e = std::min(re, a + rows);
     int32_t rec[kUnitInts] = {0};
@@ -215,54 +298,59 @@ void push_unit(std::vector<int32_t>& units, std::vector<int64_t>& vox, const int
 }
 
 void build_units(mclahe_plan_s& pl) {
-  const int D = pl.p.rank;
   const int64_t local = pl.G.local_voxels;
   const int64_t target = std::min<int64_t>(std::max<int64_t>(local / (148 * 16), 4096), 1 << 18);
-  if (pl.hist.on) {
-    const int ko = pl.hist.ko;
+  for (int fam = 0; fam < 2; ++fam) {
+    Pencil& pc = fam == 0 ? pl.hist : pl.interp;
+    if (!pc.on) continue;
+    const bool cells = fam == 1;
+    size_boxes(pl, pc, cells);
+    // dim-0 chunks must stay multiples of the box rows along dim 0
+    const int64_t quantum = pc.ko == 1 ? pc.r1 : (pc.ko == 2 ? pc.r2 : 1);
+    std::vector<int32_t>& units = fam == 0 ? pl.hist_units : pl.interp_units;
+    std::vector<int64_t>& vox = fam == 0 ? pl.hist_vox : pl.interp_vox;
+    const int ko = pc.ko;
     int64_t idx[kMaxRank] = {0};
-    idx[0] = pl.info.count_row_begin;
-    for (int j = 1; j < ko; ++j) idx[j] = 0;
-    while (true) {
-      int64_t per_row = pl.hist.P;
-      for (int j = 1; j < ko; ++j) {
-        const TileParts tp = tile_parts(pl.d[j], idx[j]);
-        per_row *= tp.support_end() - tp.support_begin();
-      }
-      const TileParts t0 = tile_parts(pl.d[0], idx[0]);
-      const int64_t ra = std::max(t0.support_begin(), pl.info.row_begin);
-      const int64_t re = std::min(t0.support_end(), pl.info.row_end);
-      if (re > ra) push_unit(pl.hist_units, pl.hist_vox, idx, ko, ra, re, per_row, target);
-      int j = ko - 1;
-      while (j >= 1 && ++idx[j] == pl.d[j].g) idx[j--] = 0;
-      if (j == 0 && ++idx[0] == pl.info.count_row_end) break;
+    int64_t lo0, hi0;
+    if (cells) {
+      lo0 = cell_of(pl.d[0], pl.info.row_begin);
+      hi0 = cell_of(pl.d[0], pl.info.row_end - 1) + 1;
+    } else {
+      lo0 = pl.info.count_row_begin;
+      hi0 = pl.info.count_row_end;
     }
-  }
-  if (pl.interp.on) {
-    const int ko = pl.interp.ko;
-    int64_t idx[kMaxRank] = {0};
-    const int64_t c0 = cell_of(pl.d[0], pl.info.row_begin);
-    const int64_t c1 = cell_of(pl.d[0], pl.info.row_end - 1) + 1;
-    idx[0] = c0;
+    idx[0] = lo0;
+    const int64_t lim_j = cells ? -1 : 0;  // cells: g-1 per dim, tiles: g
     while (true) {
-      int64_t per_row = pl.interp.P;
+      int64_t per_row = pc.P;
       bool empty = false;
       for (int j = 1; j < ko; ++j) {
         int64_t a, e;
-        cell_range(pl.d[j], idx[j], &a, &e);
+        if (cells) {
+          cell_range(pl.d[j], idx[j], &a, &e);
+        } else {
+          const TileParts tp = tile_parts(pl.d[j], idx[j]);
+          a = tp.support_begin();
+          e = tp.support_end();
+        }
         per_row *= e - a;
         empty = empty || e <= a;
       }
       int64_t a0, e0;
-      cell_range(pl.d[0], idx[0], &a0, &e0);
+      if (cells) {
+        cell_range(pl.d[0], idx[0], &a0, &e0);
+      } else {
+        const TileParts t0 = tile_parts(pl.d[0], idx[0]);
+        a0 = t0.support_begin();
+        e0 = t0.support_end();
+      }
       const int64_t ra = std::max(a0, pl.info.row_begin), re = std::min(e0, pl.info.row_end);
-      if (!empty && re > ra) push_unit(pl.interp_units, pl.interp_vox, idx, ko, ra, re, per_row, target);
+      if (!empty && re > ra) push_unit(units, vox, idx, ko, ra, re, per_row, target, quantum);
       int j = ko - 1;
-      while (j >= 1 && ++idx[j] == pl.d[j].g - 1) idx[j--] = 0;
-      if (j == 0 && ++idx[0] == c1) break;
+      while (j >= 1 && ++idx[j] == pl.d[j].g + lim_j) idx[j--] = 0;
+      if (j == 0 && ++idx[0] == hi0) break;
     }
   }
-  (void)D;
 }
 
 // Contiguous, voxel-balanced unit ranges per CTA.
@@ -279,6 +367,60 @@ std::vector<int32_t> balance(const std::vector<int64_t>& vox, int grid) {
   while (c <= grid) cta[c++] = (int32_t)vox.size();
   cta[grid] = (int32_t)vox.size();
   return cta;
+}
+
+// ---- TMA tensor view of the (slab) input --------------------------------
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<EncodeTiledFn>(p);
+  }();
+  return fn;
+}
+
+// [outer dims KO-1..0 with strides][P/width][width], box [R2 x R1 rows][P].
+int tensor_map(mclahe_plan_s* pl, int fam, const void* in) {
+  if (pl->map_ptr[fam] == in) return MCLAHE_OK;
+  const Pencil& c = fam == 0 ? pl->hist : pl->interp;
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return fail(MCLAHE_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[5], strides[5];
+  cuuint32_t box[5], es[5];
+  int r = 0;
+  dims[r] = (cuuint64_t)c.width;
+  box[r] = (cuuint32_t)c.width;
+  ++r;
+  if (c.tma_rank - c.ko == 2) {
+    dims[r] = (cuuint64_t)(c.P / c.width);
+    strides[r - 1] = (cuuint64_t)c.width * 4;
+    box[r] = (cuuint32_t)(c.P / c.width);
+    ++r;
+  }
+  for (int j = c.ko - 1; j >= 0; --j) {
+    dims[r] = (cuuint64_t)(j == 0 ? pl->info.row_end - pl->info.row_begin : pl->d[j].s);
+    strides[r - 1] = (cuuint64_t)pl->G.vstride[j] * 4;
+    box[r] = (cuuint32_t)(j == c.ko - 1 ? c.r1 : (j == c.ko - 2 ? c.r2 : 1));
+    ++r;
+  }
+  for (int i = 0; i < r; ++i) es[i] = 1;
+  const CUresult res = enc(&pl->map[fam], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, (cuuint32_t)r,
+                           const_cast<void*>(in), dims, strides, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (res != CUDA_SUCCESS)
+    return fail(MCLAHE_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)res) + ")");
+  pl->map_ptr[fam] = in;
+  return MCLAHE_OK;
 }
 
 int plan_describe(const mclahe_params_t* params, int64_t row_begin, int64_t row_end,
@@ -327,7 +469,9 @@ int plan_describe(const mclahe_params_t* params, int64_t row_begin, int64_t row_
   I.off_counts = align_up(I.off_tile_range + (params->adaptive ? win_tiles * 16 : 16), 256);
   I.off_tparams = align_up(I.off_counts + win_tiles * n * 4, 256);
   I.off_lut = align_up(I.off_tparams + (params->adaptive ? win_tiles : 1) * tp_size, 256);
-  I.workspace_bytes = align_up(I.off_lut + win_tiles * n * 4, 256);
+  I.off_thr = align_up(I.off_lut + win_tiles * n * 4, 256);
+  I.workspace_bytes =
+      align_up(I.off_thr + (pl->f32() ? (params->adaptive ? win_tiles : 1) * n * 4 : 0), 256);
 
   KGeom& G = pl->G;
   std::memset(&G, 0, sizeof G);
@@ -373,11 +517,24 @@ WS ws_view(const mclahe_plan_s* pl, void* ws) {
   W.counts = reinterpret_cast<uint32_t*>(b + pl->info.off_counts);
   W.tparams = b + pl->info.off_tparams;
   W.lut = reinterpret_cast<float*>(b + pl->info.off_lut);
+  W.thr = reinterpret_cast<float*>(b + pl->info.off_thr);
   return W;
 }
 
 int64_t range_smem(const mclahe_plan_s* pl) {
-  return kPipeBytes + pl->hist.nst * pl->hist.stage_rows * pl->hist.P * 4 + pl->hist.gtr * 8;
+  return kPipeBytes + pl->hist.nst * pl->hist.stage_stride * 4 + pl->hist.gtr * 8;
+}
+
+// Raises a kernel's dynamic shared-memory cap to the device opt-in maximum
+// minus its static shared memory.
+template <typename F>
+cudaError_t raise_smem_cap(F f, int optin) {
+  cudaFuncAttributes fa;
+  cudaError_t e = cudaFuncGetAttributes(&fa, reinterpret_cast<const void*>(f));
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(reinterpret_cast<const void*>(f),
+                              cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              optin - (int)fa.sharedSizeBytes);
 }
 
 int device_init(mclahe_plan_s* pl) {
@@ -386,17 +543,21 @@ int device_init(mclahe_plan_s* pl) {
   if (pl->device == dev) return MCLAHE_OK;
   if (pl->device >= 0) return fail(MCLAHE_ERR_CUDA, "plan used on a different device");
   MG_CUDA(cudaDeviceGetAttribute(&pl->sms, cudaDevAttrMultiProcessorCount, dev));
+  // Shared-memory caps are per kernel, not per plan: raise them to the
+  // device's opt-in maximum once so plans sharing an instantiation never
+  // undercut each other (occupancy still follows each launch's real size).
+  int max_smem = 0;
+  MG_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
   const bool A = pl->p.adaptive != 0;
   std::vector<int32_t> hist_cta, interp_cta;
   if (pl->hist.on) {
     int occ = 0;
     HistFn f = hist_fn(pl->hist.ko, A);
-    MG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl->hist.smem));
+    MG_CUDA(raise_smem_cap(f, max_smem));
     MG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f, kPencilThreads, pl->hist.smem));
     if (A) {
       RangeFn r = range_fn(pl->hist.ko);
-      MG_CUDA(cudaFuncSetAttribute(r, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)range_smem(pl)));
+      MG_CUDA(raise_smem_cap(r, max_smem));
     }
     pl->hist_grid = (int)std::max<int64_t>(
         1, std::min<int64_t>((int64_t)pl->hist_vox.size(), (int64_t)std::max(occ, 1) * pl->sms));
@@ -405,7 +566,7 @@ int device_init(mclahe_plan_s* pl) {
   if (pl->interp.on) {
     int occ = 0;
     InterpFn f = interp_fn(pl->interp.ko, pl->interp.kt, A);
-    MG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl->interp.smem));
+    MG_CUDA(raise_smem_cap(f, max_smem));
     MG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f, kPencilThreads, pl->interp.smem));
     pl->interp_grid = (int)std::max<int64_t>(
         1, std::min<int64_t>((int64_t)pl->interp_vox.size(), (int64_t)std::max(occ, 1) * pl->sms));
@@ -433,11 +594,9 @@ int device_init(mclahe_plan_s* pl) {
   pl->map_block = warps * 32;
   pl->map_smem = (int64_t)warps * n * 8;
   if (pl->f32())
-    MG_CUDA(cudaFuncSetAttribute(k_mappings<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)pl->map_smem));
+    MG_CUDA(raise_smem_cap(k_mappings<float>, max_smem));
   else
-    MG_CUDA(cudaFuncSetAttribute(k_mappings<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)pl->map_smem));
+    MG_CUDA(raise_smem_cap(k_mappings<double>, max_smem));
   const int64_t tiles = pl->G.win_tiles;
   pl->map_grid = (int)std::max<int64_t>(1, std::min<int64_t>((tiles + warps - 1) / warps, 1 << 20));
   pl->device = dev;
@@ -474,7 +633,9 @@ int do_range(mclahe_plan_s* pl, const void* in, void* ws, cudaStream_t st) {
   if (pl->hist.on) {
     const KGeom G = pencil_geom(*pl, pl->hist);
     RangeFn f = range_fn(pl->hist.ko);
-    f<<<pl->hist_grid, kPencilThreads, range_smem(pl), st>>>(G, static_cast<const float*>(in),
+    int rc = tensor_map(pl, 0, in);
+    if (rc) return rc;
+    f<<<pl->hist_grid, kPencilThreads, range_smem(pl), st>>>(G, pl->map[0], static_cast<const float*>(in),
                                                     pl->d_tables + pl->off_hist_units,
                                                     pl->d_tables + pl->off_hist_cta, W);
     MG_LAUNCHED();
@@ -496,6 +657,12 @@ int do_params(mclahe_plan_s* pl, void* ws, cudaStream_t st) {
   if (pl->f32()) k_params<float><<<grid, 128, 0, st>>>(pl->G, W);
   else k_params<double><<<grid, 128, 0, st>>>(pl->G, W);
   MG_LAUNCHED();
+  if (pl->f32()) {
+    const int64_t total = n * pl->p.n_bins;
+    const int tg = (int)std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 8192));
+    k_thresholds<<<tg, 256, 0, st>>>(pl->G, W);
+    MG_LAUNCHED();
+  }
   return MCLAHE_OK;
 }
 
@@ -505,7 +672,9 @@ int do_hist(mclahe_plan_s* pl, const void* in, void* ws, cudaStream_t st) {
   if (pl->hist.on) {
     const KGeom G = pencil_geom(*pl, pl->hist);
     HistFn f = hist_fn(pl->hist.ko, A);
-    f<<<pl->hist_grid, kPencilThreads, pl->hist.smem, st>>>(G, static_cast<const float*>(in),
+    int rc = tensor_map(pl, 0, in);
+    if (rc) return rc;
+    f<<<pl->hist_grid, kPencilThreads, pl->hist.smem, st>>>(G, pl->map[0], static_cast<const float*>(in),
                                                  pl->d_tables + pl->off_hist_units,
                                                  pl->d_tables + pl->off_hist_cta, W);
     MG_LAUNCHED();
@@ -548,7 +717,9 @@ int do_interp(mclahe_plan_s* pl, const void* in, void* out, void* ws, cudaStream
   if (pl->interp.on) {
     const KGeom G = pencil_geom(*pl, pl->interp);
     InterpFn f = interp_fn(pl->interp.ko, pl->interp.kt, A);
-    f<<<pl->interp_grid, kPencilThreads, pl->interp.smem, st>>>(G, static_cast<const float*>(in),
+    int rc = tensor_map(pl, 1, in);
+    if (rc) return rc;
+    f<<<pl->interp_grid, kPencilThreads, pl->interp.smem, st>>>(G, pl->map[1], static_cast<const float*>(in),
                                                      static_cast<float*>(out),
                                                      pl->d_tables + pl->off_interp_units,
                                                      pl->d_tables + pl->off_interp_cta, W);
@@ -840,13 +1011,20 @@ int mclahe_debug_bin_index(int32_t dtype, const void* values, int64_t n, double 
   if (n <= 0) return MCLAHE_OK;
   const int grid = (int)std::min<int64_t>((n + 255) / 256, 4096);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (dtype == MCLAHE_F32)
+  if (dtype == MCLAHE_F32) {
+    float* thr = nullptr;
+    MG_CUDA(cudaMallocAsync(&thr, (size_t)n_bins * sizeof(float), st));
+    k_debug_thresholds<<<(int)((n_bins + 127) / 128), 128, 0, st>>>(lo, hi, (int)n_bins, thr);
+    MG_LAUNCHED();
     k_debug_bins<float><<<grid, 256, 0, st>>>(static_cast<const float*>(values), n, lo, hi,
-                                              (int)n_bins, out);
-  else
+                                              (int)n_bins, thr, out);
+    MG_LAUNCHED();
+    MG_CUDA(cudaFreeAsync(thr, st));
+  } else {
     k_debug_bins<double><<<grid, 256, 0, st>>>(static_cast<const double*>(values), n, lo, hi,
-                                               (int)n_bins, out);
-  MG_LAUNCHED();
+                                               (int)n_bins, nullptr, out);
+    MG_LAUNCHED();
+  }
   return MCLAHE_OK;
 }
 
