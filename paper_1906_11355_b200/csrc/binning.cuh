@@ -111,7 +111,7 @@ __device__ __forceinline__ int bin_of(float v, const TileParam<float>& tp, const
     return bin_exact(static_cast<double>(v), static_cast<double>(tp.lo),
                      static_cast<double>(tp.hi), n);
   const int k = __float2int_rn(y);
-  return v >= __ldg(thr + k) ? k : k - 1;
+  return v >= thr[k] ? k : k - 1;  // thr: shared (pencil kernels) or global memory
 }
 
 __device__ __forceinline__ int bin_of(double v, const TileParam<double>& tp, const double*, int n,
@@ -153,6 +153,90 @@ __device__ inline float bin_threshold(double lo, double hi, int n, int k) {
     else a = m;
   }
   return unkey(b);
+}
+
+// ---- packed (f32x2) guarded binning for the pencil kernels ----------------
+// Same bound as bin_of, two voxels per FADD2/FMUL2.  Out-of-range y is
+// clamped on the integer side (the magic-number floor is exact for
+// |y| < 2^22 and monotone beyond, so clamping k is still the reference's
+// clamp).  Near an integer the edge table decides (k in [1, n-1]).
+// lc = {lo, c}; degenerate tiles use lc = kDegenerateLC (y == 0.5 exactly,
+// constant 0.5 LUT), pathological ranges (make_tile_param lim < 0) are
+// routed by the caller to bin_search.
+typedef unsigned long long u64;
+
+__device__ __forceinline__ u64 pk2(float x, float y) {
+  u64 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(x), "f"(y));
+  return r;
+}
+__device__ __forceinline__ void upk2(u64 r, float& x, float& y) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(x), "=f"(y) : "l"(r));
+}
+__device__ __forceinline__ u64 sub2(u64 a, u64 b) {
+  u64 d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ u64 mul2(u64 a, u64 b) {
+  u64 d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ u64 add2rm(u64 a, u64 b) {
+  u64 d;
+  asm("add.rm.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+
+constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23
+constexpr int kMagicBits = 0x4B400000;
+
+__device__ __forceinline__ float2 degenerate_lc() {
+  return make_float2(-4.2535295865117308e37f /* -2^125 */, 1.1754943508222875e-38f /* 2^-126 */);
+}
+
+__device__ __forceinline__ float guard_lim(int n) { return 0.5f - (float)n * 2.5e-7f; }
+
+__device__ __forceinline__ int near_fix(float v, int k, float d, const float* th, int n) {
+  int kk = k + (d > 0.0f ? 1 : 0);
+  kk = min(max(kk, 1), n - 1);
+  return v >= th[kk] ? kk : kk - 1;
+}
+
+// Bins of two voxels (packed in V = {v0, v1}) against one tile.
+__device__ __forceinline__ void bins2(u64 V, float v0, float v1, float2 lc, const float* th,
+                                      int n, float lim, int& b0, int& b1) {
+  const u64 y = mul2(sub2(V, pk2(lc.x, lc.x)), pk2(lc.y, lc.y));
+  const u64 M = pk2(kMagic, kMagic);
+  const u64 t = add2rm(y, M);
+  const u64 d = sub2(sub2(y, sub2(t, M)), pk2(0.5f, 0.5f));
+  float t0, t1, d0, d1;
+  upk2(t, t0, t1);
+  upk2(d, d0, d1);
+  b0 = min(max(__float_as_int(t0) - kMagicBits, 0), n - 1);
+  b1 = min(max(__float_as_int(t1) - kMagicBits, 0), n - 1);
+  if (!(fabsf(d0) < lim)) b0 = near_fix(v0, b0, d0, th, n);
+  if (!(fabsf(d1) < lim)) b1 = near_fix(v1, b1, d1, th, n);
+}
+
+// Exact bin from the edge table alone (binary search over thr[1..n-1]);
+// used for ranges the float guard does not cover.
+__device__ __forceinline__ int bin_search(float v, const float* th, int n) {
+  int lo = 0, hi = n - 1;  // answer in [lo, hi]
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (v >= th[mid]) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+// {lo, c} table entry for a tile (NaN c marks a pathological range).
+__device__ __forceinline__ float2 tile_lc(const TileParam<float>& tp) {
+  if (tp_degenerate(tp.lim)) return degenerate_lc();
+  if (tp.lim < 0.0f) return make_float2(tp.lo, __int_as_float(0x7fc00000));
+  return make_float2(tp.lo, tp.c);
 }
 
 #endif  // __CUDACC__

@@ -28,8 +28,10 @@ constexpr int kUnitInts = 10;      // unit record: [0..7] tile/cell per outer di
 constexpr int kMaxOuterDims = 5;   // pencil kernels: KO in [1, 5]
 constexpr int kMaxRuns = 16;       // runs gathered into one stage
 constexpr int kMaxStages = 6;
-constexpr int kConsumers = 256;    // 8 consumer warps
+constexpr int kConsumers = 256;    // 8 consumer warps (K2 kernels)
 constexpr int kPencilThreads = kConsumers + 32;  // + producer warp
+constexpr int kConsumersBlend = 512;  // 16 consumer warps (K4: one CTA per SM)
+constexpr int kBlendThreads = kConsumersBlend + 32;
 
 // Kernel-side geometry (passed by value).
 struct KGeom {
@@ -103,7 +105,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n"
       "MG_WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 1000000;\n\t"
       "@!p bra MG_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
@@ -119,8 +121,9 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 __device__ __forceinline__ void fence_barrier_init() {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
+template <int NC = kConsumers>
 __device__ __forceinline__ void consumers_sync() {
-  asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory");
+  asm volatile("bar.sync 1, %0;" ::"n"(NC) : "memory");
 }
 
 // One pipeline stage = one TMA box of one unit: R2 x R1 rows of P floats.
@@ -154,11 +157,11 @@ __device__ __forceinline__ size_t pipe_bytes() { return (sizeof(Pipe) + 127) & ~
 
 // Initialises the barriers (thread 0) -- call before the role split, then
 // __syncthreads().
-__device__ __forceinline__ void pipe_init(Pipe& pp, int nst) {
+__device__ __forceinline__ void pipe_init(Pipe& pp, int nst, int consumer_warps = kConsumers / 32) {
   if (threadIdx.x == 0) {
     for (int s = 0; s < nst; ++s) {
       mbar_init(&pp.full[s], 1);
-      mbar_init(&pp.empty[s], kConsumers / 32);
+      mbar_init(&pp.empty[s], consumer_warps);
     }
     fence_barrier_init();
   }
@@ -204,7 +207,17 @@ __device__ __forceinline__ void tma_load(void* dst, const CUtensorMap* map, int 
 // every unit extent along dims KO-1 / KO-2 a multiple of R1 / R2) and issues
 // one TMA box load per stage.  CELLS selects interpolation-cell boxes (K4)
 // instead of tile-support boxes (K2).
-template <int KO, bool CELLS>
+// Is the multiplicity of tile parts p constant over [x, x + r)?  (no
+// interval end strictly inside the range)
+__device__ __forceinline__ bool parts_uniform(const TileParts& p, int64_t x, int64_t r) {
+  const int64_t e[6] = {p.id_a, p.id_e, p.lo_a, p.lo_e, p.hi_a, p.hi_e};
+  bool u = true;
+#pragma unroll
+  for (int i = 0; i < 6; ++i) u = u && !(e[i] > x && e[i] < x + r);
+  return u;
+}
+
+template <int KO, bool CELLS, bool WEIGHTS = !CELLS>
 __device__ __noinline__ void pipe_produce(const KGeom& G, const CUtensorMap* map,
                                           const int32_t* __restrict__ units, int u0, int u1,
                                           Pipe& pp, float* bufs) {
@@ -257,7 +270,7 @@ __device__ __noinline__ void pipe_produce(const KGeom& G, const CUtensorMap* map
       for (int j = KO - 3; j >= 0; --j) {
         xf[j] = (int32_t)(B.a[j] + rem % B.ext[j]);
         rem /= B.ext[j];
-        if (!CELLS) wfix *= B.parts[j].weight(xf[j]);
+        if (WEIGHTS) wfix *= B.parts[j].weight(xf[j]);
       }
 #pragma unroll 1
       for (int i2 = 0; i2 < n2; ++i2) {
@@ -279,25 +292,12 @@ __device__ __noinline__ void pipe_produce(const KGeom& G, const CUtensorMap* map
           }
 #pragma unroll 1
           for (int j = 0; j < KO; ++j) S.cell[j] = U[j];
-          if (!CELLS) {
+          if (WEIGHTS) {
             S.p1 = B.parts[KO - 1];
             if (KO >= 2) S.p2 = B.parts[KO - 2];
-            // uniform multiplicity over the box?  (ends of each box range)
-            const int w1a = S.p1.weight(x1), w1b = S.p1.weight(x1 + R1 - 1);
-            int w2a = 1, w2b = 1;
-            if (KO >= 2) {
-              w2a = S.p2.weight(x2);
-              w2b = S.p2.weight(x2 + R2 - 1);
-            }
-            bool uni = w1a == w1b && w2a == w2b;
-            if (uni) {  // a range of equal end weights can still dip in between: check all
-#pragma unroll 1
-              for (int r = 1; r < R1 - 1 && uni; ++r) uni = S.p1.weight(x1 + r) == w1a;
-#pragma unroll 1
-              for (int r = 1; r < R2 - 1 && uni; ++r) uni = S.p2.weight(x2 + r) == w2a;
-            }
+            const bool uni = parts_uniform(S.p1, x1, R1) && (KO < 2 || parts_uniform(S.p2, x2, R2));
             S.wuni = uni ? 1 : 0;
-            S.wfix = uni ? wfix * w1a * w2a : wfix;
+            S.wfix = uni ? wfix * S.p1.weight(x1) * (KO >= 2 ? S.p2.weight(x2) : 1) : wfix;
           }
           // TMA coordinates, innermost first: trailing block, then dims KO-1 .. 0
           int c[6];

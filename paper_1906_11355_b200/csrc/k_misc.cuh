@@ -301,9 +301,8 @@ __global__ void k_thresholds(const KGeom G, WS W) {
     const int64_t t = i / n;
     const int k = (int)(i - t * n);
     const TileParam<float> p = tp[t];
-    W.thr[i] = (k == 0 || tp_degenerate(p.lim) || p.lim < 0.0f)
-                   ? -INFINITY
-                   : bin_threshold((double)p.lo, (double)p.hi, n, k);
+    W.thr[i] = (k == 0 || tp_degenerate(p.lim)) ? -INFINITY
+                                                : bin_threshold((double)p.lo, (double)p.hi, n, k);
   }
 }
 

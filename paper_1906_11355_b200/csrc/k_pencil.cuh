@@ -56,7 +56,8 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
   __syncthreads();
   const int u0 = cta_units[blockIdx.x], u1 = cta_units[blockIdx.x + 1];
   if (threadIdx.x >= kConsumers) {
-    if (threadIdx.x == kConsumers) pipe_produce<KO, false>(G, &tmap, units, u0, u1, *P.pipe, P.bufs);
+    if (threadIdx.x == kConsumers)
+      pipe_produce<KO, false, false>(G, &tmap, units, u0, u1, *P.pipe, P.bufs);
     return;
   }
   const int tid = threadIdx.x;
@@ -138,14 +139,15 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
 template <int KO, bool ADAPT>
 __global__ void __launch_bounds__(kPencilThreads, 3)
     k_hist_pencil(const __grid_constant__ KGeom G, const __grid_constant__ CUtensorMap tmap,
-                   const float* __restrict__ in, const int32_t* __restrict__ units,
+                  const float* __restrict__ in, const int32_t* __restrict__ units,
                   const int32_t* __restrict__ cta_units, WS W) {
   extern __shared__ __align__(128) unsigned char smem[];
   const PencilSmem P = pencil_smem(G, smem);
   const int n = G.n_bins;
   uint32_t* hist = reinterpret_cast<uint32_t*>(P.tail);  // [gtr][n]
-  TileParam<float>* rng =
-      reinterpret_cast<TileParam<float>*>(P.tail + ((G.gtr * n * 4 + 15) & ~15LL));
+  float2* lcS = reinterpret_cast<float2*>(P.tail + ((G.gtr * n * 4 + 15) & ~15LL));  // [gtr]
+  // bin-edge tables of the pencil's tiles (adaptive) or of the global range
+  float* thrS = reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(lcS) + G.gtr * 16);
   const TileParam<float>* tparams = reinterpret_cast<const TileParam<float>*>(W.tparams);
   const TileParam<float> g0 = tparams[0];
   if (!ADAPT && tp_degenerate(g0.lim)) return;  // constant image: every mapping is 0.5
@@ -156,7 +158,7 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
     if (threadIdx.x == kConsumers) pipe_produce<KO, false>(G, &tmap, units, u0, u1, *P.pipe, P.bufs);
     return;
   }
-  const float nm05 = (float)n - 0.5f;
+  const float lim = guard_lim(n);
   const int tid = threadIdx.x;
   const int slot = tid / G.tpr;
   const int64_t e0 = (int64_t)(tid % G.tpr) * 4;
@@ -165,7 +167,11 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
 #pragma unroll
   for (int i = 0; i < 4; ++i) trailing_tile(G, e0 + i, &trt[i], &trw[i]);
   const int64_t stage_elems = G.stage_stride;
+  const float2 glc = tile_lc(g0);
   int64_t cur = -1;
+  bool patho = !ADAPT && isnan(glc.y);  // a range the float guard does not cover
+  __shared__ int s_bad;
+  const float kDegC = degenerate_lc().y;
 
   uint32_t it = 0;
   while (true) {
@@ -176,30 +182,37 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
     const int64_t key = S.key;
     if (key != cur) {
       consumers_sync();
+      if (tid == 0) s_bad = 0;
       if (cur >= 0) {
         uint32_t* dst = W.counts + cur * n;
         for (int64_t k = tid; k < G.gtr * n; k += kConsumers) {
           const uint32_t c = hist[k];
           if (c) atomicAdd(dst + k, c);
         }
-        consumers_sync();
       }
-      for (int64_t k = tid; k < G.gtr * n; k += kConsumers) hist[k] = 0;
-      if (ADAPT)
-        for (int64_t t = tid; t < G.gtr; t += kConsumers) rng[t] = tparams[key + t];
       consumers_sync();
+      for (int64_t k = tid; k < G.gtr * n; k += kConsumers) hist[k] = 0;
+      if (ADAPT) {
+        for (int64_t t = tid; t < G.gtr; t += kConsumers) {
+          const float2 lc = tile_lc(tparams[key + t]);
+          lcS[t] = lc;
+          if (isnan(lc.y)) s_bad = 1;
+        }
+        for (int64_t k = tid; k < G.gtr * n; k += kConsumers) thrS[k] = W.thr[key * n + k];
+      } else if (cur < 0) {
+        for (int k = tid; k < n; k += kConsumers) thrS[k] = W.thr[k];
+      }
+      consumers_sync();
+      if (ADAPT) patho = s_bad != 0;
       cur = key;
     }
     const int rows = G.stage_rows;
     const float* buf = P.bufs + s * stage_elems;
-    const bool wuni = S.wuni != 0;
-    const int32_t wfix = S.wfix;
-    for (int q0 = 0; q0 < rows; q0 += G.rpi) {  // trip count uniform over the warp
-      const int q = q0 + slot;
-      const bool ok = lane_on && q < rows;
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      uint32_t wrow = 0;
-      if (ok) {
+    if (lane_on) {
+      const bool wuni = S.wuni != 0;
+      const int32_t wfix = S.wfix;
+      for (int q = slot; q < rows; q += G.rpi) {
+        uint32_t wrow;
         if (wuni) {
           wrow = (uint32_t)wfix;
         } else {
@@ -208,25 +221,50 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
           if (KO >= 2) w *= S.p2.weight(S.x[KO >= 2 ? KO - 2 : 0] + r2);
           wrow = (uint32_t)w;
         }
-        v = *reinterpret_cast<const float4*>(buf + q * G.P + e0);
-      }
-      const float a[4] = {v.x, v.y, v.z, v.w};
+        const float4 v = *reinterpret_cast<const float4*>(buf + q * G.P + e0);
+        int b[4];
+        const float2 l0 = ADAPT ? lcS[trt[0]] : glc, l1 = ADAPT ? lcS[trt[1]] : glc;
+        const float2 l2 = ADAPT ? lcS[trt[2]] : glc, l3 = ADAPT ? lcS[trt[3]] : glc;
+        if (!patho) {
+          if (!ADAPT || (trt[0] == trt[1] && trt[2] == trt[3])) {
+            bins2(pk2(v.x, v.y), v.x, v.y, l0, thrS + (ADAPT ? trt[0] * n : 0), n, lim, b[0], b[1]);
+            bins2(pk2(v.z, v.w), v.z, v.w, l2, thrS + (ADAPT ? trt[2] * n : 0), n, lim, b[2], b[3]);
+          } else {  // pairs straddle a tile boundary: evaluate each against its own tile
+            int dmy;
+            bins2(pk2(v.x, v.x), v.x, v.x, l0, thrS + trt[0] * n, n, lim, b[0], dmy);
+            bins2(pk2(v.y, v.y), v.y, v.y, l1, thrS + trt[1] * n, n, lim, b[1], dmy);
+            bins2(pk2(v.z, v.z), v.z, v.z, l2, thrS + trt[2] * n, n, lim, b[2], dmy);
+            bins2(pk2(v.w, v.w), v.w, v.w, l3, thrS + trt[3] * n, n, lim, b[3], dmy);
+          }
+        } else {
+          const float a4[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        unsigned long long k64 = ~0ull - tid;  // unique: never merges
-        int cell = -1;
-        uint32_t wgt = 0;
-        if (ok) {
-          const TileParam<float> tp = ADAPT ? rng[trt[i]] : g0;
-          if (!tp_degenerate(tp.lim)) {
-            cell = trt[i] * n + bin_of(a[i], tp, W.thr + (ADAPT ? (cur + trt[i]) * n : 0), n, nm05);
-            wgt = wrow * (uint32_t)trw[i];
-            k64 = ((unsigned long long)cell << 16) | wgt;
+          for (int i = 0; i < 4; ++i) {
+            const float2 lc = ADAPT ? lcS[trt[i]] : glc;
+            const float* th = thrS + (ADAPT ? trt[i] * n : 0);
+            if (isnan(lc.y)) b[i] = bin_search(a4[i], th, n);
+            else bins2(pk2(a4[i], a4[i]), a4[i], a4[i], lc, th, n, lim, b[i], b[i]);
           }
         }
-        const unsigned peers = __match_any_sync(0xffffffffu, k64);
-        if (cell >= 0 && (__ffs(peers) - 1) == (tid & 31))
-          atomicAdd(&hist[cell], wgt * (uint32_t)__popc(peers));
+        // skip degenerate tiles (no histogram), merge equal neighbours, one
+        // shared atomic per distinct (tile, bin)
+        const float cs[4] = {l0.y, l1.y, l2.y, l3.y};
+        int kprev = -1;
+        uint32_t acc = 0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const bool live = !ADAPT || cs[i] != kDegC;
+          const int key2 = live ? trt[i] * n + b[i] : -2 - i;
+          const uint32_t w = wrow * (uint32_t)trw[i];
+          if (key2 == kprev) {
+            acc += w;
+          } else {
+            if (kprev >= 0) atomicAdd(&hist[kprev], acc);
+            kprev = key2;
+            acc = w;
+          }
+        }
+        if (kprev >= 0) atomicAdd(&hist[kprev], acc);
       }
     }
     __syncwarp();
@@ -249,7 +287,7 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
 // corner tiles and weights are registers; outer weights come per row from
 // the exact half-integer distances (d_lo = twice_dlo / 2).  FP32 sum.
 template <int KO, int KT, bool ADAPT>
-__global__ void __launch_bounds__(kPencilThreads, 2)
+__global__ void __launch_bounds__(kBlendThreads, 1)
     k_interp_pencil(const __grid_constant__ KGeom G, const __grid_constant__ CUtensorMap tmap,
                     const float* __restrict__ in, float* __restrict__ out,
                     const int32_t* __restrict__ units, const int32_t* __restrict__ cta_units, WS W) {
@@ -260,22 +298,26 @@ __global__ void __launch_bounds__(kPencilThreads, 2)
   const int n = G.n_bins;
   const int64_t gtr = G.gtr;
   float* lutS = reinterpret_cast<float*>(P.tail);  // [NCO][gtr][n]
-  TileParam<float>* rngS =
-      reinterpret_cast<TileParam<float>*>(P.tail + ((NCO * gtr * n * 4 + 15) & ~15LL));
-  pipe_init(*P.pipe, G.nst);
+  float* thrS = lutS + NCO * gtr * n;  // bin-edge tables: [NCO][gtr][n] (adaptive) or [n]
+  float2* lcS = reinterpret_cast<float2*>(  // [NCO][gtr] {lo, c} (adaptive)
+      P.tail + (((ADAPT ? 2 * NCO * gtr * n : NCO * gtr * n + n) * 4 + 15) & ~15LL));
+  __shared__ int s_bad;
+  pipe_init(*P.pipe, G.nst, kConsumersBlend / 32);
   __syncthreads();
   const int u0 = cta_units[blockIdx.x], u1 = cta_units[blockIdx.x + 1];
-  if (threadIdx.x >= kConsumers) {
-    if (threadIdx.x == kConsumers) pipe_produce<KO, true>(G, &tmap, units, u0, u1, *P.pipe, P.bufs);
+  if (threadIdx.x >= kConsumersBlend) {
+    if (threadIdx.x == kConsumersBlend)
+      pipe_produce<KO, true>(G, &tmap, units, u0, u1, *P.pipe, P.bufs);
     return;
   }
   const TileParam<float>* tparams = reinterpret_cast<const TileParam<float>*>(W.tparams);
-  const TileParam<float> g0 = tparams[0];
-  const float nm05 = (float)n - 0.5f;
+  const float2 glc = tile_lc(tparams[0]);
+  const float lim = guard_lim(n);
+  bool patho = !ADAPT && isnan(glc.y);  // a range the float guard does not cover
   const int tid = threadIdx.x;
   const int slot = tid / G.tpr;
   const int64_t e0 = (int64_t)(tid % G.tpr) * 4;
-  const bool lane_on = slot < G.rpi;
+  const bool lane_on = slot < G.rpi;  // rpi = kConsumersBlend / tpr for this kernel
 
   // The plan only picks this kernel when a thread's 4 columns share their
   // trailing cell (cell boundaries along the last dim are multiples of 4), so
@@ -314,7 +356,6 @@ __global__ void __launch_bounds__(kPencilThreads, 2)
   for (int j = 0; j < KO; ++j) inv2b[j] = 1.0f / (float)(2 * G.d[j].b);
 
   const int64_t stage_elems = G.stage_stride;
-  __shared__ int64_t s_of[NCO];  // window tile offset of each outer corner
   int64_t cur = -1;
   uint32_t it = 0;
   while (true) {
@@ -324,18 +365,29 @@ __global__ void __launch_bounds__(kPencilThreads, 2)
     if (S.unit < 0) break;
     const int64_t key = S.key;
     if (key != cur) {
-      consumers_sync();
+      consumers_sync<kConsumersBlend>();
+      if (tid == 0) s_bad = 0;
+      if (!ADAPT && cur < 0)
+        for (int k = tid; k < n; k += kConsumersBlend) thrS[k] = W.thr[k];
       for (int co = 0; co < NCO; ++co) {
         int64_t of = (S.cell[0] + ((co >> (KO - 1)) & 1) - G.trow0) * G.tstride[0];
         for (int j = 1; j < KO; ++j) of += (S.cell[j] + ((co >> (KO - 1 - j)) & 1)) * G.tstride[j];
-        if (tid == 0) s_of[co] = of;
         const float4* src = reinterpret_cast<const float4*>(W.lut + of * n);
         float4* dst = reinterpret_cast<float4*>(lutS + co * gtr * n);
-        for (int64_t k = tid; k < gtr * n / 4; k += kConsumers) dst[k] = __ldg(src + k);
-        if (ADAPT)
-          for (int64_t t = tid; t < gtr; t += kConsumers) rngS[co * gtr + t] = tparams[of + t];
+        for (int64_t k = tid; k < gtr * n / 4; k += kConsumersBlend) dst[k] = __ldg(src + k);
+        if (ADAPT) {
+          const float4* ts = reinterpret_cast<const float4*>(W.thr + of * n);
+          float4* td = reinterpret_cast<float4*>(thrS + co * gtr * n);
+          for (int64_t k = tid; k < gtr * n / 4; k += kConsumersBlend) td[k] = __ldg(ts + k);
+          for (int64_t t = tid; t < gtr; t += kConsumersBlend) {
+            const float2 lc = tile_lc(tparams[of + t]);
+            lcS[co * gtr + t] = lc;
+            if (isnan(lc.y)) s_bad = 1;
+          }
+        }
       }
-      consumers_sync();
+      consumers_sync<kConsumersBlend>();
+      if (ADAPT) patho = s_bad != 0;
       cur = key;
     }
     const int rows = G.stage_rows;
@@ -363,12 +415,19 @@ __global__ void __launch_bounds__(kPencilThreads, 2)
           if (j >= KO - 2) ooff += (j == 0 ? xj - G.row0 : xj) * G.vstride[j];
         }
         const float4 v4 = *reinterpret_cast<const float4*>(buf + q * G.P + e0);
-        const float v[4] = {v4.x, v4.y, v4.z, v4.w};
+        const u64 V01 = pk2(v4.x, v4.y), V23 = pk2(v4.z, v4.w);
         float acc[4] = {0.f, 0.f, 0.f, 0.f};
         int bg[4];
         if (!ADAPT) {
-#pragma unroll
-          for (int i = 0; i < 4; ++i) bg[i] = bin_of(v[i], g0, W.thr, n, nm05);
+          if (!patho) {
+            bins2(V01, v4.x, v4.y, glc, thrS, n, lim, bg[0], bg[1]);
+            bins2(V23, v4.z, v4.w, glc, thrS, n, lim, bg[2], bg[3]);
+          } else {
+            bg[0] = bin_search(v4.x, thrS, n);
+            bg[1] = bin_search(v4.y, thrS, n);
+            bg[2] = bin_search(v4.z, thrS, n);
+            bg[3] = bin_search(v4.w, thrS, n);
+          }
         }
 #pragma unroll
         for (int co = 0; co < NCO; ++co) {
@@ -377,17 +436,27 @@ __global__ void __launch_bounds__(kPencilThreads, 2)
           for (int j = 0; j < KO; ++j) wo *= ((co >> (KO - 1 - j)) & 1) ? fo[j] : (1.0f - fo[j]);
 #pragma unroll
           for (int ct = 0; ct < NCT; ++ct) {
-            const float* L = lutS + (co * gtr + tt[ct]) * n;
+            const int tile = co * gtr + tt[ct];
+            const float* L = lutS + tile * n;
+            int b[4];
             if (ADAPT) {
-              const TileParam<float> tp = rngS[co * gtr + tt[ct]];
-              const float* thr_co = W.thr + (s_of[co] + tt[ct]) * n;
-#pragma unroll
-              for (int i = 0; i < 4; ++i)
-                acc[i] = fmaf(wo * tw[i][ct], L[bin_of(v[i], tp, thr_co, n, nm05)], acc[i]);
+              const float2 lc = lcS[tile];
+              const float* th = thrS + tile * n;
+              if (!patho || !isnan(lc.y)) {
+                bins2(V01, v4.x, v4.y, lc, th, n, lim, b[0], b[1]);
+                bins2(V23, v4.z, v4.w, lc, th, n, lim, b[2], b[3]);
+              } else {
+                b[0] = bin_search(v4.x, th, n);
+                b[1] = bin_search(v4.y, th, n);
+                b[2] = bin_search(v4.z, th, n);
+                b[3] = bin_search(v4.w, th, n);
+              }
             } else {
 #pragma unroll
-              for (int i = 0; i < 4; ++i) acc[i] = fmaf(wo * tw[i][ct], L[bg[i]], acc[i]);
+              for (int i = 0; i < 4; ++i) b[i] = bg[i];
             }
+#pragma unroll
+            for (int i = 0; i < 4; ++i) acc[i] = fmaf(wo * tw[i][ct], L[b[i]], acc[i]);
           }
         }
         float4 r;

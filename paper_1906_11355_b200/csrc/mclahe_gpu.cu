@@ -7,6 +7,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -42,12 +43,13 @@ int cuda_fail(cudaError_t e, const char* where) {
     if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
   } while (0)
 
-#define MG_LAUNCHED()                                         \
+#define MG_LAUNCHED_AT(what)                                  \
   do {                                                        \
     ++g_launches;                                             \
     cudaError_t e_ = cudaGetLastError();                      \
-    if (e_ != cudaSuccess) return cuda_fail(e_, "kernel launch"); \
+    if (e_ != cudaSuccess) return cuda_fail(e_, what);        \
   } while (0)
+#define MG_LAUNCHED() MG_LAUNCHED_AT(__func__)
 
 int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
@@ -181,7 +183,7 @@ Pencil choose_pencil(const mclahe_plan_s& pl, bool for_hist) {
     if (for_hist) {
       if (!merged) continue;
       if (c.gtr * n >= (int64_t{1} << 31) / 2) continue;
-      c.tail = align_up(c.gtr * n * 4, 16) + c.gtr * 16;
+      c.tail = align_up(c.gtr * n * 4, 16) + c.gtr * 16 + (pl.p.adaptive ? c.gtr : 1) * n * 4;
       if (c.tail > 64 * 1024) continue;
       c.stage_budget = kStageBytes;  // 3 stages, ~3 CTAs per SM
     } else {
@@ -196,12 +198,15 @@ Pencil choose_pencil(const mclahe_plan_s& pl, bool for_hist) {
         shared = (ca % 4) == 0;
       }
       if (!shared) continue;
-      c.tail = align_up((int64_t{1} << ko) * c.gtr * n * 4, 16) + (int64_t{1} << ko) * c.gtr * 16;
-      // two CTAs per SM when the LUTs allow >= 3 stages of >= 4 KB, else one
-      const int64_t two = 113 * 1024 - kPipeBytes - c.tail;
-      if (two >= 3 * 4096) c.stage_budget = std::min<int64_t>(kStageBytes, two / 3);
-      else if (224 * 1024 - kPipeBytes - c.tail >= 3 * 4096)
-        c.stage_budget = std::min<int64_t>(kStageBytes, (224 * 1024 - kPipeBytes - c.tail) / 4);
+      // LUTs (+ bin-edge tables: per tile when adaptive, one row when global)
+      // + per-tile ranges; one CTA per SM with 16 consumer warps
+      const int64_t luts = (int64_t{1} << ko) * c.gtr * n;
+      c.tail = align_up((pl.p.adaptive ? 2 * luts : luts + n) * 4, 16) +
+               (int64_t{1} << ko) * c.gtr * 16;
+      c.rpi = kConsumersBlend / c.tpr;
+      const int64_t avail = 226 * 1024 - kPipeBytes - c.tail;
+      if (avail >= 4 * 4096) c.stage_budget = std::min<int64_t>(kStageBytes, avail / 4);
+      else if (avail >= 2 * 4096) c.stage_budget = avail / 2;
       else continue;
     }
     if (c.stage_budget < c.P * 4) continue;
@@ -275,9 +280,7 @@ void size_boxes(const mclahe_plan_s& pl, Pencil& c, bool cells) {
   if (!cells) {
     c.nst = 3;
   } else {
-    const int64_t two = 113 * 1024 - kPipeBytes - c.tail;
-    c.nst = (int)std::max<int64_t>(2, std::min<int64_t>(4, (two >= 3 * stage ? two : 224 * 1024 -
-                                                             kPipeBytes - c.tail) / stage));
+    c.nst = (int)std::max<int64_t>(2, std::min<int64_t>(4, (226 * 1024 - kPipeBytes - c.tail) / stage));
   }
   c.smem = kPipeBytes + c.nst * stage + c.tail;
 }
@@ -567,7 +570,7 @@ int device_init(mclahe_plan_s* pl) {
     int occ = 0;
     InterpFn f = interp_fn(pl->interp.ko, pl->interp.kt, A);
     MG_CUDA(raise_smem_cap(f, max_smem));
-    MG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f, kPencilThreads, pl->interp.smem));
+    MG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f, kBlendThreads, pl->interp.smem));
     pl->interp_grid = (int)std::max<int64_t>(
         1, std::min<int64_t>((int64_t)pl->interp_vox.size(), (int64_t)std::max(occ, 1) * pl->sms));
     interp_cta = balance(pl->interp_vox, pl->interp_grid);
@@ -712,6 +715,9 @@ int do_map(mclahe_plan_s* pl, void* ws, const mclahe_debug_t* dbg, cudaStream_t 
 }
 
 int do_interp(mclahe_plan_s* pl, const void* in, void* out, void* ws, cudaStream_t st) {
+  if (getenv("MCLAHE_DEBUG"))
+    fprintf(stderr, "[mclahe] do_interp pencil=%d pending=%s\n", (int)pl->interp.on,
+            cudaGetErrorString(cudaPeekAtLastError()));
   WS W = ws_view(pl, ws);
   const bool A = pl->p.adaptive != 0;
   if (pl->interp.on) {
@@ -719,7 +725,18 @@ int do_interp(mclahe_plan_s* pl, const void* in, void* out, void* ws, cudaStream
     InterpFn f = interp_fn(pl->interp.ko, pl->interp.kt, A);
     int rc = tensor_map(pl, 1, in);
     if (rc) return rc;
-    f<<<pl->interp_grid, kPencilThreads, pl->interp.smem, st>>>(G, pl->map[1], static_cast<const float*>(in),
+    if (getenv("MCLAHE_DEBUG")) {
+      cudaFuncAttributes fa;
+      cudaFuncGetAttributes(&fa, reinterpret_cast<const void*>(f));
+      fprintf(stderr,
+              "[mclahe] interp ko=%d kt=%d grid=%d block=%d smem=%lld nst=%d rows=%d P=%lld regs=%d "
+              "maxthr=%d static=%zu maxdyn=%d\n",
+              pl->interp.ko, pl->interp.kt, pl->interp_grid, kBlendThreads,
+              (long long)pl->interp.smem, pl->interp.nst, pl->interp.stage_rows,
+              (long long)pl->interp.P, fa.numRegs, fa.maxThreadsPerBlock, fa.sharedSizeBytes,
+              fa.maxDynamicSharedSizeBytes);
+    }
+    f<<<pl->interp_grid, kBlendThreads, pl->interp.smem, st>>>(G, pl->map[1], static_cast<const float*>(in),
                                                      static_cast<float*>(out),
                                                      pl->d_tables + pl->off_interp_units,
                                                      pl->d_tables + pl->off_interp_cta, W);

@@ -1,0 +1,33 @@
+"""Runs the MCLAHE passes on one BASELINE config a few times (for ncu / nsight).
+
+    python tools/profile_run.py --config 4d --iters 2
+"""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="4d")
+    ap.add_argument("--iters", type=int, default=2)
+    a = ap.parse_args()
+    import torch
+    import paper_1906_11355_b200 as M
+    from paper_1906_11355_b200 import datasets
+    c = datasets.CONFIGS[a.config]
+    x = datasets.make(a.config, seed=0, device="cuda")
+    plan = M.Plan(x.shape, c["kernel"], c["n_bins"], c["clip_limit"], c["adaptive"])
+    ws = plan.new_workspace()
+    out = torch.empty_like(x)
+    for _ in range(a.iters):
+        plan.enqueue(x, out, ws)
+    plan.check(ws)
+    torch.cuda.synchronize()
+    print("ok", a.config, float(out.mean()))
+
+
+if __name__ == "__main__":
+    main()
