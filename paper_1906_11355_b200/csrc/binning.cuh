@@ -198,9 +198,10 @@ __device__ __forceinline__ float2 degenerate_lc() {
 
 __device__ __forceinline__ float guard_lim(int n) { return 0.5f - (float)n * 2.5e-7f; }
 
-__device__ __forceinline__ int near_fix(float v, int k, float d, const float* th, int n) {
-  int kk = k + (d > 0.0f ? 1 : 0);
-  kk = min(max(kk, 1), n - 1);
+// th has n+1 entries, th[0] = -inf and th[n] = +inf, so kk in [0, n] needs
+// no clamp: the reference bin is kk if v >= th[kk], else kk - 1.
+__device__ __forceinline__ int near_fix(float v, int k, float d, const float* th, int) {
+  const int kk = k + (d > 0.0f ? 1 : 0);
   return v >= th[kk] ? kk : kk - 1;
 }
 

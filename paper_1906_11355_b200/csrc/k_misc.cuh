@@ -17,7 +17,7 @@ template <typename T>
 __device__ __forceinline__ const T* thr_row(const WS& W, int64_t idx, int n);
 template <>
 __device__ __forceinline__ const float* thr_row<float>(const WS& W, int64_t idx, int n) {
-  return W.thr + idx * n;
+  return W.thr + idx * (n + 1);
 }
 template <>
 __device__ __forceinline__ const double* thr_row<double>(const WS&, int64_t, int) {
@@ -294,24 +294,26 @@ __global__ void __launch_bounds__(256) k_interp_generic(const KGeom G, const T* 
 // float whose reference bin is >= k; thr[t][0] = -inf.
 __global__ void k_thresholds(const KGeom G, WS W) {
   const TileParam<float>* tp = reinterpret_cast<const TileParam<float>*>(W.tparams);
-  const int n = G.n_bins;
-  const int64_t total = (G.adaptive ? G.win_tiles : 1) * (int64_t)n;
+  const int n = G.n_bins, n1 = n + 1;
+  const int64_t total = (G.adaptive ? G.win_tiles : 1) * (int64_t)n1;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t t = i / n;
-    const int k = (int)(i - t * n);
+    const int64_t t = i / n1;
+    const int k = (int)(i - t * n1);
     const TileParam<float> p = tp[t];
-    W.thr[i] = (k == 0 || tp_degenerate(p.lim)) ? -INFINITY
-                                                : bin_threshold((double)p.lo, (double)p.hi, n, k);
+    W.thr[i] = k == n ? INFINITY
+                      : (k == 0 || tp_degenerate(p.lim))
+                            ? -INFINITY
+                            : bin_threshold((double)p.lo, (double)p.hi, n, k);
   }
 }
 
 __global__ void k_debug_thresholds(double lo, double hi, int n, float* thr) {
   const TileParam<float> p = make_tile_param<float>(lo, hi, n);
-  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x)
-    thr[k] = (k == 0 || tp_degenerate(p.lim) || p.lim < 0.0f)
-                 ? -INFINITY
-                 : bin_threshold((double)p.lo, (double)p.hi, n, k);
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k <= n; k += gridDim.x * blockDim.x)
+    thr[k] = k == n ? INFINITY
+                    : (k == 0 || tp_degenerate(p.lim)) ? -INFINITY
+                                                       : bin_threshold((double)p.lo, (double)p.hi, n, k);
 }
 
 template <typename T>

@@ -148,6 +148,7 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
   float2* lcS = reinterpret_cast<float2*>(P.tail + ((G.gtr * n * 4 + 15) & ~15LL));  // [gtr]
   // bin-edge tables of the pencil's tiles (adaptive) or of the global range
   float* thrS = reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(lcS) + G.gtr * 16);
+  const int n1 = n + 1;  // edge-table stride: thr[0] = -inf ... thr[n] = +inf
   const TileParam<float>* tparams = reinterpret_cast<const TileParam<float>*>(W.tparams);
   const TileParam<float> g0 = tparams[0];
   if (!ADAPT && tp_degenerate(g0.lim)) return;  // constant image: every mapping is 0.5
@@ -198,9 +199,9 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
           lcS[t] = lc;
           if (isnan(lc.y)) s_bad = 1;
         }
-        for (int64_t k = tid; k < G.gtr * n; k += kConsumers) thrS[k] = W.thr[key * n + k];
+        for (int64_t k = tid; k < G.gtr * n1; k += kConsumers) thrS[k] = W.thr[key * n1 + k];
       } else if (cur < 0) {
-        for (int k = tid; k < n; k += kConsumers) thrS[k] = W.thr[k];
+        for (int k = tid; k < n1; k += kConsumers) thrS[k] = W.thr[k];
       }
       consumers_sync();
       if (ADAPT) patho = s_bad != 0;
@@ -227,21 +228,21 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
         const float2 l2 = ADAPT ? lcS[trt[2]] : glc, l3 = ADAPT ? lcS[trt[3]] : glc;
         if (!patho) {
           if (!ADAPT || (trt[0] == trt[1] && trt[2] == trt[3])) {
-            bins2(pk2(v.x, v.y), v.x, v.y, l0, thrS + (ADAPT ? trt[0] * n : 0), n, lim, b[0], b[1]);
-            bins2(pk2(v.z, v.w), v.z, v.w, l2, thrS + (ADAPT ? trt[2] * n : 0), n, lim, b[2], b[3]);
+            bins2(pk2(v.x, v.y), v.x, v.y, l0, thrS + (ADAPT ? trt[0] * n1 : 0), n, lim, b[0], b[1]);
+            bins2(pk2(v.z, v.w), v.z, v.w, l2, thrS + (ADAPT ? trt[2] * n1 : 0), n, lim, b[2], b[3]);
           } else {  // pairs straddle a tile boundary: evaluate each against its own tile
             int dmy;
-            bins2(pk2(v.x, v.x), v.x, v.x, l0, thrS + trt[0] * n, n, lim, b[0], dmy);
-            bins2(pk2(v.y, v.y), v.y, v.y, l1, thrS + trt[1] * n, n, lim, b[1], dmy);
-            bins2(pk2(v.z, v.z), v.z, v.z, l2, thrS + trt[2] * n, n, lim, b[2], dmy);
-            bins2(pk2(v.w, v.w), v.w, v.w, l3, thrS + trt[3] * n, n, lim, b[3], dmy);
+            bins2(pk2(v.x, v.x), v.x, v.x, l0, thrS + trt[0] * n1, n, lim, b[0], dmy);
+            bins2(pk2(v.y, v.y), v.y, v.y, l1, thrS + trt[1] * n1, n, lim, b[1], dmy);
+            bins2(pk2(v.z, v.z), v.z, v.z, l2, thrS + trt[2] * n1, n, lim, b[2], dmy);
+            bins2(pk2(v.w, v.w), v.w, v.w, l3, thrS + trt[3] * n1, n, lim, b[3], dmy);
           }
         } else {
           const float a4[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
             const float2 lc = ADAPT ? lcS[trt[i]] : glc;
-            const float* th = thrS + (ADAPT ? trt[i] * n : 0);
+            const float* th = thrS + (ADAPT ? trt[i] * n1 : 0);
             if (isnan(lc.y)) b[i] = bin_search(a4[i], th, n);
             else bins2(pk2(a4[i], a4[i]), a4[i], a4[i], lc, th, n, lim, b[i], b[i]);
           }
@@ -297,10 +298,14 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
   const PencilSmem P = pencil_smem(G, smem);
   const int n = G.n_bins;
   const int64_t gtr = G.gtr;
-  float* lutS = reinterpret_cast<float*>(P.tail);  // [NCO][gtr][n]
-  float* thrS = lutS + NCO * gtr * n;  // bin-edge tables: [NCO][gtr][n] (adaptive) or [n]
+  // LUTs and edge tables with row stride n+1: rows of consecutive tiles start
+  // in different banks, so lanes gathering the same bin of different tiles
+  // do not conflict.
+  const int n1 = n + 1;
+  float* lutS = reinterpret_cast<float*>(P.tail);  // [NCO][gtr][n1]
+  float* thrS = lutS + NCO * gtr * n1;  // edge tables: [NCO][gtr][n1] (adaptive) or [n1]
   float2* lcS = reinterpret_cast<float2*>(  // [NCO][gtr] {lo, c} (adaptive)
-      P.tail + (((ADAPT ? 2 * NCO * gtr * n : NCO * gtr * n + n) * 4 + 15) & ~15LL));
+      P.tail + (((ADAPT ? 2 * NCO * gtr * n1 : NCO * gtr * n1 + n1) * 4 + 15) & ~15LL));
   __shared__ int s_bad;
   pipe_init(*P.pipe, G.nst, kConsumersBlend / 32);
   __syncthreads();
@@ -351,9 +356,6 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
       tw[i][ct] = w;
     }
   }
-  float inv2b[KO];
-#pragma unroll
-  for (int j = 0; j < KO; ++j) inv2b[j] = 1.0f / (float)(2 * G.d[j].b);
 
   const int64_t stage_elems = G.stage_stride;
   int64_t cur = -1;
@@ -368,17 +370,25 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
       consumers_sync<kConsumersBlend>();
       if (tid == 0) s_bad = 0;
       if (!ADAPT && cur < 0)
-        for (int k = tid; k < n; k += kConsumersBlend) thrS[k] = W.thr[k];
+        for (int k = tid; k < n1; k += kConsumersBlend) thrS[k] = W.thr[k];
       for (int co = 0; co < NCO; ++co) {
         int64_t of = (S.cell[0] + ((co >> (KO - 1)) & 1) - G.trow0) * G.tstride[0];
         for (int j = 1; j < KO; ++j) of += (S.cell[j] + ((co >> (KO - 1 - j)) & 1)) * G.tstride[j];
         const float4* src = reinterpret_cast<const float4*>(W.lut + of * n);
-        float4* dst = reinterpret_cast<float4*>(lutS + co * gtr * n);
-        for (int64_t k = tid; k < gtr * n / 4; k += kConsumersBlend) dst[k] = __ldg(src + k);
+        float* dst = lutS + co * gtr * n1;
+        for (int64_t k = tid; k < gtr * n / 4; k += kConsumersBlend) {
+          const float4 q = __ldg(src + k);
+          const int64_t t = (4 * k) / n, b = 4 * k - t * n;  // n % 4 == 0: one row
+          float* d = dst + t * n1 + b;
+          d[0] = q.x;
+          d[1] = q.y;
+          d[2] = q.z;
+          d[3] = q.w;
+        }
         if (ADAPT) {
-          const float4* ts = reinterpret_cast<const float4*>(W.thr + of * n);
-          float4* td = reinterpret_cast<float4*>(thrS + co * gtr * n);
-          for (int64_t k = tid; k < gtr * n / 4; k += kConsumersBlend) td[k] = __ldg(ts + k);
+          const float* ts = W.thr + of * n1;
+          float* td = thrS + co * gtr * n1;
+          for (int64_t k = tid; k < gtr * n1; k += kConsumersBlend) td[k] = __ldg(ts + k);
           for (int64_t t = tid; t < gtr; t += kConsumersBlend) {
             const float2 lc = tile_lc(tparams[of + t]);
             lcS[co * gtr + t] = lc;
@@ -393,32 +403,65 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
     const int rows = G.stage_rows;
     const float* buf = P.bufs + s * stage_elems;
     if (lane_on) {
-      int cellv[KO], xb[KO];
-#pragma unroll
-      for (int j = 0; j < KO; ++j) {
-        cellv[j] = S.cell[j];
-        xb[j] = S.x[j];
-      }
-      // outer factors and output offset of the fixed dims (< KO-2)
+      // Per-dimension factor f_j(x) = d_lo/b = (2(x + before) - 2cb - b + 1) / 2b
+      //                             = x * (1/b) + t_j   (exact half-integer numerators)
+      // Dims < KO-2 are fixed for the stage; dims KO-2 / KO-1 vary by row.
+      float wfix[NCO / (KO >= 2 ? 4 : 2)];
+      float s1, t1, s2 = 0.f, t2 = 0.f;
       int64_t obase = e0;
-#pragma unroll
-      for (int j = 0; j < KO; ++j)
-        if (j < KO - 2) obase += (int64_t)(j == 0 ? xb[j] - G.row0 : xb[j]) * G.vstride[j];
-      for (int q = slot; q < rows; q += G.rpi) {
-        const int r1 = q & (G.r1 - 1), r2 = q >> G.lg_r1;
-        float fo[KO];
-        int64_t ooff = obase;
+      {
+        float ff[KO];
 #pragma unroll
         for (int j = 0; j < KO; ++j) {
-          const int64_t xj = xb[j] + (j == KO - 1 ? r1 : (j == KO - 2 ? r2 : 0));
-          fo[j] = (float)twice_dlo(G.d[j], xj, cellv[j]) * inv2b[j];
-          if (j >= KO - 2) ooff += (j == 0 ? xj - G.row0 : xj) * G.vstride[j];
+          const Dim& d = G.d[j];
+          const float sj = 1.0f / (float)d.b;
+          const float tj = (float)(2 * d.before - 2 * (int64_t)S.cell[j] * d.b - d.b + 1) /
+                           (float)(2 * d.b);
+          if (j == KO - 1) { s1 = sj; t1 = tj; }
+          else if (j == KO - 2) { s2 = sj; t2 = tj; }
+          else {
+            ff[j] = fmaf((float)S.x[j], sj, tj);
+            obase += (int64_t)(j == 0 ? S.x[j] - G.row0 : S.x[j]) * G.vstride[j];
+          }
+        }
+        constexpr int NF = NCO / (KO >= 2 ? 4 : 2);
+#pragma unroll
+        for (int cf = 0; cf < NF; ++cf) {
+          float w = 1.0f;
+#pragma unroll
+          for (int j = 0; j < KO - 2; ++j)
+            w *= ((cf >> (KO - 3 - j)) & 1) ? ff[j] : 1.0f - ff[j];
+          wfix[cf] = w;
+        }
+      }
+      const int xb1 = S.x[KO - 1], xb2 = KO >= 2 ? S.x[KO >= 2 ? KO - 2 : 0] : 0;
+      const int64_t vs1 = G.vstride[KO - 1], vs2 = KO >= 2 ? G.vstride[KO >= 2 ? KO - 2 : 0] : 0;
+      const int64_t r0 = (KO == 1 ? G.row0 : 0), r0b = (KO == 2 ? G.row0 : 0);
+      const int tile_stride = (int)(gtr * n1);  // floats between outer corners
+      for (int q = slot; q < rows; q += G.rpi) {
+        const int r1 = q & (G.r1 - 1), r2 = q >> G.lg_r1;
+        const int x1 = xb1 + r1, x2 = xb2 + r2;
+        const int64_t ooff = obase + (int64_t)(x1 - r0) * vs1 + (KO >= 2 ? (int64_t)(x2 - r0b) * vs2 : 0);
+        const float f1 = fmaf((float)x1, s1, t1);
+        const float f2 = KO >= 2 ? fmaf((float)x2, s2, t2) : 0.f;
+        // outer corner weights: fixed dims x (dim KO-2) x (dim KO-1)
+        float wo[NCO];
+        {
+          const float g1[2] = {1.0f - f1, f1};
+#pragma unroll
+          for (int co = 0; co < NCO; ++co) {
+            const int b1 = co & 1;
+            float w = g1[b1];
+            if (KO >= 2) w *= ((co >> 1) & 1) ? f2 : 1.0f - f2;
+            wo[co] = w * wfix[co >> (KO >= 2 ? 2 : 1)];
+          }
         }
         const float4 v4 = *reinterpret_cast<const float4*>(buf + q * G.P + e0);
         const u64 V01 = pk2(v4.x, v4.y), V23 = pk2(v4.z, v4.w);
         float acc[4] = {0.f, 0.f, 0.f, 0.f};
-        int bg[4];
+        int off[NCT][4];  // float offset of (trailing corner, column) in an outer corner's LUTs
         if (!ADAPT) {
+          int bg[4];
           if (!patho) {
             bins2(V01, v4.x, v4.y, glc, thrS, n, lim, bg[0], bg[1]);
             bins2(V23, v4.z, v4.w, glc, thrS, n, lim, bg[2], bg[3]);
@@ -428,20 +471,22 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
             bg[2] = bin_search(v4.z, thrS, n);
             bg[3] = bin_search(v4.w, thrS, n);
           }
+#pragma unroll
+          for (int ct = 0; ct < NCT; ++ct)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) off[ct][i] = tt[ct] * n1 + bg[i];
         }
 #pragma unroll
         for (int co = 0; co < NCO; ++co) {
-          float wo = 1.0f;
-#pragma unroll
-          for (int j = 0; j < KO; ++j) wo *= ((co >> (KO - 1 - j)) & 1) ? fo[j] : (1.0f - fo[j]);
+          const float* Lco = lutS + co * tile_stride;
+          float m[NCT][4];
 #pragma unroll
           for (int ct = 0; ct < NCT; ++ct) {
-            const int tile = co * gtr + tt[ct];
-            const float* L = lutS + tile * n;
-            int b[4];
             if (ADAPT) {
+              const int tile = co * gtr + tt[ct];
               const float2 lc = lcS[tile];
-              const float* th = thrS + tile * n;
+              const float* th = thrS + tile * n1;
+              int b[4];
               if (!patho || !isnan(lc.y)) {
                 bins2(V01, v4.x, v4.y, lc, th, n, lim, b[0], b[1]);
                 bins2(V23, v4.z, v4.w, lc, th, n, lim, b[2], b[3]);
@@ -451,12 +496,20 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
                 b[2] = bin_search(v4.z, th, n);
                 b[3] = bin_search(v4.w, th, n);
               }
+#pragma unroll
+              for (int i = 0; i < 4; ++i) m[ct][i] = Lco[tt[ct] * n1 + b[i]];
             } else {
 #pragma unroll
-              for (int i = 0; i < 4; ++i) b[i] = bg[i];
+              for (int i = 0; i < 4; ++i) m[ct][i] = Lco[off[ct][i]];
             }
+          }
+          // multilinear blend of the trailing corners, then the outer weight
 #pragma unroll
-            for (int i = 0; i < 4; ++i) acc[i] = fmaf(wo * tw[i][ct], L[b[i]], acc[i]);
+          for (int i = 0; i < 4; ++i) {
+            float mi = 0.f;
+#pragma unroll
+            for (int ct = 0; ct < NCT; ++ct) mi = fmaf(tw[i][ct], m[ct][i], mi);
+            acc[i] = fmaf(wo[co], mi, acc[i]);
           }
         }
         float4 r;

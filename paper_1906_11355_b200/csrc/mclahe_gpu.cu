@@ -183,7 +183,7 @@ Pencil choose_pencil(const mclahe_plan_s& pl, bool for_hist) {
     if (for_hist) {
       if (!merged) continue;
       if (c.gtr * n >= (int64_t{1} << 31) / 2) continue;
-      c.tail = align_up(c.gtr * n * 4, 16) + c.gtr * 16 + (pl.p.adaptive ? c.gtr : 1) * n * 4;
+      c.tail = align_up(c.gtr * n * 4, 16) + c.gtr * 16 + (pl.p.adaptive ? c.gtr : 1) * (n + 1) * 4;
       if (c.tail > 64 * 1024) continue;
       c.stage_budget = kStageBytes;  // 3 stages, ~3 CTAs per SM
     } else {
@@ -200,8 +200,8 @@ Pencil choose_pencil(const mclahe_plan_s& pl, bool for_hist) {
       if (!shared) continue;
       // LUTs (+ bin-edge tables: per tile when adaptive, one row when global)
       // + per-tile ranges; one CTA per SM with 16 consumer warps
-      const int64_t luts = (int64_t{1} << ko) * c.gtr * n;
-      c.tail = align_up((pl.p.adaptive ? 2 * luts : luts + n) * 4, 16) +
+      const int64_t luts1 = (int64_t{1} << ko) * c.gtr * (n + 1);  // rows padded to n+1
+      c.tail = align_up((pl.p.adaptive ? 2 * luts1 : luts1 + n + 1) * 4, 16) +
                (int64_t{1} << ko) * c.gtr * 16;
       c.rpi = kConsumersBlend / c.tpr;
       const int64_t avail = 226 * 1024 - kPipeBytes - c.tail;
@@ -474,7 +474,7 @@ int plan_describe(const mclahe_params_t* params, int64_t row_begin, int64_t row_
   I.off_lut = align_up(I.off_tparams + (params->adaptive ? win_tiles : 1) * tp_size, 256);
   I.off_thr = align_up(I.off_lut + win_tiles * n * 4, 256);
   I.workspace_bytes =
-      align_up(I.off_thr + (pl->f32() ? (params->adaptive ? win_tiles : 1) * n * 4 : 0), 256);
+      align_up(I.off_thr + (pl->f32() ? (params->adaptive ? win_tiles : 1) * (n + 1) * 4 : 0), 256);
 
   KGeom& G = pl->G;
   std::memset(&G, 0, sizeof G);
@@ -661,7 +661,7 @@ int do_params(mclahe_plan_s* pl, void* ws, cudaStream_t st) {
   else k_params<double><<<grid, 128, 0, st>>>(pl->G, W);
   MG_LAUNCHED();
   if (pl->f32()) {
-    const int64_t total = n * pl->p.n_bins;
+    const int64_t total = n * (pl->p.n_bins + 1);
     const int tg = (int)std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 8192));
     k_thresholds<<<tg, 256, 0, st>>>(pl->G, W);
     MG_LAUNCHED();
@@ -1030,8 +1030,8 @@ int mclahe_debug_bin_index(int32_t dtype, const void* values, int64_t n, double 
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (dtype == MCLAHE_F32) {
     float* thr = nullptr;
-    MG_CUDA(cudaMallocAsync(&thr, (size_t)n_bins * sizeof(float), st));
-    k_debug_thresholds<<<(int)((n_bins + 127) / 128), 128, 0, st>>>(lo, hi, (int)n_bins, thr);
+    MG_CUDA(cudaMallocAsync(&thr, (size_t)(n_bins + 1) * sizeof(float), st));
+    k_debug_thresholds<<<(int)((n_bins + 128) / 128), 128, 0, st>>>(lo, hi, (int)n_bins, thr);
     MG_LAUNCHED();
     k_debug_bins<float><<<grid, 256, 0, st>>>(static_cast<const float*>(values), n, lo, hi,
                                               (int)n_bins, thr, out);
