@@ -1,0 +1,90 @@
+// include/mclahe_b200.hpp -- C++ drop-in for the reference's public MCLAHE API.
+//
+// Source-compatible with the reference's mclahe:: pipeline interface
+// (/root/reference/proj/core/include/mclahe/pipeline.hpp:12-43 and the types
+// it uses from nd_image.hpp / histogram.hpp): the same namespace, type names,
+// fields and call
+//
+//     mclahe::NdImage out = mclahe::mclahe(request, &timings);
+//
+// so a caller swaps the include and links libmclahe_cpp.so (+ libmclahe_gpu.so)
+// instead of libmclahe.a.  Compute runs on the GPU through the C ABI in
+// mclahe_gpu.h; float64 images whose values are all float32-representable
+// take the float32 pencil kernels (bit-identical bins, since f32 -> f64 is
+// exact), others the exact float64 path.  Errors: ValidationError with the
+// reference's messages; CUDA failures as std::runtime_error.
+#pragma once
+
+#include <cstddef>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace mclahe {
+
+inline constexpr std::size_t kMaxRank = 8;
+
+class ValidationError : public std::invalid_argument {
+ public:
+  using std::invalid_argument::invalid_argument;
+};
+
+using Shape = std::vector<std::size_t>;
+
+// Dense row-major N-D array of doubles (nd_image.hpp:54-77).
+class NdImage {
+ public:
+  NdImage(Shape shape, std::vector<double> data);
+  static NdImage zeros(Shape shape);
+  static NdImage constant(Shape shape, double value);
+
+  const Shape& shape() const noexcept { return shape_; }
+  std::size_t rank() const noexcept { return shape_.size(); }
+  std::size_t size() const noexcept { return data_.size(); }
+  const std::vector<double>& data() const noexcept { return data_; }
+  std::vector<double>& data() noexcept { return data_; }
+  double operator[](std::size_t i) const noexcept { return data_[i]; }
+  double& operator[](std::size_t i) noexcept { return data_[i]; }
+
+ private:
+  Shape shape_;
+  std::vector<double> data_;
+};
+
+struct KernelSpec {
+  std::vector<std::size_t> sizes;
+};
+
+enum class RangeMode { Global, Adaptive };
+
+struct EnhanceParams {
+  double clip_limit = 1.0;
+  std::size_t n_bins = 256;
+  RangeMode range_mode = RangeMode::Global;
+};
+
+struct McLaheRequest {
+  NdImage image;
+  KernelSpec kernel;
+  EnhanceParams params;
+  unsigned threads = 0;  // accepted for compatibility; the GPU path ignores it
+};
+
+struct PhaseTimings {
+  double pad_s = 0.0;
+  double histograms_s = 0.0;
+  double interpolation_s = 0.0;
+};
+
+// pipeline.hpp:30 -- full MCLAHE on the current CUDA device.
+NdImage mclahe(const McLaheRequest& request, PhaseTimings* timings = nullptr);
+
+// pipeline.hpp:37-40 -- mclahe on every slice along frame_axis.
+NdImage mclahe_framewise(const NdImage& image, std::size_t frame_axis, const KernelSpec& kernel,
+                         const EnhanceParams& params, unsigned threads = 0,
+                         bool renormalize_slices = false, PhaseTimings* timings = nullptr);
+
+// pipeline.hpp:43 -- affine map of [min, max] onto [0, 1]; constant -> 0.5.
+NdImage normalize_to_unit(const NdImage& image);
+
+}  // namespace mclahe

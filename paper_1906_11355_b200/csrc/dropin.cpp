@@ -1,0 +1,146 @@
+// dropin.cpp -- the C++ drop-in (include/mclahe_b200.hpp) over the C ABI.
+// Host-side only: validation messages, dtype selection, frame loop; all
+// compute goes through mclahe_gpu_run (include/mclahe_gpu.h).
+#include "../../include/mclahe_b200.hpp"
+
+#include <cmath>
+#include <cstring>
+#include <limits>
+
+#include "../../include/mclahe_gpu.h"
+
+namespace mclahe {
+
+namespace {
+
+std::size_t product(const Shape& s) {
+  std::size_t p = 1;
+  for (std::size_t e : s) {
+    if (e == 0) throw ValidationError("shape extents must be positive");
+    if (e > std::numeric_limits<std::size_t>::max() / p)
+      throw ValidationError("shape product overflows size_t");
+    p *= e;
+  }
+  return p;
+}
+
+void raise(int rc) {
+  const std::string msg = mclahe_last_error();
+  if (rc == MCLAHE_ERR_VALIDATION) throw ValidationError(msg);
+  throw std::runtime_error("mclahe GPU error " + std::to_string(rc) + ": " + msg);
+}
+
+bool all_f32_exact(const std::vector<double>& v) {
+  for (double x : v)
+    if (static_cast<double>(static_cast<float>(x)) != x) return false;
+  return true;
+}
+
+}  // namespace
+
+NdImage::NdImage(Shape shape, std::vector<double> data)
+    : shape_(std::move(shape)), data_(std::move(data)) {
+  if (shape_.empty() || shape_.size() > kMaxRank)
+    throw ValidationError("rank must be in [1, " + std::to_string(kMaxRank) + "]");
+  if (product(shape_) != data_.size())
+    throw ValidationError("data length does not match shape product");
+}
+
+NdImage NdImage::zeros(Shape shape) {
+  const std::size_t n = product(shape);
+  return NdImage(std::move(shape), std::vector<double>(n, 0.0));
+}
+
+NdImage NdImage::constant(Shape shape, double value) {
+  const std::size_t n = product(shape);
+  return NdImage(std::move(shape), std::vector<double>(n, value));
+}
+
+NdImage mclahe(const McLaheRequest& request, PhaseTimings* timings) {
+  const NdImage& img = request.image;
+  // validate_request (src/pipeline.cpp:19-23): the kernel-rank message
+  if (request.kernel.sizes.size() != img.rank())
+    throw ValidationError("kernel rank " + std::to_string(request.kernel.sizes.size()) +
+                          " does not match image rank " + std::to_string(img.rank()));
+  mclahe_params_t p;
+  std::memset(&p, 0, sizeof p);
+  p.rank = static_cast<int32_t>(img.rank());
+  p.adaptive = request.params.range_mode == RangeMode::Adaptive ? 1 : 0;
+  for (std::size_t i = 0; i < img.rank(); ++i) {
+    p.shape[i] = static_cast<int64_t>(img.shape()[i]);
+    p.kernel[i] = static_cast<int64_t>(request.kernel.sizes[i]);
+  }
+  p.n_bins = static_cast<int64_t>(request.params.n_bins);
+  p.clip_limit = request.params.clip_limit;
+  mclahe_timings_t t{0.0, 0.0, 0.0};
+  std::vector<double> out(img.size());
+  const std::vector<double>& src = img.data();
+  int rc;
+  if (all_f32_exact(src)) {  // float32 pencil kernels, bit-identical bins
+    p.dtype = MCLAHE_F32;
+    std::vector<float> in32(src.begin(), src.end()), out32(src.size());
+    rc = mclahe_gpu_run(&p, in32.data(), out32.data(), &t);
+    if (rc == MCLAHE_OK) out.assign(out32.begin(), out32.end());
+  } else {
+    p.dtype = MCLAHE_F64;
+    rc = mclahe_gpu_run(&p, src.data(), out.data(), &t);
+  }
+  if (rc != MCLAHE_OK) raise(rc);
+  if (timings) {
+    timings->pad_s += t.pad_s;
+    timings->histograms_s += t.histograms_s;
+    timings->interpolation_s += t.interpolation_s;
+  }
+  return NdImage(img.shape(), std::move(out));
+}
+
+NdImage mclahe_framewise(const NdImage& image, std::size_t frame_axis, const KernelSpec& kernel,
+                         const EnhanceParams& params, unsigned threads, bool renormalize_slices,
+                         PhaseTimings* timings) {
+  // src/pipeline.cpp:131-153
+  if (image.rank() < 2) throw ValidationError("framewise mode needs rank >= 2");
+  if (frame_axis >= image.rank())
+    throw ValidationError("frame axis " + std::to_string(frame_axis) + " out of range for rank " +
+                          std::to_string(image.rank()));
+  if (kernel.sizes.size() != image.rank() - 1)
+    throw ValidationError("framewise kernel rank must be image rank - 1");
+  const Shape& sh = image.shape();
+  std::size_t outer = 1, inner = 1;
+  for (std::size_t i = 0; i < frame_axis; ++i) outer *= sh[i];
+  for (std::size_t i = frame_axis + 1; i < sh.size(); ++i) inner *= sh[i];
+  Shape slice_shape;
+  for (std::size_t i = 0; i < sh.size(); ++i)
+    if (i != frame_axis) slice_shape.push_back(sh[i]);
+  NdImage out = NdImage::zeros(sh);
+  const std::size_t frames = sh[frame_axis];
+  for (std::size_t f = 0; f < frames; ++f) {
+    std::vector<double> buf(outer * inner);
+    for (std::size_t o = 0; o < outer; ++o)
+      std::memcpy(&buf[o * inner], &image.data()[(o * frames + f) * inner], inner * sizeof(double));
+    NdImage slice(slice_shape, std::move(buf));
+    if (renormalize_slices) slice = normalize_to_unit(slice);
+    const NdImage enh = mclahe(McLaheRequest{std::move(slice), kernel, params, threads}, timings);
+    for (std::size_t o = 0; o < outer; ++o)
+      std::memcpy(&out.data()[(o * frames + f) * inner], &enh.data()[o * inner],
+                  inner * sizeof(double));
+  }
+  return out;
+}
+
+NdImage normalize_to_unit(const NdImage& image) {
+  // src/pipeline.cpp:155-165
+  for (double v : image.data())
+    if (!std::isfinite(v)) throw ValidationError("image contains non-finite values");
+  double lo = image.data().front(), hi = lo;
+  for (double v : image.data()) {
+    if (v < lo) lo = v;
+    if (v > hi) hi = v;
+  }
+  if (!(hi > lo)) return NdImage::constant(image.shape(), 0.5);
+  const double span = hi - lo;
+  std::vector<double> d(image.size());
+  for (std::size_t i = 0; i < d.size(); ++i) d[i] = (image.data()[i] - lo) / span;
+  return NdImage(image.shape(), std::move(d));
+}
+
+}  // namespace mclahe
