@@ -221,6 +221,25 @@ __device__ __forceinline__ void bins2(u64 V, float v0, float v1, float2 lc, cons
   if (!(fabsf(d1) < lim)) b1 = near_fix(v1, b1, d1, th, n);
 }
 
+// Branch-free exact bins of two voxels against one tile, edge table only.
+// k = rint(y) (magic-number add in round-to-nearest); since |y - q| < 0.5 for
+// every y that matters, the reference bin floor(q) is k or k - 1, and it is k
+// iff v >= th[k].  Clamping k to [0, n] against the sentinels th[0] = -inf,
+// th[n] = +inf reproduces the reference's clamp for y outside [0, n) (and
+// for |y| >= 2^22, where the magic add saturates monotonically).
+__device__ __forceinline__ void bins2_edge(u64 V, float v0, float v1, float2 lc, const float* th,
+                                           int n, int& b0, int& b1) {
+  const u64 y = mul2(sub2(V, pk2(lc.x, lc.x)), pk2(lc.y, lc.y));
+  u64 t;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(t) : "l"(y), "l"(pk2(kMagic, kMagic)));
+  float t0, t1;
+  upk2(t, t0, t1);
+  const int k0 = min(max(__float_as_int(t0) - kMagicBits, 0), n);
+  const int k1 = min(max(__float_as_int(t1) - kMagicBits, 0), n);
+  b0 = v0 >= th[k0] ? k0 : k0 - 1;
+  b1 = v1 >= th[k1] ? k1 : k1 - 1;
+}
+
 // Exact bin from the edge table alone (binary search over thr[1..n-1]);
 // used for ranges the float guard does not cover.
 __device__ __forceinline__ int bin_search(float v, const float* th, int n) {

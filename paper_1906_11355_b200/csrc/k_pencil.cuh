@@ -159,7 +159,6 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
     if (threadIdx.x == kConsumers) pipe_produce<KO, false>(G, &tmap, units, u0, u1, *P.pipe, P.bufs);
     return;
   }
-  const float lim = guard_lim(n);
   const int tid = threadIdx.x;
   const int slot = tid / G.tpr;
   const int64_t e0 = (int64_t)(tid % G.tpr) * 4;
@@ -228,14 +227,14 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
         const float2 l2 = ADAPT ? lcS[trt[2]] : glc, l3 = ADAPT ? lcS[trt[3]] : glc;
         if (!patho) {
           if (!ADAPT || (trt[0] == trt[1] && trt[2] == trt[3])) {
-            bins2(pk2(v.x, v.y), v.x, v.y, l0, thrS + (ADAPT ? trt[0] * n1 : 0), n, lim, b[0], b[1]);
-            bins2(pk2(v.z, v.w), v.z, v.w, l2, thrS + (ADAPT ? trt[2] * n1 : 0), n, lim, b[2], b[3]);
+            bins2_edge(pk2(v.x, v.y), v.x, v.y, l0, thrS + (ADAPT ? trt[0] * n1 : 0), n, b[0], b[1]);
+            bins2_edge(pk2(v.z, v.w), v.z, v.w, l2, thrS + (ADAPT ? trt[2] * n1 : 0), n, b[2], b[3]);
           } else {  // pairs straddle a tile boundary: evaluate each against its own tile
             int dmy;
-            bins2(pk2(v.x, v.x), v.x, v.x, l0, thrS + trt[0] * n1, n, lim, b[0], dmy);
-            bins2(pk2(v.y, v.y), v.y, v.y, l1, thrS + trt[1] * n1, n, lim, b[1], dmy);
-            bins2(pk2(v.z, v.z), v.z, v.z, l2, thrS + trt[2] * n1, n, lim, b[2], dmy);
-            bins2(pk2(v.w, v.w), v.w, v.w, l3, thrS + trt[3] * n1, n, lim, b[3], dmy);
+            bins2_edge(pk2(v.x, v.x), v.x, v.x, l0, thrS + trt[0] * n1, n, b[0], dmy);
+            bins2_edge(pk2(v.y, v.y), v.y, v.y, l1, thrS + trt[1] * n1, n, b[1], dmy);
+            bins2_edge(pk2(v.z, v.z), v.z, v.z, l2, thrS + trt[2] * n1, n, b[2], dmy);
+            bins2_edge(pk2(v.w, v.w), v.w, v.w, l3, thrS + trt[3] * n1, n, b[3], dmy);
           }
         } else {
           const float a4[4] = {v.x, v.y, v.z, v.w};
@@ -244,7 +243,7 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
             const float2 lc = ADAPT ? lcS[trt[i]] : glc;
             const float* th = thrS + (ADAPT ? trt[i] * n1 : 0);
             if (isnan(lc.y)) b[i] = bin_search(a4[i], th, n);
-            else bins2(pk2(a4[i], a4[i]), a4[i], a4[i], lc, th, n, lim, b[i], b[i]);
+            else bins2_edge(pk2(a4[i], a4[i]), a4[i], a4[i], lc, th, n, b[i], b[i]);
           }
         }
         // skip degenerate tiles (no histogram), merge equal neighbours, one
@@ -317,7 +316,6 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
   }
   const TileParam<float>* tparams = reinterpret_cast<const TileParam<float>*>(W.tparams);
   const float2 glc = tile_lc(tparams[0]);
-  const float lim = guard_lim(n);
   bool patho = !ADAPT && isnan(glc.y);  // a range the float guard does not cover
   const int tid = threadIdx.x;
   const int slot = tid / G.tpr;
@@ -463,8 +461,8 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
         if (!ADAPT) {
           int bg[4];
           if (!patho) {
-            bins2(V01, v4.x, v4.y, glc, thrS, n, lim, bg[0], bg[1]);
-            bins2(V23, v4.z, v4.w, glc, thrS, n, lim, bg[2], bg[3]);
+            bins2_edge(V01, v4.x, v4.y, glc, thrS, n, bg[0], bg[1]);
+            bins2_edge(V23, v4.z, v4.w, glc, thrS, n, bg[2], bg[3]);
           } else {
             bg[0] = bin_search(v4.x, thrS, n);
             bg[1] = bin_search(v4.y, thrS, n);
@@ -488,8 +486,8 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
               const float* th = thrS + tile * n1;
               int b[4];
               if (!patho || !isnan(lc.y)) {
-                bins2(V01, v4.x, v4.y, lc, th, n, lim, b[0], b[1]);
-                bins2(V23, v4.z, v4.w, lc, th, n, lim, b[2], b[3]);
+                bins2_edge(V01, v4.x, v4.y, lc, th, n, b[0], b[1]);
+                bins2_edge(V23, v4.z, v4.w, lc, th, n, b[2], b[3]);
               } else {
                 b[0] = bin_search(v4.x, th, n);
                 b[1] = bin_search(v4.y, th, n);
