@@ -46,7 +46,8 @@ struct KGeom {
   int r1, lg_r1;    // box rows along outer dim KO-1 (power of two) and log2
   int r2;           // box rows along outer dim KO-2 (1 if KO == 1)
   int tma_rank;     // rank of the TMA tensor view of the input
-  int64_t stage_stride;  // floats between stage buffers (128-byte multiple)
+  int nseg;         // K4: 32-float segments of the trailing block (one per stage)
+  int64_t stage_stride;  // floats between stage buffers (1024-byte multiple)
   int64_t P;        // elements of one trailing block
   int64_t gtr;      // tiles of one trailing block
   Dim d[kMaxRank];
@@ -131,7 +132,7 @@ struct Stage {
   int32_t unit;   // -1: end of stream
   int32_t wuni;   // K2: 1 if the multiplicity is uniform over the box (= wfix)
   int32_t wfix;   // K2: multiplicity over dims < KO-2 (or over the whole box if wuni)
-  int32_t pad_;
+  int32_t seg;    // K4: 32-float segment of the trailing block held by the stage
   int64_t key;    // tile window offset (K2) or cell key (K4) of the unit
   int32_t x[kMaxOuterDims];     // absolute coordinates of the box origin (dim 0 global)
   int32_t cell[kMaxOuterDims];  // K4: cells of the unit (K2: tiles)
@@ -153,7 +154,8 @@ struct Pipe {
   ProdBox box;
 };
 
-__device__ __forceinline__ size_t pipe_bytes() { return (sizeof(Pipe) + 127) & ~size_t(127); }
+// 1024-byte aligned so stage buffers meet the TMA 128B-swizzle alignment.
+__device__ __forceinline__ size_t pipe_bytes() { return (sizeof(Pipe) + 1023) & ~size_t(1023); }
 
 // Initialises the barriers (thread 0) -- call before the role split, then
 // __syncthreads().
@@ -223,7 +225,7 @@ __device__ __noinline__ void pipe_produce(const KGeom& G, const CUtensorMap* map
                                           Pipe& pp, float* bufs) {
   const int nst = G.nst;
   const int64_t stage_elems = G.stage_stride;
-  const uint32_t box_bytes = (uint32_t)((int64_t)G.stage_rows * G.P * 4);
+  const uint32_t box_bytes = (uint32_t)((int64_t)G.stage_rows * (G.P / G.nseg) * 4);
   const int R1 = G.r1, R2 = G.r2;
   ProdBox& B = pp.box;
   uint32_t it = 0;
@@ -276,10 +278,13 @@ __device__ __noinline__ void pipe_produce(const KGeom& G, const CUtensorMap* map
       for (int i2 = 0; i2 < n2; ++i2) {
 #pragma unroll 1
         for (int i1 = 0; i1 < n1; ++i1) {
+#pragma unroll 1
+        for (int seg = 0; seg < G.nseg; ++seg) {
           const int slot = it % nst;
           mbar_wait(&pp.empty[slot], ((it / nst) & 1) ^ 1);
           Stage& S = pp.st[slot];
           S.unit = u;
+          S.seg = seg;
           S.key = key;
 #pragma unroll 1
           for (int j = 0; j < KO - 2; ++j) S.x[j] = xf[j];
@@ -303,7 +308,7 @@ __device__ __noinline__ void pipe_produce(const KGeom& G, const CUtensorMap* map
           int c[6];
           int r = 0;
           c[r++] = 0;
-          if (G.tma_rank - KO == 2) c[r++] = 0;
+          if (G.tma_rank - KO == 2) c[r++] = seg;  // segment (K4) / second trailing dim (K2: 0)
 #pragma unroll 1
           for (int j = KO - 1; j >= 0; --j) {
             const int32_t xj = j == KO - 1 ? x1 : (j == KO - 2 ? x2 : xf[j]);
@@ -312,6 +317,7 @@ __device__ __noinline__ void pipe_produce(const KGeom& G, const CUtensorMap* map
           mbar_expect_tx(&pp.full[slot], box_bytes);
           tma_load(bufs + slot * stage_elems, map, G.tma_rank, c, &pp.full[slot]);
           ++it;
+        }
         }
       }
     }

@@ -282,31 +282,39 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
 }
 
 // ---------------------------------------------------------------- K4 -----
-// The pencil's 2^KO x gtr LUTs (and ranges) are staged in shared memory once
-// per cell.  Each thread owns a fixed 4-voxel column, so its 2^KT trailing
-// corner tiles and weights are registers; outer weights come per row from
-// the exact half-integer distances (d_lo = twice_dlo / 2).  FP32 sum.
+// One cell pencil (2^KO outer corners x every trailing tile) per unit; its
+// LUTs, edge tables and {lo, c} pairs are staged in shared memory (rows padded
+// to n+1 floats so different tiles start in different banks).  A stage holds
+// R rows x one 32-float segment of the trailing block, TMA-loaded with the
+// 128B swizzle.  Work item = (16-byte column, 32 rows): a warp owns one column
+// -- so its 2^D corner tiles, ranges and trailing weights are warp-uniform --
+// and each lane one row (outer weights per lane; neighbouring rows gather
+// correlated bins).  The corner weights are products of per-dimension factors
+// d/b with exact half-integer numerators; FP32 sum (the reference's sorted
+// f64 sum is reproduced to <= 1e-6).
 template <int KO, int KT, bool ADAPT>
 __global__ void __launch_bounds__(kBlendThreads, 1)
     k_interp_pencil(const __grid_constant__ KGeom G, const __grid_constant__ CUtensorMap tmap,
                     const float* __restrict__ in, float* __restrict__ out,
                     const int32_t* __restrict__ units, const int32_t* __restrict__ cta_units, WS W) {
   constexpr int NCO = 1 << KO, NCT = 1 << KT;
+  constexpr int NW = kConsumersBlend / 32;
   if (W.range[2] != 0) return;  // non-finite input: write nothing
-  extern __shared__ __align__(128) unsigned char smem[];
+  extern __shared__ __align__(1024) unsigned char smem[];
   const PencilSmem P = pencil_smem(G, smem);
   const int n = G.n_bins;
-  const int64_t gtr = G.gtr;
-  // LUTs and edge tables with row stride n+1: rows of consecutive tiles start
-  // in different banks, so lanes gathering the same bin of different tiles
-  // do not conflict.
   const int n1 = n + 1;
+  const int64_t gtr = G.gtr;
   float* lutS = reinterpret_cast<float*>(P.tail);  // [NCO][gtr][n1]
   float* thrS = lutS + NCO * gtr * n1;  // edge tables: [NCO][gtr][n1] (adaptive) or [n1]
   float2* lcS = reinterpret_cast<float2*>(  // [NCO][gtr] {lo, c} (adaptive)
       P.tail + (((ADAPT ? 2 * NCO * gtr * n1 : NCO * gtr * n1 + n1) * 4 + 15) & ~15LL));
+  // per trailing column: first corner tile and the 4 x NCT trailing weights
+  const int ncol = (int)(G.P / 4);
+  int* colT = reinterpret_cast<int*>(lcS + NCO * gtr);
+  float* colW = reinterpret_cast<float*>(colT + ncol);  // [ncol][4][NCT]
   __shared__ int s_bad;
-  pipe_init(*P.pipe, G.nst, kConsumersBlend / 32);
+  pipe_init(*P.pipe, G.nst, NW);
   __syncthreads();
   const int u0 = cta_units[blockIdx.x], u1 = cta_units[blockIdx.x + 1];
   if (threadIdx.x >= kConsumersBlend) {
@@ -314,48 +322,55 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
       pipe_produce<KO, true>(G, &tmap, units, u0, u1, *P.pipe, P.bufs);
     return;
   }
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const TileParam<float>* tparams = reinterpret_cast<const TileParam<float>*>(W.tparams);
   const float2 glc = tile_lc(tparams[0]);
   bool patho = !ADAPT && isnan(glc.y);  // a range the float guard does not cover
-  const int tid = threadIdx.x;
-  const int slot = tid / G.tpr;
-  const int64_t e0 = (int64_t)(tid % G.tpr) * 4;
-  const bool lane_on = slot < G.rpi;  // rpi = kConsumersBlend / tpr for this kernel
 
-  // The plan only picks this kernel when a thread's 4 columns share their
-  // trailing cell (cell boundaries along the last dim are multiples of 4), so
-  // corner tiles are per thread and only the weights are per column.
-  int tt[NCT];
-  float tw[4][NCT];
+  // column table (independent of the unit): cells are shared by the column's
+  // 4 voxels (the plan checks cell boundaries along the last dim are x4)
+  for (int col = tid; col < ncol; col += kConsumersBlend) {
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    int64_t e = e0 + i;
-    int64_t c[KT];
-    float f1[KT];
+    for (int i = 0; i < 4; ++i) {
+      int64_t e = (int64_t)col * 4 + i;
+      int64_t c[KT];
+      float f1[KT];
 #pragma unroll
-    for (int q = KT - 1; q >= 0; --q) {
-      const int j = G.rank - KT + q;
-      const int64_t x = e % G.d[j].s;
-      e /= G.d[j].s;
-      c[q] = cell_of(G.d[j], x);
-      f1[q] = (float)twice_dlo(G.d[j], x, c[q]) / (float)(2 * G.d[j].b);
-    }
-#pragma unroll
-    for (int ct = 0; ct < NCT; ++ct) {
-      int64_t t = 0;
-      float w = 1.0f;
-#pragma unroll
-      for (int q = 0; q < KT; ++q) {
-        const int bit = (ct >> (KT - 1 - q)) & 1;
-        t += (c[q] + bit) * G.tstride[G.rank - KT + q];
-        w *= bit ? f1[q] : (1.0f - f1[q]);
+      for (int q = KT - 1; q >= 0; --q) {
+        const int j = G.rank - KT + q;
+        const int64_t x = e % G.d[j].s;
+        e /= G.d[j].s;
+        c[q] = cell_of(G.d[j], x);
+        f1[q] = (float)twice_dlo(G.d[j], x, c[q]) / (float)(2 * G.d[j].b);
       }
-      if (i == 0) tt[ct] = (int)t;
-      tw[i][ct] = w;
+      if (i == 0) {
+        int64_t t = 0;
+#pragma unroll
+        for (int q = 0; q < KT; ++q) t += c[q] * G.tstride[G.rank - KT + q];
+        colT[col] = (int)t;
+      }
+#pragma unroll
+      for (int ct = 0; ct < NCT; ++ct) {
+        float w = 1.0f;
+#pragma unroll
+        for (int q = 0; q < KT; ++q) w *= ((ct >> (KT - 1 - q)) & 1) ? f1[q] : (1.0f - f1[q]);
+        colW[(col * 4 + i) * NCT + ct] = w;
+      }
     }
+  }
+  // trailing corner ct of a column's first tile: + bit_q * tstride[D-KT+q]
+  int ctoff[NCT];
+#pragma unroll
+  for (int ct = 0; ct < NCT; ++ct) {
+    int o = 0;
+#pragma unroll
+    for (int q = 0; q < KT; ++q) o += ((ct >> (KT - 1 - q)) & 1) * (int)G.tstride[G.rank - KT + q];
+    ctoff[ct] = o;
   }
 
   const int64_t stage_elems = G.stage_stride;
+  const int rows = G.stage_rows;
+  const int nrb = (rows + 31) >> 5;
   int64_t cur = -1;
   uint32_t it = 0;
   while (true) {
@@ -398,68 +413,77 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
       if (ADAPT) patho = s_bad != 0;
       cur = key;
     }
-    const int rows = G.stage_rows;
-    const float* buf = P.bufs + s * stage_elems;
-    if (lane_on) {
-      // Per-dimension factor f_j(x) = d_lo/b = (2(x + before) - 2cb - b + 1) / 2b
-      //                             = x * (1/b) + t_j   (exact half-integer numerators)
-      // Dims < KO-2 are fixed for the stage; dims KO-2 / KO-1 vary by row.
-      float wfix[NCO / (KO >= 2 ? 4 : 2)];
-      float s1, t1, s2 = 0.f, t2 = 0.f;
-      int64_t obase = e0;
-      {
-        float ff[KO];
+    // stage geometry: factor f_j(x) = x / b + t_j (exact half-integer numerators)
+    float wfix[NCO / (KO >= 2 ? 4 : 2)];
+    float s1, t1, s2 = 0.f, t2 = 0.f;
+    int64_t obase = 0;
+    {
+      float ff[KO];
 #pragma unroll
-        for (int j = 0; j < KO; ++j) {
-          const Dim& d = G.d[j];
-          const float sj = 1.0f / (float)d.b;
-          const float tj = (float)(2 * d.before - 2 * (int64_t)S.cell[j] * d.b - d.b + 1) /
-                           (float)(2 * d.b);
-          if (j == KO - 1) { s1 = sj; t1 = tj; }
-          else if (j == KO - 2) { s2 = sj; t2 = tj; }
-          else {
-            ff[j] = fmaf((float)S.x[j], sj, tj);
-            obase += (int64_t)(j == 0 ? S.x[j] - G.row0 : S.x[j]) * G.vstride[j];
-          }
-        }
-        constexpr int NF = NCO / (KO >= 2 ? 4 : 2);
-#pragma unroll
-        for (int cf = 0; cf < NF; ++cf) {
-          float w = 1.0f;
-#pragma unroll
-          for (int j = 0; j < KO - 2; ++j)
-            w *= ((cf >> (KO - 3 - j)) & 1) ? ff[j] : 1.0f - ff[j];
-          wfix[cf] = w;
+      for (int j = 0; j < KO; ++j) {
+        const Dim& d = G.d[j];
+        const float sj = 1.0f / (float)d.b;
+        const float tj =
+            (float)(2 * d.before - 2 * (int64_t)S.cell[j] * d.b - d.b + 1) / (float)(2 * d.b);
+        if (j == KO - 1) {
+          s1 = sj;
+          t1 = tj;
+        } else if (j == KO - 2) {
+          s2 = sj;
+          t2 = tj;
+        } else {
+          ff[j] = fmaf((float)S.x[j], sj, tj);
+          obase += (int64_t)(j == 0 ? S.x[j] - G.row0 : S.x[j]) * G.vstride[j];
         }
       }
-      const int xb1 = S.x[KO - 1], xb2 = KO >= 2 ? S.x[KO >= 2 ? KO - 2 : 0] : 0;
-      const int64_t vs1 = G.vstride[KO - 1], vs2 = KO >= 2 ? G.vstride[KO >= 2 ? KO - 2 : 0] : 0;
-      const int64_t r0 = (KO == 1 ? G.row0 : 0), r0b = (KO == 2 ? G.row0 : 0);
-      const int tile_stride = (int)(gtr * n1);  // floats between outer corners
-      for (int q = slot; q < rows; q += G.rpi) {
+      constexpr int NF = NCO / (KO >= 2 ? 4 : 2);
+#pragma unroll
+      for (int cf = 0; cf < NF; ++cf) {
+        float w = 1.0f;
+#pragma unroll
+        for (int j = 0; j < KO - 2; ++j) w *= ((cf >> (KO - 3 - j)) & 1) ? ff[j] : 1.0f - ff[j];
+        wfix[cf] = w;
+      }
+    }
+    const int xb1 = S.x[KO - 1], xb2 = KO >= 2 ? S.x[KO >= 2 ? KO - 2 : 0] : 0;
+    const int64_t vs1 = G.vstride[KO - 1], vs2 = KO >= 2 ? G.vstride[KO >= 2 ? KO - 2 : 0] : 0;
+    const int64_t r0 = (KO == 1 ? G.row0 : 0), r0b = (KO == 2 ? G.row0 : 0);
+    const int seg = S.seg;
+    const unsigned char* buf = reinterpret_cast<const unsigned char*>(P.bufs + s * stage_elems);
+    for (int item = warp; item < 8 * nrb; item += NW) {
+      const int c = item & 7, rb = item >> 3;
+      const int q = rb * 32 + lane;
+      if (q < rows) {
+        const int col = seg * 8 + c;
+        const int tt = colT[col];
+        float tw[4][NCT];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int ct = 0; ct < NCT; ++ct) tw[i][ct] = colW[(col * 4 + i) * NCT + ct];
         const int r1 = q & (G.r1 - 1), r2 = q >> G.lg_r1;
         const int x1 = xb1 + r1, x2 = xb2 + r2;
-        const int64_t ooff = obase + (int64_t)(x1 - r0) * vs1 + (KO >= 2 ? (int64_t)(x2 - r0b) * vs2 : 0);
+        const int64_t ooff = obase + (int64_t)(x1 - r0) * vs1 +
+                             (KO >= 2 ? (int64_t)(x2 - r0b) * vs2 : 0) + col * 4;
         const float f1 = fmaf((float)x1, s1, t1);
         const float f2 = KO >= 2 ? fmaf((float)x2, s2, t2) : 0.f;
-        // outer corner weights: fixed dims x (dim KO-2) x (dim KO-1)
         float wo[NCO];
         {
           const float g1[2] = {1.0f - f1, f1};
 #pragma unroll
           for (int co = 0; co < NCO; ++co) {
-            const int b1 = co & 1;
-            float w = g1[b1];
+            float w = g1[co & 1];
             if (KO >= 2) w *= ((co >> 1) & 1) ? f2 : 1.0f - f2;
             wo[co] = w * wfix[co >> (KO >= 2 ? 2 : 1)];
           }
         }
-        const float4 v4 = *reinterpret_cast<const float4*>(buf + q * G.P + e0);
+        // 128B-swizzled stage row: 16-byte chunk c of row q sits at c ^ (q & 7)
+        const float4 v4 =
+            *reinterpret_cast<const float4*>(buf + q * 128 + ((c ^ (q & 7)) << 4));
         const u64 V01 = pk2(v4.x, v4.y), V23 = pk2(v4.z, v4.w);
         float acc[4] = {0.f, 0.f, 0.f, 0.f};
-        int off[NCT][4];  // float offset of (trailing corner, column) in an outer corner's LUTs
+        int bg[4];
         if (!ADAPT) {
-          int bg[4];
           if (!patho) {
             bins2_edge(V01, v4.x, v4.y, glc, thrS, n, bg[0], bg[1]);
             bins2_edge(V23, v4.z, v4.w, glc, thrS, n, bg[2], bg[3]);
@@ -469,19 +493,15 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
             bg[2] = bin_search(v4.z, thrS, n);
             bg[3] = bin_search(v4.w, thrS, n);
           }
-#pragma unroll
-          for (int ct = 0; ct < NCT; ++ct)
-#pragma unroll
-            for (int i = 0; i < 4; ++i) off[ct][i] = tt[ct] * n1 + bg[i];
         }
 #pragma unroll
         for (int co = 0; co < NCO; ++co) {
-          const float* Lco = lutS + co * tile_stride;
           float m[NCT][4];
 #pragma unroll
           for (int ct = 0; ct < NCT; ++ct) {
+            const int tile = co * (int)gtr + tt + ctoff[ct];  // warp-uniform
+            const float* L = lutS + tile * n1;
             if (ADAPT) {
-              const int tile = co * gtr + tt[ct];
               const float2 lc = lcS[tile];
               const float* th = thrS + tile * n1;
               int b[4];
@@ -495,13 +515,12 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
                 b[3] = bin_search(v4.w, th, n);
               }
 #pragma unroll
-              for (int i = 0; i < 4; ++i) m[ct][i] = Lco[tt[ct] * n1 + b[i]];
+              for (int i = 0; i < 4; ++i) m[ct][i] = L[b[i]];
             } else {
 #pragma unroll
-              for (int i = 0; i < 4; ++i) m[ct][i] = Lco[off[ct][i]];
+              for (int i = 0; i < 4; ++i) m[ct][i] = L[bg[i]];
             }
           }
-          // multilinear blend of the trailing corners, then the outer weight
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
             float mi = 0.f;
@@ -519,7 +538,7 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
       }
     }
     __syncwarp();
-    if ((tid & 31) == 0) mbar_arrive(&P.pipe->empty[s]);
+    if (lane == 0) mbar_arrive(&P.pipe->empty[s]);
     ++it;
   }
 }

@@ -91,13 +91,14 @@ struct Pencil {
   int nst = 0, stage_rows = 0;
   int r1 = 1, lg_r1 = 0, r2 = 1;  // TMA box rows along outer dims KO-1, KO-2
   int tma_rank = 0, width = 0;    // TMA view: [outer dims..., P/width, width]
+  int nseg = 1;                   // blend: 32-float segments per trailing block
   int64_t stage_stride = 0;       // floats per stage buffer
   int64_t tail = 0;               // kernel-specific shared memory (hist / LUTs)
   int64_t stage_budget = 0;
   int64_t smem = 0;
 };
 
-constexpr int64_t kPipeBytes = (sizeof(mg::Pipe) + 127) & ~int64_t(127);
+constexpr int64_t kPipeBytes = (sizeof(mg::Pipe) + 1023) & ~int64_t(1023);
 constexpr int64_t kStageBytes = 16384;
 
 }  // namespace
@@ -138,6 +139,7 @@ KGeom pencil_geom(const mclahe_plan_s& pl, const Pencil& pc) {
   G.lg_r1 = pc.lg_r1;
   G.r2 = pc.r2;
   G.tma_rank = pc.tma_rank;
+  G.nseg = pc.nseg;
   G.stage_stride = pc.stage_stride;
   return G;
 }
@@ -187,7 +189,10 @@ Pencil choose_pencil(const mclahe_plan_s& pl, bool for_hist) {
       if (c.tail > 64 * 1024) continue;
       c.stage_budget = kStageBytes;  // 3 stages, ~3 CTAs per SM
     } else {
-      if (n % 4 != 0) continue;
+      if (n % 4 != 0 || c.P % 32 != 0) continue;
+      c.nseg = (int)(c.P / 32);
+      c.tma_rank = ko + (c.nseg > 1 ? 2 : 1);
+      if (c.tma_rank > 5) continue;
       // a thread's 4 columns must share their trailing cell
       const Dim& dl = pl.d[D - 1];
       if (dl.s % 4 != 0) continue;
@@ -202,7 +207,7 @@ Pencil choose_pencil(const mclahe_plan_s& pl, bool for_hist) {
       // + per-tile ranges; one CTA per SM with 16 consumer warps
       const int64_t luts1 = (int64_t{1} << ko) * c.gtr * (n + 1);  // rows padded to n+1
       c.tail = align_up((pl.p.adaptive ? 2 * luts1 : luts1 + n + 1) * 4, 16) +
-               (int64_t{1} << ko) * c.gtr * 16;
+               (int64_t{1} << ko) * c.gtr * 16 + (c.P / 4) * (4 + 16 * (int64_t{1} << kt));
       c.rpi = kConsumersBlend / c.tpr;
       const int64_t avail = 226 * 1024 - kPipeBytes - c.tail;
       if (avail >= 4 * 4096) c.stage_budget = std::min<int64_t>(kStageBytes, avail / 4);
@@ -260,22 +265,31 @@ void extents(const mclahe_plan_s& pl, bool cells, int j, std::vector<std::pair<i
 // Box rows (powers of two dividing every unit extent, so boxes never cross a
 // unit), pipeline depth and shared memory of a pencil family.
 void size_boxes(const mclahe_plan_s& pl, Pencil& c, bool cells) {
-  const int64_t rows_cap = std::max<int64_t>(1, std::min<int64_t>(c.stage_budget / (c.P * 4), 256));
+  const int64_t row_bytes = cells ? 128 : c.P * 4;  // blend stages hold one 32-float segment
+  const int64_t rows_cap = std::max<int64_t>(1, std::min<int64_t>(c.stage_budget / row_bytes, 256));
   std::vector<std::pair<int64_t, int64_t>> ex;
   int64_t g1 = 0, g2 = 0;
   extents(pl, cells, c.ko - 1, ex);
   for (auto& p : ex) g1 = gcd64(g1, p.second - p.first);
-  c.r1 = (int)pow2_divisor(g1, std::min<int64_t>(rows_cap, 256));
+  // when dim 0 is a box dim (KO <= 2) keep >= ~2 units per SM: cap its box rows
+  int64_t n_other = 1;
+  for (int j = 1; j < c.ko; ++j) n_other *= cells ? pl.d[j].g - 1 : pl.d[j].g;
+  const int64_t local_rows = pl.info.row_end - pl.info.row_begin;
+  int64_t cap0 = 1;
+  while (cap0 * 2 <= std::max<int64_t>(1, local_rows * n_other / 296)) cap0 *= 2;
+  c.r1 = (int)pow2_divisor(g1, std::min<int64_t>(std::min<int64_t>(rows_cap, 256),
+                                                 c.ko == 1 ? cap0 : 256));
   c.r2 = 1;
   if (c.ko >= 2) {
     extents(pl, cells, c.ko - 2, ex);
     for (auto& p : ex) g2 = gcd64(g2, p.second - p.first);
-    c.r2 = (int)pow2_divisor(g2, std::min<int64_t>(rows_cap / c.r1, 256));
+    c.r2 = (int)pow2_divisor(g2, std::min<int64_t>(std::min<int64_t>(rows_cap / c.r1, 256),
+                                                   c.ko == 2 ? cap0 : 256));
   }
   c.lg_r1 = 0;
   while ((1 << c.lg_r1) < c.r1) ++c.lg_r1;
   c.stage_rows = c.r1 * c.r2;
-  c.stage_stride = align_up(c.stage_rows * c.P * 4, 128) / 4;
+  c.stage_stride = cells ? align_up(c.stage_rows * 128, 1024) / 4 : align_up(c.stage_rows * c.P * 4, 128) / 4;
   const int64_t stage = c.stage_stride * 4;
   if (!cells) {
     c.nst = 3;
@@ -391,7 +405,8 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
-// [outer dims KO-1..0 with strides][P/width][width], box [R2 x R1 rows][P].
+// K2: [outer dims KO-1..0][P/width][width], box [R2 x R1 rows][P].
+// K4: [outer dims KO-1..0][P/32 segments][32], box [R2 x R1 rows][1][32], 128B swizzle.
 int tensor_map(mclahe_plan_s* pl, int fam, const void* in) {
   if (pl->map_ptr[fam] == in) return MCLAHE_OK;
   const Pencil& c = fam == 0 ? pl->hist : pl->interp;
@@ -400,13 +415,15 @@ int tensor_map(mclahe_plan_s* pl, int fam, const void* in) {
   cuuint64_t dims[5], strides[5];
   cuuint32_t box[5], es[5];
   int r = 0;
-  dims[r] = (cuuint64_t)c.width;
-  box[r] = (cuuint32_t)c.width;
+  const bool seg = fam == 1;
+  const int64_t inner = seg ? 32 : c.width;
+  dims[r] = (cuuint64_t)inner;
+  box[r] = (cuuint32_t)inner;
   ++r;
   if (c.tma_rank - c.ko == 2) {
-    dims[r] = (cuuint64_t)(c.P / c.width);
-    strides[r - 1] = (cuuint64_t)c.width * 4;
-    box[r] = (cuuint32_t)(c.P / c.width);
+    dims[r] = (cuuint64_t)(c.P / inner);
+    strides[r - 1] = (cuuint64_t)inner * 4;
+    box[r] = seg ? 1 : (cuuint32_t)(c.P / inner);
     ++r;
   }
   for (int j = c.ko - 1; j >= 0; --j) {
@@ -418,7 +435,8 @@ int tensor_map(mclahe_plan_s* pl, int fam, const void* in) {
   for (int i = 0; i < r; ++i) es[i] = 1;
   const CUresult res = enc(&pl->map[fam], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, (cuuint32_t)r,
                            const_cast<void*>(in), dims, strides, box, es,
-                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           seg ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (res != CUDA_SUCCESS)
     return fail(MCLAHE_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)res) + ")");
