@@ -240,6 +240,25 @@ __device__ __forceinline__ void bins2_edge(u64 V, float v0, float v1, float2 lc,
   b1 = v1 >= th[k1] ? k1 : k1 - 1;
 }
 
+// Same rule, fused with the LUT gather: returns LUT[bin] for two voxels.
+// thb / Lb are the tile's edge table and LUT (byte pointers, warp-uniform in
+// the blend kernel); n4 = 4 * n.  Byte offsets throughout so each gather is a
+// single LDS [reg + base].
+__device__ __forceinline__ void lut2_edge(u64 V, float v0, float v1, float2 lc, const char* thb,
+                                          const char* Lb, int n4, float& m0, float& m1) {
+  const u64 y = mul2(sub2(V, pk2(lc.x, lc.x)), pk2(lc.y, lc.y));
+  u64 t;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(t) : "l"(y), "l"(pk2(kMagic, kMagic)));
+  float t0, t1;
+  upk2(t, t0, t1);
+  const int k0 = min(max((__float_as_int(t0) - kMagicBits) << 2, 0), n4);
+  const int k1 = min(max((__float_as_int(t1) - kMagicBits) << 2, 0), n4);
+  const int b0 = v0 >= *reinterpret_cast<const float*>(thb + k0) ? k0 : k0 - 4;
+  const int b1 = v1 >= *reinterpret_cast<const float*>(thb + k1) ? k1 : k1 - 4;
+  m0 = *reinterpret_cast<const float*>(Lb + b0);
+  m1 = *reinterpret_cast<const float*>(Lb + b1);
+}
+
 // Exact bin from the edge table alone (binary search over thr[1..n-1]);
 // used for ranges the float guard does not cover.
 __device__ __forceinline__ int bin_search(float v, const float* th, int n) {

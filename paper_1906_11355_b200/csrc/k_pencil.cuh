@@ -482,7 +482,7 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
             *reinterpret_cast<const float4*>(buf + q * 128 + ((c ^ (q & 7)) << 4));
         const u64 V01 = pk2(v4.x, v4.y), V23 = pk2(v4.z, v4.w);
         float acc[4] = {0.f, 0.f, 0.f, 0.f};
-        int bg[4];
+        int bg[4] = {0, 0, 0, 0};
         if (!ADAPT) {
           if (!patho) {
             bins2_edge(V01, v4.x, v4.y, glc, thrS, n, bg[0], bg[1]);
@@ -494,39 +494,66 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
             bg[3] = bin_search(v4.w, thrS, n);
           }
         }
+        const int n4 = 4 * n;
+        if (ADAPT && !patho) {  // hot path: branch-free edge-table gathers
 #pragma unroll
-        for (int co = 0; co < NCO; ++co) {
-          float m[NCT][4];
+          for (int co = 0; co < NCO; ++co) {
+            float m[NCT][4];
 #pragma unroll
-          for (int ct = 0; ct < NCT; ++ct) {
-            const int tile = co * (int)gtr + tt + ctoff[ct];  // warp-uniform
-            const float* L = lutS + tile * n1;
-            if (ADAPT) {
+            for (int ct = 0; ct < NCT; ++ct) {
+              const int tile = co * (int)gtr + tt + ctoff[ct];  // warp-uniform
               const float2 lc = lcS[tile];
-              const float* th = thrS + tile * n1;
-              int b[4];
-              if (!patho || !isnan(lc.y)) {
-                bins2_edge(V01, v4.x, v4.y, lc, th, n, b[0], b[1]);
-                bins2_edge(V23, v4.z, v4.w, lc, th, n, b[2], b[3]);
-              } else {
-                b[0] = bin_search(v4.x, th, n);
-                b[1] = bin_search(v4.y, th, n);
-                b[2] = bin_search(v4.z, th, n);
-                b[3] = bin_search(v4.w, th, n);
-              }
+              const char* thb = reinterpret_cast<const char*>(thrS + tile * n1);
+              const char* Lb = reinterpret_cast<const char*>(lutS + tile * n1);
+              lut2_edge(V01, v4.x, v4.y, lc, thb, Lb, n4, m[ct][0], m[ct][1]);
+              lut2_edge(V23, v4.z, v4.w, lc, thb, Lb, n4, m[ct][2], m[ct][3]);
+            }
 #pragma unroll
-              for (int i = 0; i < 4; ++i) m[ct][i] = L[b[i]];
-            } else {
+            for (int i = 0; i < 4; ++i) {
+              float mi = 0.f;
 #pragma unroll
-              for (int i = 0; i < 4; ++i) m[ct][i] = L[bg[i]];
+              for (int ct = 0; ct < NCT; ++ct) mi = fmaf(tw[i][ct], m[ct][i], mi);
+              acc[i] = fmaf(wo[co], mi, acc[i]);
             }
           }
+        } else {
+          int bo[4];  // global mode: byte offsets of the voxel's bin
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            float mi = 0.f;
+          for (int i = 0; i < 4; ++i) bo[i] = bg[i] * 4;
 #pragma unroll
-            for (int ct = 0; ct < NCT; ++ct) mi = fmaf(tw[i][ct], m[ct][i], mi);
-            acc[i] = fmaf(wo[co], mi, acc[i]);
+          for (int co = 0; co < NCO; ++co) {
+            float m[NCT][4];
+#pragma unroll
+            for (int ct = 0; ct < NCT; ++ct) {
+              const int tile = co * (int)gtr + tt + ctoff[ct];  // warp-uniform
+              const char* Lb = reinterpret_cast<const char*>(lutS + tile * n1);
+              if (ADAPT) {  // a pathological range in the pencil: exact search
+                const float2 lc = lcS[tile];
+                const float* th = thrS + tile * n1;
+                int b[4];
+                if (!isnan(lc.y)) {
+                  bins2_edge(V01, v4.x, v4.y, lc, th, n, b[0], b[1]);
+                  bins2_edge(V23, v4.z, v4.w, lc, th, n, b[2], b[3]);
+                } else {
+                  b[0] = bin_search(v4.x, th, n);
+                  b[1] = bin_search(v4.y, th, n);
+                  b[2] = bin_search(v4.z, th, n);
+                  b[3] = bin_search(v4.w, th, n);
+                }
+#pragma unroll
+                for (int i = 0; i < 4; ++i) m[ct][i] = *reinterpret_cast<const float*>(Lb + 4 * b[i]);
+              } else {
+#pragma unroll
+                for (int i = 0; i < 4; ++i) m[ct][i] = *reinterpret_cast<const float*>(Lb + bo[i]);
+              }
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              float mi = 0.f;
+#pragma unroll
+              for (int ct = 0; ct < NCT; ++ct) mi = fmaf(tw[i][ct], m[ct][i], mi);
+              acc[i] = fmaf(wo[co], mi, acc[i]);
+            }
           }
         }
         float4 r;
