@@ -277,6 +277,7 @@ void size_boxes(const mclahe_plan_s& pl, Pencil& c, bool cells) {
   const int64_t local_rows = pl.info.row_end - pl.info.row_begin;
   int64_t cap0 = 1;
   while (cap0 * 2 <= std::max<int64_t>(1, local_rows * n_other / 296)) cap0 *= 2;
+  if (cells) cap0 = std::max<int64_t>(cap0, 32);  // blend: keep a warp's worth of rows per box
   c.r1 = (int)pow2_divisor(g1, std::min<int64_t>(std::min<int64_t>(rows_cap, 256),
                                                  c.ko == 1 ? cap0 : 256));
   c.r2 = 1;
