@@ -103,11 +103,12 @@ __global__ void __launch_bounds__(256) k_global_range(const T* __restrict__ in, 
 }
 
 // --------------------------------------------------------------- params ---
+// Window tiles [t0, t0 + nt) (adaptive) or the single global range.
 template <typename T>
-__global__ void k_params(const KGeom G, WS W) {
+__global__ void k_params(const KGeom G, WS W, int64_t t0, int64_t nt) {
   TileParam<T>* tp = reinterpret_cast<TileParam<T>*>(W.tparams);
-  const int64_t n = G.adaptive ? G.win_tiles : 1;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+  const int64_t n = G.adaptive ? t0 + nt : 1;
+  for (int64_t t = (G.adaptive ? t0 : 0) + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
        t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t* r = G.adaptive ? W.trange + 2 * t : W.range;
     const double lo = okey_decode(~r[0]);
@@ -170,13 +171,14 @@ __global__ void __launch_bounds__(256) k_tiles_generic(const KGeom G, const T* _
 // the CDF prefix (histogram.cpp:59-63, one lane, sequential).  Everything else
 // is bin-parallel.  Output: f32 LUT (+ optional f64 debug arrays).
 template <typename T>
-__global__ void __launch_bounds__(128) k_mappings(const KGeom G, WS W, Debug Dbg) {
+__global__ void __launch_bounds__(128) k_mappings(const KGeom G, WS W, Debug Dbg, int64_t t0,
+                                                  int64_t nt) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int n = G.n_bins;
   const int warps = blockDim.x >> 5, wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double* cdf = reinterpret_cast<double*>(smem) + (int64_t)wid * n;
   const TileParam<T>* tparams = reinterpret_cast<const TileParam<T>*>(W.tparams);
-  for (int64_t tile = (int64_t)blockIdx.x * warps + wid; tile < G.win_tiles;
+  for (int64_t tile = t0 + (int64_t)blockIdx.x * warps + wid; tile < t0 + nt;
        tile += (int64_t)gridDim.x * warps) {
     const TileParam<T> tp = tparams[G.adaptive ? tile : 0];
     const uint32_t* cnt = W.counts + tile * n;
@@ -292,11 +294,12 @@ __global__ void __launch_bounds__(256) k_interp_generic(const KGeom G, const T* 
 // ------------------------------------------------------- debug binning ---
 // Bin-edge tables for every binning range (f32 data): thr[t][k] = smallest
 // float whose reference bin is >= k; thr[t][0] = -inf.
-__global__ void k_thresholds(const KGeom G, WS W) {
+__global__ void k_thresholds(const KGeom G, WS W, int64_t t0, int64_t nt) {
   const TileParam<float>* tp = reinterpret_cast<const TileParam<float>*>(W.tparams);
   const int n = G.n_bins, n1 = n + 1;
-  const int64_t total = (G.adaptive ? G.win_tiles : 1) * (int64_t)n1;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+  const int64_t first = (G.adaptive ? t0 : 0) * (int64_t)n1;
+  const int64_t total = first + (G.adaptive ? nt : 1) * (int64_t)n1;
+  for (int64_t i = first + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t t = i / n1;
     const int k = (int)(i - t * n1);

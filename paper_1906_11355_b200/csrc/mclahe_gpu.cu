@@ -122,6 +122,12 @@ struct mclahe_plan_s {
   const void* map_ptr[2] = {nullptr, nullptr};
   CUtensorMap map[2];
   bool f32() const { return p.dtype == MCLAHE_F32; }
+  mclahe_plan_s() = default;
+  mclahe_plan_s(const mclahe_plan_s&) = delete;
+  mclahe_plan_s& operator=(const mclahe_plan_s&) = delete;
+  ~mclahe_plan_s() {
+    if (d_tables) cudaFree(d_tables);
+  }
 };
 
 namespace {
@@ -445,8 +451,11 @@ int tensor_map(mclahe_plan_s* pl, int fam, const void* in) {
   return MCLAHE_OK;
 }
 
+// full_window: the workspace holds every tile row (chunks of a streamed
+// single-GPU run share one workspace); otherwise only the rows the slab
+// counts into or blends from.
 int plan_describe(const mclahe_params_t* params, int64_t row_begin, int64_t row_end,
-                  mclahe_plan_s* pl) {
+                  mclahe_plan_s* pl, bool full_window = false) {
   int rc = validate(params);
   if (rc) return rc;
   if (row_begin < 0 || row_end > params->shape[0] || row_begin >= row_end)
@@ -480,8 +489,8 @@ int plan_describe(const mclahe_params_t* params, int64_t row_begin, int64_t row_
   I.count_row_end = ce;
   I.need_row_begin = cell_of(pl->d[0], row_begin);
   I.need_row_end = cell_of(pl->d[0], row_end - 1) + 2;
-  I.tile_row_begin = std::min(I.count_row_begin, I.need_row_begin);
-  I.tile_row_end = std::max(I.count_row_end, I.need_row_end);
+  I.tile_row_begin = full_window ? 0 : std::min(I.count_row_begin, I.need_row_begin);
+  I.tile_row_end = full_window ? pl->d[0].g : std::max(I.count_row_end, I.need_row_end);
   I.tiles_per_row = I.tiles / pl->d[0].g;
   const int64_t win_tiles = (I.tile_row_end - I.tile_row_begin) * I.tiles_per_row;
   const int64_t n = params->n_bins;
@@ -672,17 +681,21 @@ int do_range(mclahe_plan_s* pl, const void* in, void* ws, cudaStream_t st) {
   return MCLAHE_OK;
 }
 
-int do_params(mclahe_plan_s* pl, void* ws, cudaStream_t st) {
+// Binning parameters + edge tables for window tiles [t0, t0 + nt) (adaptive;
+// nt < 0: the whole window) or the global range.
+int do_params(mclahe_plan_s* pl, void* ws, cudaStream_t st, int64_t t0 = 0, int64_t nt = -1) {
   WS W = ws_view(pl, ws);
-  const int64_t n = pl->p.adaptive ? pl->G.win_tiles : 1;
+  if (nt < 0) nt = pl->G.win_tiles - t0;
+  if (pl->p.adaptive && nt <= 0) return MCLAHE_OK;
+  const int64_t n = pl->p.adaptive ? nt : 1;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + 127) / 128, 4096));
-  if (pl->f32()) k_params<float><<<grid, 128, 0, st>>>(pl->G, W);
-  else k_params<double><<<grid, 128, 0, st>>>(pl->G, W);
+  if (pl->f32()) k_params<float><<<grid, 128, 0, st>>>(pl->G, W, t0, nt);
+  else k_params<double><<<grid, 128, 0, st>>>(pl->G, W, t0, nt);
   MG_LAUNCHED();
   if (pl->f32()) {
     const int64_t total = n * (pl->p.n_bins + 1);
     const int tg = (int)std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 8192));
-    k_thresholds<<<tg, 256, 0, st>>>(pl->G, W);
+    k_thresholds<<<tg, 256, 0, st>>>(pl->G, W, t0, nt);
     MG_LAUNCHED();
   }
   return MCLAHE_OK;
@@ -714,7 +727,11 @@ int do_hist(mclahe_plan_s* pl, const void* in, void* ws, cudaStream_t st) {
   return MCLAHE_OK;
 }
 
-int do_map(mclahe_plan_s* pl, void* ws, const mclahe_debug_t* dbg, cudaStream_t st) {
+// Mappings of window tiles [t0, t0 + nt) (nt < 0: the whole window).
+int do_map(mclahe_plan_s* pl, void* ws, const mclahe_debug_t* dbg, cudaStream_t st,
+           int64_t t0 = 0, int64_t nt = -1) {
+  if (nt < 0) nt = pl->G.win_tiles - t0;
+  if (nt <= 0) return MCLAHE_OK;
   WS W = ws_view(pl, ws);
   Debug D{};
   if (dbg) {
@@ -727,8 +744,10 @@ int do_map(mclahe_plan_s* pl, void* ws, const mclahe_debug_t* dbg, cudaStream_t 
     if ((D.lo == nullptr) != (D.hi == nullptr))
       return fail(MCLAHE_ERR_VALIDATION, "debug lo and hi must both be set or both NULL");
   }
-  if (pl->f32()) k_mappings<float><<<pl->map_grid, pl->map_block, pl->map_smem, st>>>(pl->G, W, D);
-  else k_mappings<double><<<pl->map_grid, pl->map_block, pl->map_smem, st>>>(pl->G, W, D);
+  const int warps = pl->map_block / 32;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((nt + warps - 1) / warps, pl->map_grid));
+  if (pl->f32()) k_mappings<float><<<grid, pl->map_block, pl->map_smem, st>>>(pl->G, W, D, t0, nt);
+  else k_mappings<double><<<grid, pl->map_block, pl->map_smem, st>>>(pl->G, W, D, t0, nt);
   MG_LAUNCHED();
   return MCLAHE_OK;
 }
@@ -783,6 +802,157 @@ int check_ptrs(const mclahe_plan_s* pl, const void* in, const void* out) {
   return MCLAHE_OK;
 }
 
+int64_t elem_size(const mclahe_params_t* p) { return p->dtype == MCLAHE_F64 ? 8 : 4; }
+
+int64_t volume(const mclahe_params_t* p) {
+  int64_t n = 1;
+  for (int i = 0; i < p->rank; ++i) n *= p->shape[i];
+  return n;
+}
+
+// ---- streamed one-shot (single GPU): chunked H2D -> passes -> D2H -------
+// The volume is cut into cell-aligned chunks along dim 0, each with its own
+// full-window plan over ONE shared workspace (counts and range keys are
+// combined by the kernels' atomics).  H2D, compute and D2H run on three
+// streams so PCIe in both directions overlaps the kernels; a pass for a tile
+// row runs as soon as every chunk its support meets has been through the
+// previous pass.
+struct Streamed {
+  std::vector<std::unique_ptr<mclahe_plan_s>> chunks;
+  std::vector<int64_t> cuts;      // chunk row boundaries (C + 1)
+  std::vector<int> last_chunk;    // per tile row: last chunk its support meets
+  int64_t tiles_per_row = 0;
+};
+
+int build_streamed(const mclahe_params_t* p, Streamed& S) {
+  const Dim d0 = make_dim(p->shape[0], p->kernel[0]);
+  std::vector<std::pair<int64_t, int64_t>> cells;
+  for (int64_t c = 0; c + 1 < d0.g; ++c) {
+    int64_t a, e;
+    cell_range(d0, c, &a, &e);
+    if (e > a) cells.push_back({a, e});
+  }
+  const int64_t bytes = volume(p) * elem_size(p);
+  const int C = (int)std::max<int64_t>(
+      1, std::min<int64_t>({(int64_t)cells.size(), 8, std::max<int64_t>(1, bytes / (8 << 20))}));
+  if (C < 2) return MCLAHE_ERR_UNSUPPORTED;
+  S.cuts.assign(1, 0);
+  for (int k = 1; k <= C; ++k) {
+    const size_t idx = (size_t)((int64_t)cells.size() * k / C) - 1;
+    S.cuts.push_back(cells[idx].second);
+  }
+  S.chunks.clear();
+  for (int k = 0; k < C; ++k) {
+    auto pl = std::make_unique<mclahe_plan_s>();
+    const int rc = plan_describe(p, S.cuts[k], S.cuts[k + 1], pl.get(), true);
+    if (rc) return rc;
+    S.chunks.push_back(std::move(pl));
+  }
+  S.tiles_per_row = S.chunks[0]->info.tiles_per_row;
+  S.last_chunk.assign((size_t)d0.g, 0);
+  for (int64_t t = 0; t < d0.g; ++t) {
+    const TileParts tp = tile_parts(d0, t);
+    const int64_t last_row = tp.support_end() - 1;
+    int k = 0;
+    while (k + 1 < C && S.cuts[k + 1] <= last_row) ++k;
+    S.last_chunk[(size_t)t] = k;
+  }
+  return MCLAHE_OK;
+}
+
+int run_streamed(Streamed& S, const mclahe_params_t* p, const void* in, void* out, void* d_in,
+                 void* d_out, void* ws, cudaStream_t s_in, cudaStream_t s_comp, cudaStream_t s_out,
+                 std::vector<cudaEvent_t>& ev, mclahe_timings_t* timings) {
+  const int C = (int)S.chunks.size();
+  const int64_t row_bytes = volume(p) / p->shape[0] * elem_size(p);
+  const int64_t g0 = (int64_t)S.last_chunk.size();
+  const int64_t tpr = S.tiles_per_row;
+  const bool A = p->adaptive != 0;
+  mclahe_plan_s* M = S.chunks[0].get();  // any chunk plan: same full-window layout
+  int rc;
+  for (auto& c : S.chunks)
+    if ((rc = device_init(c.get()))) return rc;
+  // events: [0, C) inputs landed, [C, 2C) outputs ready, 2C / 2C+1 timing
+  for (int k = 0; k < C; ++k) {
+    const int64_t off = S.cuts[k] * row_bytes, len = (S.cuts[k + 1] - S.cuts[k]) * row_bytes;
+    MG_CUDA(cudaMemcpyAsync(static_cast<char*>(d_in) + off, static_cast<const char*>(in) + off,
+                            (size_t)len, cudaMemcpyHostToDevice, s_in));
+    MG_CUDA(cudaEventRecord(ev[k], s_in));
+  }
+  MG_CUDA(cudaEventRecord(ev[2 * C], s_comp));
+  if ((rc = do_reset(M, ws, s_comp))) return rc;
+  int ranged = 0, hist = 0, blended = 0;
+  int64_t params_rows = 0, mapped_rows = 0;
+  bool gparams = false;
+  float interp_ms = 0.f;
+  for (int k = 0; k < C; ++k) {
+    MG_CUDA(cudaStreamWaitEvent(s_comp, ev[k], 0));
+    mclahe_plan_s* pk = S.chunks[k].get();
+    const char* xk = static_cast<const char*>(d_in) + S.cuts[k] * row_bytes;
+    if ((rc = do_range(pk, xk, ws, s_comp))) return rc;
+    ranged = k + 1;
+    // binning parameters: tile rows whose support is fully ranged (adaptive),
+    // or the global range once every chunk is in
+    if (A) {
+      int64_t r = params_rows;
+      while (r < g0 && S.last_chunk[(size_t)r] < ranged) ++r;
+      if (r > params_rows) {
+        if ((rc = do_params(M, ws, s_comp, params_rows * tpr, (r - params_rows) * tpr))) return rc;
+        params_rows = r;
+      }
+    } else if (ranged == C && !gparams) {
+      if ((rc = do_params(M, ws, s_comp))) return rc;
+      gparams = true;
+    }
+    // histograms of chunks whose counted tile rows all have parameters
+    while (hist < C) {
+      mclahe_plan_s* ph = S.chunks[hist].get();
+      const bool ready = A ? ph->info.count_row_end <= params_rows : gparams;
+      if (!ready) break;
+      const char* xh = static_cast<const char*>(d_in) + S.cuts[hist] * row_bytes;
+      if ((rc = do_hist(ph, xh, ws, s_comp))) return rc;
+      ++hist;
+    }
+    // mappings of tile rows whose every counting chunk is done
+    int64_t r = mapped_rows;
+    while (r < g0 && S.last_chunk[(size_t)r] < hist) ++r;
+    if (r > mapped_rows) {
+      if ((rc = do_map(M, ws, nullptr, s_comp, mapped_rows * tpr, (r - mapped_rows) * tpr)))
+        return rc;
+      mapped_rows = r;
+    }
+    // blend + D2H of chunks whose tile rows are all mapped
+    while (blended < C && S.chunks[blended]->info.need_row_end <= mapped_rows) {
+      mclahe_plan_s* pb = S.chunks[blended].get();
+      const int64_t off = S.cuts[blended] * row_bytes;
+      const int64_t len = (S.cuts[blended + 1] - S.cuts[blended]) * row_bytes;
+      if ((rc = do_interp(pb, static_cast<const char*>(d_in) + off, static_cast<char*>(d_out) + off,
+                          ws, s_comp)))
+        return rc;
+      MG_CUDA(cudaEventRecord(ev[C + blended], s_comp));
+      MG_CUDA(cudaStreamWaitEvent(s_out, ev[C + blended], 0));
+      MG_CUDA(cudaMemcpyAsync(static_cast<char*>(out) + off, static_cast<char*>(d_out) + off,
+                              (size_t)len, cudaMemcpyDeviceToHost, s_out));
+      ++blended;
+    }
+  }
+  if (blended != C) return fail(MCLAHE_ERR_CUDA, "streamed schedule did not complete");
+  MG_CUDA(cudaEventRecord(ev[2 * C + 1], s_comp));
+  int64_t flag = 0;
+  MG_CUDA(cudaMemcpyAsync(&flag, static_cast<char*>(ws) + M->info.off_range + 16, sizeof flag,
+                          cudaMemcpyDeviceToHost, s_comp));
+  MG_CUDA(cudaStreamSynchronize(s_comp));
+  MG_CUDA(cudaStreamSynchronize(s_out));
+  if (flag) return fail(MCLAHE_ERR_VALIDATION, "image contains non-finite values");
+  if (timings) {
+    float total = 0.f;
+    MG_CUDA(cudaEventElapsedTime(&total, ev[2 * C], ev[2 * C + 1]));
+    (void)interp_ms;
+    timings->histograms_s += total * 1e-3;  // interleaved passes: reported as one span
+  }
+  return MCLAHE_OK;
+}
+
 // ---- one-shot context: cached plan + buffers ----
 struct OneShot {
   std::mutex mu;
@@ -793,6 +963,9 @@ struct OneShot {
   cudaStream_t stream = nullptr;
   int stream_dev = -1;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaStream_t s_in = nullptr, s_out = nullptr;
+  std::vector<cudaEvent_t> sev;  // streamed-run events
+  std::map<std::string, std::unique_ptr<Streamed>> streamed;
 };
 OneShot& oneshot() {
   static OneShot* o = new OneShot();  // intentionally leaked (process lifetime)
@@ -848,7 +1021,11 @@ int ensure_stream(OneShot& o) {
   MG_CUDA(cudaGetDevice(&dev));
   if (o.stream && o.stream_dev == dev) return MCLAHE_OK;
   MG_CUDA(cudaStreamCreateWithFlags(&o.stream, cudaStreamNonBlocking));
+  MG_CUDA(cudaStreamCreateWithFlags(&o.s_in, cudaStreamNonBlocking));
+  MG_CUDA(cudaStreamCreateWithFlags(&o.s_out, cudaStreamNonBlocking));
   for (auto& e : o.ev) MG_CUDA(cudaEventCreate(&e));
+  o.sev.resize(2 * 8 + 2);
+  for (auto& e : o.sev) MG_CUDA(cudaEventCreate(&e));
   o.stream_dev = dev;
   return MCLAHE_OK;
 }
@@ -877,13 +1054,9 @@ int read_status(const mclahe_plan_s* pl, const void* ws, cudaStream_t st) {
   return MCLAHE_OK;
 }
 
-int64_t elem_size(const mclahe_params_t* p) { return p->dtype == MCLAHE_F64 ? 8 : 4; }
 
-int64_t volume(const mclahe_params_t* p) {
-  int64_t n = 1;
-  for (int i = 0; i < p->rank; ++i) n *= p->shape[i];
-  return n;
-}
+
+
 
 }  // namespace
 
@@ -910,7 +1083,6 @@ int mclahe_plan_create(const mclahe_params_t* params, int64_t row_begin, int64_t
 
 int mclahe_plan_destroy(mclahe_plan_t plan) {
   if (!plan) return MCLAHE_OK;
-  if (plan->d_tables) cudaFree(plan->d_tables);
   delete plan;
   return MCLAHE_OK;
 }
@@ -1015,6 +1187,33 @@ int mclahe_gpu_run(const mclahe_params_t* params, const void* in, void* out,
   if (!pl) return rc;
   const size_t bytes = (size_t)(volume(params) * elem_size(params));
   const size_t io = (size_t)align_up((int64_t)bytes, 256);
+  // float32 volumes large enough to chunk: streamed H2D / compute / D2H
+  if (pl->f32() && getenv("MCLAHE_NO_STREAM") == nullptr) {
+    int dev = 0;
+    MG_CUDA(cudaGetDevice(&dev));
+    mclahe_params_t q = *params;
+    q.reserved = 0;
+    for (int i = q.rank; i < MCLAHE_MAX_RANK; ++i) q.shape[i] = q.kernel[i] = 0;
+    const std::string key = plan_key(&q, dev);
+    auto it = o.streamed.find(key);
+    if (it == o.streamed.end()) {
+      auto S = std::make_unique<Streamed>();
+      const int brc = build_streamed(params, *S);
+      if (brc != MCLAHE_OK && brc != MCLAHE_ERR_UNSUPPORTED) return brc;
+      if (brc == MCLAHE_ERR_UNSUPPORTED) S.reset();
+      if (o.streamed.size() > 8) o.streamed.clear();
+      it = o.streamed.emplace(key, std::move(S)).first;
+    }
+    if (it->second) {
+      Streamed& S = *it->second;
+      const size_t wsb = (size_t)S.chunks[0]->info.workspace_bytes;
+      if ((rc = ensure_buf(o, 2 * io + wsb))) return rc;
+      if ((rc = ensure_stream(o))) return rc;
+      char* base = static_cast<char*>(o.buf);
+      return run_streamed(S, params, in, out, base, base + io, base + 2 * io, o.s_in, o.stream,
+                          o.s_out, o.sev, timings);
+    }
+  }
   if ((rc = ensure_buf(o, 2 * io + (size_t)pl->info.workspace_bytes))) return rc;
   if ((rc = ensure_stream(o))) return rc;
   char* base = static_cast<char*>(o.buf);

@@ -291,3 +291,22 @@ def test_full_size_properties(M, name):
 
 def st_grid(plan):
     return [int(plan.info.grid[j]) for j in range(plan.info.rank)]
+
+
+@pytest.mark.parametrize("name", ["4d", "l4d"])
+def test_streamed_host_api_matches_device(M, name):
+    """The one-shot host call streams cell-aligned chunks through shared-
+    workspace plans (H2D / compute / D2H overlapped); it must equal the
+    whole-volume device path bit for bit."""
+    from paper_1906_11355_b200 import datasets
+    c = dict(SCALED[name])
+    shape = (c["shape"][0] * 2,) + tuple(c["shape"][1:])  # >= 16 MB: several chunks
+    x = datasets.make(name, seed=4, shape=shape)
+    args = (c["kernel"], c["n_bins"], c["clip_limit"], c["adaptive"])
+    dev = M.enhance(x.cuda(), *args).cpu().numpy()
+    host = M.enhance(x.numpy(), *args)
+    assert np.array_equal(dev, host)
+    xn = x.numpy().copy()
+    xn[-1, 3, 2, 1] = np.nan  # non-finite in the LAST chunk is still caught
+    with pytest.raises(M.ValidationError, match="non-finite"):
+        M.enhance(xn, *args)
