@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--config", default="4d", choices=["2d", "3d", "4d", "l4d", "5d"])
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: test the multi-rank path with ranks sharing GPUs")
     return ap.parse_args()
 
 
@@ -207,10 +209,14 @@ def main():
     from paper_1906_11355_b200 import slabs as S
 
     rank, world, local = dist_env()
+    local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
     shape, kernel = tuple(cfg["shape"]), tuple(cfg["kernel"])
     nb, clip, ad = cfg["n_bins"], cfg["clip_limit"], cfg["adaptive"]
     N_total = _numel(cfg)
@@ -284,7 +290,7 @@ def main():
         if world > 1:
             dist.barrier()
         plan.check(ws)
-        ms_t = torch.tensor([ms_local], device=dev)
+        ms_t = torch.tensor([ms_local], device=dev if args.dist_backend == "nccl" else "cpu")
         if world > 1:
             dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
         ms = float(ms_t.item())

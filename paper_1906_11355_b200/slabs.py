@@ -152,8 +152,17 @@ class DistExchange:
     def __init__(self, windows: list[Window], rank: int, group=None):
         self.windows, self.rank, self.group = windows, rank, group
 
+    def _host_staged(self) -> bool:
+        import torch.distributed as dist
+        return dist.get_backend(self.group) == "gloo"
+
     def allreduce_max(self, t):
         import torch.distributed as dist
+        if t.is_cuda and self._host_staged():  # gloo: exchange through host memory
+            h = t.cpu()
+            dist.all_reduce(h, op=dist.ReduceOp.MAX, group=self.group)
+            t.copy_(h)
+            return
         dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
 
     def rows(self, buf, op: str):
@@ -166,14 +175,19 @@ class DistExchange:
         if not peers:
             return
         ops, recv = [], []
+        staged = buf.is_cuda and self._host_staged()
         for r, a, b in peers:
             send = buf[a - me.begin:b - me.begin].clone()
+            if staged:
+                send = send.cpu()
             rbuf = torch.empty_like(send)
             ops.append(dist.P2POp(dist.isend, send, r, group=self.group))
             ops.append(dist.P2POp(dist.irecv, rbuf, r, group=self.group))
             recv.append((a, b, rbuf))
         for req in dist.batch_isend_irecv(ops):
             req.wait()
+        if staged:
+            recv = [(a, b, t.to(buf.device)) for a, b, t in recv]
         combine_rows(buf, recv, 0, me, op)
 
 
