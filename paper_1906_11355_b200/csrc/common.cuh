@@ -137,6 +137,7 @@ struct Stage {
   int32_t x[kMaxOuterDims];     // absolute coordinates of the box origin (dim 0 global)
   int32_t cell[kMaxOuterDims];  // K4: cells of the unit (K2: tiles)
   TileParts p1, p2;             // K2: tile parts along dims KO-1 and KO-2
+  int32_t tc[6];                // TMA box coordinates of the stage (K4 reuses them to store)
 };
 
 // Producer-private per-unit box (kept in shared memory, not registers, so
@@ -205,6 +206,48 @@ __device__ __forceinline__ void tma_load(void* dst, const CUtensorMap* map, int 
   }
 }
 
+// TMA tensor store of one box from shared memory (bulk-group completion).
+__device__ __forceinline__ void tma_store(const CUtensorMap* map, int rank, const int* c,
+                                          const void* src) {
+  const uint64_t m = reinterpret_cast<uint64_t>(map);
+  const uint32_t s = smem_u32(src);
+  switch (rank) {
+    case 2:
+      asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(m),
+                   "r"(c[0]), "r"(c[1]), "r"(s)
+                   : "memory");
+      break;
+    case 3:
+      asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(m),
+                   "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(s)
+                   : "memory");
+      break;
+    case 4:
+      asm volatile(
+          "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::"l"(m),
+          "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(s)
+          : "memory");
+      break;
+    default:
+      asm volatile(
+          "cp.async.bulk.tensor.5d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];" ::"l"(m),
+          "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(s)
+          : "memory");
+      break;
+  }
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void tma_store_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void tma_store_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+// Makes this thread's generic-proxy shared-memory writes visible to the TMA.
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
 // Producer (one thread): walks the CTA's units box by box (the plan makes
 // every unit extent along dims KO-1 / KO-2 a multiple of R1 / R2) and issues
 // one TMA box load per stage.  CELLS selects interpolation-cell boxes (K4)
@@ -219,10 +262,14 @@ __device__ __forceinline__ bool parts_uniform(const TileParts& p, int64_t x, int
   return u;
 }
 
-template <int KO, bool CELLS, bool WEIGHTS = !CELLS>
+// STORE: consumers leave each stage's results in place; before a slot is
+// refilled (and after the last stage) its box is written back with a TMA
+// tensor store through out_map.
+template <int KO, bool CELLS, bool WEIGHTS = !CELLS, bool STORE = false>
 __device__ __noinline__ void pipe_produce(const KGeom& G, const CUtensorMap* map,
                                           const int32_t* __restrict__ units, int u0, int u1,
-                                          Pipe& pp, float* bufs) {
+                                          Pipe& pp, float* bufs,
+                                          const CUtensorMap* out_map = nullptr) {
   const int nst = G.nst;
   const int64_t stage_elems = G.stage_stride;
   const uint32_t box_bytes = (uint32_t)((int64_t)G.stage_rows * (G.P / G.nseg) * 4);
@@ -283,6 +330,10 @@ __device__ __noinline__ void pipe_produce(const KGeom& G, const CUtensorMap* map
           const int slot = it % nst;
           mbar_wait(&pp.empty[slot], ((it / nst) & 1) ^ 1);
           Stage& S = pp.st[slot];
+          if (STORE && it >= (uint32_t)nst) {  // write back the slot's previous results
+            tma_store(out_map, G.tma_rank, S.tc, bufs + slot * stage_elems);
+            tma_store_wait_read();
+          }
           S.unit = u;
           S.seg = seg;
           S.key = key;
@@ -314,6 +365,8 @@ __device__ __noinline__ void pipe_produce(const KGeom& G, const CUtensorMap* map
             const int32_t xj = j == KO - 1 ? x1 : (j == KO - 2 ? x2 : xf[j]);
             c[r++] = j == 0 ? (int)(xj - G.row0) : xj;
           }
+          if (STORE)
+            for (int i = 0; i < G.tma_rank; ++i) S.tc[i] = c[i];
           mbar_expect_tx(&pp.full[slot], box_bytes);
           tma_load(bufs + slot * stage_elems, map, G.tma_rank, c, &pp.full[slot]);
           ++it;
@@ -324,8 +377,20 @@ __device__ __noinline__ void pipe_produce(const KGeom& G, const CUtensorMap* map
   }
   const int slot = it % nst;
   mbar_wait(&pp.empty[slot], ((it / nst) & 1) ^ 1);
+  if (STORE && it >= (uint32_t)nst) {
+    tma_store(out_map, G.tma_rank, pp.st[slot].tc, bufs + slot * stage_elems);
+    tma_store_wait_read();
+  }
   pp.st[slot].unit = -1;
   mbar_arrive(&pp.full[slot]);
+  if (STORE) {  // drain: the stages still in flight after the sentinel
+    for (uint32_t j = (it >= (uint32_t)nst ? it - nst + 1 : 0); j < it; ++j) {
+      const int s = j % nst;
+      mbar_wait(&pp.empty[s], (j / nst) & 1);
+      tma_store(out_map, G.tma_rank, pp.st[s].tc, bufs + s * stage_elems);
+    }
+    tma_store_wait_all();
+  }
 }
 
 }  // namespace mg

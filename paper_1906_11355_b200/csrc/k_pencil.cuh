@@ -295,7 +295,8 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
 template <int KO, int KT, bool ADAPT>
 __global__ void __launch_bounds__(kBlendThreads, 1)
     k_interp_pencil(const __grid_constant__ KGeom G, const __grid_constant__ CUtensorMap tmap,
-                    const float* __restrict__ in, float* __restrict__ out,
+                    const __grid_constant__ CUtensorMap omap, const float* __restrict__ in,
+                    float* __restrict__ out,
                     const int32_t* __restrict__ units, const int32_t* __restrict__ cta_units, WS W) {
   constexpr int NCO = 1 << KO, NCT = 1 << KT;
   constexpr int NW = kConsumersBlend / 32;
@@ -305,10 +306,18 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
   const int n = G.n_bins;
   const int n1 = n + 1;
   const int64_t gtr = G.gtr;
-  float* lutS = reinterpret_cast<float*>(P.tail);  // [NCO][gtr][n1]
-  float* thrS = lutS + NCO * gtr * n1;  // edge tables: [NCO][gtr][n1] (adaptive) or [n1]
+  // Global mode with one trailing dim (PAIR): a voxel has one bin for all
+  // corners, so the two trailing-corner LUTs of a column are stored side by
+  // side, pairS[co][tt][b] = {L(co, tt)[b], L(co, tt+1)[b]}: one LDS.64 per
+  // outer corner.  Otherwise LUT rows [NCO][gtr][n1].
+  constexpr bool PAIR = !ADAPT && KT == 1;
+  float* lutS = reinterpret_cast<float*>(P.tail);  // [NCO][gtr][n1] or pairs [NCO][gtr-1][n1]
+  float2* pairS = reinterpret_cast<float2*>(P.tail);
+  float* thrS = lutS + (PAIR ? 2 * NCO * (gtr - 1) * n1 : NCO * gtr * n1);  // edge tables
   float2* lcS = reinterpret_cast<float2*>(  // [NCO][gtr] {lo, c} (adaptive)
-      P.tail + (((ADAPT ? 2 * NCO * gtr * n1 : NCO * gtr * n1 + n1) * 4 + 15) & ~15LL));
+      P.tail + (((ADAPT ? 2 * NCO * gtr * n1
+                        : (PAIR ? 2 * NCO * (gtr - 1) * n1 : NCO * gtr * n1) + n1) * 4 + 15) &
+                ~15LL));
   // per trailing column: first corner tile and the 4 x NCT trailing weights
   const int ncol = (int)(G.P / 4);
   int* colT = reinterpret_cast<int*>(lcS + NCO * gtr);
@@ -319,7 +328,7 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
   const int u0 = cta_units[blockIdx.x], u1 = cta_units[blockIdx.x + 1];
   if (threadIdx.x >= kConsumersBlend) {
     if (threadIdx.x == kConsumersBlend)
-      pipe_produce<KO, true>(G, &tmap, units, u0, u1, *P.pipe, P.bufs);
+      pipe_produce<KO, true, false, true>(G, &tmap, units, u0, u1, *P.pipe, P.bufs, &omap);
     return;
   }
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -388,15 +397,29 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
         int64_t of = (S.cell[0] + ((co >> (KO - 1)) & 1) - G.trow0) * G.tstride[0];
         for (int j = 1; j < KO; ++j) of += (S.cell[j] + ((co >> (KO - 1 - j)) & 1)) * G.tstride[j];
         const float4* src = reinterpret_cast<const float4*>(W.lut + of * n);
-        float* dst = lutS + co * gtr * n1;
-        for (int64_t k = tid; k < gtr * n / 4; k += kConsumersBlend) {
-          const float4 q = __ldg(src + k);
-          const int64_t t = (4 * k) / n, b = 4 * k - t * n;  // n % 4 == 0: one row
-          float* d = dst + t * n1 + b;
-          d[0] = q.x;
-          d[1] = q.y;
-          d[2] = q.z;
-          d[3] = q.w;
+        if (PAIR) {
+          float* dp = reinterpret_cast<float*>(pairS + co * (gtr - 1) * n1);
+          for (int64_t k = tid; k < gtr * n / 4; k += kConsumersBlend) {
+            const float4 q = __ldg(src + k);
+            const int64_t t = (4 * k) / n, b = 4 * k - t * n;
+            const float qv[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              if (t < gtr - 1) dp[2 * (t * n1 + b + j)] = qv[j];           // .x of pair t
+              if (t >= 1) dp[2 * ((t - 1) * n1 + b + j) + 1] = qv[j];     // .y of pair t-1
+            }
+          }
+        } else {
+          float* dst = lutS + co * gtr * n1;
+          for (int64_t k = tid; k < gtr * n / 4; k += kConsumersBlend) {
+            const float4 q = __ldg(src + k);
+            const int64_t t = (4 * k) / n, b = 4 * k - t * n;  // n % 4 == 0: one row
+            float* d = dst + t * n1 + b;
+            d[0] = q.x;
+            d[1] = q.y;
+            d[2] = q.z;
+            d[3] = q.w;
+          }
         }
         if (ADAPT) {
           const float* ts = W.thr + of * n1;
@@ -449,7 +472,7 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
     const int64_t vs1 = G.vstride[KO - 1], vs2 = KO >= 2 ? G.vstride[KO >= 2 ? KO - 2 : 0] : 0;
     const int64_t r0 = (KO == 1 ? G.row0 : 0), r0b = (KO == 2 ? G.row0 : 0);
     const int seg = S.seg;
-    const unsigned char* buf = reinterpret_cast<const unsigned char*>(P.bufs + s * stage_elems);
+    unsigned char* buf = reinterpret_cast<unsigned char*>(P.bufs + s * stage_elems);
     for (int item = warp; item < 8 * nrb; item += NW) {
       const int c = item & 7, rb = item >> 3;
       const int q = rb * 32 + lane;
@@ -478,8 +501,8 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
           }
         }
         // 128B-swizzled stage row: 16-byte chunk c of row q sits at c ^ (q & 7)
-        const float4 v4 =
-            *reinterpret_cast<const float4*>(buf + q * 128 + ((c ^ (q & 7)) << 4));
+        float4* slot4 = reinterpret_cast<float4*>(buf + q * 128 + ((c ^ (q & 7)) << 4));
+        const float4 v4 = *slot4;
         const u64 V01 = pk2(v4.x, v4.y), V23 = pk2(v4.z, v4.w);
         float acc[4] = {0.f, 0.f, 0.f, 0.f};
         int bg[4] = {0, 0, 0, 0};
@@ -519,7 +542,18 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
         } else {
           int bo[4];  // global mode: byte offsets of the voxel's bin
 #pragma unroll
-          for (int i = 0; i < 4; ++i) bo[i] = bg[i] * 4;
+          for (int i = 0; i < 4; ++i) bo[i] = bg[i] * (PAIR ? 8 : 4);
+          if (PAIR) {
+#pragma unroll
+            for (int co = 0; co < NCO; ++co) {
+              const char* Pb = reinterpret_cast<const char*>(pairS + (co * ((int)gtr - 1) + tt) * n1);
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const float2 p = *reinterpret_cast<const float2*>(Pb + bo[i]);
+                acc[i] = fmaf(wo[co], fmaf(tw[i][1], p.y, tw[i][0] * p.x), acc[i]);
+              }
+            }
+          } else
 #pragma unroll
           for (int co = 0; co < NCO; ++co) {
             float m[NCT][4];
@@ -561,9 +595,11 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
         r.y = fminf(fmaxf(acc[1], 0.f), 1.f);
         r.z = fminf(fmaxf(acc[2], 0.f), 1.f);
         r.w = fminf(fmaxf(acc[3], 0.f), 1.f);
-        __stcs(reinterpret_cast<float4*>(out + ooff), r);
+        *slot4 = r;  // in place; the producer TMA-stores the box
+        (void)ooff;
       }
     }
+    fence_proxy_async_smem();
     __syncwarp();
     if (lane == 0) mbar_arrive(&P.pipe->empty[s]);
     ++it;
@@ -574,8 +610,8 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
 using PencilRangeFn = void (*)(const KGeom, const CUtensorMap, const float*, const int32_t*,
                                const int32_t*, WS);
 using PencilHistFn = PencilRangeFn;
-using PencilInterpFn = void (*)(const KGeom, const CUtensorMap, const float*, float*,
-                                const int32_t*, const int32_t*, WS);
+using PencilInterpFn = void (*)(const KGeom, const CUtensorMap, const CUtensorMap, const float*,
+                                float*, const int32_t*, const int32_t*, WS);
 PencilRangeFn get_range_pencil(int ko);
 PencilHistFn get_hist_pencil(int ko, bool adaptive);
 PencilInterpFn get_interp_pencil(int ko, int kt, bool adaptive);

@@ -119,8 +119,8 @@ struct mclahe_plan_s {
   int hist_grid = 0, interp_grid = 0, range_grid = 0, map_grid = 0, map_block = 128;
   int64_t map_smem = 0;
   // TMA views of the last input buffer (re-encoded when the pointer changes)
-  const void* map_ptr[2] = {nullptr, nullptr};
-  CUtensorMap map[2];
+  const void* map_ptr[3] = {nullptr, nullptr, nullptr};
+  CUtensorMap map[3];  // [0] hist view of the input, [1] blend view of the input, [2] of the output
   bool f32() const { return p.dtype == MCLAHE_F32; }
   mclahe_plan_s() = default;
   mclahe_plan_s(const mclahe_plan_s&) = delete;
@@ -212,7 +212,8 @@ Pencil choose_pencil(const mclahe_plan_s& pl, bool for_hist) {
       // LUTs (+ bin-edge tables: per tile when adaptive, one row when global)
       // + per-tile ranges; one CTA per SM with 16 consumer warps
       const int64_t luts1 = (int64_t{1} << ko) * c.gtr * (n + 1);  // rows padded to n+1
-      c.tail = align_up((pl.p.adaptive ? 2 * luts1 : luts1 + n + 1) * 4, 16) +
+      const int64_t pairs = (int64_t{1} << ko) * (c.gtr - 1) * (n + 1) * 2;  // global, KT == 1
+      c.tail = align_up((pl.p.adaptive ? 2 * luts1 : (kt == 1 ? pairs : luts1) + n + 1) * 4, 16) +
                (int64_t{1} << ko) * c.gtr * 16 + (c.P / 4) * (4 + 16 * (int64_t{1} << kt));
       c.rpi = kConsumersBlend / c.tpr;
       const int64_t avail = 226 * 1024 - kPipeBytes - c.tail;
@@ -416,6 +417,8 @@ EncodeTiledFn encode_fn() {
 // K4: [outer dims KO-1..0][P/32 segments][32], box [R2 x R1 rows][1][32], 128B swizzle.
 int tensor_map(mclahe_plan_s* pl, int fam, const void* in) {
   if (pl->map_ptr[fam] == in) return MCLAHE_OK;
+  const int slot = fam;
+  if (fam == 2) fam = 1;  // output view of the blend family
   const Pencil& c = fam == 0 ? pl->hist : pl->interp;
   EncodeTiledFn enc = encode_fn();
   if (!enc) return fail(MCLAHE_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
@@ -440,14 +443,14 @@ int tensor_map(mclahe_plan_s* pl, int fam, const void* in) {
     ++r;
   }
   for (int i = 0; i < r; ++i) es[i] = 1;
-  const CUresult res = enc(&pl->map[fam], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, (cuuint32_t)r,
+  const CUresult res = enc(&pl->map[slot], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, (cuuint32_t)r,
                            const_cast<void*>(in), dims, strides, box, es,
                            CU_TENSOR_MAP_INTERLEAVE_NONE,
                            seg ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (res != CUDA_SUCCESS)
     return fail(MCLAHE_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)res) + ")");
-  pl->map_ptr[fam] = in;
+  pl->map_ptr[slot] = in;
   return MCLAHE_OK;
 }
 
@@ -763,6 +766,7 @@ int do_interp(mclahe_plan_s* pl, const void* in, void* out, void* ws, cudaStream
     InterpFn f = interp_fn(pl->interp.ko, pl->interp.kt, A);
     int rc = tensor_map(pl, 1, in);
     if (rc) return rc;
+    if ((rc = tensor_map(pl, 2, out))) return rc;
     if (getenv("MCLAHE_DEBUG")) {
       cudaFuncAttributes fa;
       cudaFuncGetAttributes(&fa, reinterpret_cast<const void*>(f));
@@ -774,7 +778,7 @@ int do_interp(mclahe_plan_s* pl, const void* in, void* out, void* ws, cudaStream
               (long long)pl->interp.P, fa.numRegs, fa.maxThreadsPerBlock, fa.sharedSizeBytes,
               fa.maxDynamicSharedSizeBytes);
     }
-    f<<<pl->interp_grid, kBlendThreads, pl->interp.smem, st>>>(G, pl->map[1], static_cast<const float*>(in),
+    f<<<pl->interp_grid, kBlendThreads, pl->interp.smem, st>>>(G, pl->map[1], pl->map[2], static_cast<const float*>(in),
                                                      static_cast<float*>(out),
                                                      pl->d_tables + pl->off_interp_units,
                                                      pl->d_tables + pl->off_interp_cta, W);
