@@ -505,6 +505,11 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
         const float4 v4 = *slot4;
         const u64 V01 = pk2(v4.x, v4.y), V23 = pk2(v4.z, v4.w);
         float acc[4] = {0.f, 0.f, 0.f, 0.f};
+        float act[NCT][4];  // per trailing corner: sum over outer corners of wo * LUT
+#pragma unroll
+        for (int ct = 0; ct < NCT; ++ct)
+#pragma unroll
+          for (int i = 0; i < 4; ++i) act[ct][i] = 0.f;
         int bg[4] = {0, 0, 0, 0};
         if (!ADAPT) {
           if (!patho) {
@@ -532,12 +537,9 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
               lut2_edge(V23, v4.z, v4.w, lc, thb, Lb, n4, m[ct][2], m[ct][3]);
             }
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              float mi = 0.f;
+            for (int ct = 0; ct < NCT; ++ct)
 #pragma unroll
-              for (int ct = 0; ct < NCT; ++ct) mi = fmaf(tw[i][ct], m[ct][i], mi);
-              acc[i] = fmaf(wo[co], mi, acc[i]);
-            }
+              for (int i = 0; i < 4; ++i) act[ct][i] = fmaf(wo[co], m[ct][i], act[ct][i]);
           }
         } else {
           int bo[4];  // global mode: byte offsets of the voxel's bin
@@ -550,7 +552,8 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
 #pragma unroll
               for (int i = 0; i < 4; ++i) {
                 const float2 p = *reinterpret_cast<const float2*>(Pb + bo[i]);
-                acc[i] = fmaf(wo[co], fmaf(tw[i][1], p.y, tw[i][0] * p.x), acc[i]);
+                act[0][i] = fmaf(wo[co], p.x, act[0][i]);
+                act[1 % NCT][i] = fmaf(wo[co], p.y, act[1 % NCT][i]);
               }
             }
           } else
@@ -582,14 +585,16 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
               }
             }
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              float mi = 0.f;
+            for (int ct = 0; ct < NCT; ++ct)
 #pragma unroll
-              for (int ct = 0; ct < NCT; ++ct) mi = fmaf(tw[i][ct], m[ct][i], mi);
-              acc[i] = fmaf(wo[co], mi, acc[i]);
-            }
+              for (int i = 0; i < 4; ++i) act[ct][i] = fmaf(wo[co], m[ct][i], act[ct][i]);
           }
         }
+        // trailing weights last: acc = sum_ct tw[ct] * (sum_co wo[co] * L)
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int ct = 0; ct < NCT; ++ct) acc[i] = fmaf(tw[i][ct], act[ct][i], acc[i]);
         float4 r;
         r.x = fminf(fmaxf(acc[0], 0.f), 1.f);
         r.y = fminf(fmaxf(acc[1], 0.f), 1.f);
