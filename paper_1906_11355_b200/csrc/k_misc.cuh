@@ -51,7 +51,30 @@ __global__ void __launch_bounds__(256) k_global_range(const T* __restrict__ in, 
   int bad = 0;
   const int64_t nv = ((reinterpret_cast<uintptr_t>(in) & 15) == 0) ? n / V : 0;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nv; i += stride) {
+  constexpr int U = 4;  // 16-byte loads in flight per thread
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  for (; i + (U - 1) * stride < nv; i += U * stride) {
+    T v[U][V];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if constexpr (V == 4) {
+        const float4 q = __ldcs(reinterpret_cast<const float4*>(in) + i + u * stride);
+        v[u][0] = q.x; v[u][1] = q.y; v[u][2] = q.z; v[u][3] = q.w;
+      } else {
+        const double2 q = __ldcs(reinterpret_cast<const double2*>(in) + i + u * stride);
+        v[u][0] = q.x; v[u][1] = q.y;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int k = 0; k < V; ++k) {
+        bad |= !isfinite(v[u][k]);
+        lo = fmin(lo, v[u][k]);
+        hi = fmax(hi, v[u][k]);
+      }
+  }
+  for (; i < nv; i += stride) {
     T v[V];
     if constexpr (V == 4) {
       const float4 q = __ldcs(reinterpret_cast<const float4*>(in) + i);
