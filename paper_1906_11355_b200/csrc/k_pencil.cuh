@@ -172,6 +172,10 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
   bool patho = !ADAPT && isnan(glc.y);  // a range the float guard does not cover
   __shared__ int s_bad;
   const float kDegC = degenerate_lc().y;
+  float2 lcv[4];
+  const float* thv[4];
+  int hb[4];
+  const bool same_pairs = !ADAPT || (trt[0] == trt[1] && trt[2] == trt[3]);
 
   uint32_t it = 0;
   while (true) {
@@ -205,12 +209,20 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
       consumers_sync();
       if (ADAPT) patho = s_bad != 0;
       cur = key;
+      // per-thread tile constants for this pencil
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        lcv[i] = ADAPT ? lcS[trt[i]] : glc;
+        thv[i] = thrS + (ADAPT ? trt[i] * n1 : 0);
+        hb[i] = (!ADAPT || lcv[i].y != kDegC) ? trt[i] * n : -1;  // degenerate: no histogram
+      }
     }
     const int rows = G.stage_rows;
     const float* buf = P.bufs + s * stage_elems;
     if (lane_on) {
       const bool wuni = S.wuni != 0;
       const int32_t wfix = S.wfix;
+#pragma unroll 4
       for (int q = slot; q < rows; q += G.rpi) {
         uint32_t wrow;
         if (wuni) {
@@ -223,38 +235,32 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
         }
         const float4 v = *reinterpret_cast<const float4*>(buf + q * G.P + e0);
         int b[4];
-        const float2 l0 = ADAPT ? lcS[trt[0]] : glc, l1 = ADAPT ? lcS[trt[1]] : glc;
-        const float2 l2 = ADAPT ? lcS[trt[2]] : glc, l3 = ADAPT ? lcS[trt[3]] : glc;
         if (!patho) {
-          if (!ADAPT || (trt[0] == trt[1] && trt[2] == trt[3])) {
-            bins2_edge(pk2(v.x, v.y), v.x, v.y, l0, thrS + (ADAPT ? trt[0] * n1 : 0), n, b[0], b[1]);
-            bins2_edge(pk2(v.z, v.w), v.z, v.w, l2, thrS + (ADAPT ? trt[2] * n1 : 0), n, b[2], b[3]);
+          if (same_pairs) {
+            bins2_edge(pk2(v.x, v.y), v.x, v.y, lcv[0], thv[0], n, b[0], b[1]);
+            bins2_edge(pk2(v.z, v.w), v.z, v.w, lcv[2], thv[2], n, b[2], b[3]);
           } else {  // pairs straddle a tile boundary: evaluate each against its own tile
             int dmy;
-            bins2_edge(pk2(v.x, v.x), v.x, v.x, l0, thrS + trt[0] * n1, n, b[0], dmy);
-            bins2_edge(pk2(v.y, v.y), v.y, v.y, l1, thrS + trt[1] * n1, n, b[1], dmy);
-            bins2_edge(pk2(v.z, v.z), v.z, v.z, l2, thrS + trt[2] * n1, n, b[2], dmy);
-            bins2_edge(pk2(v.w, v.w), v.w, v.w, l3, thrS + trt[3] * n1, n, b[3], dmy);
+            bins2_edge(pk2(v.x, v.x), v.x, v.x, lcv[0], thv[0], n, b[0], dmy);
+            bins2_edge(pk2(v.y, v.y), v.y, v.y, lcv[1], thv[1], n, b[1], dmy);
+            bins2_edge(pk2(v.z, v.z), v.z, v.z, lcv[2], thv[2], n, b[2], dmy);
+            bins2_edge(pk2(v.w, v.w), v.w, v.w, lcv[3], thv[3], n, b[3], dmy);
           }
         } else {
           const float a4[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
-            const float2 lc = ADAPT ? lcS[trt[i]] : glc;
-            const float* th = thrS + (ADAPT ? trt[i] * n1 : 0);
-            if (isnan(lc.y)) b[i] = bin_search(a4[i], th, n);
-            else bins2_edge(pk2(a4[i], a4[i]), a4[i], a4[i], lc, th, n, b[i], b[i]);
+            if (isnan(lcv[i].y)) b[i] = bin_search(a4[i], thv[i], n);
+            else bins2_edge(pk2(a4[i], a4[i]), a4[i], a4[i], lcv[i], thv[i], n, b[i], b[i]);
           }
         }
-        // skip degenerate tiles (no histogram), merge equal neighbours, one
-        // shared atomic per distinct (tile, bin)
-        const float cs[4] = {l0.y, l1.y, l2.y, l3.y};
+        // merge equal neighbours, one shared atomic per distinct (tile, bin);
+        // degenerate tiles (hb < 0) build no histogram
         int kprev = -1;
         uint32_t acc = 0;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          const bool live = !ADAPT || cs[i] != kDegC;
-          const int key2 = live ? trt[i] * n + b[i] : -2 - i;
+          const int key2 = hb[i] >= 0 ? hb[i] + b[i] : -2 - i;
           const uint32_t w = wrow * (uint32_t)trw[i];
           if (key2 == kprev) {
             acc += w;
