@@ -179,6 +179,13 @@ int mclahe_plan_check(mclahe_plan_t plan, const void* workspace, void* stream);
 int mclahe_debug_bin_index(int32_t dtype, const void* values_dev, int64_t n, double lo,
                            double hi, int64_t n_bins, int32_t* out_dev, void* stream);
 
+/* The pencil kernels' packed f32x2 binning on n device float32 values (pairs
+ * of consecutive values): variant 1 = the histogram routine, 2 = the blend
+ * gather (through an identity LUT).  Must equal mclahe_debug_bin_index. */
+int mclahe_debug_bin_index_packed(const float* values_dev, int64_t n, double lo, double hi,
+                                  int64_t n_bins, int32_t variant, int32_t* out_dev,
+                                  void* stream);
+
 /* Number of kernel launches the last pass call on this thread issued. */
 int64_t mclahe_launch_count(void);
 

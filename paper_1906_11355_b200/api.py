@@ -296,12 +296,21 @@ def enhance(image, kernel_size, n_bins: int = 256, clip_limit: float = 1.0,
     return mclahe(req)
 
 
-def bin_index_device(values, lo: float, hi: float, n_bins: int):
+def bin_index_device(values, lo: float, hi: float, n_bins: int, variant: int = 0):
     """bin_index (src/histogram.cpp:24-32) of a CUDA tensor through the kernels'
-    guarded fast routine; int32 result (-1 for a degenerate range)."""
+    binning; int32 result (-1 for a degenerate range).  variant 0: the generic
+    kernels' guarded routine (f32 or f64); 1 / 2: the pencil kernels' packed
+    histogram / blend-gather routines (float32 only)."""
     import torch
     v = values.contiguous()
     out = torch.empty(v.shape, dtype=torch.int32, device=v.device)
+    if variant:
+        if v.dtype != torch.float32:
+            raise ValidationError("packed binning variants take float32 values")
+        N.check(N.lib().mclahe_debug_bin_index_packed(v.data_ptr(), v.numel(), float(lo),
+                                                      float(hi), int(n_bins), int(variant),
+                                                      out.data_ptr(), _stream_handle()))
+        return out
     code = N.F64 if v.dtype == torch.float64 else N.F32
     N.check(N.lib().mclahe_debug_bin_index(code, v.data_ptr(), v.numel(), float(lo), float(hi),
                                            int(n_bins), out.data_ptr(), _stream_handle()))

@@ -146,13 +146,14 @@ __device__ inline float bin_threshold(double lo, double hi, int n, int k) {
   // bisection on monotone int keys: bin(lo) = 0 < k <= n-1 = bin(hi)
   auto key = [](float f) { int i = __float_as_int(f); return i >= 0 ? i : (i ^ 0x7FFFFFFF); };
   auto unkey = [](int i) { return __int_as_float(i >= 0 ? i : (i ^ 0x7FFFFFFF)); };
-  int a = key(static_cast<float>(lo)), b = key(static_cast<float>(hi));  // bin(a) < k <= bin(b)
+  // bin(a) < k <= bin(b); 64-bit keys (the key span of [-FLT_MAX, FLT_MAX] exceeds INT_MAX)
+  long long a = key(static_cast<float>(lo)), b = key(static_cast<float>(hi));
   while (b - a > 1) {
-    const int m = a + (b - a) / 2;
-    if (bin_exact(unkey(m), lo, hi, n) >= k) b = m;
+    const long long m = a + (b - a) / 2;
+    if (bin_exact(unkey(static_cast<int>(m)), lo, hi, n) >= k) b = m;
     else a = m;
   }
-  return unkey(b);
+  return unkey(static_cast<int>(b));
 }
 
 // ---- packed (f32x2) guarded binning for the pencil kernels ----------------
@@ -196,29 +197,13 @@ __device__ __forceinline__ float2 degenerate_lc() {
   return make_float2(-4.2535295865117308e37f /* -2^125 */, 1.1754943508222875e-38f /* 2^-126 */);
 }
 
-__device__ __forceinline__ float guard_lim(int n) { return 0.5f - (float)n * 2.5e-7f; }
-
-// th has n+1 entries, th[0] = -inf and th[n] = +inf, so kk in [0, n] needs
-// no clamp: the reference bin is kk if v >= th[kk], else kk - 1.
-__device__ __forceinline__ int near_fix(float v, int k, float d, const float* th, int) {
-  const int kk = k + (d > 0.0f ? 1 : 0);
-  return v >= th[kk] ? kk : kk - 1;
-}
-
-// Bins of two voxels (packed in V = {v0, v1}) against one tile.
-__device__ __forceinline__ void bins2(u64 V, float v0, float v1, float2 lc, const float* th,
-                                      int n, float lim, int& b0, int& b1) {
-  const u64 y = mul2(sub2(V, pk2(lc.x, lc.x)), pk2(lc.y, lc.y));
-  const u64 M = pk2(kMagic, kMagic);
-  const u64 t = add2rm(y, M);
-  const u64 d = sub2(sub2(y, sub2(t, M)), pk2(0.5f, 0.5f));
-  float t0, t1, d0, d1;
-  upk2(t, t0, t1);
-  upk2(d, d0, d1);
-  b0 = min(max(__float_as_int(t0) - kMagicBits, 0), n - 1);
-  b1 = min(max(__float_as_int(t1) - kMagicBits, 0), n - 1);
-  if (!(fabsf(d0) < lim)) b0 = near_fix(v0, b0, d0, th, n);
-  if (!(fabsf(d1) < lim)) b1 = near_fix(v1, b1, d1, th, n);
+// k = rint(y) clamped to [0, n], from t = y + kMagic (round to nearest).
+// The clamp runs on the raw bits as signed ints, which order every float
+// t >= +0 by value and put every negative t (y < -kMagic) below kMagicBits;
+// subtracting first would wrap for |t| >= 2^23-ish and misbin voxels far
+// outside a narrow tile range (blend corners see such voxels).
+__device__ __forceinline__ int clamp_bits(float t, int n) {
+  return min(max(__float_as_int(t), kMagicBits), kMagicBits + n) - kMagicBits;
 }
 
 // Branch-free exact bins of two voxels against one tile, edge table only.
@@ -234,8 +219,8 @@ __device__ __forceinline__ void bins2_edge(u64 V, float v0, float v1, float2 lc,
   asm("add.rn.f32x2 %0, %1, %2;" : "=l"(t) : "l"(y), "l"(pk2(kMagic, kMagic)));
   float t0, t1;
   upk2(t, t0, t1);
-  const int k0 = min(max(__float_as_int(t0) - kMagicBits, 0), n);
-  const int k1 = min(max(__float_as_int(t1) - kMagicBits, 0), n);
+  const int k0 = clamp_bits(t0, n);
+  const int k1 = clamp_bits(t1, n);
   b0 = v0 >= th[k0] ? k0 : k0 - 1;
   b1 = v1 >= th[k1] ? k1 : k1 - 1;
 }
@@ -251,8 +236,8 @@ __device__ __forceinline__ void lut2_edge(u64 V, float v0, float v1, float2 lc, 
   asm("add.rn.f32x2 %0, %1, %2;" : "=l"(t) : "l"(y), "l"(pk2(kMagic, kMagic)));
   float t0, t1;
   upk2(t, t0, t1);
-  const int k0 = min(max((__float_as_int(t0) - kMagicBits) << 2, 0), n4);
-  const int k1 = min(max((__float_as_int(t1) - kMagicBits) << 2, 0), n4);
+  const int k0 = clamp_bits(t0, n4 >> 2) << 2;
+  const int k1 = clamp_bits(t1, n4 >> 2) << 2;
   const int b0 = v0 >= *reinterpret_cast<const float*>(thb + k0) ? k0 : k0 - 4;
   const int b1 = v1 >= *reinterpret_cast<const float*>(thb + k1) ? k1 : k1 - 4;
   m0 = *reinterpret_cast<const float*>(Lb + b0);

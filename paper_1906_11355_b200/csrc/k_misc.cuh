@@ -352,4 +352,40 @@ __global__ void k_debug_bins(const T* __restrict__ v, int64_t count, double lo, 
     out[i] = tp_degenerate(tp.lim) ? -1 : bin_of(v[i], tp, thr, n, nm05);
 }
 
+// The pencil kernels' packed binning (bins2_edge: histograms; lut2_edge:
+// blend gathers, here through an identity LUT) on arbitrary values against
+// one range, pairs of consecutive values per thread.
+__global__ void k_debug_bins_packed(const float* __restrict__ v, int64_t count, double lo,
+                                    double hi, int n, const float* thr, const float* lut,
+                                    int variant, int32_t* __restrict__ out) {
+  const TileParam<float> tp = make_tile_param_f32(lo, hi, n);
+  const float2 lc = tile_lc(tp);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; 2 * i < count;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float v0 = v[2 * i], v1 = 2 * i + 1 < count ? v[2 * i + 1] : v0;
+    int b0, b1;
+    if (tp_degenerate(tp.lim)) {
+      b0 = b1 = -1;
+    } else if (isnan(lc.y)) {
+      b0 = bin_search(v0, thr, n);
+      b1 = bin_search(v1, thr, n);
+    } else if (variant == 1) {
+      bins2_edge(pk2(v0, v1), v0, v1, lc, thr, n, b0, b1);
+    } else {
+      float m0, m1;
+      lut2_edge(pk2(v0, v1), v0, v1, lc, reinterpret_cast<const char*>(thr),
+                reinterpret_cast<const char*>(lut), 4 * n, m0, m1);
+      b0 = (int)m0;
+      b1 = (int)m1;
+    }
+    out[2 * i] = b0;
+    if (2 * i + 1 < count) out[2 * i + 1] = b1;
+  }
+}
+
+__global__ void k_debug_identity(float* lut, int n) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x)
+    lut[k] = (float)k;
+}
+
 }  // namespace mg

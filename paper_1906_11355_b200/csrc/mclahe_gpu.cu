@@ -1267,4 +1267,25 @@ int mclahe_debug_bin_index(int32_t dtype, const void* values, int64_t n, double 
   return MCLAHE_OK;
 }
 
+int mclahe_debug_bin_index_packed(const float* values, int64_t n, double lo, double hi,
+                                  int64_t n_bins, int32_t variant, int32_t* out, void* stream) {
+  if (n_bins < 2 || n_bins > 16384) return fail(MCLAHE_ERR_VALIDATION, "n_bins out of range");
+  if (variant != 1 && variant != 2) return fail(MCLAHE_ERR_VALIDATION, "variant must be 1 or 2");
+  if (n <= 0) return MCLAHE_OK;
+  const int grid = (int)std::min<int64_t>((n / 2 + 256) / 256, 4096);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  float* thr = nullptr;
+  MG_CUDA(cudaMallocAsync(&thr, (size_t)(2 * n_bins + 1) * sizeof(float), st));
+  float* lut = thr + n_bins + 1;
+  k_debug_thresholds<<<(int)((n_bins + 128) / 128), 128, 0, st>>>(lo, hi, (int)n_bins, thr);
+  MG_LAUNCHED();
+  k_debug_identity<<<(int)((n_bins + 127) / 128), 128, 0, st>>>(lut, (int)n_bins);
+  MG_LAUNCHED();
+  k_debug_bins_packed<<<grid, 256, 0, st>>>(values, n, lo, hi, (int)n_bins, thr, lut, variant,
+                                            out);
+  MG_LAUNCHED();
+  MG_CUDA(cudaFreeAsync(thr, st));
+  return MCLAHE_OK;
+}
+
 }  // extern "C"

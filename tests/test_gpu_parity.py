@@ -129,19 +129,45 @@ def test_bin_index_adversarial(M):
     up = np.nextafter(base, np.float32(2))
     dn = np.nextafter(base, np.float32(-1))
     rng = np.random.default_rng(5)
-    v = np.concatenate([base, up, dn, rng.random(200000).astype(np.float32),
-                        np.array([-1e30, 1e30, 0.0, -0.0], np.float32)])
+    # far outside narrow ranges: y = (v - lo) * n / (hi - lo) spans +-1e38, the
+    # magic-number add's whole domain (blend corners evaluate such voxels)
+    mag = np.geomspace(1e-9, 3e38, 4000)
+    far = np.concatenate([0.3 + mag, 0.3 - mag, mag, -mag]).astype(np.float32)
+    v = np.concatenate([base, up, dn, rng.random(200000).astype(np.float32), far,
+                        np.array([-1e30, 1e30, 0.0, -0.0, 3.4e38, -3.4e38], np.float32)])
     vt = torch.from_numpy(v).cuda()
     for lo, hi, n in [(0.0, 1.0, 256), (0.0, 1.0, 512), (0.02, 0.98, 128), (1 / 7, 6 / 7, 256),
-                      (0.0, 3.0 / 500, 256), (-2.5, 1.0, 7), (0.3, 0.30000003, 64)]:
+                      (0.0, 3.0 / 500, 256), (-2.5, 1.0, 7), (0.3, 0.30000003, 64),
+                      (0.3, 0.3000001, 256), (1e-30, 3e-30, 16384), (-3e38, 3e38, 256)]:
         lo32, hi32 = float(np.float32(lo)), float(np.float32(hi))
-        got = M.bin_index_device(vt, lo32, hi32, n).cpu().numpy()
         want = O.bin_index_array(v.astype(np.float64), lo32, hi32, n)
-        assert np.array_equal(got, want), (lo, hi, n, np.flatnonzero(got != want)[:5])
+        for variant in (0, 1, 2):  # generic, packed histogram, packed blend gather
+            got = M.bin_index_device(vt, lo32, hi32, n, variant).cpu().numpy()
+            bad = np.flatnonzero(got != want)
+            assert bad.size == 0, (lo, hi, n, variant, v[bad[:5]], got[bad[:5]], want[bad[:5]])
     # f64 values that are not float32-representable
     v64 = np.concatenate([np.arange(0, 3001) / 3000.0, rng.random(100000)])
     got = M.bin_index_device(torch.from_numpy(v64).cuda(), 0.0, 1.0, 256).cpu().numpy()
     assert np.array_equal(got, O.bin_index_array(v64, 0.0, 1.0, 256))
+
+
+@pytest.mark.parametrize("ad", [True, False])
+def test_flat_tile_beside_far_values(M, ad):
+    # near-constant tiles (ranges of a few ulp) whose blend cells reach into
+    # much darker / brighter regions: corners bin voxels with y far outside
+    # [0, n) (here y ~ -1e9).  With kernel 32 on 128 columns the tiles cover
+    # columns [32t-16, 32t+16) and cell t..t+1 spans [32t, 32t+32).
+    rng = np.random.default_rng(21)
+    x = np.empty((96, 128), np.float32)
+    x[:, :48] = 0.5 + rng.integers(0, 3, (96, 48)) * np.float32(6e-8)
+    x[:, 48:] = rng.random((96, 80)) * 0.01
+    x[:48, 80:] = 0.9 + rng.random((48, 48)) * 1e-3
+    args = ((32, 32), 256, 0.02, ad)
+    st, plan = gpu_stats(M, x, *args)
+    assert plan.info.fast_hist and plan.info.fast_interp
+    assert_stats_equal(st, O.tile_stats(x, *args, "c"), "flat")
+    out = M.enhance(x, *args)
+    assert np.max(np.abs(out.astype(np.float64) - O.mclahe(x, *args, "c"))) <= OUT_TOL
 
 
 def test_float64_input(M):
