@@ -206,6 +206,16 @@ __device__ __forceinline__ int clamp_bits(float t, int n) {
   return min(max(__float_as_int(t), kMagicBits), kMagicBits + n) - kMagicBits;
 }
 
+// Same value as an opaque max / sub / min sequence, so the compiler cannot
+// fold the magic offset into later address arithmetic.
+__device__ __forceinline__ int clamp_bits_k(float t, int n) {
+  int k;
+  asm("{\n\t.reg .s32 x;\n\tmax.s32 x, %1, %2;\n\tsub.s32 x, x, %2;\n\tmin.s32 %0, x, %3;\n\t}"
+      : "=r"(k)
+      : "r"(__float_as_int(t)), "r"(kMagicBits), "r"(n));
+  return k;
+}
+
 // Branch-free exact bins of two voxels against one tile, edge table only.
 // k = rint(y) (magic-number add in round-to-nearest); since |y - q| < 0.5 for
 // every y that matters, the reference bin floor(q) is k or k - 1, and it is k
@@ -242,6 +252,28 @@ __device__ __forceinline__ void lut2_edge(u64 V, float v0, float v1, float2 lc, 
   const int b1 = v1 >= *reinterpret_cast<const float*>(thb + k1) ? k1 : k1 - 4;
   m0 = *reinterpret_cast<const float*>(Lb + b0);
   m1 = *reinterpret_cast<const float*>(Lb + b1);
+}
+
+// One edge test + LUT gather against a tile block in shared memory (the NB
+// blend layout, NbBlock): k in [0, n] (clamp_bits), a = base + 4 pad(k); the
+// reference bin is k if v >= th[k] (at a + TH) else k - 1 (at a - 4, pads
+// repeat the entry before); returns LUT[bin] (at . + L).  Inline
+// PTX so both loads keep their [reg + imm] form off one address register.
+template <int TH, int L>
+__device__ __forceinline__ float edge_gather(uint32_t base, int k, float v) {
+  float m;
+  asm volatile(
+      "{\n\t.reg .u32 a;\n\t.reg .f32 t;\n\t.reg .pred p;\n\t"
+      "shr.u32 a, %1, 5;\n\t"
+      "add.u32 a, a, %1;\n\t"
+      "mad.lo.u32 a, a, 4, %2;\n\t"
+      "ld.shared.f32 t, [a+%4];\n\t"
+      "setp.lt.f32 p, %3, t;\n\t"
+      "@p sub.u32 a, a, 4;\n\t"
+      "ld.shared.f32 %0, [a+%5];\n\t}"
+      : "=f"(m)
+      : "r"(k), "r"(base), "f"(v), "n"(TH), "n"(L));
+  return m;
 }
 
 // Exact bin from the edge table alone (binary search over thr[1..n-1]);

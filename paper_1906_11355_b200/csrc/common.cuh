@@ -14,6 +14,8 @@
 // LDS, every thread owning a fixed 4-voxel column of the trailing block.
 #pragma once
 
+#include <type_traits>
+
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -23,6 +25,16 @@
 #include "geometry.h"
 
 namespace mg {
+
+// Compile-time loop: f(std::integral_constant<int, I>) for I in [B, E).
+template <int B, int E, typename F>
+__device__ __forceinline__ void static_for(F&& f) {
+  if constexpr (B < E) {
+    f(std::integral_constant<int, B>{});
+    static_for<B + 1, E>(f);
+  }
+}
+
 
 constexpr int kUnitInts = 10;      // unit record: [0..7] tile/cell per outer dim, [8] ra, [9] re
 constexpr int kMaxOuterDims = 5;   // pencil kernels: KO in [1, 5]
@@ -58,6 +70,8 @@ struct KGeom {
   int64_t win_tiles;
   int64_t local_voxels;
   double clip;
+  float inv_b[kMaxRank];   // 1 / b per dim (K4 weight factors)
+  float inv_2b[kMaxRank];  // 1 / (2 b)
 };
 
 // Workspace views.
@@ -108,6 +122,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "MG_WAIT_%=:\n\t"
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 1000000;\n\t"
       "@!p bra MG_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// Busy-poll variant (no suspend-time hint): for consumers whose stage is
+// normally already full, where the sleep/wake round trip costs issue slots.
+__device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "MG_SPIN_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra MG_SPIN_%=;\n}" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
 }

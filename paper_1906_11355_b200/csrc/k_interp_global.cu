@@ -21,7 +21,10 @@ PencilInterpFn get_interp_pencil_global(int ko, int kt) {
 
 namespace mg {
 PencilInterpFn get_interp_pencil_adaptive(int ko, int kt);
-PencilInterpFn get_interp_pencil(int ko, int kt, bool adaptive) {
-  return adaptive ? get_interp_pencil_adaptive(ko, kt) : get_interp_pencil_global(ko, kt);
+PencilInterpFn get_interp_pencil_adaptive_nb(int ko, int kt, int n_bins);
+PencilInterpFn get_interp_pencil(int ko, int kt, bool adaptive, int n_bins) {
+  if (!adaptive) return get_interp_pencil_global(ko, kt);
+  if (PencilInterpFn f = get_interp_pencil_adaptive_nb(ko, kt, n_bins)) return f;
+  return get_interp_pencil_adaptive(ko, kt);
 }
 }  // namespace mg

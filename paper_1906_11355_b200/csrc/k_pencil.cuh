@@ -298,7 +298,13 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
 // correlated bins).  The corner weights are products of per-dimension factors
 // d/b with exact half-integer numerators; FP32 sum (the reference's sorted
 // f64 sum is reproduced to <= 1e-6).
-template <int KO, int KT, bool ADAPT>
+//
+// NB > 0 (adaptive mode, n_bins == NB): each staged tile is one block
+// [lo, c | th[0..NB] | LUT[0..NB-1] | pad] of 2*NB+4 floats, blocks ordered
+// [trailing tile][outer corner], so a column's 2^D corner blocks sit at
+// compile-time offsets from one or two per-item base addresses and every
+// edge-table / LUT gather is a single LDS [reg + imm].
+template <int KO, int KT, bool ADAPT, int NB = 0>
 __global__ void __launch_bounds__(kBlendThreads, 1)
     k_interp_pencil(const __grid_constant__ KGeom G, const __grid_constant__ CUtensorMap tmap,
                     const __grid_constant__ CUtensorMap omap, const float* __restrict__ in,
@@ -326,7 +332,8 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
                 ~15LL));
   // per trailing column: first corner tile and the 4 x NCT trailing weights
   const int ncol = (int)(G.P / 4);
-  int* colT = reinterpret_cast<int*>(lcS + NCO * gtr);
+  int* colT = NB > 0 ? reinterpret_cast<int*>(P.tail + NCO * gtr * NbBlock::words(NB) * 4)
+                     : reinterpret_cast<int*>(lcS + NCO * gtr);
   float* colW = reinterpret_cast<float*>(colT + ncol);  // [ncol][4][NCT]
   __shared__ int s_bad;
   pipe_init(*P.pipe, G.nst, NW);
@@ -390,7 +397,7 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
   uint32_t it = 0;
   while (true) {
     const int s = it % G.nst;
-    mbar_wait(&P.pipe->full[s], (it / G.nst) & 1);
+    mbar_wait_spin(&P.pipe->full[s], (it / G.nst) & 1);
     const Stage& S = P.pipe->st[s];
     if (S.unit < 0) break;
     const int64_t key = S.key;
@@ -403,6 +410,28 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
         int64_t of = (S.cell[0] + ((co >> (KO - 1)) & 1) - G.trow0) * G.tstride[0];
         for (int j = 1; j < KO; ++j) of += (S.cell[j] + ((co >> (KO - 1 - j)) & 1)) * G.tstride[j];
         const float4* src = reinterpret_cast<const float4*>(W.lut + of * n);
+        if constexpr (NB > 0) {
+          constexpr int TBW = NbBlock::words(NB);
+          constexpr int PT = NbBlock::th_words(NB), PL = NbBlock::lut_words(NB);
+          float* blk = reinterpret_cast<float*>(P.tail) + co * TBW;  // + t * NCO * TBW
+          const float* ls = W.lut + of * NB;
+          for (int64_t k = tid; k < gtr * PL; k += kConsumersBlend) {
+            const int t = (int)(k / PL), q = (int)(k - (int64_t)t * PL);
+            blk[t * NCO * TBW + NbBlock::lut_off(NB) + q] = __ldg(ls + t * NB + NbBlock::src(q));
+          }
+          const float* ts = W.thr + of * (NB + 1);
+          for (int64_t k = tid; k < gtr * PT; k += kConsumersBlend) {
+            const int t = (int)(k / PT), q = (int)(k - (int64_t)t * PT);
+            blk[t * NCO * TBW + NbBlock::th_off(NB) + q] =
+                __ldg(ts + t * (NB + 1) + NbBlock::src(q));
+          }
+          for (int64_t t = tid; t < gtr; t += kConsumersBlend) {
+            const float2 lc = tile_lc(tparams[of + t]);
+            *reinterpret_cast<float2*>(blk + t * NCO * TBW) = lc;
+            if (isnan(lc.y)) s_bad = 1;
+          }
+          continue;
+        }
         if (PAIR) {
           float* dp = reinterpret_cast<float*>(pairS + co * (gtr - 1) * n1);
           for (int64_t k = tid; k < gtr * n / 4; k += kConsumersBlend) {
@@ -451,9 +480,8 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
 #pragma unroll
       for (int j = 0; j < KO; ++j) {
         const Dim& d = G.d[j];
-        const float sj = 1.0f / (float)d.b;
-        const float tj =
-            (float)(2 * d.before - 2 * (int64_t)S.cell[j] * d.b - d.b + 1) / (float)(2 * d.b);
+        const float sj = G.inv_b[j];
+        const float tj = (float)(2 * d.before - 2 * (int64_t)S.cell[j] * d.b - d.b + 1) * G.inv_2b[j];
         if (j == KO - 1) {
           s1 = sj;
           t1 = tj;
@@ -529,7 +557,80 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
           }
         }
         const int n4 = 4 * n;
-        if (ADAPT && !patho) {  // hot path: branch-free edge-table gathers
+        if constexpr (NB > 0) {
+          // corner (co, ct) block: base[ct >> 1] + ((ct & 1) * NCO + co) * TB
+          constexpr int TB = NbBlock::words(NB) * 4;
+          const char* blkc = reinterpret_cast<const char*>(P.tail);
+          const char* base[KT];
+          base[0] = blkc + tt * (NCO * TB);
+          if (KT == 2) base[KT - 1] = base[0] + ctoff[KT == 2 ? 2 : 0] * (NCO * TB);
+          uint32_t sbase[KT];
+#pragma unroll
+          for (int j = 0; j < KT; ++j) sbase[j] = (uint32_t)__cvta_generic_to_shared(base[j]);
+          const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
+          if (!patho) {  // hot path: one LDS per edge test and per gather
+            static_for<0, NCO>([&](auto coc) {
+              constexpr int co = decltype(coc)::value;
+              float m[NCT][4];
+              static_for<0, NCT>([&](auto ctc) {
+                constexpr int ct = decltype(ctc)::value;
+                constexpr int OFF = ((ct & 1) * NCO + co) * TB;
+                const float2 lc = *reinterpret_cast<const float2*>(base[ct >> 1] + OFF);
+                u64 tq[2];
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                  const u64 y = mul2(sub2(h ? V23 : V01, pk2(lc.x, lc.x)), pk2(lc.y, lc.y));
+                  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(tq[h]) : "l"(y), "l"(pk2(kMagic, kMagic)));
+                }
+                float tf[4];
+                upk2(tq[0], tf[0], tf[1]);
+                upk2(tq[1], tf[2], tf[3]);
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                  m[ct][i] = edge_gather<OFF + NbBlock::th_off(NB) * 4,
+                                         OFF + NbBlock::lut_off(NB) * 4>(
+                      sbase[ct >> 1], clamp_bits_k(tf[i], NB), vv[i]);
+              });
+#pragma unroll
+              for (int ct = 0; ct < NCT; ++ct)
+#pragma unroll
+                for (int i = 0; i < 4; ++i) act[ct][i] = fmaf(wo[co], m[ct][i], act[ct][i]);
+            });
+          } else {  // a pathological range in the pencil: exact search where needed
+#pragma unroll
+            for (int co = 0; co < NCO; ++co) {
+#pragma unroll
+              for (int ct = 0; ct < NCT; ++ct) {
+                const char* B = base[ct >> 1] + ((ct & 1) * NCO + co) * TB;
+                const float2 lc = *reinterpret_cast<const float2*>(B);
+                const float* th = reinterpret_cast<const float*>(B) + NbBlock::th_off(NB);
+                const float* L = reinterpret_cast<const float*>(B) + NbBlock::lut_off(NB);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                  int b = 0;
+                  if (isnan(lc.y)) {  // binary search over the padded edge table
+                    int lo = 0, hi = NB - 1;
+                    while (lo < hi) {
+                      const int mid = (lo + hi + 1) >> 1;
+                      if (vv[i] >= th[NbBlock::pad(mid)]) lo = mid;
+                      else hi = mid - 1;
+                    }
+                    b = lo;
+                  } else {
+                    const u64 y = mul2(sub2(pk2(vv[i], vv[i]), pk2(lc.x, lc.x)), pk2(lc.y, lc.y));
+                    u64 t2;
+                    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(t2) : "l"(y), "l"(pk2(kMagic, kMagic)));
+                    float t0, t1;
+                    upk2(t2, t0, t1);
+                    const int k = clamp_bits(t0, NB);
+                    b = vv[i] >= th[NbBlock::pad(k)] ? k : k - 1;
+                  }
+                  act[ct][i] = fmaf(wo[co], L[NbBlock::pad(b)], act[ct][i]);
+                }
+              }
+            }
+          }
+        } else if (ADAPT && !patho) {  // hot path: branch-free edge-table gathers
 #pragma unroll
           for (int co = 0; co < NCO; ++co) {
             float m[NCT][4];
@@ -625,6 +726,6 @@ using PencilInterpFn = void (*)(const KGeom, const CUtensorMap, const CUtensorMa
                                 float*, const int32_t*, const int32_t*, WS);
 PencilRangeFn get_range_pencil(int ko);
 PencilHistFn get_hist_pencil(int ko, bool adaptive);
-PencilInterpFn get_interp_pencil(int ko, int kt, bool adaptive);
+PencilInterpFn get_interp_pencil(int ko, int kt, bool adaptive, int n_bins);
 
 }  // namespace mg

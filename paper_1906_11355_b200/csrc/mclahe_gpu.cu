@@ -147,6 +147,10 @@ KGeom pencil_geom(const mclahe_plan_s& pl, const Pencil& pc) {
   G.tma_rank = pc.tma_rank;
   G.nseg = pc.nseg;
   G.stage_stride = pc.stage_stride;
+  for (int j = 0; j < G.rank; ++j) {
+    G.inv_b[j] = 1.0f / (float)G.d[j].b;
+    G.inv_2b[j] = 1.0f / (float)(2 * G.d[j].b);
+  }
   return G;
 }
 
@@ -215,6 +219,10 @@ Pencil choose_pencil(const mclahe_plan_s& pl, bool for_hist) {
       const int64_t pairs = (int64_t{1} << ko) * (c.gtr - 1) * (n + 1) * 2;  // global, KT == 1
       c.tail = align_up((pl.p.adaptive ? 2 * luts1 : (kt == 1 ? pairs : luts1) + n + 1) * 4, 16) +
                (int64_t{1} << ko) * c.gtr * 16 + (c.P / 4) * (4 + 16 * (int64_t{1} << kt));
+      if (pl.p.adaptive)  // NB-specialised kernel: padded per-tile blocks (NbBlock)
+        c.tail = std::max<int64_t>(
+            c.tail, (int64_t{1} << ko) * c.gtr * NbBlock::words((int)n) * 4 +
+                        (c.P / 4) * (4 + 16 * (int64_t{1} << kt)));
       c.rpi = kConsumersBlend / c.tpr;
       const int64_t avail = 226 * 1024 - kPipeBytes - c.tail;
       if (avail >= 4 * 4096) c.stage_budget = std::min<int64_t>(kStageBytes, avail / 4);
@@ -541,7 +549,11 @@ using HistFn = PencilHistFn;
 using InterpFn = PencilInterpFn;
 RangeFn range_fn(int ko) { return get_range_pencil(ko); }
 HistFn hist_fn(int ko, bool a) { return get_hist_pencil(ko, a); }
-InterpFn interp_fn(int ko, int kt, bool a) { return get_interp_pencil(ko, kt, a); }
+// MCLAHE_NO_NB=1 forces the runtime-n_bins blend kernel (A/B measurements).
+InterpFn interp_fn(int ko, int kt, bool a, int64_t n_bins) {
+  static const bool no_nb = getenv("MCLAHE_NO_NB") != nullptr;
+  return get_interp_pencil(ko, kt, a, no_nb ? 0 : (int)n_bins);
+}
 
 WS ws_view(const mclahe_plan_s* pl, void* ws) {
   char* b = static_cast<char*>(ws);
@@ -599,7 +611,7 @@ int device_init(mclahe_plan_s* pl) {
   }
   if (pl->interp.on) {
     int occ = 0;
-    InterpFn f = interp_fn(pl->interp.ko, pl->interp.kt, A);
+    InterpFn f = interp_fn(pl->interp.ko, pl->interp.kt, A, pl->p.n_bins);
     MG_CUDA(raise_smem_cap(f, max_smem));
     MG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f, kBlendThreads, pl->interp.smem));
     pl->interp_grid = (int)std::max<int64_t>(
@@ -763,7 +775,7 @@ int do_interp(mclahe_plan_s* pl, const void* in, void* out, void* ws, cudaStream
   const bool A = pl->p.adaptive != 0;
   if (pl->interp.on) {
     const KGeom G = pencil_geom(*pl, pl->interp);
-    InterpFn f = interp_fn(pl->interp.ko, pl->interp.kt, A);
+    InterpFn f = interp_fn(pl->interp.ko, pl->interp.kt, A, pl->p.n_bins);
     int rc = tensor_map(pl, 1, in);
     if (rc) return rc;
     if ((rc = tensor_map(pl, 2, out))) return rc;
