@@ -179,6 +179,12 @@ int mclahe_plan_check(mclahe_plan_t plan, const void* workspace, void* stream);
 int mclahe_debug_bin_index(int32_t dtype, const void* values_dev, int64_t n, double lo,
                            double hi, int64_t n_bins, int32_t* out_dev, void* stream);
 
+/* Value-dictionary state after a run on `workspace` (synchronises `stream`):
+ * state[0] = 1 if the last blend used the dictionary path, state[1] = number
+ * of distinct values collected, state[2] = the plan's capacity (0: never). */
+int mclahe_plan_dict_state(mclahe_plan_t plan, const void* workspace, int32_t* state,
+                           void* stream);
+
 /* The pencil kernels' packed f32x2 binning on n device float32 values (pairs
  * of consecutive values): variant 1 = the histogram routine, 2 = the blend
  * gather (through an identity LUT).  Must equal mclahe_debug_bin_index. */

@@ -197,6 +197,14 @@ class Plan:
     def check(self, ws, stream=None):
         N.check(N.lib().mclahe_plan_check(self._h, self._ptr(ws), _stream_handle(stream)))
 
+    def dict_state(self, ws, stream=None) -> dict:
+        """Value-dictionary state after a run on ``ws``: ``used`` (the blend took
+        the dictionary path), ``values`` (distinct values collected), ``capacity``
+        (0 when the plan never arms it)."""
+        st = (C.c_int32 * 3)()
+        N.check(N.lib().mclahe_plan_dict_state(self._h, self._ptr(ws), st, _stream_handle(stream)))
+        return dict(used=bool(st[0]), values=int(st[1]), capacity=int(st[2]))
+
     def tile_stats(self, x, stream=None) -> dict:
         """Runs passes 1-3 and returns the per-tile intermediates of the
         workspace window (debug arrays of build_mappings, histogram.cpp:72-106)."""

@@ -72,7 +72,53 @@ struct KGeom {
   double clip;
   float inv_b[kMaxRank];   // 1 / b per dim (K4 weight factors)
   float inv_2b[kMaxRank];  // 1 / (2 b)
+  int dict;                // 1: the value-dictionary blend is armed (K2a builds the dictionary)
 };
+
+// Value dictionary (adaptive mode, float32): when the volume holds few
+// distinct values (quantised counts), K2a collects them, k_dict_finalize
+// numbers them and builds a lookup hash, k_dict_luts tabulates every tile's
+// LUT[bin(value)] per value, and the blend gathers those directly.
+constexpr int kDictHG = 8192;        // global set slots (accepts <= kDictHG / 2 values)
+// Shared-memory sets are bucketised: 4 keys per 16-byte bucket, so a present
+// value is found with one LDS.128 and four compares (no divergent probe loop).
+constexpr int kDictLgBS = 10;        // K2a per-CTA set: 1024 buckets (16 KB)
+constexpr int kDictHS = 4 << kDictLgBS;
+constexpr int kDictLgHL = 11;        // blend lookup: cuckoo table of 2048 {bits, index}
+constexpr int kDictHL = 1 << kDictLgHL;
+constexpr int kDictKC = 576;         // values per tile row in the blend (capacity)
+constexpr uint32_t kDictEmpty = 0xFFFFFFFFu;  // a NaN pattern: never a finite input
+__host__ __device__ __forceinline__ uint32_t dict_hash(uint32_t b, int lg) {
+  return (b * 0x9E3779B1u) >> (32 - lg);
+}
+// meta[0]: values inserted, [1]: overflow, [2]: dictionary usable, [3]: K
+
+// Cuckoo lookup: a value sits at one of two slots (branch-free, two LDS.64);
+// -1 when absent.
+__host__ __device__ __forceinline__ uint32_t dict_h1(uint32_t b) {
+  return (b * 0x9E3779B1u) >> (32 - kDictLgHL);
+}
+__host__ __device__ __forceinline__ uint32_t dict_h2(uint32_t b) {
+  return ((b ^ (b >> 15)) * 0x85EBCA77u) >> (32 - kDictLgHL);
+}
+__device__ __forceinline__ int dict_lookup(const uint2* t, uint32_t b) {
+  const uint2 e1 = t[dict_h1(b)], e2 = t[dict_h2(b)];
+  return e1.x == b ? (int)e1.y : e2.x == b ? (int)e2.y : -1;
+}
+
+// Slot of b in a bucketised key table (4 keys per bucket, nb = 2^lg
+// buckets), or -1 after a full sweep; b must not be kDictEmpty.
+__device__ __forceinline__ int dict_find(const uint4* keys, uint32_t b, int lg) {
+  uint32_t bk = dict_hash(b, lg);
+  for (int probe = 0; probe < (1 << lg); ++probe) {
+    const uint4 q = keys[bk];
+    const int j = q.x == b ? 0 : q.y == b ? 1 : q.z == b ? 2 : q.w == b ? 3 : -1;
+    if (j >= 0) return (int)(bk * 4 + j);
+    if (q.w == kDictEmpty) return -1;  // buckets fill in slot order
+    bk = (bk + 1) & ((1u << lg) - 1);
+  }
+  return -1;
+}
 
 // Workspace views.
 struct WS {
@@ -82,6 +128,11 @@ struct WS {
   void* tparams;        // TileParam<T>[adaptive ? win_tiles : 1]
   float* lut;           // [win_tiles][n_bins]
   float* thr;           // [adaptive ? win_tiles : 1][n_bins] bin-edge tables (f32 data)
+  int32_t* dmeta;       // [8] value dictionary state (see kDict*)
+  uint32_t* dkeys;      // [kDictHG] value bits (open addressing)
+  float* dvals;         // [kDictHG / 2] values by index
+  uint2* dlt;           // [kDictHL] cuckoo lookup {bits, index}
+  float* lutd;          // [win_tiles][kDictKC] LUT[bin(value)] per value
 };
 
 struct Debug {

@@ -4,14 +4,19 @@
 
 namespace mg {
 
-PencilRangeFn get_range_pencil(int ko) {
+template <bool DICT>
+static PencilRangeFn range_t(int ko) {
   switch (ko) {
-    case 1: return k_range_pencil<1>;
-    case 2: return k_range_pencil<2>;
-    case 3: return k_range_pencil<3>;
-    case 4: return k_range_pencil<4>;
-    default: return k_range_pencil<5>;
+    case 1: return k_range_pencil<1, DICT>;
+    case 2: return k_range_pencil<2, DICT>;
+    case 3: return k_range_pencil<3, DICT>;
+    case 4: return k_range_pencil<4, DICT>;
+    default: return k_range_pencil<5, DICT>;
   }
+}
+
+PencilRangeFn get_range_pencil(int ko, bool dict) {
+  return dict ? range_t<true>(ko) : range_t<false>(ko);
 }
 
 template <bool A>

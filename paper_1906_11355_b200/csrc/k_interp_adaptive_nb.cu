@@ -23,4 +23,18 @@ PencilInterpFn get_interp_pencil_adaptive_nb(int ko, int kt, int n_bins) {
   }
 }
 
+template <int KT>
+static PencilInterpFn interp_dict(int ko) {
+  switch (ko) {
+    case 1: return k_interp_pencil<1, KT, true, -1>;
+    case 2: return k_interp_pencil<2, KT, true, -1>;
+    case 3: return k_interp_pencil<3, KT, true, -1>;
+    default: return k_interp_pencil<4, KT, true, -1>;
+  }
+}
+
+PencilInterpFn get_interp_pencil_dict(int ko, int kt) {
+  return kt == 1 ? interp_dict<1>(ko) : interp_dict<2>(ko);
+}
+
 }  // namespace mg

@@ -34,10 +34,88 @@ __device__ __forceinline__ void decode_local(const KGeom& G, int64_t idx, int64_
 }
 
 // ---------------------------------------------------------------- reset ---
-__global__ void k_reset(int64_t* range, int64_t* trange, int64_t n_trange) {
+__global__ void k_reset(int64_t* range, int64_t* trange, int64_t n_trange, WS W, int dict) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < 4) range[i] = i < 2 ? INT64_MIN : 0;
   for (int64_t k = i; k < n_trange; k += (int64_t)gridDim.x * blockDim.x) trange[k] = INT64_MIN;
+  if (dict) {
+    if (i < 8) W.dmeta[i] = 0;
+    for (int64_t k = i; k < kDictHG; k += (int64_t)gridDim.x * blockDim.x) W.dkeys[k] = kDictEmpty;
+  }
+}
+
+// Numbers the collected values (slot order), fills dvals and the {bits,
+// index} lookup hash, and marks the dictionary usable when it fits the
+// blend's capacity.  One CTA of 1024 threads.
+__global__ void __launch_bounds__(1024) k_dict_finalize(WS W, int cap) {
+  __shared__ int s_part[1024];
+  const int tid = threadIdx.x;
+  constexpr int PER = kDictHG / 1024;
+  if (W.dmeta[1] != 0 || W.dmeta[0] > cap) {
+    if (tid == 0) W.dmeta[2] = 0;
+    return;
+  }
+  for (int k = tid; k < kDictHL; k += 1024) W.dlt[k] = make_uint2(kDictEmpty, 0);
+  int c = 0;
+  for (int j = 0; j < PER; ++j) c += W.dkeys[tid * PER + j] != kDictEmpty;
+  s_part[tid] = c;
+  __syncthreads();
+  for (int off = 1; off < 1024; off <<= 1) {  // inclusive scan
+    const int v = tid >= off ? s_part[tid - off] : 0;
+    __syncthreads();
+    s_part[tid] += v;
+    __syncthreads();
+  }
+  int idx = s_part[tid] - c;
+  for (int j = 0; j < PER; ++j) {
+    const uint32_t b = W.dkeys[tid * PER + j];
+    if (b == kDictEmpty) continue;
+    W.dvals[idx++] = __uint_as_float(b);
+  }
+  __syncthreads();
+  if (tid == 0) {  // cuckoo placement, values in index order
+    const int K = s_part[1023];
+    bool ok = true;
+    for (int i = 0; i < K && ok; ++i) {
+      uint2 e = make_uint2(__float_as_uint(W.dvals[i]), (uint32_t)i);
+      uint32_t h = dict_h1(e.x);
+      int steps = 0;
+      while (true) {
+        const uint2 o = W.dlt[h];
+        W.dlt[h] = e;
+        if (o.x == kDictEmpty) break;
+        if (++steps > 4 * kDictHL) {
+          ok = false;
+          break;
+        }
+        e = o;  // evict to its other slot
+        h = dict_h1(e.x) == h ? dict_h2(e.x) : dict_h1(e.x);
+      }
+    }
+    W.dmeta[3] = K;
+    W.dmeta[2] = ok ? 1 : 0;
+  }
+}
+
+// lutd[t][i] = LUT_t[bin_t(value_i)] with the reference bin rule in f64
+// (degenerate tiles: any bin, their LUT is constant).  Grid: tiles x values.
+template <typename T>
+__global__ void k_dict_luts(WS W, int64_t win_tiles, int n) {
+  if (W.dmeta[2] == 0) return;
+  const int K = W.dmeta[3];
+  const TileParam<T>* tp = reinterpret_cast<const TileParam<T>*>(W.tparams);
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < win_tiles * kDictKC;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = e / kDictKC;
+    const int i = (int)(e - t * kDictKC);
+    float r = 0.0f;
+    if (i < K) {
+      const double lo = (double)tp[t].lo, hi = (double)tp[t].hi;
+      const int b = lo < hi ? bin_exact((double)W.dvals[i], lo, hi, n) : 0;
+      r = W.lut[t * n + b];
+    }
+    W.lutd[e] = r;
+  }
 }
 
 // ------------------------------------------------------------------ K1 ----

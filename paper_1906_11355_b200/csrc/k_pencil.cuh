@@ -43,7 +43,9 @@ __device__ __forceinline__ void trailing_tile(const KGeom& G, int64_t e, int* ti
 }
 
 // --------------------------------------------------------------- K2a -----
-template <int KO>
+// DICT: also collects the distinct values (bit patterns) of the slab into a
+// per-CTA hash set, merged into the workspace set at the end (kDict*).
+template <int KO, bool DICT>
 __global__ void __launch_bounds__(kPencilThreads, 3)
     k_range_pencil(const __grid_constant__ KGeom G, const __grid_constant__ CUtensorMap tmap,
                    const float* __restrict__ in, const int32_t* __restrict__ units,
@@ -52,6 +54,13 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
   const PencilSmem P = pencil_smem(G, smem);
   int32_t* smin = reinterpret_cast<int32_t*>(P.tail);  // [gtr] ~key32(lo)
   int32_t* smax = smin + G.gtr;                         // [gtr] key32(hi)
+  uint32_t* sset =  // [kDictHS] (DICT), 16-byte buckets
+      reinterpret_cast<uint32_t*>(P.tail + ((G.gtr * 8 + 15) & ~15LL));
+  __shared__ int s_n, s_over;
+  if (DICT) {
+    for (int k = threadIdx.x; k < kDictHS; k += blockDim.x) sset[k] = kDictEmpty;
+    if (threadIdx.x == 0) s_n = s_over = 0;
+  }
   pipe_init(*P.pipe, G.nst);
   __syncthreads();
   const int u0 = cta_units[blockIdx.x], u1 = cta_units[blockIdx.x + 1];
@@ -64,6 +73,31 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
   const int slot = tid / G.tpr;
   const int64_t e0 = (int64_t)(tid % G.tpr) * 4;
   const bool lane_on = slot < G.rpi;
+  // bucketised insert: a present value costs one LDS.128 and four compares
+  auto dict_add = [&](float f) {
+    const uint32_t b = __float_as_uint(f);
+    uint32_t bk = dict_hash(b, kDictLgBS);
+    const uint4 q = reinterpret_cast<const uint4*>(sset)[bk];
+    if (q.x == b || q.y == b || q.z == b || q.w == b) return;
+    for (int probe = 0; probe < (1 << kDictLgBS); ++probe) {
+#pragma unroll 1
+      for (int j = 0; j < 4; ++j) {
+        uint32_t* sl = sset + bk * 4 + j;
+        const uint32_t k = *reinterpret_cast<volatile uint32_t*>(sl);
+        if (k == b) return;
+        if (k == kDictEmpty) {
+          const uint32_t old = atomicCAS(sl, kDictEmpty, b);
+          if (old == kDictEmpty) {
+            if (atomicAdd(&s_n, 1) >= kDictHS / 2) s_over = 1;
+            return;
+          }
+          if (old == b) return;
+        }
+      }
+      bk = (bk + 1) & ((1u << kDictLgBS) - 1);
+    }
+    s_over = 1;
+  };
   int trt[4], dummy;
 #pragma unroll
   for (int i = 0; i < 4; ++i) trailing_tile(G, e0 + i, &trt[i], &dummy);
@@ -111,7 +145,8 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
     const int rows = G.stage_rows;
     const float* buf = P.bufs + s * stage_elems;
     if (lane_on) {
-      for (int q = slot; q < rows; q += G.rpi) {
+      int k = 0;
+      for (int q = slot; q < rows; q += G.rpi, ++k) {
         const float4 v = *reinterpret_cast<const float4*>(buf + q * G.P + e0);
         const float a[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
@@ -119,6 +154,13 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
           bad |= !isfinite(a[i]);
           mn[i] = fminf(mn[i], a[i]);
           mx[i] = fmaxf(mx[i], a[i]);
+        }
+        // every fourth row pass (warp-uniform, rotating with the stage): values
+        // the sample misses are rare ones, which the blend resolves from the
+        // edge tables
+        if (DICT && ((k + it) & 3) == 0 && !*reinterpret_cast<volatile int*>(&s_over)) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) dict_add(a[i]);
         }
       }
     }
@@ -128,6 +170,27 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
   }
   if (cur >= 0) flush();
   if (bad) atomicMax(reinterpret_cast<long long*>(&W.range[2]), 1LL);
+  if (DICT) {  // merge the CTA's values into the workspace set
+    consumers_sync();
+    if (s_over) {
+      if (tid == 0) atomicExch(&W.dmeta[1], 1);
+      return;
+    }
+    for (int k = tid; k < kDictHS; k += kConsumers) {
+      const uint32_t b = sset[k];
+      if (b == kDictEmpty) continue;
+      uint32_t h = dict_hash(b, 13);  // kDictHG = 2^13 slots, linear probing
+      for (int probe = 0; probe < kDictHG; ++probe) {
+        const uint32_t old = atomicCAS(&W.dkeys[h], kDictEmpty, b);
+        if (old == b) break;
+        if (old == kDictEmpty) {
+          if (atomicAdd(&W.dmeta[0], 1) >= kDictHG / 2) atomicExch(&W.dmeta[1], 1);
+          break;
+        }
+        h = (h + 1) & (kDictHG - 1);
+      }
+    }
+  }
 }
 
 // --------------------------------------------------------------- K2b -----
@@ -287,6 +350,15 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
   }
 }
 
+// LUT value of one voxel against one window tile straight from the workspace
+// (reference bin rule in f64): the dictionary blend's path for values its
+// sampled dictionary does not hold.
+static __device__ __noinline__ float lut_value_global(const WS& W, int n, int64_t tile, float v) {
+  const TileParam<float> tp = reinterpret_cast<const TileParam<float>*>(W.tparams)[tile];
+  const int b = tp_degenerate(tp.lim) ? 0 : bin_exact((double)v, (double)tp.lo, (double)tp.hi, n);
+  return W.lut[tile * n + b];
+}
+
 // ---------------------------------------------------------------- K4 -----
 // One cell pencil (2^KO outer corners x every trailing tile) per unit; its
 // LUTs, edge tables and {lo, c} pairs are staged in shared memory (rows padded
@@ -304,6 +376,12 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
 // [trailing tile][outer corner], so a column's 2^D corner blocks sit at
 // compile-time offsets from one or two per-item base addresses and every
 // edge-table / LUT gather is a single LDS [reg + imm].
+//
+// NB < 0 (adaptive mode, value dictionary usable -- kDict*): blocks of
+// kDictKC floats hold LUT_t[bin_t(value_i)] per dictionary value i, so a voxel
+// looks its value up once (smem hash) and each corner is one LDS [reg + imm];
+// no binning at all.  The dictionary and the edge-table kernels are both
+// launched and whichever the device-side flag does not select exits at once.
 template <int KO, int KT, bool ADAPT, int NB = 0>
 __global__ void __launch_bounds__(kBlendThreads, 1)
     k_interp_pencil(const __grid_constant__ KGeom G, const __grid_constant__ CUtensorMap tmap,
@@ -312,7 +390,13 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
                     const int32_t* __restrict__ units, const int32_t* __restrict__ cta_units, WS W) {
   constexpr int NCO = 1 << KO, NCT = 1 << KT;
   constexpr int NW = kConsumersBlend / 32;
+  constexpr bool DICT = NB < 0;
   if (W.range[2] != 0) return;  // non-finite input: write nothing
+  if (DICT) {
+    if (W.dmeta[2] == 0) return;
+  } else if (ADAPT && G.dict) {
+    if (W.dmeta[2] != 0) return;
+  }
   extern __shared__ __align__(1024) unsigned char smem[];
   const PencilSmem P = pencil_smem(G, smem);
   const int n = G.n_bins;
@@ -332,8 +416,12 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
                 ~15LL));
   // per trailing column: first corner tile and the 4 x NCT trailing weights
   const int ncol = (int)(G.P / 4);
-  int* colT = NB > 0 ? reinterpret_cast<int*>(P.tail + NCO * gtr * NbBlock::words(NB) * 4)
-                     : reinterpret_cast<int*>(lcS + NCO * gtr);
+  uint2* dltS =  // DICT: cuckoo lookup {bits, index} [kDictHL] after the value blocks
+      reinterpret_cast<uint2*>(P.tail + NCO * gtr * kDictKC * 4);
+  int* ofS = reinterpret_cast<int*>(dltS + kDictHL);  // [NCO] window tile of corner co's row
+  int* colT = DICT     ? ofS + NCO
+              : NB > 0 ? reinterpret_cast<int*>(P.tail + NCO * gtr * NbBlock::words(NB) * 4)
+                       : reinterpret_cast<int*>(lcS + NCO * gtr);
   float* colW = reinterpret_cast<float*>(colT + ncol);  // [ncol][4][NCT]
   __shared__ int s_bad;
   pipe_init(*P.pipe, G.nst, NW);
@@ -406,10 +494,23 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
       if (tid == 0) s_bad = 0;
       if (!ADAPT && cur < 0)
         for (int k = tid; k < n1; k += kConsumersBlend) thrS[k] = W.thr[k];
+      if (DICT && cur < 0)
+        for (int k = tid; k < kDictHL; k += kConsumersBlend) dltS[k] = W.dlt[k];
       for (int co = 0; co < NCO; ++co) {
         int64_t of = (S.cell[0] + ((co >> (KO - 1)) & 1) - G.trow0) * G.tstride[0];
         for (int j = 1; j < KO; ++j) of += (S.cell[j] + ((co >> (KO - 1 - j)) & 1)) * G.tstride[j];
         const float4* src = reinterpret_cast<const float4*>(W.lut + of * n);
+        if constexpr (DICT) {
+          constexpr int KC4 = kDictKC / 4;
+          if (tid == 0) ofS[co] = (int)of;
+          float4* blk = reinterpret_cast<float4*>(P.tail) + co * KC4;  // + t * NCO * KC4
+          const float4* ds = reinterpret_cast<const float4*>(W.lutd + of * kDictKC);
+          for (int64_t k = tid; k < gtr * KC4; k += kConsumersBlend) {
+            const int t = (int)(k / KC4), q = (int)(k - (int64_t)t * KC4);
+            blk[t * NCO * KC4 + q] = __ldg(ds + k);
+          }
+          continue;
+        }
         if constexpr (NB > 0) {
           constexpr int TBW = NbBlock::words(NB);
           constexpr int PT = NbBlock::th_words(NB), PL = NbBlock::lut_words(NB);
@@ -557,7 +658,48 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
           }
         }
         const int n4 = 4 * n;
-        if constexpr (NB > 0) {
+        if constexpr (DICT) {
+          // corner (co, ct) row: base[ct >> 1] + ((ct & 1) * NCO + co) * KC floats
+          constexpr int TB = kDictKC * 4;
+          const char* blkc = reinterpret_cast<const char*>(P.tail);
+          const char* base[KT];
+          base[0] = blkc + tt * (NCO * TB);
+          if (KT == 2) base[KT - 1] = base[0] + ctoff[KT == 2 ? 2 : 0] * (NCO * TB);
+          const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
+          const char* A[KT][4];
+          int miss = 0;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int di = dict_lookup(dltS, __float_as_uint(vv[i]));
+            miss |= (di < 0) << i;
+            const int off = di >= 0 ? di * 4 : 0;
+#pragma unroll
+            for (int j = 0; j < KT; ++j) A[j][i] = base[j] + off;
+          }
+          static_for<0, NCO>([&](auto coc) {
+            constexpr int co = decltype(coc)::value;
+            float m[NCT][4];
+            static_for<0, NCT>([&](auto ctc) {
+              constexpr int ct = decltype(ctc)::value;
+              constexpr int OFF = ((ct & 1) * NCO + co) * TB;
+#pragma unroll
+              for (int i = 0; i < 4; ++i)
+                m[ct][i] = *reinterpret_cast<const float*>(A[ct >> 1][i] + OFF);
+            });
+            if (miss) {  // values outside the (sampled) dictionary: edge tables in L2
+#pragma unroll
+              for (int i = 0; i < 4; ++i)
+                if ((miss >> i) & 1)
+#pragma unroll
+                  for (int ct = 0; ct < NCT; ++ct)
+                    m[ct][i] = lut_value_global(W, n, ofS[co] + tt + ctoff[ct], vv[i]);
+            }
+#pragma unroll
+            for (int ct = 0; ct < NCT; ++ct)
+#pragma unroll
+              for (int i = 0; i < 4; ++i) act[ct][i] = fmaf(wo[co], m[ct][i], act[ct][i]);
+          });
+        } else if constexpr (NB > 0) {
           // corner (co, ct) block: base[ct >> 1] + ((ct & 1) * NCO + co) * TB
           constexpr int TB = NbBlock::words(NB) * 4;
           const char* blkc = reinterpret_cast<const char*>(P.tail);
@@ -724,8 +866,9 @@ using PencilRangeFn = void (*)(const KGeom, const CUtensorMap, const float*, con
 using PencilHistFn = PencilRangeFn;
 using PencilInterpFn = void (*)(const KGeom, const CUtensorMap, const CUtensorMap, const float*,
                                 float*, const int32_t*, const int32_t*, WS);
-PencilRangeFn get_range_pencil(int ko);
+PencilRangeFn get_range_pencil(int ko, bool dict);
 PencilHistFn get_hist_pencil(int ko, bool adaptive);
 PencilInterpFn get_interp_pencil(int ko, int kt, bool adaptive, int n_bins);
+PencilInterpFn get_interp_pencil_dict(int ko, int kt);
 
 }  // namespace mg

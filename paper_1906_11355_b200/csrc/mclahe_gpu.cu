@@ -101,6 +101,13 @@ struct Pencil {
 constexpr int64_t kPipeBytes = (sizeof(mg::Pipe) + 1023) & ~int64_t(1023);
 constexpr int64_t kStageBytes = 16384;
 
+// dictionary workspace: meta[8] | keys[HG] | vals[HG/2] | lookup[HL] | lutd[tiles][KC]
+constexpr int64_t kDictOffKeys = 256;
+constexpr int64_t kDictOffVals = kDictOffKeys + kDictHG * 4;
+constexpr int64_t kDictOffLt = kDictOffVals + kDictHG / 2 * 4;
+constexpr int64_t kDictOffLutd = kDictOffLt + kDictHL * 8;
+int64_t dict_bytes(int64_t win_tiles) { return kDictOffLutd + win_tiles * kDictKC * 4; }
+
 }  // namespace
 
 struct mclahe_plan_s {
@@ -118,6 +125,9 @@ struct mclahe_plan_s {
   int64_t off_hist_units = 0, off_hist_cta = 0, off_interp_units = 0, off_interp_cta = 0;
   int hist_grid = 0, interp_grid = 0, range_grid = 0, map_grid = 0, map_block = 128;
   int64_t map_smem = 0;
+  // value dictionary (kDict*): armed when the blend's tables fit shared memory
+  int dict_cap = 0, dict_nst = 0;
+  int64_t dict_smem = 0, off_dict = 0;
   // TMA views of the last input buffer (re-encoded when the pointer changes)
   const void* map_ptr[3] = {nullptr, nullptr, nullptr};
   CUtensorMap map[3];  // [0] hist view of the input, [1] blend view of the input, [2] of the output
@@ -147,6 +157,7 @@ KGeom pencil_geom(const mclahe_plan_s& pl, const Pencil& pc) {
   G.tma_rank = pc.tma_rank;
   G.nseg = pc.nseg;
   G.stage_stride = pc.stage_stride;
+  G.dict = pl.dict_cap > 0 ? 1 : 0;
   for (int j = 0; j < G.rank; ++j) {
     G.inv_b[j] = 1.0f / (float)G.d[j].b;
     G.inv_2b[j] = 1.0f / (float)(2 * G.d[j].b);
@@ -313,6 +324,27 @@ void size_boxes(const mclahe_plan_s& pl, Pencil& c, bool cells) {
     c.nst = (int)std::max<int64_t>(2, std::min<int64_t>(4, (226 * 1024 - kPipeBytes - c.tail) / stage));
   }
   c.smem = kPipeBytes + c.nst * stage + c.tail;
+}
+
+// Arms the value-dictionary blend (adaptive float32 pencils) when its value
+// tables, lookup hash and two pipeline stages fit one CTA's shared memory, and
+// appends the dictionary state to the workspace.  MCLAHE_NO_DICT=1 disarms it.
+void plan_dict(mclahe_plan_s* pl) {
+  pl->dict_cap = 0;
+  const Pencil& c = pl->interp;
+  if (!pl->p.adaptive || !pl->f32() || !c.on || !pl->hist.on || getenv("MCLAHE_NO_DICT")) return;
+  const int64_t nco = int64_t{1} << c.ko, nct = int64_t{1} << c.kt;
+  const int64_t tail =  // value blocks + cuckoo table + corner rows + column tables
+      nco * c.gtr * kDictKC * 4 + kDictHL * 8 + nco * 4 + (c.P / 4) * (4 + 16 * nct);
+  const int64_t stage = c.stage_stride * 4;
+  const int64_t nst = std::min<int64_t>(4, (226 * 1024 - kPipeBytes - tail) / stage);
+  if (nst < 2) return;
+  pl->dict_cap = kDictKC;
+  pl->dict_nst = (int)nst;
+  pl->dict_smem = kPipeBytes + nst * stage + tail;
+  mclahe_plan_info_t& I = pl->info;
+  pl->off_dict = align_up(I.workspace_bytes, 256);
+  I.workspace_bytes = align_up(pl->off_dict + dict_bytes(pl->G.win_tiles), 256);
 }
 
 void push_unit(std::vector<int32_t>& units, std::vector<int64_t>& vox, const int64_t* idx, int ko,
@@ -541,13 +573,16 @@ int plan_describe(const mclahe_params_t* params, int64_t row_begin, int64_t row_
   build_units(*pl);
   I.hist_units = (int64_t)pl->hist_vox.size();
   I.interp_units = (int64_t)pl->interp_vox.size();
+  // streamed chunk plans (full_window) interleave range passes with mappings,
+  // so a dictionary numbered per chunk would not be stable: edge tables only
+  if (!full_window) plan_dict(pl);
   return MCLAHE_OK;
 }
 
 using RangeFn = PencilRangeFn;
 using HistFn = PencilHistFn;
 using InterpFn = PencilInterpFn;
-RangeFn range_fn(int ko) { return get_range_pencil(ko); }
+RangeFn range_fn(int ko, bool dict) { return get_range_pencil(ko, dict); }
 HistFn hist_fn(int ko, bool a) { return get_hist_pencil(ko, a); }
 // MCLAHE_NO_NB=1 forces the runtime-n_bins blend kernel (A/B measurements).
 InterpFn interp_fn(int ko, int kt, bool a, int64_t n_bins) {
@@ -564,11 +599,25 @@ WS ws_view(const mclahe_plan_s* pl, void* ws) {
   W.tparams = b + pl->info.off_tparams;
   W.lut = reinterpret_cast<float*>(b + pl->info.off_lut);
   W.thr = reinterpret_cast<float*>(b + pl->info.off_thr);
+  W.dmeta = nullptr;
+  W.dkeys = nullptr;
+  W.dvals = nullptr;
+  W.dlt = nullptr;
+  W.lutd = nullptr;
+  if (pl->dict_cap) {
+    char* d = b + pl->off_dict;
+    W.dmeta = reinterpret_cast<int32_t*>(d);
+    W.dkeys = reinterpret_cast<uint32_t*>(d + kDictOffKeys);
+    W.dvals = reinterpret_cast<float*>(d + kDictOffVals);
+    W.dlt = reinterpret_cast<uint2*>(d + kDictOffLt);
+    W.lutd = reinterpret_cast<float*>(d + kDictOffLutd);
+  }
   return W;
 }
 
 int64_t range_smem(const mclahe_plan_s* pl) {
-  return kPipeBytes + pl->hist.nst * pl->hist.stage_stride * 4 + pl->hist.gtr * 8;
+  return kPipeBytes + pl->hist.nst * pl->hist.stage_stride * 4 + align_up(pl->hist.gtr * 8, 16) +
+         (pl->dict_cap ? kDictHS * 4 : 0);
 }
 
 // Raises a kernel's dynamic shared-memory cap to the device opt-in maximum
@@ -602,7 +651,7 @@ int device_init(mclahe_plan_s* pl) {
     MG_CUDA(raise_smem_cap(f, max_smem));
     MG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f, kPencilThreads, pl->hist.smem));
     if (A) {
-      RangeFn r = range_fn(pl->hist.ko);
+      RangeFn r = range_fn(pl->hist.ko, pl->dict_cap > 0);
       MG_CUDA(raise_smem_cap(r, max_smem));
     }
     pl->hist_grid = (int)std::max<int64_t>(
@@ -613,6 +662,7 @@ int device_init(mclahe_plan_s* pl) {
     int occ = 0;
     InterpFn f = interp_fn(pl->interp.ko, pl->interp.kt, A, pl->p.n_bins);
     MG_CUDA(raise_smem_cap(f, max_smem));
+    if (pl->dict_cap) MG_CUDA(raise_smem_cap(get_interp_pencil_dict(pl->interp.ko, pl->interp.kt), max_smem));
     MG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f, kBlendThreads, pl->interp.smem));
     pl->interp_grid = (int)std::max<int64_t>(
         1, std::min<int64_t>((int64_t)pl->interp_vox.size(), (int64_t)std::max(occ, 1) * pl->sms));
@@ -658,8 +708,9 @@ int do_reset(mclahe_plan_s* pl, void* ws, cudaStream_t st) {
   WS W = ws_view(pl, ws);
   const int64_t ntr = pl->p.adaptive ? pl->G.win_tiles * 2 : 0;
   MG_CUDA(cudaMemsetAsync(W.counts, 0, (size_t)pl->G.win_tiles * pl->p.n_bins * 4, st));
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((ntr + 255) / 256, 1024));
-  k_reset<<<grid, 256, 0, st>>>(W.range, W.trange, ntr);
+  const int64_t nr = std::max<int64_t>(ntr, pl->dict_cap ? kDictHG : 0);
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((nr + 255) / 256, 1024));
+  k_reset<<<grid, 256, 0, st>>>(W.range, W.trange, ntr, W, pl->dict_cap > 0 ? 1 : 0);
   MG_LAUNCHED();
   return MCLAHE_OK;
 }
@@ -678,13 +729,17 @@ int do_range(mclahe_plan_s* pl, const void* in, void* ws, cudaStream_t st) {
   }
   if (pl->hist.on) {
     const KGeom G = pencil_geom(*pl, pl->hist);
-    RangeFn f = range_fn(pl->hist.ko);
+    RangeFn f = range_fn(pl->hist.ko, pl->dict_cap > 0);
     int rc = tensor_map(pl, 0, in);
     if (rc) return rc;
     f<<<pl->hist_grid, kPencilThreads, range_smem(pl), st>>>(G, pl->map[0], static_cast<const float*>(in),
                                                     pl->d_tables + pl->off_hist_units,
                                                     pl->d_tables + pl->off_hist_cta, W);
     MG_LAUNCHED();
+    if (pl->dict_cap) {  // number the collected values once the slab's range pass is in
+      k_dict_finalize<<<1, 1024, 0, st>>>(W, pl->dict_cap);
+      MG_LAUNCHED();
+    }
     return MCLAHE_OK;
   }
   const int grid = generic_grid(pl);
@@ -764,6 +819,15 @@ int do_map(mclahe_plan_s* pl, void* ws, const mclahe_debug_t* dbg, cudaStream_t 
   if (pl->f32()) k_mappings<float><<<grid, pl->map_block, pl->map_smem, st>>>(pl->G, W, D, t0, nt);
   else k_mappings<double><<<grid, pl->map_block, pl->map_smem, st>>>(pl->G, W, D, t0, nt);
   MG_LAUNCHED();
+  if (pl->dict_cap) {  // per-value LUT rows of the mapped tiles
+    WS Wt = W;
+    Wt.tparams = static_cast<char*>(W.tparams) + t0 * (int64_t)sizeof(TileParam<float>);
+    Wt.lut = W.lut + t0 * pl->p.n_bins;
+    Wt.lutd = W.lutd + t0 * kDictKC;
+    const int g = (int)std::min<int64_t>((nt * kDictKC + 255) / 256, (int64_t)pl->sms * 16);
+    k_dict_luts<float><<<g, 256, 0, st>>>(Wt, nt, (int)pl->p.n_bins);
+    MG_LAUNCHED();
+  }
   return MCLAHE_OK;
 }
 
@@ -789,6 +853,15 @@ int do_interp(mclahe_plan_s* pl, const void* in, void* out, void* ws, cudaStream
               (long long)pl->interp.smem, pl->interp.nst, pl->interp.stage_rows,
               (long long)pl->interp.P, fa.numRegs, fa.maxThreadsPerBlock, fa.sharedSizeBytes,
               fa.maxDynamicSharedSizeBytes);
+    }
+    if (pl->dict_cap) {  // value-dictionary blend; exits at once when the dictionary is unusable
+      KGeom Gd = G;
+      Gd.nst = pl->dict_nst;
+      get_interp_pencil_dict(pl->interp.ko, pl->interp.kt)<<<pl->interp_grid, kBlendThreads,
+                                                            pl->dict_smem, st>>>(
+          Gd, pl->map[1], pl->map[2], static_cast<const float*>(in), static_cast<float*>(out),
+          pl->d_tables + pl->off_interp_units, pl->d_tables + pl->off_interp_cta, W);
+      MG_LAUNCHED();
     }
     f<<<pl->interp_grid, kBlendThreads, pl->interp.smem, st>>>(G, pl->map[1], pl->map[2], static_cast<const float*>(in),
                                                      static_cast<float*>(out),
@@ -1276,6 +1349,23 @@ int mclahe_debug_bin_index(int32_t dtype, const void* values, int64_t n, double 
                                                (int)n_bins, nullptr, out);
     MG_LAUNCHED();
   }
+  return MCLAHE_OK;
+}
+
+int mclahe_plan_dict_state(mclahe_plan_t plan, const void* workspace, int32_t* state,
+                           void* stream) {
+  if (!plan || !state) return fail(MCLAHE_ERR_VALIDATION, "plan and state must be non-NULL");
+  state[0] = state[1] = 0;
+  state[2] = plan->dict_cap;
+  if (!plan->dict_cap) return MCLAHE_OK;
+  if (!workspace) return fail(MCLAHE_ERR_VALIDATION, "workspace must be non-NULL");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int32_t m[4];
+  MG_CUDA(cudaMemcpyAsync(m, static_cast<const char*>(workspace) + plan->off_dict, sizeof m,
+                          cudaMemcpyDeviceToHost, st));
+  MG_CUDA(cudaStreamSynchronize(st));
+  state[0] = m[2];
+  state[1] = m[3];
   return MCLAHE_OK;
 }
 

@@ -336,3 +336,53 @@ def test_streamed_host_api_matches_device(M, name):
     xn[-1, 3, 2, 1] = np.nan  # non-finite in the LAST chunk is still caught
     with pytest.raises(M.ValidationError, match="non-finite"):
         M.enhance(xn, *args)
+
+
+def _run_plan(M, x, kernel, nb, clip, ad, no_dict=False):
+    old = os.environ.pop("MCLAHE_NO_DICT", None)
+    if no_dict:
+        os.environ["MCLAHE_NO_DICT"] = "1"
+    try:
+        plan = M.Plan(x.shape, kernel, nb, clip, ad)
+    finally:
+        os.environ.pop("MCLAHE_NO_DICT", None)
+        if old is not None:
+            os.environ["MCLAHE_NO_DICT"] = old
+    xt = x if isinstance(x, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    ws = plan.new_workspace()
+    out = torch.empty_like(xt)
+    plan.enqueue(xt, out, ws)
+    plan.check(ws)
+    return out, plan.dict_state(ws)
+
+
+@pytest.mark.parametrize("case", ["poisson", "edges", "scaled4d", "many"])
+def test_value_dictionary_blend(M, case):
+    # quantised volumes (few distinct values) take the value-dictionary blend;
+    # it must equal the oracle and, bit for bit, the edge-table blend
+    rng = np.random.default_rng({"poisson": 1, "edges": 2, "scaled4d": 3, "many": 4}[case])
+    if case == "poisson":
+        x = (rng.poisson(3.0, (48, 40, 24, 32)) / 11.0).astype(np.float32)
+        args = ((12, 10, 6, 4), 256, 0.02, True)
+    elif case == "edges":
+        x = (np.round(rng.random((40, 36, 32)) * 9) / 9).astype(np.float32)
+        x[:8] = 0.5  # constant (degenerate) tiles too
+        args = ((8, 12, 8), 128, 0.05, True)
+    elif case == "scaled4d":
+        from paper_1906_11355_b200 import datasets
+        c = SCALED["4d"]
+        x = datasets.make("4d", seed=2, shape=c["shape"]).numpy()
+        args = (c["kernel"], c["n_bins"], c["clip_limit"], True)
+    else:  # more distinct values than the dictionary holds: edge-table blend
+        x = rng.random((32, 32, 16, 32)).astype(np.float32)
+        args = ((8, 8, 4, 4), 256, 0.02, True)
+    out, st = _run_plan(M, x, *args)
+    ref, st0 = _run_plan(M, x, *args, no_dict=True)
+    assert st0["capacity"] == 0 and not st0["used"]
+    assert st["capacity"] > 0
+    assert st["used"] == (case != "many"), st
+    if case != "many":  # K2a samples a quarter of the rows
+        assert 0 < st["values"] <= len(np.unique(x.view(np.uint32))), st
+    assert torch.equal(out, ref)
+    want = O.mclahe(x, *args, "c")
+    assert np.max(np.abs(out.cpu().numpy().astype(np.float64) - want)) <= OUT_TOL
