@@ -51,7 +51,7 @@ __global__ void __launch_bounds__(1024) k_dict_finalize(WS W, int cap) {
   __shared__ int s_part[1024];
   const int tid = threadIdx.x;
   constexpr int PER = kDictHG / 1024;
-  if (W.dmeta[1] != 0 || W.dmeta[0] > cap) {
+  if (W.dmeta[1] != 0 || W.dmeta[0] > cap || W.dmeta[0] > 1024) {
     if (tid == 0) W.dmeta[2] = 0;
     return;
   }
@@ -66,15 +66,37 @@ __global__ void __launch_bounds__(1024) k_dict_finalize(WS W, int cap) {
     s_part[tid] += v;
     __syncthreads();
   }
+  // index = rank by value: lanes gathering neighbouring values then hit
+  // neighbouring shared-memory banks in the blend
+  __shared__ uint32_t s_key[1024];
+  const int K = s_part[1023];
+  s_key[tid] = 0xFFFFFFFFu;
+  __syncthreads();
   int idx = s_part[tid] - c;
   for (int j = 0; j < PER; ++j) {
     const uint32_t b = W.dkeys[tid * PER + j];
     if (b == kDictEmpty) continue;
-    W.dvals[idx++] = __uint_as_float(b);
+    s_key[idx++] = (b & 0x80000000u) ? ~b : (b | 0x80000000u);  // order-preserving key
+  }
+  __syncthreads();
+  for (int k = 2; k <= 1024; k <<= 1)  // bitonic sort, ascending
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      const int p = tid ^ j;
+      if (p > tid) {
+        const uint32_t a = s_key[tid], b = s_key[p];
+        if (((tid & k) == 0) == (a > b)) {
+          s_key[tid] = b;
+          s_key[p] = a;
+        }
+      }
+      __syncthreads();
+    }
+  if (tid < K) {
+    const uint32_t k = s_key[tid];
+    W.dvals[tid] = __uint_as_float((k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k);
   }
   __syncthreads();
   if (tid == 0) {  // cuckoo placement, values in index order
-    const int K = s_part[1023];
     bool ok = true;
     for (int i = 0; i < K && ok; ++i) {
       uint2 e = make_uint2(__float_as_uint(W.dvals[i]), (uint32_t)i);

@@ -7,7 +7,23 @@ import csv, sys, subprocess
 from collections import Counter
 rep, kn = sys.argv[1], sys.argv[2]
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--kernel-name", f"regex:{kn}", "--print-source", "sass"], capture_output=True, text=True).stdout
-rows = list(csv.reader(out.splitlines()))
+allrows = list(csv.reader(out.splitlines()))
+# several kernels may match: keep the section with the most stall samples
+secs, cur = [], None
+for r in allrows:
+    if r and r[0] == "Kernel Name":
+        cur = []
+        secs.append(cur)
+    if cur is not None:
+        cur.append(r)
+def _samples(sec):
+    try:
+        i = sec[1].index("Warp Stall Sampling (All Samples)")
+        return sum(int(x[i] or 0) for x in sec[2:] if len(x) > i and x[i].isdigit())
+    except Exception:
+        return 0
+rows = max(secs, key=_samples)
+print(rows[0][1][:110])
 hdr = rows[1]
 si, st, ex = hdr.index("Source"), hdr.index("Warp Stall Sampling (All Samples)"), hdr.index("Instructions Executed")
 data = []
