@@ -276,6 +276,30 @@ __device__ __forceinline__ float edge_gather(uint32_t base, int k, float v) {
   return m;
 }
 
+// Reference bin of v given k = rint(y) clamped to [0, n] (clamp_bits_k) and
+// the tile's edge table at shared address th: k if v >= th[k], else k - 1.
+__device__ __forceinline__ int edge_bin(uint32_t th, int k, float v) {
+  int b;
+  asm volatile(
+      "{\n\t.reg .u32 a;\n\t.reg .f32 t;\n\t.reg .pred p;\n\t"
+      "mad.lo.u32 a, %1, 4, %2;\n\t"
+      "ld.shared.f32 t, [a];\n\t"
+      "setp.lt.f32 p, %3, t;\n\t"
+      "selp.s32 %0, 1, 0, p;\n\t"
+      "sub.s32 %0, %1, %0;\n\t}"
+      : "=r"(b)
+      : "r"(k), "r"(th), "f"(v));
+  return b;
+}
+
+// Shared-memory add of val at addr when flag != 0 (predicated, no branch).
+__device__ __forceinline__ void red_add_if(uint32_t addr, uint32_t val, uint32_t flag) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p red.shared.add.u32 [%0], %1;\n\t}" ::"r"(addr),
+      "r"(val), "r"(flag)
+      : "memory");
+}
+
 // Exact bin from the edge table alone (binary search over thr[1..n-1]);
 // used for ranges the float guard does not cover.
 __device__ __forceinline__ int bin_search(float v, const float* th, int n) {

@@ -239,6 +239,8 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
   const float* thv[4];
   int hb[4];
   const bool same_pairs = !ADAPT || (trt[0] == trt[1] && trt[2] == trt[3]);
+  const uint32_t hist_s = (uint32_t)__cvta_generic_to_shared(hist);
+  const int trips = slot < G.stage_rows ? (G.stage_rows - slot + G.rpi - 1) / G.rpi : 0;
 
   uint32_t it = 0;
   while (true) {
@@ -282,7 +284,51 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
     }
     const int rows = G.stage_rows;
     const float* buf = P.bufs + s * stage_elems;
-    if (lane_on) {
+    if (lane_on && !patho && same_pairs && S.wuni != 0) {
+      // hot path: uniform row weights, both voxel pairs share a tile.  Bins via
+      // the edge table (edge_bin); equal neighbouring (tile, bin) runs merge
+      // into one predicated shared-memory add each -- no branches.
+      const uint32_t wf = (uint32_t)S.wfix;
+      uint32_t w[4], ha[4], ok[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        w[i] = wf * (uint32_t)trw[i];
+        ok[i] = hb[i] >= 0;
+        ha[i] = hist_s + (uint32_t)(hb[i] >= 0 ? hb[i] : 0) * 4u;
+      }
+      const uint32_t th0 = (uint32_t)__cvta_generic_to_shared(thv[0]);
+      const uint32_t th2 = (uint32_t)__cvta_generic_to_shared(thv[2]);
+      const u64 L0 = pk2(lcv[0].x, lcv[0].x), C0 = pk2(lcv[0].y, lcv[0].y);
+      const u64 L2 = pk2(lcv[2].x, lcv[2].x), C2 = pk2(lcv[2].y, lcv[2].y);
+      const float* rp = buf + slot * G.P + e0;
+      const int64_t rstep = (int64_t)G.rpi * G.P;
+#pragma unroll 2
+      for (int k = 0; k < trips; ++k, rp += rstep) {
+        const float4 v = *reinterpret_cast<const float4*>(rp);
+        u64 t01, t23;
+        asm("add.rn.f32x2 %0, %1, %2;" : "=l"(t01) : "l"(mul2(sub2(pk2(v.x, v.y), L0), C0)), "l"(pk2(kMagic, kMagic)));
+        asm("add.rn.f32x2 %0, %1, %2;" : "=l"(t23) : "l"(mul2(sub2(pk2(v.z, v.w), L2), C2)), "l"(pk2(kMagic, kMagic)));
+        float tf[4];
+        upk2(t01, tf[0], tf[1]);
+        upk2(t23, tf[2], tf[3]);
+        const float vv[4] = {v.x, v.y, v.z, v.w};
+        uint32_t a[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {  // degenerate tiles: distinct dummy keys, never merged
+          a[i] = ha[i] + 4u * (uint32_t)edge_bin(i < 2 ? th0 : th2, clamp_bits_k(tf[i], n), vv[i]);
+          if (!ok[i]) a[i] = 0xFFFFFFF0u + i;
+        }
+        const bool e01 = a[0] == a[1], e12 = a[1] == a[2], e23 = a[2] == a[3];
+        const uint32_t s3 = w[3];
+        const uint32_t s2 = w[2] + (e23 ? s3 : 0u);
+        const uint32_t s1 = w[1] + (e12 ? s2 : 0u);
+        const uint32_t s0 = w[0] + (e01 ? s1 : 0u);
+        red_add_if(a[0], s0, ok[0]);
+        red_add_if(a[1], s1, ok[1] & !e01);
+        red_add_if(a[2], s2, ok[2] & !e12);
+        red_add_if(a[3], s3, ok[3] & !e23);
+      }
+    } else if (lane_on) {
       const bool wuni = S.wuni != 0;
       const int32_t wfix = S.wfix;
 #pragma unroll 4

@@ -386,3 +386,23 @@ def test_value_dictionary_blend(M, case):
     assert torch.equal(out, ref)
     want = O.mclahe(x, *args, "c")
     assert np.max(np.abs(out.cpu().numpy().astype(np.float64) - want)) <= OUT_TOL
+
+
+@pytest.mark.parametrize("ad", [True, False])
+def test_sparse_counts_degenerate_neighbours(M, ad):
+    # counts on one half of the trailing dim, zeros on the other: constant
+    # (degenerate) tiles beside live ones along the trailing dim, so merged
+    # histogram runs meet tiles that build no histogram
+    rng = np.random.default_rng(33)
+    x = np.zeros((32, 32, 16, 32), np.float32)
+    x[..., :2] = rng.poisson(0.7, (32, 32, 16, 2)) / 3.0  # trailing tile 0: x in [0, 2)
+    x[..., 20:] = rng.poisson(0.7, (32, 32, 16, 12)) / 3.0
+    args = ((8, 8, 4, 4), 256, 0.02, ad)
+    st, plan = gpu_stats(M, x, *args)
+    assert plan.info.fast_hist and plan.info.fast_interp
+    ref = O.tile_stats(x, *args, "c")
+    if ad:
+        assert ref["degenerate"].any() and not ref["degenerate"].all()
+    assert_stats_equal(st, ref, "sparse")
+    out = M.enhance(x, *args)
+    assert np.max(np.abs(out.astype(np.float64) - O.mclahe(x, *args, "c"))) <= OUT_TOL
