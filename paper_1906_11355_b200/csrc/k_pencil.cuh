@@ -207,8 +207,10 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
   extern __shared__ __align__(128) unsigned char smem[];
   const PencilSmem P = pencil_smem(G, smem);
   const int n = G.n_bins;
-  uint32_t* hist = reinterpret_cast<uint32_t*>(P.tail);  // [gtr][n]
-  float2* lcS = reinterpret_cast<float2*>(P.tail + ((G.gtr * n * 4 + 15) & ~15LL));  // [gtr]
+  // [gtr][n + 1]: the pad word puts equal bins of neighbouring tiles (one per
+  // thread of a row) in different banks
+  uint32_t* hist = reinterpret_cast<uint32_t*>(P.tail);
+  float2* lcS = reinterpret_cast<float2*>(P.tail + ((G.gtr * (n + 1) * 4 + 15) & ~15LL));  // [gtr]
   // bin-edge tables of the pencil's tiles (adaptive) or of the global range
   float* thrS = reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(lcS) + G.gtr * 16);
   const int n1 = n + 1;  // edge-table stride: thr[0] = -inf ... thr[n] = +inf
@@ -255,12 +257,12 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
       if (cur >= 0) {
         uint32_t* dst = W.counts + cur * n;
         for (int64_t k = tid; k < G.gtr * n; k += kConsumers) {
-          const uint32_t c = hist[k];
+          const uint32_t c = hist[k + k / n];
           if (c) atomicAdd(dst + k, c);
         }
       }
       consumers_sync();
-      for (int64_t k = tid; k < G.gtr * n; k += kConsumers) hist[k] = 0;
+      for (int64_t k = tid; k < G.gtr * (n + 1); k += kConsumers) hist[k] = 0;
       if (ADAPT) {
         for (int64_t t = tid; t < G.gtr; t += kConsumers) {
           const float2 lc = tile_lc(tparams[key + t]);
@@ -279,7 +281,7 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
       for (int i = 0; i < 4; ++i) {
         lcv[i] = ADAPT ? lcS[trt[i]] : glc;
         thv[i] = thrS + (ADAPT ? trt[i] * n1 : 0);
-        hb[i] = (!ADAPT || lcv[i].y != kDegC) ? trt[i] * n : -1;  // degenerate: no histogram
+        hb[i] = (!ADAPT || lcv[i].y != kDegC) ? trt[i] * (n + 1) : -1;  // degenerate: none
       }
     }
     const int rows = G.stage_rows;
@@ -390,7 +392,7 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
   if (cur >= 0) {
     uint32_t* dst = W.counts + cur * n;
     for (int64_t k = tid; k < G.gtr * n; k += kConsumers) {
-      const uint32_t c = hist[k];
+      const uint32_t c = hist[k + k / n];
       if (c) atomicAdd(dst + k, c);
     }
   }
