@@ -181,7 +181,9 @@ int mclahe_debug_bin_index(int32_t dtype, const void* values_dev, int64_t n, dou
 
 /* Value-dictionary state after a run on `workspace` (synchronises `stream`):
  * state[0] = 1 if the last blend used the dictionary path, state[1] = number
- * of distinct values collected, state[2] = the plan's capacity (0: never). */
+ * of distinct values collected, state[2] = the plan's capacity (0: never),
+ * state[3] = 1 if values were looked up through the affine direct table
+ * (0: cuckoo hash).  state has 4 entries. */
 int mclahe_plan_dict_state(mclahe_plan_t plan, const void* workspace, int32_t* state,
                            void* stream);
 

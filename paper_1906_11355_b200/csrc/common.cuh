@@ -106,6 +106,29 @@ __device__ __forceinline__ int dict_lookup(const uint2* t, uint32_t b) {
   return e1.x == b ? (int)e1.y : e2.x == b ? (int)e2.y : -1;
 }
 
+// meta[4]: 1 = affine lookup (meta[5] = bits of v0, meta[6] = bits of S), 0 = cuckoo.
+// Affine cells of two values (packed, as the blend computes them), clamped to
+// the table; the second value's cell goes to *c1 when c1 != nullptr.
+#ifdef __CUDACC__
+__device__ __forceinline__ int dict_cell(float a, float b, float v0, float S, int* c1) {
+  unsigned long long V, D, Y, T;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(V) : "f"(a), "f"(b));
+  asm("mov.b64 %0, {%1, %1};" : "=l"(D) : "f"(v0));
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(Y) : "l"(V), "l"(D));
+  asm("mov.b64 %0, {%1, %1};" : "=l"(D) : "f"(S));
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(Y) : "l"(Y), "l"(D));
+  asm("mov.b64 %0, {%1, %1};" : "=l"(D) : "f"(12582912.0f));
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(T) : "l"(Y), "l"(D));
+  float t0, t1;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(t0), "=f"(t1) : "l"(T));
+  auto cl = [](float t) {
+    return min(max(__float_as_int(t), 0x4B400000), 0x4B400000 + kDictHL - 1) - 0x4B400000;
+  };
+  if (c1) *c1 = cl(t1);
+  return cl(t0);
+}
+#endif
+
 // Slot of b in a bucketised key table (4 keys per bucket, nb = 2^lg
 // buckets), or -1 after a full sweep; b must not be kDictEmpty.
 __device__ __forceinline__ int dict_find(const uint4* keys, uint32_t b, int lg) {

@@ -472,6 +472,8 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
                        : reinterpret_cast<int*>(lcS + NCO * gtr);
   float* colW = reinterpret_cast<float*>(colT + ncol);  // [ncol][4][NCT]
   __shared__ int s_bad;
+  __shared__ int s_dmode;  // DICT: 1 = affine lookup
+  __shared__ float s_dv0, s_dS;
   pipe_init(*P.pipe, G.nst, NW);
   __syncthreads();
   const int u0 = cta_units[blockIdx.x], u1 = cta_units[blockIdx.x + 1];
@@ -542,8 +544,14 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
       if (tid == 0) s_bad = 0;
       if (!ADAPT && cur < 0)
         for (int k = tid; k < n1; k += kConsumersBlend) thrS[k] = W.thr[k];
-      if (DICT && cur < 0)
+      if (DICT && cur < 0) {
         for (int k = tid; k < kDictHL; k += kConsumersBlend) dltS[k] = W.dlt[k];
+        if (tid == 0) {
+          s_dmode = W.dmeta[4];
+          s_dv0 = __int_as_float(W.dmeta[5]);
+          s_dS = __int_as_float(W.dmeta[6]);
+        }
+      }
       for (int co = 0; co < NCO; ++co) {
         int64_t of = (S.cell[0] + ((co >> (KO - 1)) & 1) - G.trow0) * G.tstride[0];
         for (int j = 1; j < KO; ++j) of += (S.cell[j] + ((co >> (KO - 1 - j)) & 1)) * G.tstride[j];
@@ -715,12 +723,25 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
           if (KT == 2) base[KT - 1] = base[0] + ctoff[KT == 2 ? 2 : 0] * (NCO * TB);
           const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
           const char* A[KT][4];
+          int di[4];
+          if (s_dmode) {  // affine cells: one LDS.64 per voxel
+            int c[4];
+            c[0] = dict_cell(vv[0], vv[1], s_dv0, s_dS, &c[1]);
+            c[2] = dict_cell(vv[2], vv[3], s_dv0, s_dS, &c[3]);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const uint2 e = dltS[c[i]];
+              di[i] = e.x == __float_as_uint(vv[i]) ? (int)e.y : -1;
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) di[i] = dict_lookup(dltS, __float_as_uint(vv[i]));
+          }
           int miss = 0;
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
-            const int di = dict_lookup(dltS, __float_as_uint(vv[i]));
-            miss |= (di < 0) << i;
-            const int off = di >= 0 ? di * 4 : 0;
+            miss |= (di[i] < 0) << i;
+            const int off = di[i] >= 0 ? di[i] * 4 : 0;
 #pragma unroll
             for (int j = 0; j < KT; ++j) A[j][i] = base[j] + off;
           }
@@ -734,19 +755,25 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
               for (int i = 0; i < 4; ++i)
                 m[ct][i] = *reinterpret_cast<const float*>(A[ct >> 1][i] + OFF);
             });
-            if (miss) {  // values outside the (sampled) dictionary: edge tables in L2
-#pragma unroll
-              for (int i = 0; i < 4; ++i)
-                if ((miss >> i) & 1)
-#pragma unroll
-                  for (int ct = 0; ct < NCT; ++ct)
-                    m[ct][i] = lut_value_global(W, n, ofS[co] + tt + ctoff[ct], vv[i]);
-            }
 #pragma unroll
             for (int ct = 0; ct < NCT; ++ct)
 #pragma unroll
               for (int i = 0; i < 4; ++i) act[ct][i] = fmaf(wo[co], m[ct][i], act[ct][i]);
           });
+          if (miss) {  // values the (sampled) dictionary lacks: redo them from the workspace
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              if ((miss >> i) & 1) {
+#pragma unroll
+                for (int ct = 0; ct < NCT; ++ct) act[ct][i] = 0.0f;
+#pragma unroll
+                for (int co = 0; co < NCO; ++co)
+#pragma unroll
+                  for (int ct = 0; ct < NCT; ++ct)
+                    act[ct][i] = fmaf(wo[co], lut_value_global(W, n, ofS[co] + tt + ctoff[ct], vv[i]),
+                                      act[ct][i]);
+              }
+          }
         } else if constexpr (NB > 0) {
           // corner (co, ct) block: base[ct >> 1] + ((ct & 1) * NCO + co) * TB
           constexpr int TB = NbBlock::words(NB) * 4;

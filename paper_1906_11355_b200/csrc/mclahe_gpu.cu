@@ -1355,17 +1355,18 @@ int mclahe_debug_bin_index(int32_t dtype, const void* values, int64_t n, double 
 int mclahe_plan_dict_state(mclahe_plan_t plan, const void* workspace, int32_t* state,
                            void* stream) {
   if (!plan || !state) return fail(MCLAHE_ERR_VALIDATION, "plan and state must be non-NULL");
-  state[0] = state[1] = 0;
+  state[0] = state[1] = state[3] = 0;
   state[2] = plan->dict_cap;
   if (!plan->dict_cap) return MCLAHE_OK;
   if (!workspace) return fail(MCLAHE_ERR_VALIDATION, "workspace must be non-NULL");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  int32_t m[4];
+  int32_t m[8];
   MG_CUDA(cudaMemcpyAsync(m, static_cast<const char*>(workspace) + plan->off_dict, sizeof m,
                           cudaMemcpyDeviceToHost, st));
   MG_CUDA(cudaStreamSynchronize(st));
   state[0] = m[2];
   state[1] = m[3];
+  state[3] = m[2] ? m[4] : 0;
   return MCLAHE_OK;
 }
 

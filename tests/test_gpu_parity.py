@@ -356,11 +356,11 @@ def _run_plan(M, x, kernel, nb, clip, ad, no_dict=False):
     return out, plan.dict_state(ws)
 
 
-@pytest.mark.parametrize("case", ["poisson", "edges", "scaled4d", "many"])
+@pytest.mark.parametrize("case", ["poisson", "edges", "scaled4d", "many", "uneven"])
 def test_value_dictionary_blend(M, case):
     # quantised volumes (few distinct values) take the value-dictionary blend;
     # it must equal the oracle and, bit for bit, the edge-table blend
-    rng = np.random.default_rng({"poisson": 1, "edges": 2, "scaled4d": 3, "many": 4}[case])
+    rng = np.random.default_rng({"poisson": 1, "edges": 2, "scaled4d": 3, "many": 4, "uneven": 5}[case])
     if case == "poisson":
         x = (rng.poisson(3.0, (48, 40, 24, 32)) / 11.0).astype(np.float32)
         args = ((12, 10, 6, 4), 256, 0.02, True)
@@ -373,6 +373,11 @@ def test_value_dictionary_blend(M, case):
         c = SCALED["4d"]
         x = datasets.make("4d", seed=2, shape=c["shape"]).numpy()
         args = (c["kernel"], c["n_bins"], c["clip_limit"], True)
+    elif case == "uneven":  # few values, unevenly spaced: cuckoo lookup
+        vals = np.sort(rng.random(300)).astype(np.float32)
+        vals[:3] = [0.0, 1e-6, 2e-6]
+        x = vals[rng.integers(0, 300, (32, 32, 16, 32))]
+        args = ((8, 8, 4, 4), 256, 0.02, True)
     else:  # more distinct values than the dictionary holds: edge-table blend
         x = rng.random((32, 32, 16, 32)).astype(np.float32)
         args = ((8, 8, 4, 4), 256, 0.02, True)
@@ -383,6 +388,7 @@ def test_value_dictionary_blend(M, case):
     assert st["used"] == (case != "many"), st
     if case != "many":  # K2a samples a quarter of the rows
         assert 0 < st["values"] <= len(np.unique(x.view(np.uint32))), st
+        assert st["affine"] == (case != "uneven"), st  # evenly quantised: direct table
     assert torch.equal(out, ref)
     want = O.mclahe(x, *args, "c")
     assert np.max(np.abs(out.cpu().numpy().astype(np.float64) - want)) <= OUT_TOL
