@@ -427,7 +427,8 @@ __device__ __noinline__ void pipe_produce(const KGeom& G, const CUtensorMap* map
 #pragma unroll 1
         for (int seg = 0; seg < G.nseg; ++seg) {
           const int slot = it % nst;
-          mbar_wait(&pp.empty[slot], ((it / nst) & 1) ^ 1);
+          if (STORE) mbar_wait_spin(&pp.empty[slot], ((it / nst) & 1) ^ 1);  // blend: latency-critical
+          else mbar_wait(&pp.empty[slot], ((it / nst) & 1) ^ 1);
           Stage& S = pp.st[slot];
           if (STORE && it >= (uint32_t)nst) {  // write back the slot's previous results
             tma_store(out_map, G.tma_rank, S.tc, bufs + slot * stage_elems);

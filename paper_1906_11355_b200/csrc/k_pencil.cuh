@@ -631,7 +631,6 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
     // stage geometry: factor f_j(x) = x / b + t_j (exact half-integer numerators)
     float wfix[NCO / (KO >= 2 ? 4 : 2)];
     float s1, t1, s2 = 0.f, t2 = 0.f;
-    int64_t obase = 0;
     {
       float ff[KO];
 #pragma unroll
@@ -647,7 +646,6 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
           t2 = tj;
         } else {
           ff[j] = fmaf((float)S.x[j], sj, tj);
-          obase += (int64_t)(j == 0 ? S.x[j] - G.row0 : S.x[j]) * G.vstride[j];
         }
       }
       constexpr int NF = NCO / (KO >= 2 ? 4 : 2);
@@ -660,8 +658,6 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
       }
     }
     const int xb1 = S.x[KO - 1], xb2 = KO >= 2 ? S.x[KO >= 2 ? KO - 2 : 0] : 0;
-    const int64_t vs1 = G.vstride[KO - 1], vs2 = KO >= 2 ? G.vstride[KO >= 2 ? KO - 2 : 0] : 0;
-    const int64_t r0 = (KO == 1 ? G.row0 : 0), r0b = (KO == 2 ? G.row0 : 0);
     const int seg = S.seg;
     unsigned char* buf = reinterpret_cast<unsigned char*>(P.bufs + s * stage_elems);
     for (int item = warp; item < 8 * nrb; item += NW) {
@@ -677,8 +673,6 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
           for (int ct = 0; ct < NCT; ++ct) tw[i][ct] = colW[(col * 4 + i) * NCT + ct];
         const int r1 = q & (G.r1 - 1), r2 = q >> G.lg_r1;
         const int x1 = xb1 + r1, x2 = xb2 + r2;
-        const int64_t ooff = obase + (int64_t)(x1 - r0) * vs1 +
-                             (KO >= 2 ? (int64_t)(x2 - r0b) * vs2 : 0) + col * 4;
         const float f1 = fmaf((float)x1, s1, t1);
         const float f2 = KO >= 2 ? fmaf((float)x2, s2, t2) : 0.f;
         float wo[NCO];
@@ -925,7 +919,6 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
         r.z = fminf(fmaxf(acc[2], 0.f), 1.f);
         r.w = fminf(fmaxf(acc[3], 0.f), 1.f);
         *slot4 = r;  // in place; the producer TMA-stores the box
-        (void)ooff;
       }
     }
     fence_proxy_async_smem();

@@ -100,6 +100,7 @@ struct Pencil {
 
 constexpr int64_t kPipeBytes = (sizeof(mg::Pipe) + 1023) & ~int64_t(1023);
 constexpr int64_t kStageBytes = 16384;
+constexpr int kMaxChunks = 32;  // streamed one-shot: chunks per call (events are sized for it)
 
 // dictionary workspace: meta[8] | keys[HG] | vals[HG/2] | lookup[HL] | lutd[tiles][KC]
 constexpr int64_t kDictOffKeys = 256;
@@ -922,14 +923,24 @@ int build_streamed(const mclahe_params_t* p, Streamed& S) {
     if (e > a) cells.push_back({a, e});
   }
   const int64_t bytes = volume(p) * elem_size(p);
-  const int C = (int)std::max<int64_t>(
-      1, std::min<int64_t>({(int64_t)cells.size(), 8, std::max<int64_t>(1, bytes / (8 << 20))}));
-  if (C < 2) return MCLAHE_ERR_UNSUPPORTED;
+  // Row-balanced chunks, not cell-aligned: a chunk's blend waits for the tile
+  // rows its last cell touches, so the D2H tail after the final H2D is about
+  // one cell of rows plus one chunk; more, smaller chunks shorten it.  Cuts on
+  // multiples of 8 rows (or 1 for short volumes) keep TMA boxes whole.
+  const int64_t S0 = p->shape[0];
+  const int64_t align = S0 >= 128 ? 8 : 1;
+  static const int max_chunks = std::max(
+      2, std::min(kMaxChunks, getenv("MCLAHE_CHUNKS") ? atoi(getenv("MCLAHE_CHUNKS")) : 16));
+  int C = (int)std::max<int64_t>(
+      1, std::min<int64_t>({S0 / align, (int64_t)max_chunks, std::max<int64_t>(1, bytes / (8 << 20))}));
+  if (C < 2 || cells.size() < 2) return MCLAHE_ERR_UNSUPPORTED;
   S.cuts.assign(1, 0);
-  for (int k = 1; k <= C; ++k) {
-    const size_t idx = (size_t)((int64_t)cells.size() * k / C) - 1;
-    S.cuts.push_back(cells[idx].second);
+  for (int k = 1; k < C; ++k) {
+    const int64_t cut = (S0 * k / C) / align * align;
+    if (cut > S.cuts.back() && cut < S0) S.cuts.push_back(cut);
   }
+  S.cuts.push_back(S0);
+  C = (int)S.cuts.size() - 1;
   S.chunks.clear();
   for (int k = 0; k < C; ++k) {
     auto pl = std::make_unique<mclahe_plan_s>();
@@ -953,6 +964,7 @@ int run_streamed(Streamed& S, const mclahe_params_t* p, const void* in, void* ou
                  void* d_out, void* ws, cudaStream_t s_in, cudaStream_t s_comp, cudaStream_t s_out,
                  std::vector<cudaEvent_t>& ev, mclahe_timings_t* timings) {
   const int C = (int)S.chunks.size();
+  if (ev.size() < (size_t)(2 * C + 2)) return fail(MCLAHE_ERR_CUDA, "streamed run: too few events");
   const int64_t row_bytes = volume(p) / p->shape[0] * elem_size(p);
   const int64_t g0 = (int64_t)S.last_chunk.size();
   const int64_t tpr = S.tiles_per_row;
@@ -1113,7 +1125,7 @@ int ensure_stream(OneShot& o) {
   MG_CUDA(cudaStreamCreateWithFlags(&o.s_in, cudaStreamNonBlocking));
   MG_CUDA(cudaStreamCreateWithFlags(&o.s_out, cudaStreamNonBlocking));
   for (auto& e : o.ev) MG_CUDA(cudaEventCreate(&e));
-  o.sev.resize(2 * 8 + 2);
+  o.sev.resize(2 * kMaxChunks + 2);
   for (auto& e : o.sev) MG_CUDA(cudaEventCreate(&e));
   o.stream_dev = dev;
   return MCLAHE_OK;
