@@ -129,19 +129,6 @@ __device__ __forceinline__ int dict_cell(float a, float b, float v0, float S, in
 }
 #endif
 
-// Slot of b in a bucketised key table (4 keys per bucket, nb = 2^lg
-// buckets), or -1 after a full sweep; b must not be kDictEmpty.
-__device__ __forceinline__ int dict_find(const uint4* keys, uint32_t b, int lg) {
-  uint32_t bk = dict_hash(b, lg);
-  for (int probe = 0; probe < (1 << lg); ++probe) {
-    const uint4 q = keys[bk];
-    const int j = q.x == b ? 0 : q.y == b ? 1 : q.z == b ? 2 : q.w == b ? 3 : -1;
-    if (j >= 0) return (int)(bk * 4 + j);
-    if (q.w == kDictEmpty) return -1;  // buckets fill in slot order
-    bk = (bk + 1) & ((1u << lg) - 1);
-  }
-  return -1;
-}
 
 // Workspace views.
 struct WS {

@@ -196,9 +196,9 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
 // --------------------------------------------------------------- K2b -----
 // A voxel's multiplicity in a tile is the product of its per-dimension
 // multiplicities, so counting the support box with those weights equals
-// kernelize + compute_histogram while reading each input byte once.  Lanes
-// with equal (tile, bin, weight) merge via __match_any_sync: one shared
-// atomic carries the whole run.
+// kernelize + compute_histogram while reading each input byte once.  A
+// thread's equal neighbouring (tile, bin) keys merge: one shared add carries
+// the whole run.
 template <int KO, bool ADAPT>
 __global__ void __launch_bounds__(kPencilThreads, 3)
     k_hist_pencil(const __grid_constant__ KGeom G, const __grid_constant__ CUtensorMap tmap,
