@@ -79,7 +79,8 @@ struct PhaseTimings {
 // pipeline.hpp:30 -- full MCLAHE on the current CUDA device.
 NdImage mclahe(const McLaheRequest& request, PhaseTimings* timings = nullptr);
 
-// pipeline.hpp:37-40 -- mclahe on every slice along frame_axis.
+// pipeline.hpp:37-40 -- mclahe on every slice along frame_axis, batched into
+// one GPU run (mclahe_gpu_run_framewise); `threads` is ignored.
 NdImage mclahe_framewise(const NdImage& image, std::size_t frame_axis, const KernelSpec& kernel,
                          const EnhanceParams& params, unsigned threads = 0,
                          bool renormalize_slices = false, PhaseTimings* timings = nullptr);

@@ -194,6 +194,16 @@ int mclahe_debug_bin_index_packed(const float* values_dev, int64_t n, double lo,
                                   int64_t n_bins, int32_t variant, int32_t* out_dev,
                                   void* stream);
 
+/* Batched mclahe_framewise (src/pipeline.cpp:131-153, renormalize_slices =
+ * false): every slice along frame_axis enhanced on its own, in one run.
+ * params->shape / rank describe the whole volume; params->kernel holds the
+ * rank-1 slice kernel (the frame axis removed), as in the reference.  The
+ * frames run as one volume with kernel 1 along the frame axis (tiles one
+ * frame thick, blend weight across frames exactly 0/1); in global mode each
+ * tile takes its frame's own min/max.  Host buffers, like mclahe_gpu_run. */
+int mclahe_gpu_run_framewise(const mclahe_params_t* params, int32_t frame_axis,
+                             const void* host_in, void* host_out, mclahe_timings_t* timings);
+
 /* Number of kernel launches the last pass call on this thread issued. */
 int64_t mclahe_launch_count(void);
 

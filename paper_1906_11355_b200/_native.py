@@ -84,6 +84,7 @@ SIGNATURES = {
     "mclahe_plan_check": (C.c_int, [_vp, _vp, _vp]),
     "mclahe_debug_bin_index": (C.c_int, [C.c_int32, _vp, _i64, C.c_double, C.c_double, _i64,
                                          _vp, _vp]),
+    "mclahe_gpu_run_framewise": (C.c_int, [_vp, C.c_int32, _vp, _vp, _vp]),
     "mclahe_plan_dict_state": (C.c_int, [_vp, _vp, C.POINTER(C.c_int32), _vp]),
     "mclahe_debug_bin_index_packed": (C.c_int, [_vp, _i64, C.c_double, C.c_double, _i64,
                                                 C.c_int32, _vp, _vp]),

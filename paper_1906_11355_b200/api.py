@@ -293,6 +293,57 @@ def _mclahe_device(x, kernel, n_bins, clip, adaptive, timings=None):
     return out
 
 
+def normalize_to_unit(image):
+    """normalize_to_unit (src/pipeline.cpp:155-165): affine map of [min, max]
+    onto [0, 1] in float64; a constant image maps to 0.5."""
+    x = np.asarray(image, dtype=np.float64)
+    if not np.all(np.isfinite(x)):
+        raise ValidationError("image contains non-finite values")
+    lo, hi = float(x.min()), float(x.max())
+    if not hi > lo:
+        return np.full_like(x, 0.5)
+    return (x - lo) / (hi - lo)
+
+
+def mclahe_framewise(image, frame_axis: int, kernel: KernelSpec, params: EnhanceParams,
+                     threads: int = 0, renormalize_slices: bool = False,
+                     timings: PhaseTimings | None = None):
+    """mclahe_framewise (include/mclahe/pipeline.hpp:37-40, src/pipeline.cpp:131-153):
+    mclahe on every slice along frame_axis, batched into one GPU run
+    (mclahe_gpu_run_framewise).  numpy in -> numpy out; ``threads`` is
+    accepted and ignored.  renormalize_slices maps each slice onto [0, 1]
+    (float64) first, as the reference does."""
+    x = np.asarray(image)
+    if x.ndim < 2:
+        raise ValidationError("framewise mode needs rank >= 2")
+    if not 0 <= frame_axis < x.ndim:
+        raise ValidationError(f"frame axis {frame_axis} out of range for rank {x.ndim}")
+    ks = tuple(int(k) for k in kernel.sizes)
+    if len(ks) != x.ndim - 1:
+        raise ValidationError("framewise kernel rank must be image rank - 1")
+    if renormalize_slices:
+        x = np.stack([normalize_to_unit(np.take(x, f, axis=frame_axis))
+                      for f in range(x.shape[frame_axis])], axis=frame_axis)
+    if x.dtype != np.float32:
+        x = x.astype(np.float64)
+    x = np.ascontiguousarray(x)
+    adaptive = params.range_mode == RangeMode.Adaptive
+    full_kernel = ks[:frame_axis] + (1,) + ks[frame_axis:]  # slot the ABI ignores
+    p = N.make_params(x.shape, full_kernel, params.n_bins, params.clip_limit, adaptive,
+                      _dtype_code(x.dtype))
+    for i, k in enumerate(ks):  # the ABI takes the slice kernel, frame axis removed
+        p.kernel[i] = k
+    out = np.empty_like(x)
+    t = N.Timings()
+    N.check(N.lib().mclahe_gpu_run_framewise(C.byref(p), int(frame_axis), x.ctypes.data,
+                                             out.ctypes.data, C.byref(t)))
+    if timings is not None:
+        timings.pad_s += t.pad_s
+        timings.histograms_s += t.histograms_s
+        timings.interpolation_s += t.interpolation_s
+    return out
+
+
 def enhance(image, kernel_size, n_bins: int = 256, clip_limit: float = 1.0,
             adaptive_hist_range: bool = False):
     """Convenience form with the paper's argument names (data, kernel_size,

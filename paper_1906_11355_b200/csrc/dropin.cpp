@@ -97,7 +97,9 @@ NdImage mclahe(const McLaheRequest& request, PhaseTimings* timings) {
 NdImage mclahe_framewise(const NdImage& image, std::size_t frame_axis, const KernelSpec& kernel,
                          const EnhanceParams& params, unsigned threads, bool renormalize_slices,
                          PhaseTimings* timings) {
-  // src/pipeline.cpp:131-153
+  // src/pipeline.cpp:131-153, batched: one GPU run over all slices
+  // (mclahe_gpu_run_framewise) instead of a host loop of crops and pastes
+  (void)threads;
   if (image.rank() < 2) throw ValidationError("framewise mode needs rank >= 2");
   if (frame_axis >= image.rank())
     throw ValidationError("frame axis " + std::to_string(frame_axis) + " out of range for rank " +
@@ -108,23 +110,50 @@ NdImage mclahe_framewise(const NdImage& image, std::size_t frame_axis, const Ker
   std::size_t outer = 1, inner = 1;
   for (std::size_t i = 0; i < frame_axis; ++i) outer *= sh[i];
   for (std::size_t i = frame_axis + 1; i < sh.size(); ++i) inner *= sh[i];
-  Shape slice_shape;
-  for (std::size_t i = 0; i < sh.size(); ++i)
-    if (i != frame_axis) slice_shape.push_back(sh[i]);
-  NdImage out = NdImage::zeros(sh);
   const std::size_t frames = sh[frame_axis];
-  for (std::size_t f = 0; f < frames; ++f) {
-    std::vector<double> buf(outer * inner);
-    for (std::size_t o = 0; o < outer; ++o)
-      std::memcpy(&buf[o * inner], &image.data()[(o * frames + f) * inner], inner * sizeof(double));
-    NdImage slice(slice_shape, std::move(buf));
-    if (renormalize_slices) slice = normalize_to_unit(slice);
-    const NdImage enh = mclahe(McLaheRequest{std::move(slice), kernel, params, threads}, timings);
-    for (std::size_t o = 0; o < outer; ++o)
-      std::memcpy(&out.data()[(o * frames + f) * inner], &enh.data()[o * inner],
-                  inner * sizeof(double));
+  std::vector<double> src = image.data();
+  if (renormalize_slices) {  // normalize_to_unit per slice, in place
+    Shape slice_shape;
+    for (std::size_t i = 0; i < sh.size(); ++i)
+      if (i != frame_axis) slice_shape.push_back(sh[i]);
+    for (std::size_t f = 0; f < frames; ++f) {
+      std::vector<double> buf(outer * inner);
+      for (std::size_t o = 0; o < outer; ++o)
+        std::memcpy(&buf[o * inner], &src[(o * frames + f) * inner], inner * sizeof(double));
+      const NdImage norm = normalize_to_unit(NdImage(slice_shape, std::move(buf)));
+      for (std::size_t o = 0; o < outer; ++o)
+        std::memcpy(&src[(o * frames + f) * inner], &norm.data()[o * inner], inner * sizeof(double));
+    }
   }
-  return out;
+  mclahe_params_t p;
+  std::memset(&p, 0, sizeof p);
+  p.rank = static_cast<int32_t>(image.rank());
+  p.adaptive = params.range_mode == RangeMode::Adaptive ? 1 : 0;
+  for (std::size_t i = 0; i < image.rank(); ++i) p.shape[i] = static_cast<int64_t>(sh[i]);
+  for (std::size_t i = 0; i + 1 < image.rank(); ++i)
+    p.kernel[i] = static_cast<int64_t>(kernel.sizes[i]);
+  p.n_bins = static_cast<int64_t>(params.n_bins);
+  p.clip_limit = params.clip_limit;
+  mclahe_timings_t t{0.0, 0.0, 0.0};
+  std::vector<double> out(src.size());
+  int rc;
+  if (all_f32_exact(src)) {
+    p.dtype = MCLAHE_F32;
+    std::vector<float> in32(src.begin(), src.end()), out32(src.size());
+    rc = mclahe_gpu_run_framewise(&p, static_cast<int32_t>(frame_axis), in32.data(), out32.data(),
+                                  &t);
+    if (rc == MCLAHE_OK) out.assign(out32.begin(), out32.end());
+  } else {
+    p.dtype = MCLAHE_F64;
+    rc = mclahe_gpu_run_framewise(&p, static_cast<int32_t>(frame_axis), src.data(), out.data(), &t);
+  }
+  if (rc != MCLAHE_OK) raise(rc);
+  if (timings) {
+    timings->pad_s += t.pad_s;
+    timings->histograms_s += t.histograms_s;
+    timings->interpolation_s += t.interpolation_s;
+  }
+  return NdImage(sh, std::move(out));
 }
 
 NdImage normalize_to_unit(const NdImage& image) {

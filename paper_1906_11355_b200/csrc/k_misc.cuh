@@ -179,6 +179,58 @@ __global__ void k_dict_luts(WS W, int64_t win_tiles, int n) {
   }
 }
 
+// ------------------------------------------------------ framewise ranges ----
+// Batched mclahe_framewise (src/pipeline.cpp:131-153) in global mode: every
+// frame is enhanced with its own global range.  The volume runs as one
+// adaptive pass whose kernel is 1 along the frame axis, and each tile takes
+// its frame's min/max instead of its own.  Runs r in [0, outer * frames) are
+// the contiguous `inner`-element pieces of frame r % frames.
+template <typename T>
+__global__ void __launch_bounds__(256) k_frame_range(const T* __restrict__ in, int64_t outer,
+                                                     int64_t frames, int64_t inner,
+                                                     int64_t* __restrict__ frange,
+                                                     int64_t* __restrict__ range) {
+  for (int64_t r = blockIdx.y; r < outer * frames; r += gridDim.y) {
+    const int64_t f = r % frames;
+    const T* p = in + r * inner;
+    T lo = INFINITY, hi = -INFINITY;
+    int bad = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < inner;
+         i += (int64_t)gridDim.x * blockDim.x) {
+      const T v = p[i];
+      bad |= !isfinite(v);
+      lo = fmin(lo, v);
+      hi = fmax(hi, v);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+      hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+      bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+    }
+    if ((threadIdx.x & 31) == 0 && lo <= hi) {
+      atomicMax(reinterpret_cast<long long*>(&frange[2 * f]), (long long)~okey((double)lo));
+      atomicMax(reinterpret_cast<long long*>(&frange[2 * f + 1]), (long long)okey((double)hi));
+    }
+    if ((threadIdx.x & 31) == 0 && bad) atomicMax(reinterpret_cast<long long*>(&range[2]), 1LL);
+  }
+}
+
+// Tile range keys from the frame ranges: tile coordinate t along the frame
+// axis (kernel 1) covers frame min(t, frames - 1) (the one padded tile
+// mirrors the last frame).
+__global__ void k_frame_tiles(const KGeom G, WS W, const int64_t* __restrict__ frange, int axis) {
+  const int64_t frames = G.d[axis].s;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < G.win_tiles;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t gt = t + G.trow0 * G.tstride[0];
+    const int64_t tc = (gt / G.tstride[axis]) % G.d[axis].g;
+    const int64_t f = tc < frames ? tc : frames - 1;
+    W.trange[2 * t] = frange[2 * f];
+    W.trange[2 * t + 1] = frange[2 * f + 1];
+  }
+}
+
 // ------------------------------------------------------------------ K1 ----
 // Global min/max + finiteness over the slab (NdImage::min_max / all_finite,
 // src/nd_image.cpp:70-83).  Grid-stride, 16-byte loads, one atomic per CTA.

@@ -126,6 +126,9 @@ struct mclahe_plan_s {
   int64_t off_hist_units = 0, off_hist_cta = 0, off_interp_units = 0, off_interp_cta = 0;
   int hist_grid = 0, interp_grid = 0, range_grid = 0, map_grid = 0, map_block = 128;
   int64_t map_smem = 0;
+  // batched framewise, global mode: tiles take their frame's range (-1: off)
+  int frame_axis = -1;
+  int64_t off_frange = 0;
   // value dictionary (kDict*): armed when the blend's tables fit shared memory
   int dict_cap = 0, dict_nst = 0;
   int64_t dict_smem = 0, off_dict = 0;
@@ -718,6 +721,30 @@ int do_reset(mclahe_plan_s* pl, void* ws, cudaStream_t st) {
 
 int do_range(mclahe_plan_s* pl, const void* in, void* ws, cudaStream_t st) {
   WS W = ws_view(pl, ws);
+  if (pl->frame_axis >= 0) {  // framewise global mode: per-frame ranges
+    const int ax = pl->frame_axis;
+    int64_t outer = 1, inner = 1;
+    for (int j = 0; j < ax; ++j) outer *= pl->p.shape[j];
+    for (int j = ax + 1; j < pl->p.rank; ++j) inner *= pl->p.shape[j];
+    const int64_t frames = pl->p.shape[ax];
+    int64_t* frange = reinterpret_cast<int64_t*>(static_cast<char*>(ws) + pl->off_frange);
+    k_reset<<<(int)std::max<int64_t>(1, std::min<int64_t>((2 * frames + 255) / 256, 1024)), 256, 0, st>>>(
+        W.range, frange, 2 * frames, W, 0);
+    MG_LAUNCHED();
+    const dim3 grid((unsigned)std::max<int64_t>(1, std::min<int64_t>((inner + 255) / 256, 64)),
+                    (unsigned)std::max<int64_t>(1, std::min<int64_t>(outer * frames, 65535)));
+    if (pl->f32())
+      k_frame_range<float><<<grid, 256, 0, st>>>(static_cast<const float*>(in), outer, frames, inner,
+                                                 frange, W.range);
+    else
+      k_frame_range<double><<<grid, 256, 0, st>>>(static_cast<const double*>(in), outer, frames,
+                                                  inner, frange, W.range);
+    MG_LAUNCHED();
+    const int tg = (int)std::max<int64_t>(1, std::min<int64_t>((pl->G.win_tiles + 255) / 256, 4096));
+    k_frame_tiles<<<tg, 256, 0, st>>>(pl->G, W, frange, ax);
+    MG_LAUNCHED();
+    return MCLAHE_OK;
+  }
   if (!pl->p.adaptive) {
     if (pl->f32())
       k_global_range<float><<<pl->range_grid, 256, 0, st>>>(static_cast<const float*>(in),
@@ -1079,7 +1106,7 @@ std::string plan_key(const mclahe_params_t* p, int dev) {
   return k;
 }
 
-mclahe_plan_s* cached_plan(OneShot& o, const mclahe_params_t* p, int* rc) {
+mclahe_plan_s* cached_plan(OneShot& o, const mclahe_params_t* p, int* rc, int frame_axis = -1) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) {
@@ -1089,12 +1116,19 @@ mclahe_plan_s* cached_plan(OneShot& o, const mclahe_params_t* p, int* rc) {
   mclahe_params_t q = *p;
   q.reserved = 0;
   for (int i = q.rank; i < MCLAHE_MAX_RANK; ++i) q.shape[i] = q.kernel[i] = 0;
-  const std::string key = plan_key(&q, dev);
+  std::string key = plan_key(&q, dev);
+  key.append(reinterpret_cast<const char*>(&frame_axis), sizeof frame_axis);
   auto it = o.plans.find(key);
   if (it != o.plans.end()) return it->second.get();
   auto pl = std::make_unique<mclahe_plan_s>();
   *rc = plan_describe(&q, 0, q.shape[0], pl.get());
   if (*rc) return nullptr;
+  if (frame_axis >= 0) {  // per-frame global ranges: K2a and the dictionary stay off
+    pl->frame_axis = frame_axis;
+    pl->dict_cap = 0;
+    pl->off_frange = align_up(pl->info.workspace_bytes, 256);
+    pl->info.workspace_bytes = align_up(pl->off_frange + q.shape[frame_axis] * 16, 256);
+  }
   *rc = device_init(pl.get());
   if (*rc) return nullptr;
   if (o.plans.size() > 32) o.plans.clear();
@@ -1158,6 +1192,40 @@ int read_status(const mclahe_plan_s* pl, const void* ws, cudaStream_t st) {
 
 
 
+
+}  // namespace
+
+namespace {
+
+// One plan over the whole volume: H2D, every pass, non-finite check, D2H.
+int run_plan_host(OneShot& o, mclahe_plan_s* pl, const void* in, void* out, size_t bytes,
+                  size_t io, mclahe_timings_t* timings) {
+  int rc;
+  if ((rc = ensure_buf(o, 2 * io + (size_t)pl->info.workspace_bytes))) return rc;
+  if ((rc = ensure_stream(o))) return rc;
+  char* base = static_cast<char*>(o.buf);
+  void* d_in = base;
+  void* d_out = base + io;
+  void* ws = base + 2 * io;
+  cudaStream_t st = o.stream;
+  MG_CUDA(cudaMemcpyAsync(d_in, in, bytes, cudaMemcpyHostToDevice, st));
+  if ((rc = enqueue_all(pl, d_in, d_out, ws, st, timings ? o.ev : nullptr))) return rc;
+  int64_t flag = 0;
+  MG_CUDA(cudaMemcpyAsync(&flag, static_cast<char*>(ws) + pl->info.off_range + 16, sizeof flag,
+                          cudaMemcpyDeviceToHost, st));
+  MG_CUDA(cudaStreamSynchronize(st));
+  if (flag) return fail(MCLAHE_ERR_VALIDATION, "image contains non-finite values");
+  MG_CUDA(cudaMemcpyAsync(out, d_out, bytes, cudaMemcpyDeviceToHost, st));
+  MG_CUDA(cudaStreamSynchronize(st));
+  if (timings) {
+    float a = 0, b = 0;
+    MG_CUDA(cudaEventElapsedTime(&a, o.ev[0], o.ev[1]));
+    MG_CUDA(cudaEventElapsedTime(&b, o.ev[1], o.ev[2]));
+    timings->histograms_s += a * 1e-3;
+    timings->interpolation_s += b * 1e-3;
+  }
+  return MCLAHE_OK;
+}
 
 }  // namespace
 
@@ -1315,30 +1383,38 @@ int mclahe_gpu_run(const mclahe_params_t* params, const void* in, void* out,
                           o.s_out, o.sev, timings);
     }
   }
-  if ((rc = ensure_buf(o, 2 * io + (size_t)pl->info.workspace_bytes))) return rc;
-  if ((rc = ensure_stream(o))) return rc;
-  char* base = static_cast<char*>(o.buf);
-  void* d_in = base;
-  void* d_out = base + io;
-  void* ws = base + 2 * io;
-  cudaStream_t st = o.stream;
-  MG_CUDA(cudaMemcpyAsync(d_in, in, bytes, cudaMemcpyHostToDevice, st));
-  if ((rc = enqueue_all(pl, d_in, d_out, ws, st, timings ? o.ev : nullptr))) return rc;
-  int64_t flag = 0;
-  MG_CUDA(cudaMemcpyAsync(&flag, static_cast<char*>(ws) + pl->info.off_range + 16, sizeof flag,
-                          cudaMemcpyDeviceToHost, st));
-  MG_CUDA(cudaStreamSynchronize(st));
-  if (flag) return fail(MCLAHE_ERR_VALIDATION, "image contains non-finite values");
-  MG_CUDA(cudaMemcpyAsync(out, d_out, bytes, cudaMemcpyDeviceToHost, st));
-  MG_CUDA(cudaStreamSynchronize(st));
-  if (timings) {
-    float a = 0, b = 0;
-    MG_CUDA(cudaEventElapsedTime(&a, o.ev[0], o.ev[1]));
-    MG_CUDA(cudaEventElapsedTime(&b, o.ev[1], o.ev[2]));
-    timings->histograms_s += a * 1e-3;
-    timings->interpolation_s += b * 1e-3;
-  }
-  return MCLAHE_OK;
+  return run_plan_host(o, pl, in, out, bytes, io, timings);
+}
+
+int mclahe_gpu_run_framewise(const mclahe_params_t* params, int32_t frame_axis, const void* in,
+                             void* out, mclahe_timings_t* timings) {
+  if (!params) return fail(MCLAHE_ERR_VALIDATION, "null params");
+  const int D = params->rank;
+  if (D < 2) return fail(MCLAHE_ERR_VALIDATION, "framewise mode needs rank >= 2");
+  if (frame_axis < 0 || frame_axis >= D)
+    return fail(MCLAHE_ERR_VALIDATION, "frame axis " + std::to_string(frame_axis) +
+                                           " out of range for rank " + std::to_string(D));
+  // the slice request first, so messages match the reference's per-slice checks
+  mclahe_params_t sl = *params;
+  sl.rank = D - 1;
+  for (int j = 0, k = 0; j < D; ++j)
+    if (j != frame_axis) sl.shape[k++] = params->shape[j];
+  for (int j = D - 1; j < MCLAHE_MAX_RANK; ++j) sl.shape[j] = sl.kernel[j] = 0;
+  int rc = validate(&sl);
+  if (rc) return rc;
+  if (!in || !out) return fail(MCLAHE_ERR_VALIDATION, "null host buffer");
+  // the volume with kernel 1 along the frame axis: each tile is one frame
+  // thick and the blend weight across frames is exactly 0 / 1
+  mclahe_params_t q = *params;
+  for (int j = 0, k = 0; j < D; ++j) q.kernel[j] = j == frame_axis ? 1 : params->kernel[k++];
+  if (params->adaptive) return mclahe_gpu_run(&q, in, out, timings);
+  q.adaptive = 1;  // per-tile parameters, each tile's range = its frame's global range
+  OneShot& o = oneshot();
+  std::lock_guard<std::mutex> lock(o.mu);
+  mclahe_plan_s* pl = cached_plan(o, &q, &rc, frame_axis);
+  if (!pl) return rc;
+  const size_t bytes = (size_t)(volume(&q) * elem_size(&q));
+  return run_plan_host(o, pl, in, out, bytes, (size_t)align_up((int64_t)bytes, 256), timings);
 }
 
 int mclahe_debug_bin_index(int32_t dtype, const void* values, int64_t n, double lo, double hi,

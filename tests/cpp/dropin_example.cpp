@@ -37,6 +37,14 @@ int main(int argc, char** argv) {
     return caught == 2 ? 0 : 1;
   }
   mclahe::PhaseTimings t;
+  if (argc > 1 && std::strcmp(argv[1], "framewise") == 0) {  // slices along axis 1, global range
+    mclahe::EnhanceParams prm = req.params;
+    prm.range_mode = mclahe::RangeMode::Global;
+    const mclahe::NdImage out =
+        mclahe::mclahe_framewise(req.image, 1, mclahe::KernelSpec{{8, 4}}, prm, 0, false, &t);
+    for (std::size_t i = 0; i < out.size(); ++i) std::printf("%.17g\n", out[i]);
+    return 0;
+  }
   const mclahe::NdImage out = mclahe::mclahe(req, &t);
   for (std::size_t i = 0; i < out.size(); ++i) std::printf("%.17g\n", out[i]);
   std::fprintf(stderr, "hist %.3g s interp %.3g s\n", t.histograms_s, t.interpolation_s);

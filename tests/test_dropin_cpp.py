@@ -39,3 +39,15 @@ def test_runs_on_gpu_and_matches_oracle(exe):
     x = (((i * 37) % 101) / 100.0).reshape(24, 20, 16)
     want = O.mclahe(x, (8, 4, 4), 32, 0.05, True, "c")
     assert np.max(np.abs(got - want)) <= 1e-5
+
+
+@pytest.mark.gpu
+def test_framewise_batched_matches_per_slice_oracle(exe):
+    from oracle import oracle as O
+    r = subprocess.run([exe, "framewise"], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stderr
+    got = np.array([float(v) for v in r.stdout.split()]).reshape(24, 20, 16)
+    i = np.arange(24 * 20 * 16)
+    x = (((i * 37) % 101) / 100.0).reshape(24, 20, 16)
+    want = np.stack([O.mclahe(x[:, f, :], (8, 4), 32, 0.05, False, "c") for f in range(20)], 1)
+    assert np.max(np.abs(got - want)) <= 1e-5

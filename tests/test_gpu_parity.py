@@ -412,3 +412,43 @@ def test_sparse_counts_degenerate_neighbours(M, ad):
     assert_stats_equal(st, ref, "sparse")
     out = M.enhance(x, *args)
     assert np.max(np.abs(out.astype(np.float64) - O.mclahe(x, *args, "c"))) <= OUT_TOL
+
+
+def _framewise_oracle(x, axis, kernel, nb, clip, ad, renorm):
+    outs = []
+    for f in range(x.shape[axis]):
+        sl = np.take(x, f, axis=axis).astype(np.float64)
+        if renorm:
+            lo, hi = sl.min(), sl.max()
+            sl = (sl - lo) / (hi - lo) if hi > lo else np.full_like(sl, 0.5)
+        outs.append(O.mclahe(sl, kernel, nb, clip, ad, "c"))
+    return np.stack(outs, axis=axis)
+
+
+@pytest.mark.parametrize("axis", [0, 1, 2])
+@pytest.mark.parametrize("ad", [False, True])
+def test_framewise_batched_vs_per_slice_oracle(M, axis, ad):
+    # mclahe_framewise (src/pipeline.cpp:131-153) in one batched GPU run
+    rng = np.random.default_rng(60 + axis + 3 * ad)
+    shape = [20, 24, 28]
+    x = (rng.poisson(2.5, shape) / 9.0).astype(np.float32)
+    x[..., :3] = 0.4  # constant strips: degenerate tiles / frames
+    kernel = tuple(k for j, k in enumerate((6, 8, 7)) if j != axis)
+    params = M.EnhanceParams(0.05, 64, M.RangeMode.Adaptive if ad else M.RangeMode.Global)
+    out = M.mclahe_framewise(x, axis, M.KernelSpec(kernel), params)
+    assert out.dtype == np.float32 and out.shape == x.shape
+    want = _framewise_oracle(x, axis, kernel, 64, 0.05, ad, False)
+    assert np.max(np.abs(out.astype(np.float64) - want)) <= OUT_TOL
+
+
+@pytest.mark.parametrize("ad", [False, True])
+def test_framewise_renormalized_and_4d(M, ad):
+    rng = np.random.default_rng(71 + ad)
+    x = (rng.normal(0, 2, (6, 18, 20, 8))).astype(np.float32)
+    x[2] = 3.0  # a constant frame
+    kernel = (6, 5, 4)
+    params = M.EnhanceParams(0.1, 32, M.RangeMode.Adaptive if ad else M.RangeMode.Global)
+    for renorm in (False, True):
+        out = M.mclahe_framewise(x, 0, M.KernelSpec(kernel), params, renormalize_slices=renorm)
+        want = _framewise_oracle(x, 0, kernel, 32, 0.1, ad, renorm)
+        assert np.max(np.abs(out.astype(np.float64) - want)) <= OUT_TOL, renorm

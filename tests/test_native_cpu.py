@@ -109,3 +109,14 @@ def test_slab_cuts_ragged(N):
             assert all(a in starts for a, _ in cuts)
         with pytest.raises(Exception):
             S.slab_cuts(extent, k, len(cells) + 1)
+
+
+def test_framewise_validation_messages():
+    import paper_1906_11355_b200 as M
+    prm = M.EnhanceParams(0.1, 16)
+    with pytest.raises(M.ValidationError, match="framewise mode needs rank >= 2"):
+        M.mclahe_framewise(np.zeros(5, np.float32), 0, M.KernelSpec(()), prm)
+    with pytest.raises(M.ValidationError, match="frame axis 3 out of range for rank 3"):
+        M.mclahe_framewise(np.zeros((4, 5, 6), np.float32), 3, M.KernelSpec((2, 2)), prm)
+    with pytest.raises(M.ValidationError, match="framewise kernel rank must be image rank - 1"):
+        M.mclahe_framewise(np.zeros((4, 5, 6), np.float32), 0, M.KernelSpec((2, 2, 2)), prm)
