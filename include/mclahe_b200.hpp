@@ -88,4 +88,36 @@ NdImage mclahe_framewise(const NdImage& image, std::size_t frame_axis, const Ker
 // pipeline.hpp:43 -- affine map of [min, max] onto [0, 1]; constant -> 0.5.
 NdImage normalize_to_unit(const NdImage& image);
 
+// ---- filters.hpp / metrics.hpp: the steps either side of the path, on the GPU ----
+
+struct GaussianSpec {  // filters.hpp:11-15
+  std::vector<double> sigmas;
+  double truncate = 4.0;
+};
+
+struct MedianSpec {  // filters.hpp:17-21
+  std::vector<std::size_t> window;
+};
+
+// filters.hpp:24-25 -- bit-identical to the reference.
+NdImage gaussian_filter(const NdImage& image, const GaussianSpec& spec, unsigned threads = 1);
+
+// filters.hpp:30-32 -- windows of at most 343 values on the GPU path.
+NdImage median_filter(const NdImage& image, const MedianSpec& spec, unsigned threads = 1);
+
+struct MetricsReport {  // metrics.hpp:9-17
+  double mse = 0.0;
+  double psnr_db = 0.0;
+  double std = 0.0;
+  double entropy_bits = 0.0;
+  std::size_t n_bins_used = 0;
+};
+
+double mse(const NdImage& a, const NdImage& b);                        // metrics.hpp:19-20
+double psnr(const NdImage& a, const NdImage& b, double peak = 1.0);     // metrics.hpp:22-23
+double rms_contrast(const NdImage& a);                                  // metrics.hpp:25-26
+double shannon_entropy(const NdImage& a, std::size_t n_bins = 256);     // metrics.hpp:28-30
+MetricsReport compute_metrics(const NdImage& a, const NdImage& b, std::size_t n_bins = 256,
+                              double peak = 1.0);                       // metrics.hpp:35-36
+
 }  // namespace mclahe

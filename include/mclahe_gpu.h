@@ -204,6 +204,41 @@ int mclahe_debug_bin_index_packed(const float* values_dev, int64_t n, double lo,
 int mclahe_gpu_run_framewise(const mclahe_params_t* params, int32_t frame_axis,
                              const void* host_in, void* host_out, mclahe_timings_t* timings);
 
+/* ---- The steps either side of the path, float64 ----
+ * gaussian_filter (src/filters.cpp:82-96): separable, per-axis sigma (0 skips
+ *   the axis), radius ceil(truncate * sigma), mirror boundary; bit-identical
+ *   to the reference (taps from the host libm, unfused sequential sums).
+ * median_filter (src/filters.cpp:98-142): window extents per dimension
+ *   (offsets -floor((w-1)/2) .. floor(w/2)), mirror boundary, even windows take
+ *   the mean of the two central values; at most 343 values per window here.
+ * metrics (src/metrics.cpp:11-72): mse and psnr of (a, b) (b may be NULL:
+ *   both 0), population standard deviation of a, Shannon entropy of a over
+ *   [min, max] in n_bins bins (exact counts; sum in bin order on the host).
+ * *_device forms take device buffers and synchronise `stream`; the plain forms
+ * take host buffers. */
+typedef struct {
+  double mse;
+  double psnr_db;
+  double std;
+  double entropy_bits;
+  int64_t n_bins_used;
+} mclahe_metrics_t;
+
+int mclahe_gaussian_filter(int32_t rank, const int64_t* shape, const double* sigmas,
+                           double truncate, const double* host_in, double* host_out);
+int mclahe_gaussian_filter_device(int32_t rank, const int64_t* shape, const double* sigmas,
+                                  double truncate, const double* in_dev, double* out_dev,
+                                  void* stream);
+int mclahe_median_filter(int32_t rank, const int64_t* shape, const int64_t* window,
+                         const double* host_in, double* host_out);
+int mclahe_median_filter_device(int32_t rank, const int64_t* shape, const int64_t* window,
+                                const double* in_dev, double* out_dev, void* stream);
+int mclahe_metrics(int32_t rank, const int64_t* shape, const double* host_a,
+                   const double* host_b, int64_t n_bins, double peak, mclahe_metrics_t* report);
+int mclahe_metrics_device(int32_t rank, const int64_t* shape, const double* a_dev,
+                          const double* b_dev, int64_t n_bins, double peak,
+                          mclahe_metrics_t* report, void* stream);
+
 /* Number of kernel launches the last pass call on this thread issued. */
 int64_t mclahe_launch_count(void);
 

@@ -236,3 +236,112 @@ def transform_pixel_ref(value, luts, lo, hi, degenerate, coeff) -> float:
     return float(_lib("ref").ref_transform_pixel(float(value), coeff.size, _p(luts, _f64p),
                                                  luts.shape[1], _p(lo, _f64p), _p(hi, _f64p),
                                                  _p(dg, _u8p), _p(coeff, _f64p)))
+
+
+# ---- prefilters and metrics: numpy restatements + the reference ----
+
+def mirror_index_array(idx: np.ndarray, extent: int) -> np.ndarray:
+    """mirror_index (nd_image.cpp:27-34), vectorised: period 2n, edge-including."""
+    period = 2 * extent
+    m = np.mod(idx, period)
+    return np.where(m >= extent, period - 1 - m, m)
+
+
+def gaussian_taps(sigma: float, truncate: float) -> np.ndarray:
+    """gaussian_taps (filters.cpp:12-23): exp(-t^2/2) at k/sigma, k in
+    [-ceil(truncate*sigma), +], normalised by their sequential sum."""
+    import math
+    radius = int(math.ceil(truncate * sigma))
+    taps = [math.exp(-0.5 * (k / sigma) * (k / sigma)) for k in range(-radius, radius + 1)]
+    total = 0.0
+    for w in taps:
+        total += w
+    return np.array([w / total for w in taps])
+
+
+def gaussian_filter_np(x: np.ndarray, sigmas, truncate: float = 4.0) -> np.ndarray:
+    """gaussian_filter (filters.cpp:82-96 over convolve_axis :28-80): one pass per
+    axis with sigma > 0, acc += tap * line[mirror(x + k)] for k ascending."""
+    out = np.asarray(x, dtype=np.float64).copy()
+    for axis, s in enumerate(sigmas):
+        if s == 0.0:
+            continue
+        taps = gaussian_taps(float(s), float(truncate))
+        r = (len(taps) - 1) // 2
+        n = out.shape[axis]
+        src = np.moveaxis(out, axis, -1)
+        acc = np.zeros_like(src)
+        pos = np.arange(n)
+        for k in range(-r, r + 1):  # sequential in k, each product and sum rounded
+            acc = acc + taps[k + r] * src[..., mirror_index_array(pos + k, n)]
+        out = np.ascontiguousarray(np.moveaxis(acc, -1, axis))
+    return out
+
+
+def median_filter_np(x: np.ndarray, window) -> np.ndarray:
+    """median_filter (filters.cpp:98-142): offsets -floor((w-1)/2)..floor(w/2) per
+    dim, mirrored; even counts take the mean of the two central values."""
+    x = np.asarray(x, dtype=np.float64)
+    stack = []
+    grids = [range(-((w - 1) // 2), w // 2 + 1) for w in window]
+    import itertools
+    for offs in itertools.product(*grids):
+        idx = np.ix_(*[mirror_index_array(np.arange(n) + o, n) for n, o in zip(x.shape, offs)])
+        stack.append(x[idx])
+    st = np.sort(np.stack(stack, axis=0), axis=0)
+    m = st.shape[0] // 2
+    return st[m] if st.shape[0] % 2 else 0.5 * (st[m - 1] + st[m])
+
+
+def metrics_np(a: np.ndarray, b: np.ndarray, n_bins: int = 256, peak: float = 1.0) -> dict:
+    """compute_metrics (metrics.cpp:11-72); sums in numpy order (tolerance-equal)."""
+    a = np.asarray(a, dtype=np.float64).ravel()
+    b = np.asarray(b, dtype=np.float64).ravel()
+    d = a - b
+    mse_ = float(np.sum(d * d) / a.size)
+    psnr_ = float("inf") if mse_ == 0.0 else float(10.0 * np.log10(peak * peak / mse_))
+    mean = float(np.sum(a) / a.size)
+    std_ = float(np.sqrt(np.sum((a - mean) ** 2) / a.size))
+    lo, hi = float(a.min()), float(a.max())
+    ent = 0.0
+    if hi > lo:
+        bins = bin_index_array(a, lo, hi, n_bins)
+        counts = np.bincount(bins, minlength=n_bins).astype(np.float64)
+        for c in counts:  # bin order, as the reference
+            if c > 0:
+                p = c / a.size
+                ent -= p * np.log2(p)
+    return dict(mse=mse_, psnr_db=psnr_, std=std_, entropy_bits=float(ent))
+
+
+def gaussian_filter_ref(x: np.ndarray, sigmas, truncate: float = 4.0) -> np.ndarray:
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    sg = np.ascontiguousarray(np.asarray(sigmas, dtype=np.float64))
+    shape, out, err = _i64(x.shape), np.empty_like(x), C.create_string_buffer(256)
+    rc = _lib("ref").ref_gaussian(_p(x, _f64p), x.ndim, _p(shape, _i64p), _p(sg, _f64p),
+                                  C.c_double(truncate), _p(out, _f64p), err, 256)
+    if rc:
+        raise OracleValidationError(err.value.decode())
+    return out
+
+
+def median_filter_ref(x: np.ndarray, window) -> np.ndarray:
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    shape, win = _i64(x.shape), _i64(window)
+    out, err = np.empty_like(x), C.create_string_buffer(256)
+    rc = _lib("ref").ref_median(_p(x, _f64p), x.ndim, _p(shape, _i64p), _p(win, _i64p),
+                                _p(out, _f64p), err, 256)
+    if rc:
+        raise OracleValidationError(err.value.decode())
+    return out
+
+
+def metrics_ref(a: np.ndarray, b: np.ndarray, n_bins: int = 256, peak: float = 1.0) -> dict:
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    shape, out, err = _i64(a.shape), np.zeros(4), C.create_string_buffer(256)
+    rc = _lib("ref").ref_metrics(_p(a, _f64p), _p(b, _f64p), a.ndim, _p(shape, _i64p),
+                                 C.c_int64(n_bins), C.c_double(peak), _p(out, _f64p), err, 256)
+    if rc:
+        raise OracleValidationError(err.value.decode())
+    return dict(mse=out[0], psnr_db=out[1], std=out[2], entropy_bits=out[3])

@@ -7,15 +7,18 @@
 // mclahe::mclahe (pipeline.hpp:30), build_mappings / compute_histogram /
 // clip_histogram / normalized_cdf / bin_index / apply_mapping
 // (histogram.hpp:51-80), neighbor_kernels / interp_coefficients /
-// transform_pixel (interpolation.hpp:28-45).
+// transform_pixel (interpolation.hpp:28-45), gaussian_filter / median_filter
+// (filters.hpp:24-32) and the contrast metrics (metrics.hpp:19-36).
 #include <cstdint>
 #include <cstring>
 #include <exception>
 #include <string>
 #include <vector>
 
+#include "mclahe/filters.hpp"
 #include "mclahe/histogram.hpp"
 #include "mclahe/interpolation.hpp"
+#include "mclahe/metrics.hpp"
 #include "mclahe/nd_image.hpp"
 #include "mclahe/pipeline.hpp"
 
@@ -173,6 +176,54 @@ double ref_transform_pixel(double value, int corners, const double* luts, int64_
   }
   return mclahe::transform_pixel(value, ptrs,
                                  std::span<const double>(coeff, static_cast<size_t>(corners)));
+}
+
+// gaussian_filter (filters.hpp:24-25): 0 ok, 1 ValidationError (message in err).
+int ref_gaussian(const double* data, int rank, const int64_t* shape, const double* sigmas,
+                 double truncate, double* out, char* err, int err_len) {
+  try {
+    mclahe::GaussianSpec spec;
+    spec.sigmas.assign(sigmas, sigmas + rank);
+    spec.truncate = truncate;
+    const mclahe::NdImage r = mclahe::gaussian_filter(make_image(data, rank, shape), spec, 1);
+    std::memcpy(out, r.values().data(), r.size() * sizeof(double));
+    return 0;
+  } catch (const mclahe::ValidationError& e) {
+    put_err(err, err_len, e.what());
+    return 1;
+  }
+}
+
+// median_filter (filters.hpp:30-32).
+int ref_median(const double* data, int rank, const int64_t* shape, const int64_t* window,
+               double* out, char* err, int err_len) {
+  try {
+    mclahe::MedianSpec spec;
+    for (int i = 0; i < rank; ++i) spec.window.push_back(static_cast<size_t>(window[i]));
+    const mclahe::NdImage r = mclahe::median_filter(make_image(data, rank, shape), spec, 1);
+    std::memcpy(out, r.values().data(), r.size() * sizeof(double));
+    return 0;
+  } catch (const mclahe::ValidationError& e) {
+    put_err(err, err_len, e.what());
+    return 1;
+  }
+}
+
+// compute_metrics (metrics.hpp:35-36): out = {mse, psnr_db, std, entropy_bits}.
+int ref_metrics(const double* a, const double* b, int rank, const int64_t* shape,
+                int64_t n_bins, double peak, double* out, char* err, int err_len) {
+  try {
+    const mclahe::MetricsReport m = mclahe::compute_metrics(
+        make_image(a, rank, shape), make_image(b, rank, shape), static_cast<size_t>(n_bins), peak);
+    out[0] = m.mse;
+    out[1] = m.psnr_db;
+    out[2] = m.std;
+    out[3] = m.entropy_bits;
+    return 0;
+  } catch (const mclahe::ValidationError& e) {
+    put_err(err, err_len, e.what());
+    return 1;
+  }
 }
 
 }  // extern "C"

@@ -9,8 +9,11 @@ clip/CDF/LUT, 2^D-corner multilinear blend) as sm_100a kernels behind a C ABI
 from ._native import NativeUnavailable, ValidationError  # noqa: F401
 from .api import (EnhanceParams, KernelSpec, McLaheRequest, PhaseTimings, Plan,  # noqa: F401
                   RangeMode, bin_index_device, enhance, launch_count, mclahe, mclahe_framewise,
-                  normalize_to_unit)
+                  normalize_to_unit, GaussianSpec, MedianSpec, MetricsReport, gaussian_filter,
+                  median_filter, compute_metrics, mse, psnr, rms_contrast, shannon_entropy)
 
 __all__ = ["EnhanceParams", "KernelSpec", "McLaheRequest", "PhaseTimings", "Plan", "RangeMode",
            "ValidationError", "NativeUnavailable", "mclahe", "enhance", "bin_index_device",
-           "launch_count", "mclahe_framewise", "normalize_to_unit"]
+           "launch_count", "mclahe_framewise", "normalize_to_unit", "GaussianSpec", "MedianSpec",
+           "MetricsReport", "gaussian_filter", "median_filter", "compute_metrics", "mse", "psnr",
+           "rms_contrast", "shannon_entropy"]

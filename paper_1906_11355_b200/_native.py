@@ -46,6 +46,11 @@ class Timings(C.Structure):
                 ("interpolation_s", C.c_double)]
 
 
+class Metrics(C.Structure):
+    _fields_ = [("mse", C.c_double), ("psnr_db", C.c_double), ("std", C.c_double),
+                ("entropy_bits", C.c_double), ("n_bins_used", C.c_int64)]
+
+
 class PlanInfo(C.Structure):
     _fields_ = [("rank", C.c_int32), ("fast_hist", C.c_int32), ("fast_interp", C.c_int32),
                 ("trailing_dims", C.c_int32), ("before", C.c_int64 * MAX_RANK),
@@ -85,6 +90,12 @@ SIGNATURES = {
     "mclahe_debug_bin_index": (C.c_int, [C.c_int32, _vp, _i64, C.c_double, C.c_double, _i64,
                                          _vp, _vp]),
     "mclahe_gpu_run_framewise": (C.c_int, [_vp, C.c_int32, _vp, _vp, _vp]),
+    "mclahe_gaussian_filter": (C.c_int, [C.c_int32, _vp, _vp, C.c_double, _vp, _vp]),
+    "mclahe_gaussian_filter_device": (C.c_int, [C.c_int32, _vp, _vp, C.c_double, _vp, _vp, _vp]),
+    "mclahe_median_filter": (C.c_int, [C.c_int32, _vp, _vp, _vp, _vp]),
+    "mclahe_median_filter_device": (C.c_int, [C.c_int32, _vp, _vp, _vp, _vp, _vp]),
+    "mclahe_metrics": (C.c_int, [C.c_int32, _vp, _vp, _vp, _i64, C.c_double, _vp]),
+    "mclahe_metrics_device": (C.c_int, [C.c_int32, _vp, _vp, _vp, _i64, C.c_double, _vp, _vp]),
     "mclahe_plan_dict_state": (C.c_int, [_vp, _vp, C.POINTER(C.c_int32), _vp]),
     "mclahe_debug_bin_index_packed": (C.c_int, [_vp, _i64, C.c_double, C.c_double, _i64,
                                                 C.c_int32, _vp, _vp]),

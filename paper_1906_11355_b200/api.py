@@ -344,6 +344,118 @@ def mclahe_framewise(image, frame_axis: int, kernel: KernelSpec, params: Enhance
     return out
 
 
+# ---- the steps either side of the path: prefilters and metrics (float64) ----
+
+@dataclass
+class GaussianSpec:
+    """filters.hpp:11-15: sigma per dimension in pixels (0 skips the axis)."""
+    sigmas: tuple
+    truncate: float = 4.0
+
+
+@dataclass
+class MedianSpec:
+    """filters.hpp:17-21: window extents per dimension."""
+    window: tuple
+
+
+@dataclass
+class MetricsReport:
+    """metrics.hpp:9-17."""
+    mse: float = 0.0
+    psnr_db: float = 0.0
+    std: float = 0.0
+    entropy_bits: float = 0.0
+    n_bins_used: int = 0
+
+
+def _shape_arr(shape):
+    arr = (C.c_int64 * max(1, len(shape)))(*[int(v) for v in shape])
+    return arr
+
+
+def _filter_call(image, host_fn, dev_fn, *args):
+    """numpy -> host ABI -> numpy; CUDA tensor -> device ABI -> CUDA tensor (f64)."""
+    if _is_torch(image):
+        import torch
+        x = image.to(torch.float64).contiguous()
+        out = torch.empty_like(x)
+        N.check(dev_fn(x.dim(), _shape_arr(x.shape), *args, x.data_ptr(), out.data_ptr(),
+                       _stream_handle()))
+        return out
+    x = np.ascontiguousarray(np.asarray(image, dtype=np.float64))
+    out = np.empty_like(x)
+    N.check(host_fn(x.ndim, _shape_arr(x.shape), *args, x.ctypes.data, out.ctypes.data))
+    return out
+
+
+def gaussian_filter(image, spec: GaussianSpec):
+    """gaussian_filter (filters.hpp:24-25, filters.cpp:82-96) on the GPU, float64."""
+    x = image
+    rank = x.dim() if _is_torch(x) else np.ndim(x)
+    if len(spec.sigmas) != rank:
+        raise ValidationError("sigma count does not match image rank")
+    sg = (C.c_double * max(1, rank))(*[float(v) for v in spec.sigmas])
+    L = N.lib()
+    return _filter_call(x, L.mclahe_gaussian_filter, L.mclahe_gaussian_filter_device, sg,
+                        C.c_double(float(spec.truncate)))
+
+
+def median_filter(image, spec: MedianSpec):
+    """median_filter (filters.hpp:30-32, filters.cpp:98-142) on the GPU, float64."""
+    x = image
+    rank = x.dim() if _is_torch(x) else np.ndim(x)
+    if len(spec.window) != rank:
+        raise ValidationError("window rank does not match image rank")
+    win = (C.c_int64 * max(1, rank))(*[int(v) for v in spec.window])
+    L = N.lib()
+    return _filter_call(x, L.mclahe_median_filter, L.mclahe_median_filter_device, win)
+
+
+def compute_metrics(a, b=None, n_bins: int = 256, peak: float = 1.0) -> MetricsReport:
+    """compute_metrics (metrics.hpp:35-36): std / entropy of a, mse / psnr of (a, b)."""
+    L = N.lib()
+    rep = N.Metrics()
+    if _is_torch(a):
+        import torch
+        xa = a.to(torch.float64).contiguous()
+        xb = None if b is None else b.to(torch.float64).contiguous()
+        if xb is not None and tuple(xb.shape) != tuple(xa.shape):
+            raise ValidationError("mse operands differ in shape")
+        N.check(L.mclahe_metrics_device(xa.dim(), _shape_arr(xa.shape), xa.data_ptr(),
+                                        None if xb is None else xb.data_ptr(), int(n_bins),
+                                        float(peak), C.byref(rep), _stream_handle()))
+    else:
+        xa = np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+        xb = None if b is None else np.ascontiguousarray(np.asarray(b, dtype=np.float64))
+        if xb is not None and xb.shape != xa.shape:
+            raise ValidationError("mse operands differ in shape")
+        N.check(L.mclahe_metrics(xa.ndim, _shape_arr(xa.shape), xa.ctypes.data,
+                                 None if xb is None else xb.ctypes.data, int(n_bins),
+                                 float(peak), C.byref(rep)))
+    return MetricsReport(rep.mse, rep.psnr_db, rep.std, rep.entropy_bits, int(rep.n_bins_used))
+
+
+def mse(a, b) -> float:
+    """metrics.hpp:19-20."""
+    return compute_metrics(a, b).mse
+
+
+def psnr(a, b, peak: float = 1.0) -> float:
+    """metrics.hpp:22-23."""
+    return compute_metrics(a, b, peak=peak).psnr_db
+
+
+def rms_contrast(a) -> float:
+    """metrics.hpp:25-26."""
+    return compute_metrics(a).std
+
+
+def shannon_entropy(a, n_bins: int = 256) -> float:
+    """metrics.hpp:28-30."""
+    return compute_metrics(a, n_bins=n_bins).entropy_bits
+
+
 def enhance(image, kernel_size, n_bins: int = 256, clip_limit: float = 1.0,
             adaptive_hist_range: bool = False):
     """Convenience form with the paper's argument names (data, kernel_size,

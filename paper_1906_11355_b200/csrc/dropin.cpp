@@ -172,4 +172,72 @@ NdImage normalize_to_unit(const NdImage& image) {
   return NdImage(image.shape(), std::move(d));
 }
 
+namespace {
+
+std::vector<int64_t> shape64(const NdImage& a) {
+  return std::vector<int64_t>(a.shape().begin(), a.shape().end());
+}
+
+MetricsReport metrics_call(const NdImage& a, const NdImage* b, std::size_t n_bins, double peak) {
+  if (b && a.shape() != b->shape()) throw ValidationError("mse operands differ in shape");
+  const std::vector<int64_t> sh = shape64(a);
+  mclahe_metrics_t r{};
+  const int rc = mclahe_metrics(static_cast<int32_t>(a.rank()), sh.data(), a.data().data(),
+                                b ? b->data().data() : nullptr, static_cast<int64_t>(n_bins),
+                                peak, &r);
+  if (rc != MCLAHE_OK) raise(rc);
+  MetricsReport m;
+  m.mse = r.mse;
+  m.psnr_db = r.psnr_db;
+  m.std = r.std;
+  m.entropy_bits = r.entropy_bits;
+  m.n_bins_used = static_cast<std::size_t>(r.n_bins_used);
+  return m;
+}
+
+}  // namespace
+
+NdImage gaussian_filter(const NdImage& image, const GaussianSpec& spec, unsigned threads) {
+  (void)threads;
+  if (spec.sigmas.size() != image.rank())
+    throw ValidationError("sigma count does not match image rank");
+  const std::vector<int64_t> sh = shape64(image);
+  std::vector<double> out(image.size());
+  const int rc = mclahe_gaussian_filter(static_cast<int32_t>(image.rank()), sh.data(),
+                                        spec.sigmas.data(), spec.truncate, image.data().data(),
+                                        out.data());
+  if (rc != MCLAHE_OK) raise(rc);
+  return NdImage(image.shape(), std::move(out));
+}
+
+NdImage median_filter(const NdImage& image, const MedianSpec& spec, unsigned threads) {
+  (void)threads;
+  if (spec.window.size() != image.rank())
+    throw ValidationError("window rank does not match image rank");
+  const std::vector<int64_t> sh = shape64(image);
+  const std::vector<int64_t> win(spec.window.begin(), spec.window.end());
+  std::vector<double> out(image.size());
+  const int rc = mclahe_median_filter(static_cast<int32_t>(image.rank()), sh.data(), win.data(),
+                                      image.data().data(), out.data());
+  if (rc != MCLAHE_OK) raise(rc);
+  return NdImage(image.shape(), std::move(out));
+}
+
+double mse(const NdImage& a, const NdImage& b) { return metrics_call(a, &b, 256, 1.0).mse; }
+
+double psnr(const NdImage& a, const NdImage& b, double peak) {
+  return metrics_call(a, &b, 256, peak).psnr_db;
+}
+
+double rms_contrast(const NdImage& a) { return metrics_call(a, nullptr, 256, 1.0).std; }
+
+double shannon_entropy(const NdImage& a, std::size_t n_bins) {
+  return metrics_call(a, nullptr, n_bins, 1.0).entropy_bits;
+}
+
+MetricsReport compute_metrics(const NdImage& a, const NdImage& b, std::size_t n_bins,
+                              double peak) {
+  return metrics_call(a, &b, n_bins, peak);
+}
+
 }  // namespace mclahe

@@ -53,6 +53,18 @@ int cuda_fail(cudaError_t e, const char* where) {
 
 int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
+}  // namespace
+
+// error / launch bookkeeping shared with the other host translation units
+// (host_err.h)
+namespace mg {
+int host_fail(int code, const std::string& msg) { return fail(code, msg); }
+int host_cuda_fail(cudaError_t e, const char* where) { return cuda_fail(e, where); }
+void host_count_launch() { ++g_launches; }
+}  // namespace mg
+
+namespace {
+
 // validate_request (src/pipeline.cpp:19-34) minus the finiteness scan, which
 // runs on the device; plus the NdImage invariants (src/nd_image.cpp:52-58).
 int validate(const mclahe_params_t* p) {

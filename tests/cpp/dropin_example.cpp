@@ -45,6 +45,14 @@ int main(int argc, char** argv) {
     for (std::size_t i = 0; i < out.size(); ++i) std::printf("%.17g\n", out[i]);
     return 0;
   }
+  if (argc > 1 && std::strcmp(argv[1], "filters") == 0) {  // smooth, enhance, measure
+    const mclahe::NdImage g = mclahe::gaussian_filter(req.image, mclahe::GaussianSpec{{1.0, 0.5, 0.0}, 4.0});
+    const mclahe::NdImage m = mclahe::median_filter(g, mclahe::MedianSpec{{3, 1, 2}});
+    const mclahe::MetricsReport r = mclahe::compute_metrics(m, req.image, 64, 1.0);
+    for (std::size_t i = 0; i < m.size(); ++i) std::printf("%.17g\n", m[i]);
+    std::printf("%.17g\n%.17g\n%.17g\n%.17g\n", r.mse, r.psnr_db, r.std, r.entropy_bits);
+    return 0;
+  }
   const mclahe::NdImage out = mclahe::mclahe(req, &t);
   for (std::size_t i = 0; i < out.size(); ++i) std::printf("%.17g\n", out[i]);
   std::fprintf(stderr, "hist %.3g s interp %.3g s\n", t.histograms_s, t.interpolation_s);

@@ -51,3 +51,23 @@ def test_framewise_batched_matches_per_slice_oracle(exe):
     x = (((i * 37) % 101) / 100.0).reshape(24, 20, 16)
     want = np.stack([O.mclahe(x[:, f, :], (8, 4), 32, 0.05, False, "c") for f in range(20)], 1)
     assert np.max(np.abs(got - want)) <= 1e-5
+
+
+@pytest.mark.gpu
+def test_filters_and_metrics_match_reference(exe):
+    from oracle import oracle as O
+    if not O.have_ref():
+        pytest.skip("reference library not built")
+    r = subprocess.run([exe, "filters"], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stderr
+    vals = np.array([float(v) for v in r.stdout.split()])
+    i = np.arange(24 * 20 * 16)
+    x = (((i * 37) % 101) / 100.0).reshape(24, 20, 16)
+    g = O.gaussian_filter_ref(x, (1.0, 0.5, 0.0), 4.0)
+    m = O.median_filter_ref(g, (3, 1, 2))
+    assert np.array_equal(vals[:-4].reshape(x.shape), m)
+    want = O.metrics_ref(m, x, 64, 1.0)
+    got = vals[-4:]
+    assert got[3] == want["entropy_bits"]
+    for k, v in zip(("mse", "psnr_db", "std"), got[:3]):
+        assert abs(v - want[k]) <= 1e-12 * max(1.0, abs(want[k])), k
