@@ -84,7 +84,7 @@ constexpr int kDictHG = 8192;        // global set slots (accepts <= kDictHG / 2
 // value is found with one LDS.128 and four compares (no divergent probe loop).
 constexpr int kDictLgBS = 10;        // K2a per-CTA set: 1024 buckets (16 KB)
 constexpr int kDictHS = 4 << kDictLgBS;
-constexpr int kDictLgHL = 11;        // blend lookup: cuckoo table of 2048 {bits, index}
+constexpr int kDictLgHL = 10;        // blend lookup: 1024 {bits, index} (affine direct table or cuckoo hash)
 constexpr int kDictHL = 1 << kDictLgHL;
 constexpr int kDictKC = 576;         // values per tile row in the blend (capacity)
 constexpr uint32_t kDictEmpty = 0xFFFFFFFFu;  // a NaN pattern: never a finite input
