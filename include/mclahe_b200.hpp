@@ -18,6 +18,7 @@
 #include <cstddef>
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
 
 namespace mclahe {
@@ -119,5 +120,47 @@ double rms_contrast(const NdImage& a);                                  // metri
 double shannon_entropy(const NdImage& a, std::size_t n_bins = 256);     // metrics.hpp:28-30
 MetricsReport compute_metrics(const NdImage& a, const NdImage& b, std::size_t n_bins = 256,
                               double peak = 1.0);                       // metrics.hpp:35-36
+
+// ---- npy.hpp:12-60: array files (host code; NPY v1.0 written, v1.0/v2.0 read) ----
+
+enum class Dtype { f4, f8, u1, u2, i2, i4 };  // all little-endian
+
+std::size_t dtype_item_size(Dtype dtype);
+std::string dtype_descr(Dtype dtype);            // NPY descr string, e.g. "<f4"
+Dtype dtype_from_name(const std::string& name);  // "f4", "f8", "u1", ...
+
+enum class NpyErrc {
+  io_failure,
+  bad_magic,
+  unsupported_version,
+  bad_header,
+  unsupported_dtype,
+  fortran_order,
+  truncated_payload,
+  size_mismatch,
+  value_out_of_range,
+};
+
+class NpyError : public std::runtime_error {
+ public:
+  NpyError(NpyErrc code, const std::string& message) : std::runtime_error(message), code_(code) {}
+  NpyErrc code() const noexcept { return code_; }
+
+ private:
+  NpyErrc code_;
+};
+
+struct ArrayFileMeta {
+  Dtype dtype = Dtype::f8;
+  bool fortran_order = false;
+  Shape shape;
+};
+
+// Fortran-ordered files are rejected (NpyErrc::fortran_order), not transposed.
+std::pair<NdImage, ArrayFileMeta> read_npy(const std::string& path);
+// Integer dtypes round to nearest and reject out-of-range values.
+void write_npy(const std::string& path, const NdImage& image, Dtype dtype);
+// Headerless file whose size must equal item_size * product(meta.shape).
+NdImage read_raw(const std::string& path, const ArrayFileMeta& meta);
 
 }  // namespace mclahe

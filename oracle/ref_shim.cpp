@@ -19,6 +19,7 @@
 #include "mclahe/histogram.hpp"
 #include "mclahe/interpolation.hpp"
 #include "mclahe/metrics.hpp"
+#include "mclahe/npy.hpp"
 #include "mclahe/nd_image.hpp"
 #include "mclahe/pipeline.hpp"
 
@@ -223,6 +224,35 @@ int ref_metrics(const double* a, const double* b, int rank, const int64_t* shape
   } catch (const mclahe::ValidationError& e) {
     put_err(err, err_len, e.what());
     return 1;
+  }
+}
+
+// write_npy (npy.hpp:50-53): dtype by name ("f4", ...); 0 ok, else the NpyErrc + 1.
+int ref_write_npy(const char* path, const double* data, int rank, const int64_t* shape,
+                  const char* dtype, char* err, int err_len) {
+  try {
+    mclahe::write_npy(path, make_image(data, rank, shape), mclahe::dtype_from_name(dtype));
+    return 0;
+  } catch (const mclahe::NpyError& e) {
+    put_err(err, err_len, e.what());
+    return static_cast<int>(e.code()) + 1;
+  }
+}
+
+// read_npy (npy.hpp:46-48) into caller buffers (at most max_count values).
+int ref_read_npy(const char* path, double* data, int64_t max_count, int* rank, int64_t* shape,
+                 char* descr, char* err, int err_len) {
+  try {
+    auto [img, meta] = mclahe::read_npy(path);
+    if (static_cast<int64_t>(img.size()) > max_count) return 100;
+    std::memcpy(data, img.values().data(), img.size() * sizeof(double));
+    *rank = static_cast<int>(meta.shape.size());
+    for (size_t i = 0; i < meta.shape.size(); ++i) shape[i] = static_cast<int64_t>(meta.shape[i]);
+    std::strcpy(descr, mclahe::dtype_descr(meta.dtype).c_str());
+    return 0;
+  } catch (const mclahe::NpyError& e) {
+    put_err(err, err_len, e.what());
+    return static_cast<int>(e.code()) + 1;
   }
 }
 
