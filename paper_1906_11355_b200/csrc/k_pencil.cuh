@@ -531,6 +531,7 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
   const int64_t stage_elems = G.stage_stride;
   const int rows = G.stage_rows;
   const int nrb = (rows + 31) >> 5;
+  float ugs[KO], ugt[KO];  // unit geometry (see the stage geometry below)
   int64_t cur = -1;
   uint32_t it = 0;
   while (true) {
@@ -627,27 +628,24 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
       consumers_sync<kConsumersBlend>();
       if (ADAPT) patho = s_bad != 0;
       cur = key;
-    }
-    // stage geometry: factor f_j(x) = x / b + t_j (exact half-integer numerators)
-    float wfix[NCO / (KO >= 2 ? 4 : 2)];
-    float s1, t1, s2 = 0.f, t2 = 0.f;
-    {
-      float ff[KO];
 #pragma unroll
-      for (int j = 0; j < KO; ++j) {
-        const Dim& d = G.d[j];
-        const float sj = G.inv_b[j];
-        const float tj = (float)(2 * d.before - 2 * (int64_t)S.cell[j] * d.b - d.b + 1) * G.inv_2b[j];
-        if (j == KO - 1) {
-          s1 = sj;
-          t1 = tj;
-        } else if (j == KO - 2) {
-          s2 = sj;
-          t2 = tj;
-        } else {
-          ff[j] = fmaf((float)S.x[j], sj, tj);
-        }
+      for (int jd = 0; jd < KO; ++jd) {
+        const Dim& d = G.d[jd];
+        ugs[jd] = G.inv_b[jd];
+        ugt[jd] = (float)(2 * d.before - 2 * (int64_t)S.cell[jd] * d.b - d.b + 1) * G.inv_2b[jd];
       }
+    }
+    // stage geometry: factor f_j(x) = x * s_j + t_j (exact half-integer
+    // numerators); s_j, t_j depend on the unit's cell only (ugs / ugt, set at
+    // the unit change), the stage contributes its coordinates
+    float wfix[NCO / (KO >= 2 ? 4 : 2)];
+    const float s1 = ugs[KO - 1], t1 = ugt[KO - 1];
+    const float s2 = KO >= 2 ? ugs[KO >= 2 ? KO - 2 : 0] : 0.f;
+    const float t2 = KO >= 2 ? ugt[KO >= 2 ? KO - 2 : 0] : 0.f;
+    {
+      float ff[KO > 2 ? KO - 2 : 1];
+#pragma unroll
+      for (int j = 0; j < KO - 2; ++j) ff[j] = fmaf((float)S.x[j], ugs[j], ugt[j]);
       constexpr int NF = NCO / (KO >= 2 ? 4 : 2);
 #pragma unroll
       for (int cf = 0; cf < NF; ++cf) {
