@@ -73,6 +73,7 @@ struct KGeom {
   float inv_b[kMaxRank];   // 1 / b per dim (K4 weight factors)
   float inv_2b[kMaxRank];  // 1 / (2 b)
   int dict;                // 1: the value-dictionary blend is armed (K2a builds the dictionary)
+  int stiles;              // NB blend: trailing tiles staged at once (one segment's window)
 };
 
 // Value dictionary (adaptive mode, float32): when the volume holds few
@@ -396,6 +397,10 @@ __device__ __noinline__ void pipe_produce(const KGeom& G, const CUtensorMap* map
     for (int j = 0; j < KO - 2; ++j) nfix *= B.ext[j];
     const int n1 = B.ext[KO - 1] / R1;
     const int n2 = KO >= 2 ? B.ext[KO - 2] / R2 : 1;
+    // blend (STORE): segments outermost, so a consumer staging per segment
+    // (the n_bins-specialised blend with several segments) restages rarely
+#pragma unroll 1
+    for (int sego = 0; sego < (STORE ? G.nseg : 1); ++sego)
 #pragma unroll 1
     for (int64_t f = 0; f < nfix; ++f) {
       int32_t xf[kMaxOuterDims];
@@ -412,7 +417,8 @@ __device__ __noinline__ void pipe_produce(const KGeom& G, const CUtensorMap* map
 #pragma unroll 1
         for (int i1 = 0; i1 < n1; ++i1) {
 #pragma unroll 1
-        for (int seg = 0; seg < G.nseg; ++seg) {
+        for (int segi = 0; segi < (STORE ? 1 : G.nseg); ++segi) {
+          const int seg = STORE ? sego : segi;
           const int slot = it % nst;
           if (STORE) mbar_wait_spin(&pp.empty[slot], ((it / nst) & 1) ^ 1);  // blend: latency-critical
           else mbar_wait(&pp.empty[slot], ((it / nst) & 1) ^ 1);

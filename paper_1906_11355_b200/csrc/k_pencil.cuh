@@ -468,7 +468,7 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
       reinterpret_cast<uint2*>(P.tail + NCO * gtr * kDictKC * 4);
   int* ofS = reinterpret_cast<int*>(dltS + kDictHL);  // [NCO] window tile of corner co's row
   int* colT = DICT     ? ofS + NCO
-              : NB > 0 ? reinterpret_cast<int*>(P.tail + NCO * gtr * NbBlock::words(NB) * 4)
+              : NB > 0 ? reinterpret_cast<int*>(P.tail + NCO * G.stiles * NbBlock::words(NB) * 4)
                        : reinterpret_cast<int*>(lcS + NCO * gtr);
   float* colW = reinterpret_cast<float*>(colT + ncol);  // [ncol][4][NCT]
   __shared__ int s_bad;
@@ -531,6 +531,7 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
   const int64_t stage_elems = G.stage_stride;
   const int rows = G.stage_rows;
   const int nrb = (rows + 31) >> 5;
+  int seg_lo = 0, seg_cnt = 0;  // NB: staged trailing-tile window
   float ugs[KO], ugt[KO];  // unit geometry (see the stage geometry below)
   int64_t cur = -1;
   uint32_t it = 0;
@@ -539,9 +540,25 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
     mbar_wait_spin(&P.pipe->full[s], (it / G.nst) & 1);
     const Stage& S = P.pipe->st[s];
     if (S.unit < 0) break;
-    const int64_t key = S.key;
+    // NB with several segments stages one segment's trailing tiles at a time
+    constexpr bool SEGW = NB > 0;
+    const int64_t key = SEGW && G.nseg > 1 ? S.key * G.nseg + S.seg : S.key;
     if (key != cur) {
       consumers_sync<kConsumersBlend>();
+      if (SEGW) {  // tile window of this segment: its columns' first tiles + far corner
+        seg_lo = 0;
+        seg_cnt = (int)gtr;
+        if (G.nseg > 1) {
+          int mn = INT_MAX, mx = INT_MIN;
+#pragma unroll 1
+          for (int c = 0; c < 8; ++c) {
+            mn = min(mn, colT[S.seg * 8 + c]);
+            mx = max(mx, colT[S.seg * 8 + c]);
+          }
+          seg_lo = mn;
+          seg_cnt = min((int)gtr - mn, mx + ctoff[NCT - 1] - mn + 1);
+        }
+      }
       if (tid == 0) s_bad = 0;
       if (!ADAPT && cur < 0)
         for (int k = tid; k < n1; k += kConsumersBlend) thrS[k] = W.thr[k];
@@ -569,23 +586,39 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
           continue;
         }
         if constexpr (NB > 0) {
+          if (co + 1 < NCO) continue;  // all corner rows at once, after the last corner
+          // one pass over (tile, entry) with the NCO corners' loads independent
+          // (in flight together): edge tables, LUTs, then {lo, c}
           constexpr int TBW = NbBlock::words(NB);
           constexpr int PT = NbBlock::th_words(NB), PL = NbBlock::lut_words(NB);
-          float* blk = reinterpret_cast<float*>(P.tail) + co * TBW;  // + t * NCO * TBW
-          const float* ls = W.lut + of * NB;
-          for (int64_t k = tid; k < gtr * PL; k += kConsumersBlend) {
-            const int t = (int)(k / PL), q = (int)(k - (int64_t)t * PL);
-            blk[t * NCO * TBW + NbBlock::lut_off(NB) + q] = __ldg(ls + t * NB + NbBlock::src(q));
+          int64_t ofc[NCO];
+#pragma unroll
+          for (int c2 = 0; c2 < NCO; ++c2) {
+            int64_t o2 = (S.cell[0] + ((c2 >> (KO - 1)) & 1) - G.trow0) * G.tstride[0];
+            for (int j = 1; j < KO; ++j) o2 += (S.cell[j] + ((c2 >> (KO - 1 - j)) & 1)) * G.tstride[j];
+            ofc[c2] = o2 + seg_lo;  // first staged trailing tile of corner row c2
           }
-          const float* ts = W.thr + of * (NB + 1);
-          for (int64_t k = tid; k < gtr * PT; k += kConsumersBlend) {
-            const int t = (int)(k / PT), q = (int)(k - (int64_t)t * PT);
-            blk[t * NCO * TBW + NbBlock::th_off(NB) + q] =
-                __ldg(ts + t * (NB + 1) + NbBlock::src(q));
+          float* blk = reinterpret_cast<float*>(P.tail);
+          for (int k = tid; k < seg_cnt * PL; k += kConsumersBlend) {
+            const int t = k / PL, q = k - t * PL;
+            float v[NCO];
+#pragma unroll
+            for (int c2 = 0; c2 < NCO; ++c2) v[c2] = __ldg(W.lut + (ofc[c2] + t) * NB + NbBlock::src(q));
+#pragma unroll
+            for (int c2 = 0; c2 < NCO; ++c2) blk[(t * NCO + c2) * TBW + NbBlock::lut_off(NB) + q] = v[c2];
           }
-          for (int64_t t = tid; t < gtr; t += kConsumersBlend) {
-            const float2 lc = tile_lc(tparams[of + t]);
-            *reinterpret_cast<float2*>(blk + t * NCO * TBW) = lc;
+          for (int k = tid; k < seg_cnt * PT; k += kConsumersBlend) {
+            const int t = k / PT, q = k - t * PT;
+            float v[NCO];
+#pragma unroll
+            for (int c2 = 0; c2 < NCO; ++c2) v[c2] = __ldg(W.thr + (ofc[c2] + t) * (NB + 1) + NbBlock::src(q));
+#pragma unroll
+            for (int c2 = 0; c2 < NCO; ++c2) blk[(t * NCO + c2) * TBW + NbBlock::th_off(NB) + q] = v[c2];
+          }
+          for (int k = tid; k < seg_cnt * NCO; k += kConsumersBlend) {
+            const int t = k / NCO, c2 = k - t * NCO;
+            const float2 lc = tile_lc(tparams[ofc[c2] + t]);
+            *reinterpret_cast<float2*>(blk + (t * NCO + c2) * TBW) = lc;
             if (isnan(lc.y)) s_bad = 1;
           }
           continue;
@@ -771,7 +804,7 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
           constexpr int TB = NbBlock::words(NB) * 4;
           const char* blkc = reinterpret_cast<const char*>(P.tail);
           const char* base[KT];
-          base[0] = blkc + tt * (NCO * TB);
+          base[0] = blkc + (tt - seg_lo) * (NCO * TB);
           if (KT == 2) base[KT - 1] = base[0] + ctoff[KT == 2 ? 2 : 0] * (NCO * TB);
           uint32_t sbase[KT];
 #pragma unroll

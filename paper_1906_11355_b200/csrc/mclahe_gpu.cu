@@ -108,6 +108,7 @@ struct Pencil {
   int64_t tail = 0;               // kernel-specific shared memory (hist / LUTs)
   int64_t stage_budget = 0;
   int64_t smem = 0;
+  bool hist_family = false;
 };
 
 constexpr int64_t kPipeBytes = (sizeof(mg::Pipe) + 1023) & ~int64_t(1023);
@@ -158,6 +159,8 @@ struct mclahe_plan_s {
 
 namespace {
 
+int64_t nb_seg_tiles(const mclahe_plan_s& pl, const Pencil& c);
+
 KGeom pencil_geom(const mclahe_plan_s& pl, const Pencil& pc) {
   KGeom G = pl.G;
   G.kt = pc.kt;
@@ -174,6 +177,7 @@ KGeom pencil_geom(const mclahe_plan_s& pl, const Pencil& pc) {
   G.nseg = pc.nseg;
   G.stage_stride = pc.stage_stride;
   G.dict = pl.dict_cap > 0 ? 1 : 0;
+  G.stiles = (int)(pc.kt > 0 && !pc.hist_family ? nb_seg_tiles(pl, pc) : pc.gtr);
   for (int j = 0; j < G.rank; ++j) {
     G.inv_b[j] = 1.0f / (float)G.d[j].b;
     G.inv_2b[j] = 1.0f / (float)(2 * G.d[j].b);
@@ -187,6 +191,42 @@ bool trailing_merged(const Dim& d) {
   for (int64_t x = std::max<int64_t>(0, d.s - d.after); x < d.s; ++x)
     if ((d.before + 2 * d.s - 1 - x) / d.b != (x + d.before) / d.b) return false;
   return true;
+}
+
+bool nb_specialised(int64_t n) {
+  static const bool no_nb = getenv("MCLAHE_NO_NB") != nullptr;
+  return !no_nb && (n == 128 || n == 256);
+}
+
+// Trailing tiles the NB blend stages at once: all of them for one segment
+// (32 floats of the trailing block; nseg == 1: every trailing tile), i.e.
+// the span of the segment's columns' first tiles plus the far corner.
+int64_t nb_seg_tiles(const mclahe_plan_s& pl, const Pencil& c) {
+  const int D = pl.p.rank;
+  if (c.nseg <= 1) return c.gtr;
+  int64_t ts[kMaxRank], corner = 0;
+  int64_t st = 1;
+  for (int j = D - 1; j >= D - c.kt; --j) {
+    ts[j] = st;
+    corner += st;
+    st *= pl.d[j].g;
+  }
+  int64_t best = 0;
+  for (int seg = 0; seg < c.nseg; ++seg) {
+    int64_t lo = INT64_MAX, hi = INT64_MIN;
+    for (int k = 0; k < 8; ++k) {
+      int64_t e = (int64_t)(seg * 8 + k) * 4, t = 0;
+      for (int j = D - 1; j >= D - c.kt; --j) {
+        const int64_t x = e % pl.d[j].s;
+        e /= pl.d[j].s;
+        t += cell_of(pl.d[j], x) * ts[j];
+      }
+      lo = std::min(lo, t);
+      hi = std::max(hi, t);
+    }
+    best = std::max(best, hi + corner - lo + 1);
+  }
+  return std::min(best, c.gtr);
 }
 
 // Chooses how many trailing dims one pencil covers for a kernel family
@@ -219,6 +259,7 @@ Pencil choose_pencil(const mclahe_plan_s& pl, bool for_hist) {
     if (c.tma_rank > 5) continue;
     c.tpr = (int)(c.P / 4);
     c.rpi = 256 / c.tpr;
+    c.hist_family = for_hist;
     if (for_hist) {
       if (!merged) continue;
       if (c.gtr * n >= (int64_t{1} << 31) / 2) continue;
@@ -246,10 +287,12 @@ Pencil choose_pencil(const mclahe_plan_s& pl, bool for_hist) {
       const int64_t pairs = (int64_t{1} << ko) * (c.gtr - 1) * (n + 1) * 2;  // global, KT == 1
       c.tail = align_up((pl.p.adaptive ? 2 * luts1 : (kt == 1 ? pairs : luts1) + n + 1) * 4, 16) +
                (int64_t{1} << ko) * c.gtr * 16 + (c.P / 4) * (4 + 16 * (int64_t{1} << kt));
-      if (pl.p.adaptive)  // NB-specialised kernel: padded per-tile blocks (NbBlock)
-        c.tail = std::max<int64_t>(
-            c.tail, (int64_t{1} << ko) * c.gtr * NbBlock::words((int)n) * 4 +
-                        (c.P / 4) * (4 + 16 * (int64_t{1} << kt)));
+      if (pl.p.adaptive && nb_specialised(n)) {
+        // NB-specialised kernel (the only adaptive blend launched): padded
+        // per-tile blocks (NbBlock) for the trailing tiles of one segment
+        c.tail = (int64_t{1} << ko) * nb_seg_tiles(pl, c) * NbBlock::words((int)n) * 4 +
+                 (c.P / 4) * (4 + 16 * (int64_t{1} << kt));
+      }
       c.rpi = kConsumersBlend / c.tpr;
       const int64_t avail = 226 * 1024 - kPipeBytes - c.tail;
       if (avail >= 4 * 4096) c.stage_budget = std::min<int64_t>(kStageBytes, avail / 4);
@@ -602,8 +645,7 @@ RangeFn range_fn(int ko, bool dict) { return get_range_pencil(ko, dict); }
 HistFn hist_fn(int ko, bool a) { return get_hist_pencil(ko, a); }
 // MCLAHE_NO_NB=1 forces the runtime-n_bins blend kernel (A/B measurements).
 InterpFn interp_fn(int ko, int kt, bool a, int64_t n_bins) {
-  static const bool no_nb = getenv("MCLAHE_NO_NB") != nullptr;
-  return get_interp_pencil(ko, kt, a, no_nb ? 0 : (int)n_bins);
+  return get_interp_pencil(ko, kt, a, nb_specialised(n_bins) ? (int)n_bins : 0);
 }
 
 WS ws_view(const mclahe_plan_s* pl, void* ws) {
