@@ -537,7 +537,7 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
   uint32_t it = 0;
   while (true) {
     const int s = it % G.nst;
-    mbar_wait_spin(&P.pipe->full[s], (it / G.nst) & 1);
+    mbar_wait(&P.pipe->full[s], (it / G.nst) & 1);
     const Stage& S = P.pipe->st[s];
     if (S.unit < 0) break;
     // NB with several segments stages one segment's trailing tiles at a time
