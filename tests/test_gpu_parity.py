@@ -452,3 +452,42 @@ def test_framewise_renormalized_and_4d(M, ad):
         out = M.mclahe_framewise(x, 0, M.KernelSpec(kernel), params, renormalize_slices=renorm)
         want = _framewise_oracle(x, 0, kernel, 32, 0.1, ad, renorm)
         assert np.max(np.abs(out.astype(np.float64) - want)) <= OUT_TOL, renorm
+
+
+@pytest.mark.parametrize("rank", [6, 7, 8])
+@pytest.mark.parametrize("ad", [False, True])
+def test_high_rank_vs_oracle(M, rank, ad):
+    # the reference accepts rank <= 8 (nd_image.cpp:52-58): generic kernels
+    rng = np.random.default_rng(90 + rank)
+    shape = tuple(int(v) for v in rng.integers(2, 5, rank))
+    kernel = tuple(int(rng.integers(1, s + 1)) for s in shape)
+    x = (np.round(rng.random(shape) * 20) / 20).astype(np.float32)
+    st, _ = gpu_stats(M, x, kernel, 16, 0.2, ad)
+    assert_stats_equal(st, O.tile_stats(x, kernel, 16, 0.2, ad, "c"), f"rank {rank}")
+    out = M.enhance(x, kernel, 16, 0.2, ad)
+    assert np.max(np.abs(out.astype(np.float64) - O.mclahe(x, kernel, 16, 0.2, ad, "c"))) <= OUT_TOL
+
+
+def test_large_n_bins_and_concurrent_host_calls(M):
+    # n_bins up to the GPU limit through the pencil path, and the one-shot C
+    # entry called from several host threads at once (its state is locked)
+    import threading
+    rng = np.random.default_rng(17)
+    x = rng.random((48, 40, 32)).astype(np.float32)
+    for nb, ad in ((4096, True), (16384, False)):
+        out = M.enhance(x, (16, 8, 8), nb, 0.5, ad)
+        assert np.max(np.abs(out.astype(np.float64) - O.mclahe(x, (16, 8, 8), nb, 0.5, ad, "c"))) <= OUT_TOL
+    want = M.enhance(x, (12, 10, 8), 64, 0.05, True)
+    res, errs = [None] * 6, []
+
+    def work(i):
+        try:
+            res[i] = M.enhance(x, (12, 10, 8), 64, 0.05, True)
+        except Exception as e:  # noqa: BLE001
+            errs.append(e)
+    th = [threading.Thread(target=work, args=(i,)) for i in range(6)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs and all(np.array_equal(r, want) for r in res)
