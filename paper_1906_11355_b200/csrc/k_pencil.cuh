@@ -194,6 +194,32 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
 }
 
 // --------------------------------------------------------------- K2b -----
+// Unit switch helpers: the CTA's [gtr][n + 1] shared histogram added into the
+// workspace counts (no index division; nonzero bins only), and a row copy
+// with four loads in flight per thread.
+__device__ __forceinline__ void hist_flush(const uint32_t* hist, uint32_t* dst, int gtr, int n,
+                                           int tid) {
+  for (int t = 0; t < gtr; ++t)
+    for (int b = tid; b < n; b += kConsumers) {
+      const uint32_t c = hist[t * (n + 1) + b];
+      if (c) atomicAdd(dst + (int64_t)t * n + b, c);
+    }
+}
+
+__device__ __forceinline__ void copy_rows(float* dst, const float* __restrict__ src, int count,
+                                          int tid) {
+  int k = tid;
+  for (; k + 3 * kConsumers < count; k += 4 * kConsumers) {
+    const float a = __ldg(src + k), b = __ldg(src + k + kConsumers),
+                c = __ldg(src + k + 2 * kConsumers), d = __ldg(src + k + 3 * kConsumers);
+    dst[k] = a;
+    dst[k + kConsumers] = b;
+    dst[k + 2 * kConsumers] = c;
+    dst[k + 3 * kConsumers] = d;
+  }
+  for (; k < count; k += kConsumers) dst[k] = __ldg(src + k);
+}
+
 // A voxel's multiplicity in a tile is the product of its per-dimension
 // multiplicities, so counting the support box with those weights equals
 // kernelize + compute_histogram while reading each input byte once.  A
@@ -255,11 +281,7 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
       consumers_sync();
       if (tid == 0) s_bad = 0;
       if (cur >= 0) {
-        uint32_t* dst = W.counts + cur * n;
-        for (int64_t k = tid; k < G.gtr * n; k += kConsumers) {
-          const uint32_t c = hist[k + k / n];
-          if (c) atomicAdd(dst + k, c);
-        }
+        hist_flush(hist, W.counts + cur * n, (int)G.gtr, n, tid);
       }
       consumers_sync();
       for (int64_t k = tid; k < G.gtr * (n + 1); k += kConsumers) hist[k] = 0;
@@ -269,7 +291,7 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
           lcS[t] = lc;
           if (isnan(lc.y)) s_bad = 1;
         }
-        for (int64_t k = tid; k < G.gtr * n1; k += kConsumers) thrS[k] = W.thr[key * n1 + k];
+        copy_rows(thrS, W.thr + key * n1, (int)(G.gtr * n1), tid);
       } else if (cur < 0) {
         for (int k = tid; k < n1; k += kConsumers) thrS[k] = W.thr[k];
       }
@@ -390,11 +412,7 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
   }
   consumers_sync();
   if (cur >= 0) {
-    uint32_t* dst = W.counts + cur * n;
-    for (int64_t k = tid; k < G.gtr * n; k += kConsumers) {
-      const uint32_t c = hist[k + k / n];
-      if (c) atomicAdd(dst + k, c);
-    }
+    hist_flush(hist, W.counts + cur * n, (int)G.gtr, n, tid);
   }
 }
 
