@@ -488,7 +488,8 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
   int* colT = DICT     ? ofS + NCO
               : NB > 0 ? reinterpret_cast<int*>(P.tail + NCO * G.stiles * NbBlock::words(NB) * 4)
                        : reinterpret_cast<int*>(lcS + NCO * gtr);
-  float* colW = reinterpret_cast<float*>(colT + ncol);  // [ncol][4][NCT]
+  colT = reinterpret_cast<int*>((reinterpret_cast<uintptr_t>(colT) + 15) & ~uintptr_t(15));
+  float* colW = reinterpret_cast<float*>(colT + ncol);  // [ncol][4][NCT], 16-byte aligned
   __shared__ int s_bad;
   __shared__ int s_dmode;  // DICT: 1 = affine lookup
   __shared__ float s_dv0, s_dS;
@@ -715,11 +716,14 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
       if (q < rows) {
         const int col = seg * 8 + c;
         const int tt = colT[col];
-        float tw[4][NCT];
+        float tw[4][NCT];  // 4 * NCT consecutive floats (16-byte aligned): LDS.128s
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+        for (int h = 0; h < NCT; ++h) {
+          const float4 w4 = reinterpret_cast<const float4*>(colW + col * 4 * NCT)[h];
+          const float wv[4] = {w4.x, w4.y, w4.z, w4.w};
 #pragma unroll
-          for (int ct = 0; ct < NCT; ++ct) tw[i][ct] = colW[(col * 4 + i) * NCT + ct];
+          for (int e = 0; e < 4; ++e) tw[(4 * h + e) / NCT][(4 * h + e) % NCT] = wv[e];
+        }
         const int r1 = q & (G.r1 - 1), r2 = q >> G.lg_r1;
         const int x1 = xb1 + r1, x2 = xb2 + r2;
         const float f1 = fmaf((float)x1, s1, t1);

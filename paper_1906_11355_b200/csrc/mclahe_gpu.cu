@@ -287,11 +287,12 @@ Pencil choose_pencil(const mclahe_plan_s& pl, bool for_hist) {
       const int64_t pairs = (int64_t{1} << ko) * (c.gtr - 1) * (n + 1) * 2;  // global, KT == 1
       c.tail = align_up((pl.p.adaptive ? 2 * luts1 : (kt == 1 ? pairs : luts1) + n + 1) * 4, 16) +
                (int64_t{1} << ko) * c.gtr * 16 + (c.P / 4) * (4 + 16 * (int64_t{1} << kt));
+      c.tail += 16;  // column tables start 16-byte aligned
       if (pl.p.adaptive && nb_specialised(n)) {
         // NB-specialised kernel (the only adaptive blend launched): padded
         // per-tile blocks (NbBlock) for the trailing tiles of one segment
         c.tail = (int64_t{1} << ko) * nb_seg_tiles(pl, c) * NbBlock::words((int)n) * 4 +
-                 (c.P / 4) * (4 + 16 * (int64_t{1} << kt));
+                 (c.P / 4) * (4 + 16 * (int64_t{1} << kt)) + 16;
       }
       c.rpi = kConsumersBlend / c.tpr;
       const int64_t avail = 226 * 1024 - kPipeBytes - c.tail;
@@ -394,7 +395,7 @@ void plan_dict(mclahe_plan_s* pl) {
   if (!pl->p.adaptive || !pl->f32() || !c.on || !pl->hist.on || getenv("MCLAHE_NO_DICT")) return;
   const int64_t nco = int64_t{1} << c.ko, nct = int64_t{1} << c.kt;
   const int64_t tail =  // value blocks + cuckoo table + corner rows + column tables
-      nco * c.gtr * kDictKC * 4 + kDictHL * 8 + nco * 4 + (c.P / 4) * (4 + 16 * nct);
+      nco * c.gtr * kDictKC * 4 + kDictHL * 8 + nco * 4 + (c.P / 4) * (4 + 16 * nct) + 16;
   const int64_t stage = c.stage_stride * 4;
   const int64_t nst = std::min<int64_t>(4, (226 * 1024 - kPipeBytes - tail) / stage);
   if (nst < 2) return;
