@@ -82,7 +82,7 @@ typedef struct {
   int64_t tiles_per_row;  /* prod_{j>=1} grid[j] */
   int64_t n_bins;
   /* workspace byte offsets */
-  int64_t off_range;      /* int64[4]: ~key(lo), key(hi), nonfinite, 0 (MAX-reducible) */
+  int64_t off_range;      /* int64[4]: ~key(lo), key(hi), nonfinite, blend unit counter (MAX-reducible) */
   int64_t off_tile_range; /* int64[window tiles][2]: ~key(lo), key(hi)   (MAX-reducible) */
   int64_t off_counts;     /* int32[window tiles][n_bins]                 (SUM-reducible) */
   int64_t off_tparams;    /* per-tile binning parameters */

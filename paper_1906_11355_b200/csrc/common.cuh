@@ -74,6 +74,7 @@ struct KGeom {
   float inv_2b[kMaxRank];  // 1 / (2 b)
   int dict;                // 1: the value-dictionary blend is armed (K2a builds the dictionary)
   int stiles;              // NB blend: trailing tiles staged at once (one segment's window)
+  int dyn_units;           // blend: > 0 = units handed out dynamically (count), via W.range[3]
 };
 
 // Value dictionary (adaptive mode, float32): when the volume holds few
@@ -356,15 +357,19 @@ template <int KO, bool CELLS, bool WEIGHTS = !CELLS, bool STORE = false>
 __device__ __noinline__ void pipe_produce(const KGeom& G, const CUtensorMap* map,
                                           const int32_t* __restrict__ units, int u0, int u1,
                                           Pipe& pp, float* bufs,
-                                          const CUtensorMap* out_map = nullptr) {
+                                          const CUtensorMap* out_map = nullptr,
+                                          unsigned long long* dyn = nullptr) {
   const int nst = G.nst;
   const int64_t stage_elems = G.stage_stride;
   const uint32_t box_bytes = (uint32_t)((int64_t)G.stage_rows * (G.P / G.nseg) * 4);
   const int R1 = G.r1, R2 = G.r2;
   ProdBox& B = pp.box;
   uint32_t it = 0;
+  // dyn != nullptr: units are handed out dynamically (one atomic per unit,
+  // [u0, u1) is then the whole list); otherwise the CTA's static range
+  int u = dyn ? u0 + (int)atomicAdd(dyn, 1ULL) : u0;
 #pragma unroll 1
-  for (int u = u0; u < u1; ++u) {
+  for (; u < u1; u = dyn ? u0 + (int)atomicAdd(dyn, 1ULL) : u + 1) {
     const int32_t* U = units + (int64_t)u * kUnitInts;
     int64_t key = 0;
     B.a[0] = U[8];

@@ -498,7 +498,9 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
   const int u0 = cta_units[blockIdx.x], u1 = cta_units[blockIdx.x + 1];
   if (threadIdx.x >= kConsumersBlend) {
     if (threadIdx.x == kConsumersBlend)
-      pipe_produce<KO, true, false, true>(G, &tmap, units, u0, u1, *P.pipe, P.bufs, &omap);
+      pipe_produce<KO, true, false, true>(
+          G, &tmap, units, G.dyn_units ? 0 : u0, G.dyn_units ? G.dyn_units : u1, *P.pipe, P.bufs,
+          &omap, G.dyn_units ? reinterpret_cast<unsigned long long*>(&W.range[3]) : nullptr);
     return;
   }
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;

@@ -921,7 +921,15 @@ int do_interp(mclahe_plan_s* pl, const void* in, void* out, void* ws, cudaStream
   WS W = ws_view(pl, ws);
   const bool A = pl->p.adaptive != 0;
   if (pl->interp.on) {
-    const KGeom G = pencil_geom(*pl, pl->interp);
+    KGeom G = pencil_geom(*pl, pl->interp);
+    // Large volumes hand units out dynamically (one atomic per unit): corner
+    // tables and tile shapes make per-unit cost uneven, and a static split left
+    // some SMs 30% idle at the tail. Below ~64M voxels the memset + atomics
+    // cost more than the imbalance (3D config: 0.063 -> 0.068 ms), so the
+    // balanced static split stays. MCLAHE_STATIC_UNITS forces static.
+    static const bool static_units = getenv("MCLAHE_STATIC_UNITS") != nullptr;
+    G.dyn_units = (static_units || pl->G.local_voxels < (int64_t{1} << 26)) ? 0 : (int)pl->interp_vox.size();
+    if (G.dyn_units) MG_CUDA(cudaMemsetAsync(W.range + 3, 0, sizeof(int64_t), st));
     InterpFn f = interp_fn(pl->interp.ko, pl->interp.kt, A, pl->p.n_bins);
     int rc = tensor_map(pl, 1, in);
     if (rc) return rc;
