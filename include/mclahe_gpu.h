@@ -189,7 +189,8 @@ int mclahe_plan_dict_state(mclahe_plan_t plan, const void* workspace, int32_t* s
 
 /* The pencil kernels' packed f32x2 binning on n device float32 values (pairs
  * of consecutive values): variant 1 = the histogram routine, 2 = the blend
- * gather (through an identity LUT).  Must equal mclahe_debug_bin_index. */
+ * gather (through an identity LUT), 3 = the bracketed floors of the
+ * n_bins-specialised adaptive blend.  Must equal mclahe_debug_bin_index. */
 int mclahe_debug_bin_index_packed(const float* values_dev, int64_t n, double lo, double hi,
                                   int64_t n_bins, int32_t variant, int32_t* out_dev,
                                   void* stream);

@@ -470,8 +470,8 @@ def enhance(image, kernel_size, n_bins: int = 256, clip_limit: float = 1.0,
 def bin_index_device(values, lo: float, hi: float, n_bins: int, variant: int = 0):
     """bin_index (src/histogram.cpp:24-32) of a CUDA tensor through the kernels'
     binning; int32 result (-1 for a degenerate range).  variant 0: the generic
-    kernels' guarded routine (f32 or f64); 1 / 2: the pencil kernels' packed
-    histogram / blend-gather routines (float32 only)."""
+    kernels' guarded routine (f32 or f64); 1 / 2 / 3: the pencil kernels' packed
+    histogram / blend-gather / bracketed-floor (NB blend) routines (float32 only)."""
     import torch
     v = values.contiguous()
     out = torch.empty(v.shape, dtype=torch.int32, device=v.device)

@@ -276,6 +276,62 @@ __device__ __forceinline__ float edge_gather(uint32_t base, int k, float v) {
   return m;
 }
 
+// ---- bracketed floor (the NB blend's fast path) ----------------------------
+// With d = fl32(v - lo) and c = fl32(n / (hi - lo)), the exact product d * c
+// is within a factor (1 +- 2^-23 (1 + 2^-20)) of the reference's f64 value q
+// (two f32 roundings; the f64 ones are ~2^-51).  c_lo = RD(c (1 - 2^-22)) and
+// c_hi = RU(c (1 + 2^-22)) therefore bracket q:  d c_lo <= q <= d c_hi for
+// d >= 0 (reversed for d < 0).  fma.rm(d, c, M) = floor(d c) + M exactly
+// (one rounding, |d c| < 2^22), so when the two floors agree they ARE
+// floor(q), no edge table needed; when they differ (q within ~5e-7 |q| of an
+// integer) the bin is k or k - 1 with k the upper one and the edge table
+// decides.  Out-of-range products clamp on the raw bits (clamp_bits).
+constexpr float kWinLo = 0.99999976158142089844f;  // 1 - 2^-22
+constexpr float kWinHi = 1.00000023841857910156f;  // 1 + 2^-22
+
+__device__ __forceinline__ float2 bin_window(float c) {
+  return make_float2(__fmul_rd(c, kWinLo), __fmul_ru(c, kWinHi));
+}
+
+__device__ __forceinline__ u64 fma_rm2(u64 a, u64 b, u64 c) {
+  u64 d;
+  asm("fma.rm.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+
+// LUT entry at shared byte address lbase + 4 * bits + OFF (one IMAD + one
+// LDS [reg + imm]; lbase already carries -4 * kMagicBits, mod 2^32).
+template <int OFF>
+__device__ __forceinline__ float lut_at(uint32_t lbase, int bits) {
+  float m;
+  asm volatile(
+      "{\n\t.reg .u32 a;\n\tmad.lo.u32 a, %1, 4, %2;\n\tld.shared.f32 %0, [a+%3];\n\t}"
+      : "=f"(m)
+      : "r"(bits), "r"(lbase), "n"(OFF));
+  return m;
+}
+
+// Bins of two voxels by the bracketed floors, as the NB blend computes them
+// (fast answer clamp(floor(d c_lo)); where the clamped floors disagree, the
+// edge table th (unpadded here) decides between them).  w = bin_window(c).
+__device__ __forceinline__ void bins2_bracket(u64 V, float v0, float v1, float lo, float2 w,
+                                              const float* th, int n, int& b0, int& b1) {
+  const u64 d = sub2(V, pk2(lo, lo));
+  const u64 M2 = pk2(kMagic, kMagic);
+  float a[2], b[2];
+  upk2(fma_rm2(d, pk2(w.x, w.x), M2), a[0], a[1]);
+  upk2(fma_rm2(d, pk2(w.y, w.y), M2), b[0], b[1]);
+  const float vv[2] = {v0, v1};
+  int r[2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int ka = clamp_bits(a[i], n - 1), kb = clamp_bits(b[i], n - 1);
+    r[i] = (ka != kb && vv[i] >= th[kb]) ? kb : ka;
+  }
+  b0 = r[0];
+  b1 = r[1];
+}
+
 // Reference bin of v given k = rint(y) clamped to [0, n] (clamp_bits_k) and
 // the tile's edge table at shared address th: k if v >= th[k], else k - 1.
 __device__ __forceinline__ int edge_bin(uint32_t th, int k, float v) {

@@ -164,18 +164,19 @@ MG_HD int64_t twice_dlo(const Dim& d, int64_t x, int64_t c) {
   return 2 * (x + d.before) - 2 * c * d.b - d.b + 1;
 }
 
-// Blend tile block of the NB-specialised K4 kernel (k_pencil.cuh): {lo, c},
-// then the edge table and the LUT, each with one pad word after every 32
-// entries (entry j at j + j/32) so quantised data whose bins are multiples of
-// 32 apart do not pile into one shared-memory bank; a LUT pad repeats the
-// entry before it, so "address - 4" is always bin k - 1.
+// Blend tile block of the NB-specialised K4 kernel (k_pencil.cuh):
+// {lo, c_lo, c_hi, c} (one LDS.128; c_lo / c_hi bracket c, see
+// binning.cuh: bin_window), the edge table with one pad word after every 32
+// entries (entry j at j + j/32, a pad repeats the entry before it), then the
+// LUT unpadded (the blend's fast path addresses it straight from the floor
+// bits).  Blocks are 16-byte aligned.
 struct NbBlock {
   static constexpr MG_HD int pad(int j) { return j + (j >> 5); }
   static constexpr MG_HD int th_words(int n) { return pad(n) + 1; }
-  static constexpr MG_HD int lut_words(int n) { return pad(n); }
-  static constexpr MG_HD int th_off(int) { return 2; }
-  static constexpr MG_HD int lut_off(int n) { return 2 + th_words(n); }
-  static constexpr MG_HD int words(int n) { return (lut_off(n) + lut_words(n) + 1) & ~1; }
+  static constexpr MG_HD int lut_words(int n) { return n; }
+  static constexpr MG_HD int th_off(int) { return 4; }
+  static constexpr MG_HD int lut_off(int n) { return 4 + th_words(n); }
+  static constexpr MG_HD int words(int n) { return (lut_off(n) + lut_words(n) + 3) & ~3; }
   // table entry stored at padded position q (pads repeat the entry before)
   static constexpr MG_HD int src(int q) { return 32 * (q / 33) + (q % 33 < 31 ? q % 33 : 31); }
 };

@@ -544,7 +544,7 @@ __global__ void k_debug_bins(const T* __restrict__ v, int64_t count, double lo, 
 }
 
 // The pencil kernels' packed binning (bins2_edge: histograms; lut2_edge:
-// blend gathers, here through an identity LUT) on arbitrary values against
+// blend gathers, here through an identity LUT; bins2_bracket: the NB blend) on arbitrary values against
 // one range, pairs of consecutive values per thread.
 __global__ void k_debug_bins_packed(const float* __restrict__ v, int64_t count, double lo,
                                     double hi, int n, const float* thr, const float* lut,
@@ -562,6 +562,14 @@ __global__ void k_debug_bins_packed(const float* __restrict__ v, int64_t count, 
       b1 = bin_search(v1, thr, n);
     } else if (variant == 1) {
       bins2_edge(pk2(v0, v1), v0, v1, lc, thr, n, b0, b1);
+    } else if (variant == 3) {
+      const float2 w = bin_window(lc.y);
+      if (w.y < INFINITY) {
+        bins2_bracket(pk2(v0, v1), v0, v1, lc.x, w, thr, n, b0, b1);
+      } else {
+        b0 = bin_search(v0, thr, n);
+        b1 = bin_search(v1, thr, n);
+      }
     } else {
       float m0, m1;
       lut2_edge(pk2(v0, v1), v0, v1, lc, reinterpret_cast<const char*>(thr),

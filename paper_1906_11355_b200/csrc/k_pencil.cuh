@@ -425,6 +425,20 @@ static __device__ __noinline__ float lut_value_global(const WS& W, int n, int64_
   return W.lut[tile * n + b];
 }
 
+// a[i] for a runtime i without local memory (N small)
+// (selp in inline PTX: a plain select chain is turned back into an indexed
+// local-memory load)
+template <int N>
+__device__ __forceinline__ float pick(const float (&a)[N], int i) {
+  float r = a[0];
+#pragma unroll
+  for (int k = 1; k < N; ++k)
+    asm("{\n\t.reg .pred p;\n\tsetp.eq.s32 p, %2, %3;\n\tselp.f32 %0, %1, %0, p;\n\t}"
+        : "+f"(r)
+        : "f"(a[k]), "r"(i), "r"(k));
+  return r;
+}
+
 // ---------------------------------------------------------------- K4 -----
 // One cell pencil (2^KO outer corners x every trailing tile) per unit; its
 // LUTs, edge tables and {lo, c} pairs are staged in shared memory (rows padded
@@ -493,8 +507,16 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
   __shared__ int s_bad;
   __shared__ int s_dmode;  // DICT: 1 = affine lookup
   __shared__ float s_dv0, s_dS;
+  // 4 * kMagicBits through shared memory: kept opaque to ptxas so the NB fast
+  // path's gather address stays one IMAD off a per-item base
+  __shared__ uint32_t s_mb4;
+  if (threadIdx.x == 0) s_mb4 = 4u * (uint32_t)kMagicBits;
   pipe_init(*P.pipe, G.nst, NW);
   __syncthreads();
+  uint32_t mb4;
+  asm volatile("ld.volatile.shared.u32 %0, [%1];"
+               : "=r"(mb4)
+               : "r"((uint32_t)__cvta_generic_to_shared(&s_mb4)));
   const int u0 = cta_units[blockIdx.x], u1 = cta_units[blockIdx.x + 1];
   if (threadIdx.x >= kConsumersBlend) {
     if (threadIdx.x == kConsumersBlend)
@@ -624,7 +646,7 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
             const int t = k / PL, q = k - t * PL;
             float v[NCO];
 #pragma unroll
-            for (int c2 = 0; c2 < NCO; ++c2) v[c2] = __ldg(W.lut + (ofc[c2] + t) * NB + NbBlock::src(q));
+            for (int c2 = 0; c2 < NCO; ++c2) v[c2] = __ldg(W.lut + (ofc[c2] + t) * NB + q);
 #pragma unroll
             for (int c2 = 0; c2 < NCO; ++c2) blk[(t * NCO + c2) * TBW + NbBlock::lut_off(NB) + q] = v[c2];
           }
@@ -638,8 +660,10 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
           }
           for (int k = tid; k < seg_cnt * NCO; k += kConsumersBlend) {
             const int t = k / NCO, c2 = k - t * NCO;
-            const float2 lc = tile_lc(tparams[ofc[c2] + t]);
-            *reinterpret_cast<float2*>(blk + (t * NCO + c2) * TBW) = lc;
+            float2 lc = tile_lc(tparams[ofc[c2] + t]);
+            const float2 wn = bin_window(lc.y);
+            if (!(wn.y < INFINITY)) lc.y = __int_as_float(0x7fc00000);  // c_hi overflows: exact path
+            *reinterpret_cast<float4*>(blk + (t * NCO + c2) * TBW) = make_float4(lc.x, wn.x, wn.y, lc.y);
             if (isnan(lc.y)) s_bad = 1;
           }
           continue;
@@ -714,8 +738,11 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
     unsigned char* buf = reinterpret_cast<unsigned char*>(P.bufs + s * stage_elems);
     for (int item = warp; item < 8 * nrb; item += NW) {
       const int c = item & 7, rb = item >> 3;
-      const int q = rb * 32 + lane;
-      if (q < rows) {
+      // every lane runs the item (warp-uniform control flow for the votes);
+      // rows past the stage's end recompute its last row and store nothing
+      const bool q_on = rb * 32 + lane < rows;
+      const int q = min(rb * 32 + lane, rows - 1);
+      {
         const int col = seg * 8 + c;
         const int tt = colT[col];
         float tw[4][NCT];  // 4 * NCT consecutive floats (16-byte aligned): LDS.128s
@@ -834,41 +861,79 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
 #pragma unroll
           for (int j = 0; j < KT; ++j) sbase[j] = (uint32_t)__cvta_generic_to_shared(base[j]);
           const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
-          if (!patho) {  // hot path: one LDS per edge test and per gather
-            static_for<0, NCO>([&](auto coc) {
-              constexpr int co = decltype(coc)::value;
-              float m[NCT][4];
-              static_for<0, NCT>([&](auto ctc) {
-                constexpr int ct = decltype(ctc)::value;
-                constexpr int OFF = ((ct & 1) * NCO + co) * TB;
-                const float2 lc = *reinterpret_cast<const float2*>(base[ct >> 1] + OFF);
-                u64 tq[2];
+          if (!patho) {  // hot path: bracketed floors, one LUT gather per corner
+            // LUT byte address straight from the clamped floor bits:
+            // lbase + 4 * bits  (lbase = base - 4 * kMagicBits, mod 2^32)
+            uint32_t lbase[KT];
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                  const u64 y = mul2(sub2(h ? V23 : V01, pk2(lc.x, lc.x)), pk2(lc.y, lc.y));
-                  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(tq[h]) : "l"(y), "l"(pk2(kMagic, kMagic)));
-                }
-                float tf[4];
-                upk2(tq[0], tf[0], tf[1]);
-                upk2(tq[1], tf[2], tf[3]);
+            for (int j = 0; j < KT; ++j) lbase[j] = sbase[j] - mb4;
+            const u64 M2 = pk2(kMagic, kMagic);
+            // outer corners in pairs (runtime loop: the unrolled body is one
+            // pair's 2 x NCT corners -- code size); weights as wo[] above
+            constexpr int SF = KO >= 2 ? 2 : 1;
+            const float g2[2] = {1.0f - f2, f2};
+#pragma unroll 1
+            for (int cp = 0; cp < NCO / 2; ++cp) {
+              const float wf = pick(wfix, cp >> (SF - 1));
+              const float wg2 = KO >= 2 ? pick(g2, cp & 1) : 1.0f;
+              const uint32_t po = (uint32_t)(2 * cp * TB);
+              static_for<0, 2>([&](auto bc) {
+                constexpr int b1 = decltype(bc)::value;
+                float w = b1 ? f1 : 1.0f - f1;
+                if (KO >= 2) w *= wg2;
+                w *= wf;
+                static_for<0, NCT>([&](auto ctc) {
+                  constexpr int ct = decltype(ctc)::value;
+                  constexpr int OFF = ((ct & 1) * NCO + b1) * TB;
+                  const char* B = base[ct >> 1] + po + OFF;
+                  const float4 hd = *reinterpret_cast<const float4*>(B);
+                  u64 ta[2], tb[2];
 #pragma unroll
-                for (int i = 0; i < 4; ++i)
-                  m[ct][i] = edge_gather<OFF + NbBlock::th_off(NB) * 4,
-                                         OFF + NbBlock::lut_off(NB) * 4>(
-                      sbase[ct >> 1], clamp_bits_k(tf[i], NB), vv[i]);
+                  for (int h = 0; h < 2; ++h) {
+                    const u64 d = sub2(h ? V23 : V01, pk2(hd.x, hd.x));
+                    ta[h] = fma_rm2(d, pk2(hd.y, hd.y), M2);
+                    tb[h] = fma_rm2(d, pk2(hd.z, hd.z), M2);
+                  }
+                  float fa[4], fb[4];
+                  upk2(ta[0], fa[0], fa[1]);
+                  upk2(ta[1], fa[2], fa[3]);
+                  upk2(tb[0], fb[0], fb[1]);
+                  upk2(tb[1], fb[2], fb[3]);
+                  uint32_t amb = 0;  // any lane-voxel whose two floors disagree
+                  float m[4];
+#pragma unroll
+                  for (int i = 0; i < 4; ++i) {
+                    const int ab = __float_as_int(fa[i]);
+                    amb |= (uint32_t)(ab ^ __float_as_int(fb[i]));
+                    m[i] = lut_at<OFF + NbBlock::lut_off(NB) * 4>(
+                        lbase[ct >> 1] + po, min(max(ab, kMagicBits), kMagicBits + NB - 1));
+                  }
+                  if (__any_sync(0xffffffffu, amb != 0)) {
+                    // rare (q within ~5e-7 |q| of a bin edge): the clamped floors
+                    // are k - 1 and k and the edge table picks one
+                    const float* th = reinterpret_cast<const float*>(B) + NbBlock::th_off(NB);
+                    const float* L = reinterpret_cast<const float*>(B) + NbBlock::lut_off(NB);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {  // recomputed: fa / fb are not kept live
+                      const float dd = __fsub_rn(vv[i], hd.x);
+                      const int ka = clamp_bits(__fmaf_rd(dd, hd.y, kMagic), NB - 1);
+                      const int kb = clamp_bits(__fmaf_rd(dd, hd.z, kMagic), NB - 1);
+                      if (ka != kb && vv[i] >= th[NbBlock::pad(kb)]) m[i] = L[kb];
+                    }
+                  }
+#pragma unroll
+                  for (int i = 0; i < 4; ++i) act[ct][i] = fmaf(w, m[i], act[ct][i]);
+                });
               });
-#pragma unroll
-              for (int ct = 0; ct < NCT; ++ct)
-#pragma unroll
-                for (int i = 0; i < 4; ++i) act[ct][i] = fmaf(wo[co], m[ct][i], act[ct][i]);
-            });
+            }
           } else {  // a pathological range in the pencil: exact search where needed
 #pragma unroll
             for (int co = 0; co < NCO; ++co) {
 #pragma unroll
               for (int ct = 0; ct < NCT; ++ct) {
                 const char* B = base[ct >> 1] + ((ct & 1) * NCO + co) * TB;
-                const float2 lc = *reinterpret_cast<const float2*>(B);
+                const float4 hd = *reinterpret_cast<const float4*>(B);
+                const float2 lc = make_float2(hd.x, hd.w);
                 const float* th = reinterpret_cast<const float*>(B) + NbBlock::th_off(NB);
                 const float* L = reinterpret_cast<const float*>(B) + NbBlock::lut_off(NB);
 #pragma unroll
@@ -891,7 +956,7 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
                     const int k = clamp_bits(t0, NB);
                     b = vv[i] >= th[NbBlock::pad(k)] ? k : k - 1;
                   }
-                  act[ct][i] = fmaf(wo[co], L[NbBlock::pad(b)], act[ct][i]);
+                  act[ct][i] = fmaf(wo[co], L[b], act[ct][i]);
                 }
               }
             }
@@ -973,7 +1038,7 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
         r.y = fminf(fmaxf(acc[1], 0.f), 1.f);
         r.z = fminf(fmaxf(acc[2], 0.f), 1.f);
         r.w = fminf(fmaxf(acc[3], 0.f), 1.f);
-        *slot4 = r;  // in place; the producer TMA-stores the box
+        if (q_on) *slot4 = r;  // in place; the producer TMA-stores the box
       }
     }
     fence_proxy_async_smem();

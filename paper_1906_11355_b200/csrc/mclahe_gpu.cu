@@ -1524,7 +1524,7 @@ int mclahe_plan_dict_state(mclahe_plan_t plan, const void* workspace, int32_t* s
 int mclahe_debug_bin_index_packed(const float* values, int64_t n, double lo, double hi,
                                   int64_t n_bins, int32_t variant, int32_t* out, void* stream) {
   if (n_bins < 2 || n_bins > 16384) return fail(MCLAHE_ERR_VALIDATION, "n_bins out of range");
-  if (variant != 1 && variant != 2) return fail(MCLAHE_ERR_VALIDATION, "variant must be 1 or 2");
+  if (variant < 1 || variant > 3) return fail(MCLAHE_ERR_VALIDATION, "variant must be 1, 2 or 3");
   if (n <= 0) return MCLAHE_OK;
   const int grid = (int)std::min<int64_t>((n / 2 + 256) / 256, 4096);
   cudaStream_t st = static_cast<cudaStream_t>(stream);

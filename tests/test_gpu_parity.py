@@ -141,7 +141,8 @@ def test_bin_index_adversarial(M):
                       (0.3, 0.3000001, 256), (1e-30, 3e-30, 16384), (-3e38, 3e38, 256)]:
         lo32, hi32 = float(np.float32(lo)), float(np.float32(hi))
         want = O.bin_index_array(v.astype(np.float64), lo32, hi32, n)
-        for variant in (0, 1, 2):  # generic, packed histogram, packed blend gather
+        # generic, packed histogram, packed blend gather, bracketed floors (NB blend)
+        for variant in (0, 1, 2, 3):
             got = M.bin_index_device(vt, lo32, hi32, n, variant).cpu().numpy()
             bad = np.flatnonzero(got != want)
             assert bad.size == 0, (lo, hi, n, variant, v[bad[:5]], got[bad[:5]], want[bad[:5]])
