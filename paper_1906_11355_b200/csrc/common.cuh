@@ -75,6 +75,7 @@ struct KGeom {
   int dict;                // 1: the value-dictionary blend is armed (K2a builds the dictionary)
   int stiles;              // NB blend: trailing tiles staged at once (one segment's window)
   int dyn_units;           // blend: > 0 = units handed out dynamically (count), via W.range[3]
+  int seg_items;           // blend: 1 = a work item is (unit, ONE segment): item / nseg, item % nseg
 };
 
 // Value dictionary (adaptive mode, float32): when the volume holds few
@@ -353,28 +354,46 @@ __device__ __forceinline__ bool parts_uniform(const TileParts& p, int64_t x, int
 // STORE: consumers leave each stage's results in place; before a slot is
 // refilled (and after the last stage) its box is written back with a TMA
 // tensor store through out_map.
-template <int KO, bool CELLS, bool WEIGHTS = !CELLS, bool STORE = false>
+// SEGOUT: segments outermost in a unit (the blend kernels, which stage per
+// segment); otherwise every box walks all segments in turn.
+// The per-stage path is kept short (one thread issues every stage while 16
+// consumer warps share its SM sub-partition): slot / phase counters instead
+// of divisions, the unit record and geometry in registers, TMA coordinates in
+// registers.
+template <int KO, bool CELLS, bool WEIGHTS = !CELLS, bool STORE = false, bool SEGOUT = STORE>
 __device__ __noinline__ void pipe_produce(const KGeom& G, const CUtensorMap* map,
                                           const int32_t* __restrict__ units, int u0, int u1,
                                           Pipe& pp, float* bufs,
                                           const CUtensorMap* out_map = nullptr,
                                           unsigned long long* dyn = nullptr) {
   const int nst = G.nst;
+  const int nseg = G.nseg;
+  const bool segv = G.tma_rank - KO == 2;  // the TMA view has a segment coordinate
+  const int tma_rank = G.tma_rank;
+  const int seg_items = G.seg_items;
+  const int32_t row0 = (int32_t)G.row0;
   const int64_t stage_elems = G.stage_stride;
-  const uint32_t box_bytes = (uint32_t)((int64_t)G.stage_rows * (G.P / G.nseg) * 4);
+  const uint32_t box_bytes = (uint32_t)((int64_t)G.stage_rows * (G.P / nseg) * 4);
   const int R1 = G.r1, R2 = G.r2;
   ProdBox& B = pp.box;
   uint32_t it = 0;
+  int slot = 0;
+  uint32_t phase = 0;  // (it / nst) & 1
   // dyn != nullptr: units are handed out dynamically (one atomic per unit,
   // [u0, u1) is then the whole list); otherwise the CTA's static range
   int u = dyn ? u0 + (int)atomicAdd(dyn, 1ULL) : u0;
 #pragma unroll 1
   for (; u < u1; u = dyn ? u0 + (int)atomicAdd(dyn, 1ULL) : u + 1) {
-    const int32_t* U = units + (int64_t)u * kUnitInts;
+    // seg_items: work item u = (unit u / nseg, segment u % nseg)
+    const int seg_w = seg_items ? u % nseg : 0;
+    const int32_t* U = units + (int64_t)(seg_items ? u / nseg : u) * kUnitInts;
+    int32_t cellr[KO];
+#pragma unroll
+    for (int j = 0; j < KO; ++j) cellr[j] = U[j];
     int64_t key = 0;
     B.a[0] = U[8];
     B.ext[0] = U[9] - U[8];
-    B.parts[0] = tile_parts(G.d[0], U[0]);
+    B.parts[0] = tile_parts(G.d[0], cellr[0]);
 #pragma unroll 1
     for (int j = 1; j < KO; ++j) {
       if (CELLS) {
@@ -402,16 +421,22 @@ __device__ __noinline__ void pipe_produce(const KGeom& G, const CUtensorMap* map
     for (int j = 0; j < KO - 2; ++j) nfix *= B.ext[j];
     const int n1 = B.ext[KO - 1] / R1;
     const int n2 = KO >= 2 ? B.ext[KO - 2] / R2 : 1;
-    // blend (STORE): segments outermost, so a consumer staging per segment
-    // (the n_bins-specialised blend with several segments) restages rarely
+    const int32_t a1 = (int32_t)B.a[KO - 1], a2 = KO >= 2 ? (int32_t)B.a[KO - 2] : 0;
+    TileParts p1, p2;
+    if (WEIGHTS) {
+      p1 = B.parts[KO - 1];
+      if (KO >= 2) p2 = B.parts[KO - 2];
+    }
+    // blend (SEGOUT): segments outermost, so a consumer staging per segment
+    // restages rarely
 #pragma unroll 1
-    for (int sego = 0; sego < (STORE ? G.nseg : 1); ++sego)
+    for (int sego = seg_w; sego < (SEGOUT ? (seg_items ? seg_w + 1 : nseg) : seg_w + 1); ++sego)
 #pragma unroll 1
     for (int64_t f = 0; f < nfix; ++f) {
       int32_t xf[kMaxOuterDims];
       int32_t wfix = 1;
       int64_t rem = f;
-#pragma unroll 1
+#pragma unroll
       for (int j = KO - 3; j >= 0; --j) {
         xf[j] = (int32_t)(B.a[j] + rem % B.ext[j]);
         rem /= B.ext[j];
@@ -419,64 +444,71 @@ __device__ __noinline__ void pipe_produce(const KGeom& G, const CUtensorMap* map
       }
 #pragma unroll 1
       for (int i2 = 0; i2 < n2; ++i2) {
+        const int32_t x2 = a2 + i2 * R2;
 #pragma unroll 1
         for (int i1 = 0; i1 < n1; ++i1) {
+          const int32_t x1 = a1 + i1 * R1;
 #pragma unroll 1
-        for (int segi = 0; segi < (STORE ? 1 : G.nseg); ++segi) {
-          const int seg = STORE ? sego : segi;
-          const int slot = it % nst;
-          if (STORE) mbar_wait_spin(&pp.empty[slot], ((it / nst) & 1) ^ 1);  // blend: latency-critical
-          else mbar_wait(&pp.empty[slot], ((it / nst) & 1) ^ 1);
+        for (int segi = 0; segi < (SEGOUT ? 1 : nseg); ++segi) {
+          const int seg = SEGOUT ? sego : segi;
+          if (STORE || SEGOUT) mbar_wait_spin(&pp.empty[slot], phase ^ 1);  // blend: latency-critical
+          else mbar_wait(&pp.empty[slot], phase ^ 1);
           Stage& S = pp.st[slot];
           if (STORE && it >= (uint32_t)nst) {  // write back the slot's previous results
-            tma_store(out_map, G.tma_rank, S.tc, bufs + slot * stage_elems);
+            tma_store(out_map, tma_rank, S.tc, bufs + slot * stage_elems);
             tma_store_wait_read();
           }
           S.unit = u;
           S.seg = seg;
           S.key = key;
-#pragma unroll 1
+#pragma unroll
           for (int j = 0; j < KO - 2; ++j) S.x[j] = xf[j];
-          const int32_t x1 = (int32_t)(B.a[KO - 1] + i1 * R1);
           S.x[KO - 1] = x1;
-          int32_t x2 = 0;
-          if (KO >= 2) {
-            x2 = (int32_t)(B.a[KO - 2] + i2 * R2);
-            S.x[KO - 2] = x2;
-          }
-#pragma unroll 1
-          for (int j = 0; j < KO; ++j) S.cell[j] = U[j];
+          if (KO >= 2) S.x[KO >= 2 ? KO - 2 : 0] = x2;
+#pragma unroll
+          for (int j = 0; j < KO; ++j) S.cell[j] = cellr[j];
           if (WEIGHTS) {
-            S.p1 = B.parts[KO - 1];
-            if (KO >= 2) S.p2 = B.parts[KO - 2];
-            const bool uni = parts_uniform(S.p1, x1, R1) && (KO < 2 || parts_uniform(S.p2, x2, R2));
+            S.p1 = p1;
+            if (KO >= 2) S.p2 = p2;
+            const bool uni = parts_uniform(p1, x1, R1) && (KO < 2 || parts_uniform(p2, x2, R2));
             S.wuni = uni ? 1 : 0;
-            S.wfix = uni ? wfix * S.p1.weight(x1) * (KO >= 2 ? S.p2.weight(x2) : 1) : wfix;
+            S.wfix = uni ? wfix * p1.weight(x1) * (KO >= 2 ? p2.weight(x2) : 1) : wfix;
           }
-          // TMA coordinates, innermost first: trailing block, then dims KO-1 .. 0
+          // TMA coordinates, innermost first: trailing block (+ segment),
+          // then dims KO-1 .. 0 (dim 0 local to the slab)
           int c[6];
-          int r = 0;
-          c[r++] = 0;
-          if (G.tma_rank - KO == 2) c[r++] = seg;  // segment (K4) / second trailing dim (K2: 0)
-#pragma unroll 1
-          for (int j = KO - 1; j >= 0; --j) {
-            const int32_t xj = j == KO - 1 ? x1 : (j == KO - 2 ? x2 : xf[j]);
-            c[r++] = j == 0 ? (int)(xj - G.row0) : xj;
+          int co[KO];
+#pragma unroll
+          for (int j = 0; j < KO; ++j)
+            co[j] = j == KO - 1 ? x1 : (KO >= 2 && j == KO - 2 ? x2 : xf[j < KO - 2 ? j : 0]);
+          co[0] -= row0;
+          c[0] = 0;
+          if (segv) {
+            c[1] = seg;
+#pragma unroll
+            for (int j = 0; j < KO; ++j) c[2 + j] = co[KO - 1 - j];
+          } else {
+#pragma unroll
+            for (int j = 0; j < KO; ++j) c[1 + j] = co[KO - 1 - j];
           }
           if (STORE)
-            for (int i = 0; i < G.tma_rank; ++i) S.tc[i] = c[i];
+#pragma unroll
+            for (int i = 0; i < 6; ++i) S.tc[i] = c[i];
           mbar_expect_tx(&pp.full[slot], box_bytes);
-          tma_load(bufs + slot * stage_elems, map, G.tma_rank, c, &pp.full[slot]);
+          tma_load(bufs + slot * stage_elems, map, tma_rank, c, &pp.full[slot]);
           ++it;
+          if (++slot == nst) {
+            slot = 0;
+            phase ^= 1;
+          }
         }
         }
       }
     }
   }
-  const int slot = it % nst;
-  mbar_wait(&pp.empty[slot], ((it / nst) & 1) ^ 1);
+  mbar_wait(&pp.empty[slot], phase ^ 1);
   if (STORE && it >= (uint32_t)nst) {
-    tma_store(out_map, G.tma_rank, pp.st[slot].tc, bufs + slot * stage_elems);
+    tma_store(out_map, tma_rank, pp.st[slot].tc, bufs + slot * stage_elems);
     tma_store_wait_read();
   }
   pp.st[slot].unit = -1;
@@ -485,7 +517,7 @@ __device__ __noinline__ void pipe_produce(const KGeom& G, const CUtensorMap* map
     for (uint32_t j = (it >= (uint32_t)nst ? it - nst + 1 : 0); j < it; ++j) {
       const int s = j % nst;
       mbar_wait(&pp.empty[s], (j / nst) & 1);
-      tma_store(out_map, G.tma_rank, pp.st[s].tc, bufs + s * stage_elems);
+      tma_store(out_map, tma_rank, pp.st[s].tc, bufs + s * stage_elems);
     }
     tma_store_wait_all();
   }

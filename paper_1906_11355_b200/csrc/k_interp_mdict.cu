@@ -1,0 +1,263 @@
+// k_interp_mdict.cu -- K4, value-dictionary blend with the trailing corners
+// folded into per-frame tables (adaptive mode, one trailing dim, KO == 3).
+//
+// The reference blends 2^D corner LUTs per voxel (src/pipeline.cpp:94-127,
+// src/interpolation.cpp:44-86).  With one trailing dim, a voxel at frame i of
+// trailing column c (4 frames, one trailing cell) weighs its two trailing
+// corners with the column's fixed weights tw[c][i][0..1], so for every
+// dictionary value v the pair folds into one number
+//
+//     M[c][i][co][v] = fma(tw1, L(co, tt_c + 1)[v], tw0 * L(co, tt_c)[v])
+//
+// and a voxel needs 2^KO gathers instead of 2^(KO+1): the shared-memory
+// gathers, which bound the blend, halve.  The tables of all 8 columns would
+// not fit in shared memory (590 KB for the 4D config), so a work item is one
+// interpolation cell pencil x ONE 8-float segment of the trailing block (two
+// columns, 147 KB of tables); the four CTAs holding the segments of one cell
+// pencil take consecutive work items, and the tensor map's 256-byte L2
+// promotion turns their 32-byte TMA boxes into whole-line DRAM reads.
+//
+// Summation order per voxel: acc = fma(wo[co], M[co], acc) over co ascending
+// -- the edge-table blend (k_interp_pencil, MORD) sums in the same order, so
+// both produce the same bits.
+#include "k_pencil.cuh"
+
+namespace mg {
+
+// TSTORE: results written in place into the stage and TMA-stored by the
+// producer (otherwise each lane stores its 16 bytes straight to global).
+template <int KO, bool TSTORE>
+__global__ void __launch_bounds__(kBlendThreads, 1)
+    k_interp_mdict(const __grid_constant__ KGeom G, const __grid_constant__ CUtensorMap tmap,
+                   const __grid_constant__ CUtensorMap omap, const float* __restrict__ in,
+                   float* __restrict__ out, const int32_t* __restrict__ units,
+                   const int32_t* __restrict__ cta_units, WS W) {
+  constexpr int NCO = 1 << KO;
+  constexpr int NW = kConsumersBlend / 32;
+  constexpr int KC = kDictKC;
+  if (W.range[2] != 0) return;  // non-finite input: write nothing
+  if (W.dmeta[2] == 0) return;  // no usable dictionary: the edge-table blend runs
+  extern __shared__ __align__(1024) unsigned char smem[];
+  const PencilSmem P = pencil_smem(G, smem);
+  const int n = G.n_bins;
+  float* Ms = reinterpret_cast<float*>(P.tail);                  // [2][4][NCO][KC]
+  uint2* dltS = reinterpret_cast<uint2*>(Ms + 2 * 4 * NCO * KC);  // [kDictHL]
+  int* ofS = reinterpret_cast<int*>(dltS + kDictHL);              // [NCO]
+  const int ncol = (int)(G.P / 4);
+  int* colT = reinterpret_cast<int*>(
+      (reinterpret_cast<uintptr_t>(ofS + NCO) + 15) & ~uintptr_t(15));  // [ncol]
+  float* colW = reinterpret_cast<float*>(colT + ((ncol + 3) & ~3));    // [ncol][4][2]
+  __shared__ int s_dmode;
+  __shared__ float s_dv0, s_dS;
+  __shared__ int s_nv;
+  pipe_init(*P.pipe, G.nst, NW);
+  __syncthreads();
+  if (threadIdx.x >= kConsumersBlend) {
+    if (threadIdx.x == kConsumersBlend)
+      pipe_produce<KO, true, false, TSTORE, true>(G, &tmap, units, 0, G.dyn_units, *P.pipe,
+                                                  P.bufs, &omap,
+                                                  reinterpret_cast<unsigned long long*>(&W.range[3]));
+    return;
+  }
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const Dim& dl = G.d[G.rank - 1];
+  for (int col = tid; col < ncol; col += kConsumersBlend) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int64_t x = (int64_t)col * 4 + i;
+      const int64_t c = cell_of(dl, x);
+      const float f1 = (float)twice_dlo(dl, x, c) / (float)(2 * dl.b);
+      if (i == 0) colT[col] = (int)(c * G.tstride[G.rank - 1]);
+      colW[(col * 4 + i) * 2 + 0] = 1.0f - f1;
+      colW[(col * 4 + i) * 2 + 1] = f1;
+    }
+  }
+  for (int k = tid; k < kDictHL; k += kConsumersBlend) dltS[k] = W.dlt[k];
+  if (tid == 0) {
+    s_dmode = W.dmeta[4];
+    s_dv0 = __int_as_float(W.dmeta[5]);
+    s_dS = __int_as_float(W.dmeta[6]);
+    s_nv = min(W.dmeta[3], KC);
+  }
+  const int tstr1 = (int)G.tstride[G.rank - 1];  // trailing corner: next tile of the last dim
+  const int64_t stage_elems = G.stage_stride;
+  const int rows = G.stage_rows;
+  const int nrb = (rows + 31) >> 5;
+  float ugs[KO], ugt[KO];
+  int64_t cur = -1;
+  int seg = 0;
+  uint32_t it = 0;
+  while (true) {
+    const int s = it % G.nst;
+    mbar_wait(&P.pipe->full[s], (it / G.nst) & 1);
+    const Stage& S = P.pipe->st[s];
+    if (S.unit < 0) break;
+    const int64_t key = S.key * G.nseg + S.seg;
+    if (key != cur) {  // new work item: fold the two columns' corner pairs into M
+      consumers_sync<kConsumersBlend>();
+      seg = S.seg;
+      int64_t ofc[NCO];
+#pragma unroll
+      for (int co = 0; co < NCO; ++co) {
+        int64_t of = (S.cell[0] + ((co >> (KO - 1)) & 1) - G.trow0) * G.tstride[0];
+#pragma unroll
+        for (int j = 1; j < KO; ++j) of += (S.cell[j] + ((co >> (KO - 1 - j)) & 1)) * G.tstride[j];
+        ofc[co] = of;
+        if (tid == 0) ofS[co] = (int)of;
+      }
+      const int nv4 = (s_nv + 3) >> 2;
+      const int ntask = 2 * NCO * nv4;
+#pragma unroll 2
+      for (int k = tid; k < ntask; k += kConsumersBlend) {
+        const int v4 = k % nv4, cc = k / nv4;  // cc = c * NCO + co
+        const int c = cc / NCO, co = cc - c * NCO;
+        const int col = seg * 2 + c;
+        const int64_t t0 = ofc[co] + colT[min(col, ncol - 1)];
+        const float4 L0 = __ldg(reinterpret_cast<const float4*>(W.lutd + t0 * KC) + v4);
+        const float4 L1 = __ldg(reinterpret_cast<const float4*>(W.lutd + (t0 + tstr1) * KC) + v4);
+        const float a0[4] = {L0.x, L0.y, L0.z, L0.w}, a1[4] = {L1.x, L1.y, L1.z, L1.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float2 tw = *reinterpret_cast<const float2*>(colW + (min(col, ncol - 1) * 4 + i) * 2);
+          float r[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) r[e] = fmaf(tw.y, a1[e], tw.x * a0[e]);
+          reinterpret_cast<float4*>(Ms + ((c * 4 + i) * NCO + co) * KC)[v4] =
+              make_float4(r[0], r[1], r[2], r[3]);
+        }
+      }
+      consumers_sync<kConsumersBlend>();
+      cur = key;
+#pragma unroll
+      for (int jd = 0; jd < KO; ++jd) {
+        const Dim& d = G.d[jd];
+        ugs[jd] = G.inv_b[jd];
+        ugt[jd] = (float)(2 * d.before - 2 * (int64_t)S.cell[jd] * d.b - d.b + 1) * G.inv_2b[jd];
+      }
+    }
+    // outer weights exactly as k_interp_pencil computes them
+    float wfix[NCO / 4];
+    const float s1 = ugs[KO - 1], t1 = ugt[KO - 1];
+    const float s2 = ugs[KO - 2], t2 = ugt[KO - 2];
+    {
+      float ff[KO - 2 > 0 ? KO - 2 : 1];
+#pragma unroll
+      for (int j = 0; j < KO - 2; ++j) ff[j] = fmaf((float)S.x[j], ugs[j], ugt[j]);
+#pragma unroll
+      for (int cf = 0; cf < NCO / 4; ++cf) {
+        float w = 1.0f;
+#pragma unroll
+        for (int j = 0; j < KO - 2; ++j) w *= ((cf >> (KO - 3 - j)) & 1) ? ff[j] : 1.0f - ff[j];
+        wfix[cf] = w;
+      }
+    }
+    const int xb1 = S.x[KO - 1], xb2 = S.x[KO - 2];
+    // results go straight to global memory (16 bytes per lane and row; a
+    // stage is free once read, so loads never wait on a write-back)
+    int64_t gbase = (int64_t)(S.x[0] - G.row0) * G.vstride[0];
+#pragma unroll
+    for (int j = 1; j < KO - 2; ++j) gbase += (int64_t)S.x[j] * G.vstride[j];
+    gbase += (int64_t)xb2 * G.vstride[KO - 2] + (int64_t)xb1 * G.vstride[KO - 1];
+    unsigned char* buf = reinterpret_cast<unsigned char*>(P.bufs + s * stage_elems);
+    for (int item = warp; item < 2 * nrb; item += NW) {
+      const int c = item & 1, rb = item >> 1;
+      const bool q_on = rb * 32 + lane < rows;
+      const int q = min(rb * 32 + lane, rows - 1);
+      const int col = seg * 2 + c;
+      const bool col_on = col < ncol;  // an odd last column pair
+      const int r1 = q & (G.r1 - 1), r2 = q >> G.lg_r1;
+      const float f1 = fmaf((float)(xb1 + r1), s1, t1);
+      const float f2 = fmaf((float)(xb2 + r2), s2, t2);
+      float wo[NCO];
+      {
+        const float g1[2] = {1.0f - f1, f1};
+#pragma unroll
+        for (int co = 0; co < NCO; ++co) {
+          float w = g1[co & 1];
+          w *= ((co >> 1) & 1) ? f2 : 1.0f - f2;
+          wo[co] = w * wfix[co >> 2];
+        }
+      }
+      // 32B-swizzled stage row (32 bytes): 16-byte chunk c of row q at c ^ ((q >> 2) & 1)
+      float4* slot4 = reinterpret_cast<float4*>(buf + q * 32 + ((c ^ ((q >> 2) & 1)) << 4));
+      const float4 v4 = *slot4;
+      const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
+      int di[4];
+      if (s_dmode) {  // affine cells: one LDS.64 per voxel
+        int cl[4];
+        cl[0] = dict_cell(vv[0], vv[1], s_dv0, s_dS, &cl[1]);
+        cl[2] = dict_cell(vv[2], vv[3], s_dv0, s_dS, &cl[3]);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const uint2 e = dltS[cl[i]];
+          di[i] = e.x == __float_as_uint(vv[i]) ? (int)e.y : -1;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) di[i] = dict_lookup(dltS, __float_as_uint(vv[i]));
+      }
+      const char* A[4];
+      int miss = 0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        miss |= (di[i] < 0) << i;
+        A[i] = reinterpret_cast<const char*>(Ms + ((c * 4 + i) * NCO) * KC + (di[i] >= 0 ? di[i] : 0));
+      }
+      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+      static_for<0, NCO>([&](auto coc) {
+        constexpr int co = decltype(coc)::value;
+        float m[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) m[i] = *reinterpret_cast<const float*>(A[i] + co * KC * 4);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc[i] = fmaf(wo[co], m[i], acc[i]);
+      });
+      if (miss) {  // values the (sampled) dictionary lacks: from the workspace LUTs
+        const int tt = colT[min(col, ncol - 1)];
+#pragma unroll 1
+        for (int i = 0; i < 4; ++i)
+          if ((miss >> i) & 1) {
+            const float2 tw =
+                *reinterpret_cast<const float2*>(colW + (min(col, ncol - 1) * 4 + i) * 2);
+            float a = 0.0f;
+#pragma unroll 1
+            for (int co = 0; co < NCO; ++co) {
+              const int t0 = ofS[co] + tt;
+              const float L0 = lut_value_global(W, n, t0, vv[i]);
+              const float L1 = lut_value_global(W, n, t0 + tstr1, vv[i]);
+              a = fmaf(pick(wo, co), fmaf(tw.y, L1, tw.x * L0), a);
+            }
+            if (i == 0) acc[0] = a;
+            else if (i == 1) acc[1] = a;
+            else if (i == 2) acc[2] = a;
+            else acc[3] = a;
+          }
+      }
+      float4 r;
+      r.x = fminf(fmaxf(acc[0], 0.f), 1.f);
+      r.y = fminf(fmaxf(acc[1], 0.f), 1.f);
+      r.z = fminf(fmaxf(acc[2], 0.f), 1.f);
+      r.w = fminf(fmaxf(acc[3], 0.f), 1.f);
+      if (TSTORE) {
+        if (q_on) *slot4 = r;  // in place; the producer TMA-stores the box
+      } else if (q_on && col_on) {
+        __stcs(reinterpret_cast<float4*>(out + gbase + (int64_t)r2 * G.vstride[KO - 2] +
+                                         (int64_t)r1 * G.vstride[KO - 1] + col * 4),
+               r);
+      }
+    }
+    if (TSTORE) fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&P.pipe->empty[s]);
+    ++it;
+  }
+}
+
+PencilInterpFn get_interp_mdict(int ko, bool tma_store) {
+  switch (ko) {
+    case 3: return tma_store ? k_interp_mdict<3, true> : k_interp_mdict<3, false>;
+    default: return nullptr;
+  }
+}
+
+}  // namespace mg

@@ -471,6 +471,7 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
   constexpr int NCO = 1 << KO, NCT = 1 << KT;
   constexpr int NW = kConsumersBlend / 32;
   constexpr bool DICT = NB < 0;
+  constexpr bool MORD = ADAPT && KT == 1 && KO == 3;
   if (W.range[2] != 0) return;  // non-finite input: write nothing
   if (DICT) {
     if (W.dmeta[2] == 0) return;
@@ -777,6 +778,20 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
         for (int ct = 0; ct < NCT; ++ct)
 #pragma unroll
           for (int i = 0; i < 4; ++i) act[ct][i] = 0.f;
+        // MORD (adaptive, one trailing dim, KO == 3): the value-dictionary
+        // blend k_interp_mdict folds the two trailing corners first,
+        // M = fma(tw1, L1, tw0 * L0), and sums act = fma(wo, M, act) over
+        // co; the adaptive paths here sum in that order too (same bits)
+        auto accum = [&](float w, const float (&m)[NCT][4]) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            if constexpr (MORD)
+              act[0][i] = fmaf(w, fmaf(tw[i][1 % NCT], m[1 % NCT][i], tw[i][0] * m[0][i]), act[0][i]);
+            else
+#pragma unroll
+              for (int ct = 0; ct < NCT; ++ct) act[ct][i] = fmaf(w, m[ct][i], act[ct][i]);
+          }
+        };
         int bg[4] = {0, 0, 0, 0};
         if (!ADAPT) {
           if (!patho) {
@@ -831,10 +846,7 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
               for (int i = 0; i < 4; ++i)
                 m[ct][i] = *reinterpret_cast<const float*>(A[ct >> 1][i] + OFF);
             });
-#pragma unroll
-            for (int ct = 0; ct < NCT; ++ct)
-#pragma unroll
-              for (int i = 0; i < 4; ++i) act[ct][i] = fmaf(wo[co], m[ct][i], act[ct][i]);
+            accum(wo[co], m);
           });
           if (miss) {  // values the (sampled) dictionary lacks: redo them from the workspace
 #pragma unroll
@@ -843,11 +855,17 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
 #pragma unroll
                 for (int ct = 0; ct < NCT; ++ct) act[ct][i] = 0.0f;
 #pragma unroll
-                for (int co = 0; co < NCO; ++co)
+                for (int co = 0; co < NCO; ++co) {
+                  float L[NCT];
 #pragma unroll
                   for (int ct = 0; ct < NCT; ++ct)
-                    act[ct][i] = fmaf(wo[co], lut_value_global(W, n, ofS[co] + tt + ctoff[ct], vv[i]),
-                                      act[ct][i]);
+                    L[ct] = lut_value_global(W, n, ofS[co] + tt + ctoff[ct], vv[i]);
+                  if constexpr (MORD)
+                    act[0][i] = fmaf(wo[co], fmaf(tw[i][1 % NCT], L[1 % NCT], tw[i][0] * L[0]), act[0][i]);
+                  else
+#pragma unroll
+                    for (int ct = 0; ct < NCT; ++ct) act[ct][i] = fmaf(wo[co], L[ct], act[ct][i]);
+                }
               }
           }
         } else if constexpr (NB > 0) {
@@ -882,6 +900,8 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
                 float w = b1 ? f1 : 1.0f - f1;
                 if (KO >= 2) w *= wg2;
                 w *= wf;
+                float m0[4];  // MORD: trailing corner 0's gathers
+                (void)m0;
                 static_for<0, NCT>([&](auto ctc) {
                   constexpr int ct = decltype(ctc)::value;
                   constexpr int OFF = ((ct & 1) * NCO + b1) * TB;
@@ -921,14 +941,26 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
                       if (ka != kb && vv[i] >= th[NbBlock::pad(kb)]) m[i] = L[kb];
                     }
                   }
+                  if constexpr (MORD) {  // fold the trailing pair, then one FMA per voxel
+                    if constexpr (ct == 0) {
 #pragma unroll
-                  for (int i = 0; i < 4; ++i) act[ct][i] = fmaf(w, m[i], act[ct][i]);
+                      for (int i = 0; i < 4; ++i) m0[i] = m[i];
+                    } else {
+#pragma unroll
+                      for (int i = 0; i < 4; ++i)
+                        act[0][i] = fmaf(w, fmaf(tw[i][1], m[i], tw[i][0] * m0[i]), act[0][i]);
+                    }
+                  } else {
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) act[ct][i] = fmaf(w, m[i], act[ct][i]);
+                  }
                 });
               });
             }
           } else {  // a pathological range in the pencil: exact search where needed
 #pragma unroll
             for (int co = 0; co < NCO; ++co) {
+              float mp[NCT][4];
 #pragma unroll
               for (int ct = 0; ct < NCT; ++ct) {
                 const char* B = base[ct >> 1] + ((ct & 1) * NCO + co) * TB;
@@ -956,9 +988,10 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
                     const int k = clamp_bits(t0, NB);
                     b = vv[i] >= th[NbBlock::pad(k)] ? k : k - 1;
                   }
-                  act[ct][i] = fmaf(wo[co], L[b], act[ct][i]);
+                  mp[ct][i] = L[b];
                 }
               }
+              accum(wo[co], mp);
             }
           }
         } else if (ADAPT && !patho) {  // hot path: branch-free edge-table gathers
@@ -974,10 +1007,7 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
               lut2_edge(V01, v4.x, v4.y, lc, thb, Lb, n4, m[ct][0], m[ct][1]);
               lut2_edge(V23, v4.z, v4.w, lc, thb, Lb, n4, m[ct][2], m[ct][3]);
             }
-#pragma unroll
-            for (int ct = 0; ct < NCT; ++ct)
-#pragma unroll
-              for (int i = 0; i < 4; ++i) act[ct][i] = fmaf(wo[co], m[ct][i], act[ct][i]);
+            accum(wo[co], m);
           }
         } else {
           int bo[4];  // global mode: byte offsets of the voxel's bin
@@ -1022,17 +1052,19 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
                 for (int i = 0; i < 4; ++i) m[ct][i] = *reinterpret_cast<const float*>(Lb + bo[i]);
               }
             }
-#pragma unroll
-            for (int ct = 0; ct < NCT; ++ct)
-#pragma unroll
-              for (int i = 0; i < 4; ++i) act[ct][i] = fmaf(wo[co], m[ct][i], act[ct][i]);
+            accum(wo[co], m);
           }
         }
         // trailing weights last: acc = sum_ct tw[ct] * (sum_co wo[co] * L)
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < 4; ++i) {
+          if constexpr (MORD) {
+            acc[i] = act[0][i];
+          } else {
 #pragma unroll
-          for (int ct = 0; ct < NCT; ++ct) acc[i] = fmaf(tw[i][ct], act[ct][i], acc[i]);
+            for (int ct = 0; ct < NCT; ++ct) acc[i] = fmaf(tw[i][ct], act[ct][i], acc[i]);
+          }
+        }
         float4 r;
         r.x = fminf(fmaxf(acc[0], 0.f), 1.f);
         r.y = fminf(fmaxf(acc[1], 0.f), 1.f);
@@ -1058,5 +1090,6 @@ PencilRangeFn get_range_pencil(int ko, bool dict);
 PencilHistFn get_hist_pencil(int ko, bool adaptive);
 PencilInterpFn get_interp_pencil(int ko, int kt, bool adaptive, int n_bins);
 PencilInterpFn get_interp_pencil_dict(int ko, int kt);
+PencilInterpFn get_interp_mdict(int ko, bool tma_store);  // nullptr: none for ko
 
 }  // namespace mg

@@ -145,9 +145,15 @@ struct mclahe_plan_s {
   // value dictionary (kDict*): armed when the blend's tables fit shared memory
   int dict_cap = 0, dict_nst = 0;
   int64_t dict_smem = 0, off_dict = 0;
+  // folded-pair dictionary blend (k_interp_mdict): one 8-float segment per work item
+  Pencil interp_m;
+  bool mdict = false;
+  std::vector<int32_t> mdict_units;  // whole cells (the interp units' dim-0 chunks merged)
+  int64_t off_mdict_units = 0;
   // TMA views of the last input buffer (re-encoded when the pointer changes)
-  const void* map_ptr[3] = {nullptr, nullptr, nullptr};
-  CUtensorMap map[3];  // [0] hist view of the input, [1] blend view of the input, [2] of the output
+  const void* map_ptr[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  CUtensorMap map[5];  // [0] hist view of the input, [1] blend view of the input, [2] of the
+                       // output, [3] / [4] the folded-pair blend's 8-float views of both
   bool f32() const { return p.dtype == MCLAHE_F32; }
   mclahe_plan_s() = default;
   mclahe_plan_s(const mclahe_plan_s&) = delete;
@@ -407,6 +413,59 @@ void plan_dict(mclahe_plan_s* pl) {
   I.workspace_bytes = align_up(pl->off_dict + dict_bytes(pl->G.win_tiles), 256);
 }
 
+// Arms the folded-pair dictionary blend (k_interp_mdict) over the dictionary
+// blend: one trailing dim, three outer dims, 8-float segments.  Its stages
+// hold R2 x R1 rows of one segment (32 bytes); MCLAHE_NO_MDICT=1 disarms it.
+void plan_mdict(mclahe_plan_s* pl) {
+  pl->mdict = false;
+  const Pencil& c = pl->interp;
+  if (!pl->dict_cap || !c.on || c.kt != 1 || c.ko != 3 || c.P % 8 != 0 || !get_interp_mdict(c.ko, false) ||
+      getenv("MCLAHE_NO_MDICT"))
+    return;
+  Pencil m = c;
+  m.nseg = (int)(c.P / 8);
+  m.tma_rank = c.ko + 2;
+  if (m.tma_rank > 5) return;
+  // rows along dim KO-2: a power of two dividing every cell extent, R1 x R2 <= 512
+  std::vector<std::pair<int64_t, int64_t>> ex;
+  int64_t g2 = 0;
+  extents(*pl, true, c.ko - 2, ex);
+  for (auto& p : ex) g2 = gcd64(g2, p.second - p.first);
+  m.r1 = c.r1;
+  m.lg_r1 = c.lg_r1;
+  static const int rows_cap = getenv("MCLAHE_MDICT_ROWS") ? atoi(getenv("MCLAHE_MDICT_ROWS")) : 512;
+  static const int nst_cap = getenv("MCLAHE_MDICT_NST") ? atoi(getenv("MCLAHE_MDICT_NST")) : 4;
+  m.r2 = (int)pow2_divisor(g2, std::min<int64_t>(256, std::max(1, rows_cap / m.r1)));
+  m.stage_rows = m.r1 * m.r2;
+  if (m.stage_rows < 32) return;
+  m.stage_stride = align_up(m.stage_rows * 32, 1024) / 4;
+  const int64_t nco = int64_t{1} << c.ko;
+  m.tail = 2 * 4 * nco * kDictKC * 4 + kDictHL * 8 + nco * 4 + 16 + ((c.P / 4 + 3) & ~int64_t(3)) * 4 +
+           (c.P / 4) * 32 + 16;
+  const int64_t stage = m.stage_stride * 4;
+  const int64_t nst = std::min<int64_t>(std::min(nst_cap, kMaxStages), (226 * 1024 - kPipeBytes - m.tail) / stage);
+  if (nst < 2) return;
+  m.nst = (int)nst;
+  m.smem = kPipeBytes + nst * stage + m.tail;
+  // whole cell pencils: a work item rebuilds its tables, so units are not
+  // chunked along dim 0 (the interp units' chunks of one cell are merged)
+  std::vector<int32_t>& mu = pl->mdict_units;
+  mu.clear();
+  const std::vector<int32_t>& iu = pl->interp_units;
+  for (size_t k = 0; k < iu.size(); k += kUnitInts) {
+    const size_t last = mu.size();
+    if (last && std::equal(iu.begin() + k, iu.begin() + k + c.ko, mu.begin() + last - kUnitInts) &&
+        mu[last - 1] == iu[k + 8]) {
+      mu[last - 1] = iu[k + 9];  // contiguous dim-0 chunk of the same cell
+      continue;
+    }
+    mu.insert(mu.end(), iu.begin() + k, iu.begin() + k + kUnitInts);
+  }
+  if (mu.empty() || (int64_t)(mu.size() / kUnitInts) * m.nseg > INT32_MAX) return;
+  pl->interp_m = m;
+  pl->mdict = true;
+}
+
 void push_unit(std::vector<int32_t>& units, std::vector<int64_t>& vox, const int64_t* idx, int ko,
                int64_t ra, int64_t re, int64_t vox_per_row, int64_t target, int64_t quantum) {
   int64_t rows = std::max<int64_t>(1, target / std::max<int64_t>(1, vox_per_row));
@@ -519,14 +578,15 @@ int tensor_map(mclahe_plan_s* pl, int fam, const void* in) {
   if (pl->map_ptr[fam] == in) return MCLAHE_OK;
   const int slot = fam;
   if (fam == 2) fam = 1;  // output view of the blend family
-  const Pencil& c = fam == 0 ? pl->hist : pl->interp;
+  if (fam == 4) fam = 3;  // output view of the folded-pair blend
+  const Pencil& c = fam == 0 ? pl->hist : (fam == 3 ? pl->interp_m : pl->interp);
   EncodeTiledFn enc = encode_fn();
   if (!enc) return fail(MCLAHE_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[5], strides[5];
   cuuint32_t box[5], es[5];
   int r = 0;
-  const bool seg = fam == 1;
-  const int64_t inner = seg ? 32 : c.width;
+  const bool seg = fam == 1 || fam == 3;
+  const int64_t inner = fam == 1 ? 32 : (fam == 3 ? 8 : c.width);
   dims[r] = (cuuint64_t)inner;
   box[r] = (cuuint32_t)inner;
   ++r;
@@ -546,7 +606,8 @@ int tensor_map(mclahe_plan_s* pl, int fam, const void* in) {
   const CUresult res = enc(&pl->map[slot], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, (cuuint32_t)r,
                            const_cast<void*>(in), dims, strides, box, es,
                            CU_TENSOR_MAP_INTERLEAVE_NONE,
-                           seg ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                           fam == 1 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                    : (fam == 3 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_NONE),
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (res != CUDA_SUCCESS)
     return fail(MCLAHE_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)res) + ")");
@@ -636,6 +697,7 @@ int plan_describe(const mclahe_params_t* params, int64_t row_begin, int64_t row_
   // streamed chunk plans (full_window) interleave range passes with mappings,
   // so a dictionary numbered per chunk would not be stable: edge tables only
   if (!full_window) plan_dict(pl);
+  if (!full_window) plan_mdict(pl);
   return MCLAHE_OK;
 }
 
@@ -722,13 +784,17 @@ int device_init(mclahe_plan_s* pl) {
     InterpFn f = interp_fn(pl->interp.ko, pl->interp.kt, A, pl->p.n_bins);
     MG_CUDA(raise_smem_cap(f, max_smem));
     if (pl->dict_cap) MG_CUDA(raise_smem_cap(get_interp_pencil_dict(pl->interp.ko, pl->interp.kt), max_smem));
+    if (pl->mdict) {
+      MG_CUDA(raise_smem_cap(get_interp_mdict(pl->interp.ko, false), max_smem));
+      MG_CUDA(raise_smem_cap(get_interp_mdict(pl->interp.ko, true), max_smem));
+    }
     MG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f, kBlendThreads, pl->interp.smem));
     pl->interp_grid = (int)std::max<int64_t>(
         1, std::min<int64_t>((int64_t)pl->interp_vox.size(), (int64_t)std::max(occ, 1) * pl->sms));
     interp_cta = balance(pl->interp_vox, pl->interp_grid);
   }
   const size_t total = pl->hist_units.size() + hist_cta.size() + pl->interp_units.size() +
-                       interp_cta.size() + 4;
+                       interp_cta.size() + pl->mdict_units.size() + 4;
   MG_CUDA(cudaMalloc(&pl->d_tables, total * sizeof(int32_t)));
   std::vector<int32_t> host;
   host.reserve(total);
@@ -740,6 +806,8 @@ int device_init(mclahe_plan_s* pl) {
   host.insert(host.end(), pl->interp_units.begin(), pl->interp_units.end());
   pl->off_interp_cta = (int64_t)host.size();
   host.insert(host.end(), interp_cta.begin(), interp_cta.end());
+  pl->off_mdict_units = (int64_t)host.size();
+  host.insert(host.end(), pl->mdict_units.begin(), pl->mdict_units.end());
   host.resize(total, 0);
   MG_CUDA(cudaMemcpy(pl->d_tables, host.data(), total * sizeof(int32_t), cudaMemcpyHostToDevice));
   pl->range_grid = pl->sms * 4;
@@ -945,7 +1013,21 @@ int do_interp(mclahe_plan_s* pl, const void* in, void* out, void* ws, cudaStream
               (long long)pl->interp.P, fa.numRegs, fa.maxThreadsPerBlock, fa.sharedSizeBytes,
               fa.maxDynamicSharedSizeBytes);
     }
-    if (pl->dict_cap) {  // value-dictionary blend; exits at once when the dictionary is unusable
+    if (pl->mdict) {  // folded-pair dictionary blend; exits at once when the dictionary is unusable
+      if ((rc = tensor_map(pl, 3, in))) return rc;
+      if ((rc = tensor_map(pl, 4, out))) return rc;
+      KGeom Gm = pencil_geom(*pl, pl->interp_m);
+      Gm.seg_items = 1;
+      Gm.dyn_units = (int)(pl->mdict_units.size() / kUnitInts) * pl->interp_m.nseg;
+      if (!G.dyn_units) MG_CUDA(cudaMemsetAsync(W.range + 3, 0, sizeof(int64_t), st));
+      const int grid = (int)std::min<int64_t>(Gm.dyn_units, pl->sms);
+      // in-place results + TMA store (MCLAHE_MDICT_STG=1: per-lane global stores, A/B)
+      static const bool tstore = getenv("MCLAHE_MDICT_STG") == nullptr;
+      get_interp_mdict(pl->interp.ko, tstore)<<<grid, kBlendThreads, pl->interp_m.smem, st>>>(
+          Gm, pl->map[3], pl->map[4], static_cast<const float*>(in), static_cast<float*>(out),
+          pl->d_tables + pl->off_mdict_units, pl->d_tables + pl->off_interp_cta, W);
+      MG_LAUNCHED();
+    } else if (pl->dict_cap) {  // value-dictionary blend; exits at once when the dictionary is unusable
       KGeom Gd = G;
       Gd.nst = pl->dict_nst;
       get_interp_pencil_dict(pl->interp.ko, pl->interp.kt)<<<pl->interp_grid, kBlendThreads,
