@@ -96,34 +96,50 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
     if (key != cur) {  // new work item: fold the two columns' corner pairs into M
       consumers_sync<kConsumersBlend>();
       seg = S.seg;
-      int64_t ofc[NCO];
+      // window tile of corner co's trailing row: of0 + sum_j bit_j(co) * tstride[j]
+      int64_t of0 = (S.cell[0] - G.trow0) * G.tstride[0];
 #pragma unroll
-      for (int co = 0; co < NCO; ++co) {
-        int64_t of = (S.cell[0] + ((co >> (KO - 1)) & 1) - G.trow0) * G.tstride[0];
+      for (int j = 1; j < KO; ++j) of0 += S.cell[j] * G.tstride[j];
+      auto ofc = [&](int co) {
+        int64_t of = of0;
 #pragma unroll
-        for (int j = 1; j < KO; ++j) of += (S.cell[j] + ((co >> (KO - 1 - j)) & 1)) * G.tstride[j];
-        ofc[co] = of;
-        if (tid == 0) ofS[co] = (int)of;
-      }
+        for (int j = 0; j < KO; ++j) of += ((co >> (KO - 1 - j)) & 1) * G.tstride[j];
+        return of;
+      };
+      if (tid < NCO) ofS[tid] = (int)ofc(tid);
       const int nv4 = (s_nv + 3) >> 2;
       const int ntask = 2 * NCO * nv4;
-#pragma unroll 2
-      for (int k = tid; k < ntask; k += kConsumersBlend) {
-        const int v4 = k % nv4, cc = k / nv4;  // cc = c * NCO + co
-        const int c = cc / NCO, co = cc - c * NCO;
-        const int col = seg * 2 + c;
-        const int64_t t0 = ofc[co] + colT[min(col, ncol - 1)];
-        const float4 L0 = __ldg(reinterpret_cast<const float4*>(W.lutd + t0 * KC) + v4);
-        const float4 L1 = __ldg(reinterpret_cast<const float4*>(W.lutd + (t0 + tstr1) * KC) + v4);
-        const float a0[4] = {L0.x, L0.y, L0.z, L0.w}, a1[4] = {L1.x, L1.y, L1.z, L1.w};
+      // a thread's tasks in batches of four: all eight L2 loads in flight first
+#pragma unroll 1
+      for (int k0 = tid; k0 < ntask; k0 += 4 * kConsumersBlend) {
+        float4 L0[4], L1[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const float2 tw = *reinterpret_cast<const float2*>(colW + (min(col, ncol - 1) * 4 + i) * 2);
-          float r[4];
+        for (int b = 0; b < 4; ++b) {
+          const int k = min(k0 + b * kConsumersBlend, ntask - 1);
+          const int v4 = k % nv4, cc = k / nv4;  // cc = c * NCO + co
+          const int c = cc / NCO, co = cc - c * NCO;
+          const int64_t t0 = ofc(co) + colT[min(seg * 2 + c, ncol - 1)];
+          L0[b] = __ldg(reinterpret_cast<const float4*>(W.lutd + t0 * KC) + v4);
+          L1[b] = __ldg(reinterpret_cast<const float4*>(W.lutd + (t0 + tstr1) * KC) + v4);
+        }
 #pragma unroll
-          for (int e = 0; e < 4; ++e) r[e] = fmaf(tw.y, a1[e], tw.x * a0[e]);
-          reinterpret_cast<float4*>(Ms + ((c * 4 + i) * NCO + co) * KC)[v4] =
-              make_float4(r[0], r[1], r[2], r[3]);
+        for (int b = 0; b < 4; ++b) {
+          const int k = k0 + b * kConsumersBlend;
+          if (k >= ntask) break;
+          const int v4 = k % nv4, cc = k / nv4;
+          const int c = cc / NCO, co = cc - c * NCO;
+          const int colc = min(seg * 2 + c, ncol - 1);
+          const float a0[4] = {L0[b].x, L0[b].y, L0[b].z, L0[b].w};
+          const float a1[4] = {L1[b].x, L1[b].y, L1[b].z, L1[b].w};
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const float2 tw = *reinterpret_cast<const float2*>(colW + (colc * 4 + i) * 2);
+            float r[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) r[e] = fmaf(tw.y, a1[e], tw.x * a0[e]);
+            reinterpret_cast<float4*>(Ms + ((c * 4 + i) * NCO + co) * KC)[v4] =
+                make_float4(r[0], r[1], r[2], r[3]);
+          }
         }
       }
       consumers_sync<kConsumersBlend>();
@@ -213,25 +229,24 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
         for (int i = 0; i < 4; ++i) acc[i] = fmaf(wo[co], m[i], acc[i]);
       });
       if (miss) {  // values the (sampled) dictionary lacks: from the workspace LUTs
-        const int tt = colT[min(col, ncol - 1)];
-#pragma unroll 1
-        for (int i = 0; i < 4; ++i)
-          if ((miss >> i) & 1) {
-            const float2 tw =
-                *reinterpret_cast<const float2*>(colW + (min(col, ncol - 1) * 4 + i) * 2);
-            float a = 0.0f;
-#pragma unroll 1
-            for (int co = 0; co < NCO; ++co) {
-              const int t0 = ofS[co] + tt;
+        const int colc = min(col, ncol - 1);
+        const int tt = colT[colc];
+        float a[4] = {0.f, 0.f, 0.f, 0.f};
+        static_for<0, NCO>([&](auto coc) {  // same order as the gathers above
+          constexpr int co = decltype(coc)::value;
+          const int t0 = ofS[co] + tt;
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            if ((miss >> i) & 1) {
+              const float2 tw = *reinterpret_cast<const float2*>(colW + (colc * 4 + i) * 2);
               const float L0 = lut_value_global(W, n, t0, vv[i]);
               const float L1 = lut_value_global(W, n, t0 + tstr1, vv[i]);
-              a = fmaf(pick(wo, co), fmaf(tw.y, L1, tw.x * L0), a);
+              a[i] = fmaf(wo[co], fmaf(tw.y, L1, tw.x * L0), a[i]);
             }
-            if (i == 0) acc[0] = a;
-            else if (i == 1) acc[1] = a;
-            else if (i == 2) acc[2] = a;
-            else acc[3] = a;
-          }
+        });
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          if ((miss >> i) & 1) acc[i] = a[i];
       }
       float4 r;
       r.x = fminf(fmaxf(acc[0], 0.f), 1.f);
