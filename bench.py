@@ -434,9 +434,13 @@ def main():
             if os.path.exists(tp):
                 with open(tp) as f:
                     traffic = json.load(f).get("interp")
+            ds = plan.dict_state(ws)
+            kname = ("k_interp_mdict (K4 folded-pair dictionary blend)" if ds["folded"] else
+                     "k_interp_pencil<DICT> (K4 dictionary blend)" if ds["used"] else
+                     "k_interp_pencil (K4 blend)")
             line["roofline"] = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
                                 "frac": ach / peak, "traffic": traffic,
-                                "kernel": "k_interp_pencil (K4 blend)",
+                                "kernel": kname,
                                 "algo_bytes_per_launch": algo["interp"],
                                 "peak_source": f"{peak_kind} hbm_gbs"}
             line["passes"] = passes

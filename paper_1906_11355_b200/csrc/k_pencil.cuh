@@ -101,12 +101,20 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
   int trt[4], dummy;
 #pragma unroll
   for (int i = 0; i < 4; ++i) trailing_tile(G, e0 + i, &trt[i], &dummy);
-  float mn[4], mx[4];
+  float mn[4], mx[4], mn2[4], mx2[4];
   int bad = 0;
   int64_t cur = -1;
   const int64_t stage_elems = G.stage_stride;
+  const int P4 = (int)G.P;
+  const int rstep = G.rpi * P4;
+  const int trips = slot < G.stage_rows ? (G.stage_rows - slot + G.rpi - 1) / G.rpi : 0;
 
   auto flush = [&]() {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      mn[i] = fminf(mn[i], mn2[i]);
+      mx[i] = fmaxf(mx[i], mx2[i]);
+    }
 #pragma unroll
     for (int i = 0; i < 4; ++i)
       if (lane_on && mn[i] <= mx[i]) {
@@ -136,18 +144,48 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
       for (int64_t t = tid; t < G.gtr; t += kConsumers) smin[t] = smax[t] = INT32_MIN;
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        mn[i] = INFINITY;
-        mx[i] = -INFINITY;
+        mn[i] = mn2[i] = INFINITY;
+        mx[i] = mx2[i] = -INFINITY;
       }
       consumers_sync();
       cur = key;
     }
-    const int rows = G.stage_rows;
     const float* buf = P.bufs + s * stage_elems;
     if (lane_on) {
+      // rows in groups of four (four LDS.128 in flight, two min/max chains);
+      // every fourth row pass (warp-uniform, rotating with the stage) feeds the
+      // dictionary sample: values the sample misses are rare ones, which the
+      // blend resolves from the workspace LUTs
+      const float* rp = buf + slot * P4 + e0;
+      const int jd = (int)((0u - it) & 3u);  // sampled row of each group
       int k = 0;
-      for (int q = slot; q < rows; q += G.rpi, ++k) {
-        const float4 v = *reinterpret_cast<const float4*>(buf + q * G.P + e0);
+#pragma unroll 1
+      for (; k + 4 <= trips; k += 4, rp += 4 * rstep) {
+        float4 v[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) v[j] = *reinterpret_cast<const float4*>(rp + j * rstep);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float a[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
+          float* m0 = (j & 1) ? mn2 : mn;
+          float* m1 = (j & 1) ? mx2 : mx;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            bad |= !isfinite(a[i]);
+            m0[i] = fminf(m0[i], a[i]);
+            m1[i] = fmaxf(m1[i], a[i]);
+          }
+        }
+        if (DICT && !*reinterpret_cast<volatile int*>(&s_over)) {
+          const float4 w = jd == 0 ? v[0] : jd == 1 ? v[1] : jd == 2 ? v[2] : v[3];
+          const float a[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            if (i == 0 || a[i] != a[i - 1]) dict_add(a[i]);  // runs of equal values: once
+        }
+      }
+      for (; k < trips; ++k, rp += rstep) {
+        const float4 v = *reinterpret_cast<const float4*>(rp);
         const float a[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
@@ -155,9 +193,6 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
           mn[i] = fminf(mn[i], a[i]);
           mx[i] = fmaxf(mx[i], a[i]);
         }
-        // every fourth row pass (warp-uniform, rotating with the stage): values
-        // the sample misses are rare ones, which the blend resolves from the
-        // edge tables
         if (DICT && ((k + it) & 3) == 0 && !*reinterpret_cast<volatile int*>(&s_over)) {
 #pragma unroll
           for (int i = 0; i < 4; ++i) dict_add(a[i]);

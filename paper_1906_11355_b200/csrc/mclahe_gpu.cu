@@ -1597,7 +1597,7 @@ int mclahe_plan_dict_state(mclahe_plan_t plan, const void* workspace, int32_t* s
   MG_CUDA(cudaMemcpyAsync(m, static_cast<const char*>(workspace) + plan->off_dict, sizeof m,
                           cudaMemcpyDeviceToHost, st));
   MG_CUDA(cudaStreamSynchronize(st));
-  state[0] = m[2];
+  state[0] = m[2] ? (plan->mdict ? 2 : 1) : 0;
   state[1] = m[3];
   state[3] = m[2] ? m[4] : 0;
   return MCLAHE_OK;
