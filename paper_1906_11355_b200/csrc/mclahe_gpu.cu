@@ -271,7 +271,9 @@ Pencil choose_pencil(const mclahe_plan_s& pl, bool for_hist) {
       if (c.gtr * n >= (int64_t{1} << 31) / 2) continue;
       c.tail = align_up(c.gtr * (n + 1) * 4, 16) + c.gtr * 16 + (pl.p.adaptive ? c.gtr : 1) * (n + 1) * 4;
       if (c.tail > 64 * 1024) continue;
-      c.stage_budget = kStageBytes;  // 3 stages, ~3 CTAs per SM
+      static const int64_t k2_stage =
+          getenv("MCLAHE_K2_STAGE_KB") ? atoi(getenv("MCLAHE_K2_STAGE_KB")) * 1024 : kStageBytes;
+      c.stage_budget = k2_stage;  // 3 stages, ~3 CTAs per SM
     } else {
       if (n % 4 != 0 || c.P % 32 != 0) continue;
       c.nseg = (int)(c.P / 32);
@@ -385,7 +387,8 @@ void size_boxes(const mclahe_plan_s& pl, Pencil& c, bool cells) {
   c.stage_stride = cells ? align_up(c.stage_rows * 128, 1024) / 4 : align_up(c.stage_rows * c.P * 4, 128) / 4;
   const int64_t stage = c.stage_stride * 4;
   if (!cells) {
-    c.nst = 3;
+    static const int k2_nst = getenv("MCLAHE_K2_NST") ? atoi(getenv("MCLAHE_K2_NST")) : 3;
+    c.nst = k2_nst;
   } else {
     c.nst = (int)std::max<int64_t>(2, std::min<int64_t>(4, (226 * 1024 - kPipeBytes - c.tail) / stage));
   }
