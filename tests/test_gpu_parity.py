@@ -357,14 +357,24 @@ def _run_plan(M, x, kernel, nb, clip, ad, no_dict=False):
     return out, plan.dict_state(ws)
 
 
-@pytest.mark.parametrize("case", ["poisson", "edges", "scaled4d", "many", "uneven"])
+@pytest.mark.parametrize("case", ["poisson", "edges", "scaled4d", "many", "uneven", "rare", "wide"])
 def test_value_dictionary_blend(M, case):
-    # quantised volumes (few distinct values) take the value-dictionary blend;
+    # quantised volumes (few distinct values) take the value-dictionary blend
+    # (rank 4 with one trailing dim: the folded-pair kernel k_interp_mdict);
     # it must equal the oracle and, bit for bit, the edge-table blend
-    rng = np.random.default_rng({"poisson": 1, "edges": 2, "scaled4d": 3, "many": 4, "uneven": 5}[case])
+    rng = np.random.default_rng({"poisson": 1, "edges": 2, "scaled4d": 3, "many": 4, "uneven": 5,
+                                 "rare": 6, "wide": 7}[case])
     if case == "poisson":
         x = (rng.poisson(3.0, (48, 40, 24, 32)) / 11.0).astype(np.float32)
         args = ((12, 10, 6, 4), 256, 0.02, True)
+    elif case == "rare":  # values the sampled dictionary misses: the workspace-LUT path
+        x = (rng.poisson(3.0, (32, 32, 16, 32)) / 11.0).astype(np.float32)
+        pos = rng.choice(x.size, 400, replace=False)
+        x.reshape(-1)[pos] = (0.3 + np.arange(400) * 1e-4).astype(np.float32)
+        args = ((8, 8, 4, 4), 256, 0.02, True)
+    elif case == "wide":  # trailing cells of two columns, eight 8-float segments
+        x = (rng.poisson(2.0, (32, 24, 16, 64)) / 7.0).astype(np.float32)
+        args = ((8, 8, 4, 8), 128, 0.03, True)
     elif case == "edges":
         x = (np.round(rng.random((40, 36, 32)) * 9) / 9).astype(np.float32)
         x[:8] = 0.5  # constant (degenerate) tiles too
@@ -387,9 +397,13 @@ def test_value_dictionary_blend(M, case):
     assert st0["capacity"] == 0 and not st0["used"]
     assert st["capacity"] > 0
     assert st["used"] == (case != "many"), st
+    # folded pairs: rank 4, one trailing dim, power-of-two cells (>= 32-row stages)
+    assert st["folded"] == (case in ("scaled4d", "uneven", "rare", "wide")), st
     if case != "many":  # K2a samples a quarter of the rows
         assert 0 < st["values"] <= len(np.unique(x.view(np.uint32))), st
-        assert st["affine"] == (case != "uneven"), st  # evenly quantised: direct table
+        if case == "rare":
+            assert st["values"] < len(np.unique(x.view(np.uint32))), st  # misses exercised
+        assert st["affine"] == (case not in ("uneven", "rare")), st  # evenly quantised: direct table
     assert torch.equal(out, ref)
     want = O.mclahe(x, *args, "c")
     assert np.max(np.abs(out.cpu().numpy().astype(np.float64) - want)) <= OUT_TOL
