@@ -435,7 +435,8 @@ def main():
                 with open(tp) as f:
                     traffic = json.load(f).get("interp")
             ds = plan.dict_state(ws)
-            kname = ("k_interp_mdict (K4 folded-pair dictionary blend)" if ds["folded"] else
+            kname = ("k_interp_mdict (K4 folded-pair dictionary blend)" if ds["folded"] and ds["used"] else
+                     "k_interp_mdict (K4 folded-pair blend, global range)" if ds["folded"] else
                      "k_interp_pencil<DICT> (K4 dictionary blend)" if ds["used"] else
                      "k_interp_pencil (K4 blend)")
             line["roofline"] = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",

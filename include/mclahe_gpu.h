@@ -180,8 +180,9 @@ int mclahe_debug_bin_index(int32_t dtype, const void* values_dev, int64_t n, dou
                            double hi, int64_t n_bins, int32_t* out_dev, void* stream);
 
 /* Value-dictionary state after a run on `workspace` (synchronises `stream`):
- * state[0] = 1 if the last blend used the dictionary path (2: the folded-pair
- * dictionary blend, k_interp_mdict), 0 if it used the edge tables, state[1] = number
+ * state[0] = 1 if the last blend used the dictionary path, 2 if it used the
+ * folded-pair blend k_interp_mdict (adaptive: with the dictionary; global
+ * mode, capacity 0: always when the plan arms it), 0 otherwise, state[1] = number
  * of distinct values collected, state[2] = the plan's capacity (0: never),
  * state[3] = 1 if values were looked up through the affine direct table
  * (0: cuckoo hash).  state has 4 entries. */

@@ -204,8 +204,8 @@ class Plan:
         (0 when the plan never arms it), ``affine`` (direct-table lookup)."""
         st = (C.c_int32 * 4)()
         N.check(N.lib().mclahe_plan_dict_state(self._h, self._ptr(ws), st, _stream_handle(stream)))
-        return dict(used=bool(st[0]), folded=st[0] == 2, values=int(st[1]), capacity=int(st[2]),
-                    affine=bool(st[3]))
+        return dict(used=st[0] == 1 or (st[0] == 2 and st[2] > 0), folded=st[0] == 2,
+                    values=int(st[1]), capacity=int(st[2]), affine=bool(st[3]))
 
     def tile_stats(self, x, stream=None) -> dict:
         """Runs passes 1-3 and returns the per-tile intermediates of the

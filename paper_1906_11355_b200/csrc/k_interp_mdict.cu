@@ -27,8 +27,10 @@ namespace mg {
 
 // TSTORE: results written in place into the stage and TMA-stored by the
 // producer (otherwise each lane stores its 16 bytes straight to global).
-// NWARP consumer warps (+ one producer warp).
-template <int KO, bool TSTORE, int NWARP>
+// NWARP consumer warps (+ one producer warp).  ADAPT: value-dictionary tables
+// (TK = kDictKC values per row); global mode (!ADAPT): one bin per voxel from
+// the global edge table, tables per bin (TK = n_bins).
+template <int KO, bool TSTORE, int NWARP, bool ADAPT, int TK>
 __global__ void __launch_bounds__(NWARP * 32 + 32, 1)
     k_interp_mdict(const __grid_constant__ KGeom G, const __grid_constant__ CUtensorMap tmap,
                    const __grid_constant__ CUtensorMap omap, const float* __restrict__ in,
@@ -37,14 +39,15 @@ __global__ void __launch_bounds__(NWARP * 32 + 32, 1)
   constexpr int NCO = 1 << KO;
   constexpr int kMdictConsumers = NWARP * 32;
   constexpr int NW = NWARP;
-  constexpr int KC = kDictKC;
+  constexpr int KC = TK;
   if (W.range[2] != 0) return;  // non-finite input: write nothing
-  if (W.dmeta[2] == 0) return;  // no usable dictionary: the edge-table blend runs
+  if (ADAPT && W.dmeta[2] == 0) return;  // no usable dictionary: the edge-table blend runs
   extern __shared__ __align__(1024) unsigned char smem[];
   const PencilSmem P = pencil_smem(G, smem);
   const int n = G.n_bins;
   float* Ms = reinterpret_cast<float*>(P.tail);                  // [2][4][NCO][KC]
-  uint2* dltS = reinterpret_cast<uint2*>(Ms + 2 * 4 * NCO * KC);  // [kDictHL]
+  uint2* dltS = reinterpret_cast<uint2*>(Ms + 2 * 4 * NCO * KC);  // ADAPT: [kDictHL]
+  float* thrS = reinterpret_cast<float*>(dltS);                    // global: edge table [n + 1]
   int* ofS = reinterpret_cast<int*>(dltS + kDictHL);              // [NCO]
   const int ncol = (int)(G.P / 4);
   int* colT = reinterpret_cast<int*>(
@@ -75,13 +78,22 @@ __global__ void __launch_bounds__(NWARP * 32 + 32, 1)
       colW[(col * 4 + i) * 2 + 1] = f1;
     }
   }
-  for (int k = tid; k < kDictHL; k += kMdictConsumers) dltS[k] = W.dlt[k];
-  if (tid == 0) {
-    s_dmode = W.dmeta[4];
-    s_dv0 = __int_as_float(W.dmeta[5]);
-    s_dS = __int_as_float(W.dmeta[6]);
-    s_nv = min(W.dmeta[3], KC);
+  if (ADAPT) {
+    for (int k = tid; k < kDictHL; k += kMdictConsumers) dltS[k] = W.dlt[k];
+    if (tid == 0) {
+      s_dmode = W.dmeta[4];
+      s_dv0 = __int_as_float(W.dmeta[5]);
+      s_dS = __int_as_float(W.dmeta[6]);
+      s_nv = min(W.dmeta[3], KC);
+    }
+  } else {
+    for (int k = tid; k <= KC; k += kMdictConsumers) thrS[k] = W.thr[k];
+    if (tid == 0) s_nv = KC;
   }
+  const TileParam<float> g0 = reinterpret_cast<const TileParam<float>*>(W.tparams)[0];
+  const float2 glc = tile_lc(g0);
+  const bool patho = !ADAPT && isnan(glc.y);  // a range the float guard does not cover
+  const float* lsrc = ADAPT ? W.lutd : W.lut;  // rows of KC per tile
   const int tstr1 = (int)G.tstride[G.rank - 1];  // trailing corner: next tile of the last dim
   const int64_t stage_elems = G.stage_stride;
   const int rows = G.stage_rows;
@@ -122,8 +134,8 @@ __global__ void __launch_bounds__(NWARP * 32 + 32, 1)
           const int v4 = k % nv4, cc = k / nv4;  // cc = c * NCO + co
           const int c = cc / NCO, co = cc - c * NCO;
           const int64_t t0 = ofc(co) + colT[min(seg * 2 + c, ncol - 1)];
-          L0[b] = __ldg(reinterpret_cast<const float4*>(W.lutd + t0 * KC) + v4);
-          L1[b] = __ldg(reinterpret_cast<const float4*>(W.lutd + (t0 + tstr1) * KC) + v4);
+          L0[b] = __ldg(reinterpret_cast<const float4*>(lsrc + t0 * KC) + v4);
+          L1[b] = __ldg(reinterpret_cast<const float4*>(lsrc + (t0 + tstr1) * KC) + v4);
         }
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
@@ -206,7 +218,15 @@ __global__ void __launch_bounds__(NWARP * 32 + 32, 1)
       const float4 v4 = *slot4;
       const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
       int di[4];
-      if (s_dmode) {  // affine cells: one LDS.64 per voxel
+      if (!ADAPT) {  // one bin per voxel: the global edge table
+        if (!patho) {
+          bins2_edge(pk2(vv[0], vv[1]), vv[0], vv[1], glc, thrS, KC, di[0], di[1]);
+          bins2_edge(pk2(vv[2], vv[3]), vv[2], vv[3], glc, thrS, KC, di[2], di[3]);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) di[i] = bin_search(vv[i], thrS, KC);
+        }
+      } else if (s_dmode) {  // affine cells: one LDS.64 per voxel
         int cl[4];
         cl[0] = dict_cell(vv[0], vv[1], s_dv0, s_dS, &cl[1]);
         cl[2] = dict_cell(vv[2], vv[3], s_dv0, s_dS, &cl[3]);
@@ -235,7 +255,7 @@ __global__ void __launch_bounds__(NWARP * 32 + 32, 1)
 #pragma unroll
         for (int i = 0; i < 4; ++i) acc[i] = fmaf(wo[co], m[i], acc[i]);
       });
-      if (miss) {  // values the (sampled) dictionary lacks: from the workspace LUTs
+      if (ADAPT && miss) {  // values the (sampled) dictionary lacks: from the workspace LUTs
         const int colc = min(col, ncol - 1);
         const int tt = colT[colc];
         float a[4] = {0.f, 0.f, 0.f, 0.f};
@@ -277,9 +297,16 @@ __global__ void __launch_bounds__(NWARP * 32 + 32, 1)
 
 // 16 consumer warps at 96 registers: 20 / 24 warps (80 / 72 registers) measured
 // 0.78 / 0.86 ms against 0.72 ms on the 4D config.
-PencilInterpFn get_interp_mdict(int ko, bool tma_store) {
+PencilInterpFn get_interp_mdict(int ko, bool tma_store, bool adaptive, int n_bins) {
   if (ko != 3) return nullptr;
-  return tma_store ? k_interp_mdict<3, true, 16> : k_interp_mdict<3, false, 16>;
+  if (adaptive)
+    return tma_store ? k_interp_mdict<3, true, 16, true, kDictKC>
+                     : k_interp_mdict<3, false, 16, true, kDictKC>;
+  switch (n_bins) {
+    case 256: return tma_store ? k_interp_mdict<3, true, 16, false, 256> : k_interp_mdict<3, false, 16, false, 256>;
+    case 512: return tma_store ? k_interp_mdict<3, true, 16, false, 512> : k_interp_mdict<3, false, 16, false, 512>;
+    default: return nullptr;
+  }
 }
 
 }  // namespace mg

@@ -506,7 +506,7 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
   constexpr int NCO = 1 << KO, NCT = 1 << KT;
   constexpr int NW = kConsumersBlend / 32;
   constexpr bool DICT = NB < 0;
-  constexpr bool MORD = ADAPT && KT == 1 && KO == 3;
+  constexpr bool MORD = KT == 1 && KO == 3;
   if (W.range[2] != 0) return;  // non-finite input: write nothing
   if (DICT) {
     if (W.dmeta[2] == 0) return;
@@ -813,8 +813,8 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
         for (int ct = 0; ct < NCT; ++ct)
 #pragma unroll
           for (int i = 0; i < 4; ++i) act[ct][i] = 0.f;
-        // MORD (adaptive, one trailing dim, KO == 3): the value-dictionary
-        // blend k_interp_mdict folds the two trailing corners first,
+        // MORD (one trailing dim, KO == 3): the folded-pair blend
+        // k_interp_mdict folds the two trailing corners first,
         // M = fma(tw1, L1, tw0 * L0), and sums act = fma(wo, M, act) over
         // co; the adaptive paths here sum in that order too (same bits)
         auto accum = [&](float w, const float (&m)[NCT][4]) {
@@ -1055,8 +1055,12 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
 #pragma unroll
               for (int i = 0; i < 4; ++i) {
                 const float2 p = *reinterpret_cast<const float2*>(Pb + bo[i]);
-                act[0][i] = fmaf(wo[co], p.x, act[0][i]);
-                act[1 % NCT][i] = fmaf(wo[co], p.y, act[1 % NCT][i]);
+                if constexpr (MORD) {
+                  act[0][i] = fmaf(wo[co], fmaf(tw[i][1 % NCT], p.y, tw[i][0] * p.x), act[0][i]);
+                } else {
+                  act[0][i] = fmaf(wo[co], p.x, act[0][i]);
+                  act[1 % NCT][i] = fmaf(wo[co], p.y, act[1 % NCT][i]);
+                }
               }
             }
           } else
@@ -1125,6 +1129,7 @@ PencilRangeFn get_range_pencil(int ko, bool dict);
 PencilHistFn get_hist_pencil(int ko, bool adaptive);
 PencilInterpFn get_interp_pencil(int ko, int kt, bool adaptive, int n_bins);
 PencilInterpFn get_interp_pencil_dict(int ko, int kt);
-PencilInterpFn get_interp_mdict(int ko, bool tma_store);  // nullptr: none for ko
+// folded-pair blend; nullptr: none for this (ko, mode, n_bins)
+PencilInterpFn get_interp_mdict(int ko, bool tma_store, bool adaptive, int n_bins);
 
 }  // namespace mg

@@ -422,9 +422,11 @@ void plan_dict(mclahe_plan_s* pl) {
 void plan_mdict(mclahe_plan_s* pl) {
   pl->mdict = false;
   const Pencil& c = pl->interp;
-  if (!pl->dict_cap || !c.on || c.kt != 1 || c.ko != 3 || c.P % 8 != 0 || !get_interp_mdict(c.ko, false) ||
-      getenv("MCLAHE_NO_MDICT"))
+  const bool A = pl->p.adaptive != 0;
+  if ((A && !pl->dict_cap) || !pl->f32() || !c.on || c.kt != 1 || c.ko != 3 || c.P % 8 != 0 ||
+      !get_interp_mdict(c.ko, false, A, (int)pl->p.n_bins) || getenv("MCLAHE_NO_MDICT"))
     return;
+  const int64_t tk = A ? kDictKC : pl->p.n_bins;  // table row: dictionary values or bins
   Pencil m = c;
   m.nseg = (int)(c.P / 8);
   m.tma_rank = c.ko + 2;
@@ -443,7 +445,7 @@ void plan_mdict(mclahe_plan_s* pl) {
   if (m.stage_rows < 32) return;
   m.stage_stride = align_up(m.stage_rows * 32, 1024) / 4;
   const int64_t nco = int64_t{1} << c.ko;
-  m.tail = 2 * 4 * nco * kDictKC * 4 + kDictHL * 8 + nco * 4 + 16 + ((c.P / 4 + 3) & ~int64_t(3)) * 4 +
+  m.tail = 2 * 4 * nco * tk * 4 + kDictHL * 8 + nco * 4 + 16 + ((c.P / 4 + 3) & ~int64_t(3)) * 4 +
            (c.P / 4) * 32 + 16;
   const int64_t stage = m.stage_stride * 4;
   const int64_t nst = std::min<int64_t>(std::min(nst_cap, kMaxStages), (226 * 1024 - kPipeBytes - m.tail) / stage);
@@ -788,8 +790,8 @@ int device_init(mclahe_plan_s* pl) {
     MG_CUDA(raise_smem_cap(f, max_smem));
     if (pl->dict_cap) MG_CUDA(raise_smem_cap(get_interp_pencil_dict(pl->interp.ko, pl->interp.kt), max_smem));
     if (pl->mdict) {
-      MG_CUDA(raise_smem_cap(get_interp_mdict(pl->interp.ko, false), max_smem));
-      MG_CUDA(raise_smem_cap(get_interp_mdict(pl->interp.ko, true), max_smem));
+      MG_CUDA(raise_smem_cap(get_interp_mdict(pl->interp.ko, false, A, (int)pl->p.n_bins), max_smem));
+      MG_CUDA(raise_smem_cap(get_interp_mdict(pl->interp.ko, true, A, (int)pl->p.n_bins), max_smem));
     }
     MG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f, kBlendThreads, pl->interp.smem));
     pl->interp_grid = (int)std::max<int64_t>(
@@ -1026,10 +1028,12 @@ int do_interp(mclahe_plan_s* pl, const void* in, void* out, void* ws, cudaStream
       const int grid = (int)std::min<int64_t>(Gm.dyn_units, pl->sms);
       // in-place results + TMA store (MCLAHE_MDICT_STG=1: per-lane global stores, A/B)
       static const bool tstore = getenv("MCLAHE_MDICT_STG") == nullptr;
-      get_interp_mdict(pl->interp.ko, tstore)<<<grid, kBlendThreads, pl->interp_m.smem, st>>>(
+      get_interp_mdict(pl->interp.ko, tstore, A, (int)pl->p.n_bins)<<<grid, kBlendThreads,
+                                                                  pl->interp_m.smem, st>>>(
           Gm, pl->map[3], pl->map[4], static_cast<const float*>(in), static_cast<float*>(out),
           pl->d_tables + pl->off_mdict_units, pl->d_tables + pl->off_interp_cta, W);
       MG_LAUNCHED();
+      if (!A) return MCLAHE_OK;  // global mode: the folded-pair blend is the blend
     } else if (pl->dict_cap) {  // value-dictionary blend; exits at once when the dictionary is unusable
       KGeom Gd = G;
       Gd.nst = pl->dict_nst;
@@ -1593,7 +1597,10 @@ int mclahe_plan_dict_state(mclahe_plan_t plan, const void* workspace, int32_t* s
   if (!plan || !state) return fail(MCLAHE_ERR_VALIDATION, "plan and state must be non-NULL");
   state[0] = state[1] = state[3] = 0;
   state[2] = plan->dict_cap;
-  if (!plan->dict_cap) return MCLAHE_OK;
+  if (!plan->dict_cap) {  // global mode: the folded-pair blend runs whenever it is armed
+    state[0] = plan->mdict ? 2 : 0;
+    return MCLAHE_OK;
+  }
   if (!workspace) return fail(MCLAHE_ERR_VALIDATION, "workspace must be non-NULL");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   int32_t m[8];

@@ -409,6 +409,25 @@ def test_value_dictionary_blend(M, case):
     assert np.max(np.abs(out.cpu().numpy().astype(np.float64) - want)) <= OUT_TOL
 
 
+@pytest.mark.parametrize("nb", [256, 512])
+def test_folded_pair_blend_global_mode(M, nb):
+    # global range, one trailing dim, three outer dims: the folded-pair blend
+    # (tables per bin) runs; it equals the oracle and, bit for bit, the
+    # edge-table kernel of the streamed host call
+    rng = np.random.default_rng(nb)
+    x = np.clip(rng.normal(0.4, 0.15, (48, 64, 32, 32)), 0, 1).astype(np.float32)
+    x[:, :, 20:] = np.round(x[:, :, 20:] * 9) / 9  # values on bin edges too
+    args = ((16, 16, 8, 8), nb, 0.01, False)
+    out, st = _run_plan(M, x, *args)
+    assert st["folded"] and not st["used"] and st["capacity"] == 0, st
+    want = O.mclahe(x, *args, "c")
+    assert np.max(np.abs(out.cpu().numpy().astype(np.float64) - want)) <= OUT_TOL
+    xx = np.concatenate([x] * 4)  # >= 16 MB: the one-shot host call streams chunks
+    dev, _ = _run_plan(M, xx, *args)
+    host = M.enhance(xx, *args)
+    assert np.array_equal(dev.cpu().numpy(), host)
+
+
 @pytest.mark.parametrize("ad", [True, False])
 def test_sparse_counts_degenerate_neighbours(M, ad):
     # counts on one half of the trailing dim, zeros on the other: constant
