@@ -356,6 +356,11 @@ __device__ __forceinline__ void red_add_if(uint32_t addr, uint32_t val, uint32_t
       : "memory");
 }
 
+// Unconditional shared-memory add.
+__device__ __forceinline__ void red_add(uint32_t addr, uint32_t val) {
+  asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(val) : "memory");
+}
+
 // Exact bin from the edge table alone (binary search over thr[1..n-1]);
 // used for ranges the float guard does not cover.
 __device__ __forceinline__ int bin_search(float v, const float* th, int n) {

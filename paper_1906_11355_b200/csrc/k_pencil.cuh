@@ -271,7 +271,13 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
   // [gtr][n + 1]: the pad word puts equal bins of neighbouring tiles (one per
   // thread of a row) in different banks
   uint32_t* hist = reinterpret_cast<uint32_t*>(P.tail);
-  float2* lcS = reinterpret_cast<float2*>(P.tail + ((G.gtr * (n + 1) * 4 + 15) & ~15LL));  // [gtr]
+  // then one private dummy word per consumer thread (the hot path's suppressed
+  // adds land there: no branches, no conflicts), then {lo, c} per tile
+  const uint32_t dummy_s =
+      (uint32_t)__cvta_generic_to_shared(P.tail + ((G.gtr * (n + 1) * 4 + 15) & ~15LL)) +
+      4u * threadIdx.x;
+  float2* lcS = reinterpret_cast<float2*>(P.tail + ((G.gtr * (n + 1) * 4 + 15) & ~15LL) +
+                                          kConsumers * 4);  // [gtr]
   // bin-edge tables of the pencil's tiles (adaptive) or of the global range
   float* thrS = reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(lcS) + G.gtr * 16);
   const int n1 = n + 1;  // edge-table stride: thr[0] = -inf ... thr[n] = +inf
@@ -377,15 +383,18 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
           a[i] = ha[i] + 4u * (uint32_t)edge_bin(i < 2 ? th0 : th2, clamp_bits_k(tf[i], n), vv[i]);
           if (!ok[i]) a[i] = 0xFFFFFFF0u + i;
         }
+        // runs of equal keys carry their sum on the first add; suppressed adds
+        // (run tails, degenerate tiles) go to the thread's dummy word: every
+        // add unconditional, no branches around the atomics
         const bool e01 = a[0] == a[1], e12 = a[1] == a[2], e23 = a[2] == a[3];
         const uint32_t s3 = w[3];
         const uint32_t s2 = w[2] + (e23 ? s3 : 0u);
         const uint32_t s1 = w[1] + (e12 ? s2 : 0u);
         const uint32_t s0 = w[0] + (e01 ? s1 : 0u);
-        red_add_if(a[0], s0, ok[0]);
-        red_add_if(a[1], s1, ok[1] & !e01);
-        red_add_if(a[2], s2, ok[2] & !e12);
-        red_add_if(a[3], s3, ok[3] & !e23);
+        red_add(ok[0] ? a[0] : dummy_s, s0);
+        red_add(ok[1] && !e01 ? a[1] : dummy_s, s1);
+        red_add(ok[2] && !e12 ? a[2] : dummy_s, s2);
+        red_add(ok[3] && !e23 ? a[3] : dummy_s, s3);
       }
     } else if (lane_on) {
       const bool wuni = S.wuni != 0;

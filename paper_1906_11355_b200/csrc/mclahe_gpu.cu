@@ -269,7 +269,8 @@ Pencil choose_pencil(const mclahe_plan_s& pl, bool for_hist) {
     if (for_hist) {
       if (!merged) continue;
       if (c.gtr * n >= (int64_t{1} << 31) / 2) continue;
-      c.tail = align_up(c.gtr * (n + 1) * 4, 16) + c.gtr * 16 + (pl.p.adaptive ? c.gtr : 1) * (n + 1) * 4;
+      c.tail = align_up(c.gtr * (n + 1) * 4, 16) + kConsumers * 4 + c.gtr * 16 +
+               (pl.p.adaptive ? c.gtr : 1) * (n + 1) * 4;
       if (c.tail > 64 * 1024) continue;
       static const int64_t k2_stage =
           getenv("MCLAHE_K2_STAGE_KB") ? atoi(getenv("MCLAHE_K2_STAGE_KB")) * 1024 : kStageBytes;
