@@ -304,8 +304,10 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
   bool patho = !ADAPT && isnan(glc.y);  // a range the float guard does not cover
   __shared__ int s_bad;
   const float kDegC = degenerate_lc().y;
-  float2 lcv[4];
-  const float* thv[4];
+  float2 lc0, lc2;  // {lo, c} of voxels 0 / 2 (hot path); the others re-read
+  auto lcv = [&](int i) { return i == 0 ? lc0 : i == 2 ? lc2 : (ADAPT ? lcS[trt[i]] : glc); };
+  // a voxel's edge table: thrS + tile * (n + 1) (adaptive) or the global row
+  auto thv = [&](int i) { return thrS + (ADAPT ? trt[i] * n1 : 0); };
   int hb[4];
   const bool same_pairs = !ADAPT || (trt[0] == trt[1] && trt[2] == trt[3]);
   const uint32_t hist_s = (uint32_t)__cvta_generic_to_shared(hist);
@@ -342,9 +344,10 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
       // per-thread tile constants for this pencil
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        lcv[i] = ADAPT ? lcS[trt[i]] : glc;
-        thv[i] = thrS + (ADAPT ? trt[i] * n1 : 0);
-        hb[i] = (!ADAPT || lcv[i].y != kDegC) ? trt[i] * (n + 1) : -1;  // degenerate: none
+        const float2 lc = ADAPT ? lcS[trt[i]] : glc;
+        if (i == 0) lc0 = lc;
+        if (i == 2) lc2 = lc;
+        hb[i] = (!ADAPT || lc.y != kDegC) ? trt[i] * (n + 1) : -1;  // degenerate: none
       }
     }
     const int rows = G.stage_rows;
@@ -361,10 +364,10 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
         ok[i] = hb[i] >= 0;
         ha[i] = hist_s + (uint32_t)(hb[i] >= 0 ? hb[i] : 0) * 4u;
       }
-      const uint32_t th0 = (uint32_t)__cvta_generic_to_shared(thv[0]);
-      const uint32_t th2 = (uint32_t)__cvta_generic_to_shared(thv[2]);
-      const u64 L0 = pk2(lcv[0].x, lcv[0].x), C0 = pk2(lcv[0].y, lcv[0].y);
-      const u64 L2 = pk2(lcv[2].x, lcv[2].x), C2 = pk2(lcv[2].y, lcv[2].y);
+      const uint32_t th0 = (uint32_t)__cvta_generic_to_shared(thv(0));
+      const uint32_t th2 = (uint32_t)__cvta_generic_to_shared(thv(2));
+      const u64 L0 = pk2(lc0.x, lc0.x), C0 = pk2(lc0.y, lc0.y);
+      const u64 L2 = pk2(lc2.x, lc2.x), C2 = pk2(lc2.y, lc2.y);
       const float* rp = buf + slot * G.P + e0;
       const int64_t rstep = (int64_t)G.rpi * G.P;
 #pragma unroll 2
@@ -414,21 +417,21 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
         int b[4];
         if (!patho) {
           if (same_pairs) {
-            bins2_edge(pk2(v.x, v.y), v.x, v.y, lcv[0], thv[0], n, b[0], b[1]);
-            bins2_edge(pk2(v.z, v.w), v.z, v.w, lcv[2], thv[2], n, b[2], b[3]);
+            bins2_edge(pk2(v.x, v.y), v.x, v.y, lc0, thv(0), n, b[0], b[1]);
+            bins2_edge(pk2(v.z, v.w), v.z, v.w, lc2, thv(2), n, b[2], b[3]);
           } else {  // pairs straddle a tile boundary: evaluate each against its own tile
             int dmy;
-            bins2_edge(pk2(v.x, v.x), v.x, v.x, lcv[0], thv[0], n, b[0], dmy);
-            bins2_edge(pk2(v.y, v.y), v.y, v.y, lcv[1], thv[1], n, b[1], dmy);
-            bins2_edge(pk2(v.z, v.z), v.z, v.z, lcv[2], thv[2], n, b[2], dmy);
-            bins2_edge(pk2(v.w, v.w), v.w, v.w, lcv[3], thv[3], n, b[3], dmy);
+            bins2_edge(pk2(v.x, v.x), v.x, v.x, lc0, thv(0), n, b[0], dmy);
+            bins2_edge(pk2(v.y, v.y), v.y, v.y, lcv(1), thv(1), n, b[1], dmy);
+            bins2_edge(pk2(v.z, v.z), v.z, v.z, lc2, thv(2), n, b[2], dmy);
+            bins2_edge(pk2(v.w, v.w), v.w, v.w, lcv(3), thv(3), n, b[3], dmy);
           }
         } else {
           const float a4[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
-            if (isnan(lcv[i].y)) b[i] = bin_search(a4[i], thv[i], n);
-            else bins2_edge(pk2(a4[i], a4[i]), a4[i], a4[i], lcv[i], thv[i], n, b[i], b[i]);
+            if (isnan(lcv(i).y)) b[i] = bin_search(a4[i], thv(i), n);
+            else bins2_edge(pk2(a4[i], a4[i]), a4[i], a4[i], lcv(i), thv(i), n, b[i], b[i]);
           }
         }
         // merge equal neighbours, one shared atomic per distinct (tile, bin);
