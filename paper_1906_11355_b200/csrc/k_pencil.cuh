@@ -370,7 +370,7 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
       const u64 L2 = pk2(lc2.x, lc2.x), C2 = pk2(lc2.y, lc2.y);
       const float* rp = buf + slot * G.P + e0;
       const int64_t rstep = (int64_t)G.rpi * G.P;
-#pragma unroll 2
+#pragma unroll 4
       for (int k = 0; k < trips; ++k, rp += rstep) {
         const float4 v = *reinterpret_cast<const float4*>(rp);
         u64 t01, t23;
