@@ -453,19 +453,27 @@ void plan_mdict(mclahe_plan_s* pl) {
   if (nst < 2) return;
   m.nst = (int)nst;
   m.smem = kPipeBytes + nst * stage + m.tail;
-  // whole cell pencils: a work item rebuilds its tables, so units are not
-  // chunked along dim 0 (the interp units' chunks of one cell are merged)
+  // a work item rebuilds its tables, so units are merged from the interp
+  // units' dim-0 chunks of one cell up to ~1M voxels (the 4D config: whole
+  // cell pencils); larger ones would let the four CTAs sharing a pencil's rows
+  // (one segment each) drift apart by more than L2 holds (Large 4D read
+  // twice its input with whole 16 MB pencils)
   std::vector<int32_t>& mu = pl->mdict_units;
   mu.clear();
   const std::vector<int32_t>& iu = pl->interp_units;
-  for (size_t k = 0; k < iu.size(); k += kUnitInts) {
+  static const int lg_item = getenv("MCLAHE_MDICT_LG_ITEM") ? atoi(getenv("MCLAHE_MDICT_LG_ITEM")) : 20;
+  int64_t mvox = 0;
+  for (size_t k = 0, u = 0; k < iu.size(); k += kUnitInts, ++u) {
     const size_t last = mu.size();
+    const int64_t v = pl->interp_vox[u];
     if (last && std::equal(iu.begin() + k, iu.begin() + k + c.ko, mu.begin() + last - kUnitInts) &&
-        mu[last - 1] == iu[k + 8]) {
+        mu[last - 1] == iu[k + 8] && mvox + v <= (int64_t{1} << lg_item)) {
       mu[last - 1] = iu[k + 9];  // contiguous dim-0 chunk of the same cell
+      mvox += v;
       continue;
     }
     mu.insert(mu.end(), iu.begin() + k, iu.begin() + k + kUnitInts);
+    mvox = v;
   }
   if (mu.empty() || (int64_t)(mu.size() / kUnitInts) * m.nseg > INT32_MAX) return;
   pl->interp_m = m;
