@@ -303,6 +303,7 @@ PencilInterpFn get_interp_mdict(int ko, bool tma_store, bool adaptive, int n_bin
     return tma_store ? k_interp_mdict<3, true, 16, true, kDictKC>
                      : k_interp_mdict<3, false, 16, true, kDictKC>;
   switch (n_bins) {
+    case 128: return tma_store ? k_interp_mdict<3, true, 16, false, 128> : k_interp_mdict<3, false, 16, false, 128>;
     case 256: return tma_store ? k_interp_mdict<3, true, 16, false, 256> : k_interp_mdict<3, false, 16, false, 256>;
     case 512: return tma_store ? k_interp_mdict<3, true, 16, false, 512> : k_interp_mdict<3, false, 16, false, 512>;
     default: return nullptr;

@@ -409,7 +409,7 @@ def test_value_dictionary_blend(M, case):
     assert np.max(np.abs(out.cpu().numpy().astype(np.float64) - want)) <= OUT_TOL
 
 
-@pytest.mark.parametrize("nb", [256, 512])
+@pytest.mark.parametrize("nb", [128, 256, 512])
 def test_folded_pair_blend_global_mode(M, nb):
     # global range, one trailing dim, three outer dims: the folded-pair blend
     # (tables per bin) runs; it equals the oracle and, bit for bit, the
