@@ -91,10 +91,18 @@ __global__ void __launch_bounds__(1024) k_dict_finalize(WS W, int cap) {
       }
       __syncthreads();
     }
+  auto key_val = [](uint32_t k) { return __uint_as_float((k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k); };
+  // smallest gap between neighbouring values: block min-reduction (f64)
+  __shared__ double s_gap[32];
+  double gap = INFINITY;
   if (tid < K) {
-    const uint32_t k = s_key[tid];
-    W.dvals[tid] = __uint_as_float((k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k);
+    const float v = key_val(s_key[tid]);
+    W.dvals[tid] = v;
+    if (tid > 0) gap = (double)v - (double)key_val(s_key[tid - 1]);
   }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) gap = fmin(gap, __shfl_xor_sync(0xffffffffu, gap, o));
+  if ((tid & 31) == 0) s_gap[tid >> 5] = gap;
   __syncthreads();
   // Affine direct table when the values are evenly spread (quantised data):
   // cell = rint((v - v0) * S) with S = 1.25 / (smallest gap), so distinct
@@ -104,10 +112,10 @@ __global__ void __launch_bounds__(1024) k_dict_finalize(WS W, int cap) {
   __shared__ float s_v0, s_S;
   if (tid == 0) {
     double g = INFINITY;
-    for (int i = 1; i < K; ++i) g = fmin(g, (double)W.dvals[i] - (double)W.dvals[i - 1]);
-    const float v0 = K > 0 ? W.dvals[0] : 0.0f;
+    for (int w = 0; w < 32; ++w) g = fmin(g, s_gap[w]);
+    const float v0 = K > 0 ? key_val(s_key[0]) : 0.0f;
     const float S = K > 1 ? (float)(1.25 / g) : 1.0f;
-    const double span = K > 1 ? ((double)W.dvals[K - 1] - (double)v0) * (double)S : 0.0;
+    const double span = K > 1 ? ((double)key_val(s_key[K - 1]) - (double)v0) * (double)S : 0.0;
     s_aff = (K > 0 && isfinite(S) && S > 0.0f && span < kDictHL - 4) ? 1 : 0;
     s_v0 = v0;
     s_S = S;
@@ -115,7 +123,7 @@ __global__ void __launch_bounds__(1024) k_dict_finalize(WS W, int cap) {
   __syncthreads();
   if (s_aff) {
     for (int i = tid; i < K; i += 1024) {
-      const float v = W.dvals[i];
+      const float v = key_val(s_key[i]);
       const int cell = dict_cell(v, v, s_v0, s_S, nullptr);
       if (atomicCAS(&W.dlt[cell].x, kDictEmpty, __float_as_uint(v)) != kDictEmpty) s_aff = 0;
       else W.dlt[cell].y = (uint32_t)i;
