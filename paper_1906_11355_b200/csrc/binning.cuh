@@ -332,6 +332,26 @@ __device__ __forceinline__ void bins2_bracket(u64 V, float v0, float v1, float l
   b1 = r[1];
 }
 
+// Same rule against an NbBlock (edge table padded one word per 32 entries at
+// TH, LUT unpadded at L): the edge test decides k or k - 1, then one gather.
+template <int TH, int L>
+__device__ __forceinline__ float edge_gather_u(uint32_t base, int k, float v) {
+  float m;
+  asm volatile(
+      "{\n\t.reg .u32 a, b;\n\t.reg .f32 t;\n\t.reg .pred p;\n\t"
+      "shr.u32 a, %1, 5;\n\t"
+      "add.u32 a, a, %1;\n\t"
+      "mad.lo.u32 a, a, 4, %2;\n\t"
+      "ld.shared.f32 t, [a+%4];\n\t"
+      "mad.lo.u32 b, %1, 4, %2;\n\t"
+      "setp.lt.f32 p, %3, t;\n\t"
+      "@p sub.u32 b, b, 4;\n\t"
+      "ld.shared.f32 %0, [b+%5];\n\t}"
+      : "=f"(m)
+      : "r"(k), "r"(base), "f"(v), "n"(TH), "n"(L));
+  return m;
+}
+
 // Reference bin of v given k = rint(y) clamped to [0, n] (clamp_bits_k) and
 // the tile's edge table at shared address th: k if v >= th[k], else k - 1.
 __device__ __forceinline__ int edge_bin(uint32_t th, int k, float v) {

@@ -76,6 +76,7 @@ struct KGeom {
   int stiles;              // NB blend: trailing tiles staged at once (one segment's window)
   int dyn_units;           // blend: > 0 = units handed out dynamically (count), via W.range[3]
   int seg_items;           // blend: 1 = a work item is (unit, ONE segment): item / nseg, item % nseg
+  int nb_edges;            // NB blend: -1 auto (from the K2a value sample), 0 bracketed floors, 1 edge tables
 };
 
 // Value dictionary (adaptive mode, float32): when the volume holds few

@@ -577,6 +577,12 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
   const TileParam<float>* tparams = reinterpret_cast<const TileParam<float>*>(W.tparams);
   const float2 glc = tile_lc(tparams[0]);
   bool patho = !ADAPT && isnan(glc.y);  // a range the float guard does not cover
+  // NB: data whose values sit on bin edges (quantised counts) make the
+  // bracketed floors disagree in most corner groups; each warp then switches to
+  // the edge table for every voxel-corner (one extra dependent LDS, no votes)
+  // and re-probes the bracketed path every 64 items.  G.nb_edges forces either.
+  int nb_edges = G.nb_edges == 1 ? 1 : 0;  // warp-uniform
+  int nb_probe = 0, nb_slow = 0;
 
   // column table (independent of the unit): cells are shared by the column's
   // 4 voxels (the plan checks cell boundaries along the last dim are x4)
@@ -926,7 +932,57 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
 #pragma unroll
           for (int j = 0; j < KT; ++j) sbase[j] = (uint32_t)__cvta_generic_to_shared(base[j]);
           const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
-          if (!patho) {  // hot path: bracketed floors, one LUT gather per corner
+          if (!patho && nb_edges) {  // edge-table test for every voxel-corner
+            constexpr int SF = KO >= 2 ? 2 : 1;
+            const float g2[2] = {1.0f - f2, f2};
+            const u64 M2 = pk2(kMagic, kMagic);
+#pragma unroll 1
+            for (int cp = 0; cp < NCO / 2; ++cp) {
+              const float wf = pick(wfix, cp >> (SF - 1));
+              const float wg2 = KO >= 2 ? pick(g2, cp & 1) : 1.0f;
+              const uint32_t po = (uint32_t)(2 * cp * TB);
+              static_for<0, 2>([&](auto bc) {
+                constexpr int b1 = decltype(bc)::value;
+                float w = b1 ? f1 : 1.0f - f1;
+                if (KO >= 2) w *= wg2;
+                w *= wf;
+                float m0[4];
+                (void)m0;
+                static_for<0, NCT>([&](auto ctc) {
+                  constexpr int ct = decltype(ctc)::value;
+                  constexpr int OFF = ((ct & 1) * NCO + b1) * TB;
+                  const float4 hd = *reinterpret_cast<const float4*>(base[ct >> 1] + po + OFF);
+                  u64 tq[2];
+#pragma unroll
+                  for (int h = 0; h < 2; ++h) {
+                    const u64 y = mul2(sub2(h ? V23 : V01, pk2(hd.x, hd.x)), pk2(hd.w, hd.w));
+                    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(tq[h]) : "l"(y), "l"(M2));
+                  }
+                  float tf[4];
+                  upk2(tq[0], tf[0], tf[1]);
+                  upk2(tq[1], tf[2], tf[3]);
+                  float m[4];
+#pragma unroll
+                  for (int i = 0; i < 4; ++i)
+                    m[i] = edge_gather_u<OFF + NbBlock::th_off(NB) * 4, OFF + NbBlock::lut_off(NB) * 4>(
+                        sbase[ct >> 1] + po, clamp_bits_k(tf[i], NB), vv[i]);
+                  if constexpr (MORD) {
+                    if constexpr (ct == 0) {
+#pragma unroll
+                      for (int i = 0; i < 4; ++i) m0[i] = m[i];
+                    } else {
+#pragma unroll
+                      for (int i = 0; i < 4; ++i)
+                        act[0][i] = fmaf(w, fmaf(tw[i][1], m[i], tw[i][0] * m0[i]), act[0][i]);
+                    }
+                  } else {
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) act[ct][i] = fmaf(w, m[i], act[ct][i]);
+                  }
+                });
+              });
+            }
+          } else if (!patho) {  // hot path: bracketed floors, one LUT gather per corner
             // LUT byte address straight from the clamped floor bits:
             // lbase + 4 * bits  (lbase = base - 4 * kMagicBits, mod 2^32)
             uint32_t lbase[KT];
@@ -978,6 +1034,7 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
                   if (__any_sync(0xffffffffu, amb != 0)) {
                     // rare (q within ~5e-7 |q| of a bin edge): the clamped floors
                     // are k - 1 and k and the edge table picks one
+                    ++nb_slow;
                     const float* th = reinterpret_cast<const float*>(B) + NbBlock::th_off(NB);
                     const float* L = reinterpret_cast<const float*>(B) + NbBlock::lut_off(NB);
 #pragma unroll
@@ -1039,6 +1096,16 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
                 }
               }
               accum(wo[co], mp);
+            }
+          }
+          if constexpr (NB > 0) {  // per-warp mode switch (see nb_edges)
+            if (G.nb_edges < 0) {
+              if (nb_edges) {
+                if (++nb_probe >= 64) nb_edges = nb_probe = 0;
+              } else {
+                if (4 * nb_slow > NCO * NCT) nb_edges = 1;
+                nb_slow = 0;
+              }
             }
           }
         } else if (ADAPT && !patho) {  // hot path: branch-free edge-table gathers

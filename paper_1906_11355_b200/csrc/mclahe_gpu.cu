@@ -183,6 +183,8 @@ KGeom pencil_geom(const mclahe_plan_s& pl, const Pencil& pc) {
   G.nseg = pc.nseg;
   G.stage_stride = pc.stage_stride;
   G.dict = pl.dict_cap > 0 ? 1 : 0;
+  static const int nb_edges = getenv("MCLAHE_NB_EDGES") ? atoi(getenv("MCLAHE_NB_EDGES")) : -1;
+  G.nb_edges = nb_edges;
   G.stiles = (int)(pc.kt > 0 && !pc.hist_family ? nb_seg_tiles(pl, pc) : pc.gtr);
   for (int j = 0; j < G.rank; ++j) {
     G.inv_b[j] = 1.0f / (float)G.d[j].b;

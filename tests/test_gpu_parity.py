@@ -357,13 +357,14 @@ def _run_plan(M, x, kernel, nb, clip, ad, no_dict=False):
     return out, plan.dict_state(ws)
 
 
-@pytest.mark.parametrize("case", ["poisson", "edges", "scaled4d", "many", "uneven", "rare", "wide"])
+@pytest.mark.parametrize("case", ["poisson", "edges", "scaled4d", "many", "uneven", "rare", "wide",
+                                  "levels"])
 def test_value_dictionary_blend(M, case):
     # quantised volumes (few distinct values) take the value-dictionary blend
     # (rank 4 with one trailing dim: the folded-pair kernel k_interp_mdict);
     # it must equal the oracle and, bit for bit, the edge-table blend
     rng = np.random.default_rng({"poisson": 1, "edges": 2, "scaled4d": 3, "many": 4, "uneven": 5,
-                                 "rare": 6, "wide": 7}[case])
+                                 "rare": 6, "wide": 7, "levels": 8}[case])
     if case == "poisson":
         x = (rng.poisson(3.0, (48, 40, 24, 32)) / 11.0).astype(np.float32)
         args = ((12, 10, 6, 4), 256, 0.02, True)
@@ -389,6 +390,9 @@ def test_value_dictionary_blend(M, case):
         vals[:3] = [0.0, 1e-6, 2e-6]
         x = vals[rng.integers(0, 300, (32, 32, 16, 32))]
         args = ((8, 8, 4, 4), 256, 0.02, True)
+    elif case == "levels":  # 1501 levels: too many for the dictionary, quantised (edge mode)
+        x = (np.round(rng.random((32, 32, 16, 32)) * 1500) / 1500).astype(np.float32)
+        args = ((8, 8, 4, 4), 256, 0.02, True)
     else:  # more distinct values than the dictionary holds: edge-table blend
         x = rng.random((32, 32, 16, 32)).astype(np.float32)
         args = ((8, 8, 4, 4), 256, 0.02, True)
@@ -396,10 +400,10 @@ def test_value_dictionary_blend(M, case):
     ref, st0 = _run_plan(M, x, *args, no_dict=True)
     assert st0["capacity"] == 0 and not st0["used"]
     assert st["capacity"] > 0
-    assert st["used"] == (case != "many"), st
+    assert st["used"] == (case not in ("many", "levels")), st
     # folded pairs: rank 4, one trailing dim, power-of-two cells (>= 32-row stages)
     assert st["folded"] == (case in ("scaled4d", "uneven", "rare", "wide")), st
-    if case != "many":  # K2a samples a quarter of the rows
+    if case not in ("many", "levels"):  # K2a samples a quarter of the rows
         assert 0 < st["values"] <= len(np.unique(x.view(np.uint32))), st
         if case == "rare":
             assert st["values"] < len(np.unique(x.view(np.uint32))), st  # misses exercised
