@@ -432,6 +432,18 @@ def test_folded_pair_blend_global_mode(M, nb):
     assert np.array_equal(dev.cpu().numpy(), host)
 
 
+def test_folded_pair_blend_pathological_global_range(M):
+    # a global range of denormals (n / (hi - lo) overflows f32): the folded-pair
+    # blend bins every voxel by bisecting the edge table
+    rng = np.random.default_rng(31)
+    x = (rng.integers(1, 9, (32, 32, 16, 32)) * np.float32(1e-40)).astype(np.float32)
+    args = ((8, 8, 4, 4), 256, 0.02, False)
+    out, st = _run_plan(M, x, *args)
+    assert st["folded"], st
+    want = O.mclahe(x, *args, "c")
+    assert np.max(np.abs(out.cpu().numpy().astype(np.float64) - want)) <= OUT_TOL
+
+
 @pytest.mark.parametrize("ad", [True, False])
 def test_sparse_counts_degenerate_neighbours(M, ad):
     # counts on one half of the trailing dim, zeros on the other: constant
