@@ -190,15 +190,16 @@ __global__ void __launch_bounds__(NWARP * 32 + 32, 1)
     for (int j = 1; j < KO - 2; ++j) gbase += (int64_t)S.x[j] * G.vstride[j];
     gbase += (int64_t)xb2 * G.vstride[KO - 2] + (int64_t)xb1 * G.vstride[KO - 1];
     unsigned char* buf = reinterpret_cast<unsigned char*>(P.bufs + s * stage_elems);
-    // a warp takes one row block per iteration and both columns of the
-    // segment (the outer weights, row addresses and loop overhead are shared);
-    // row blocks of consecutive stages are dealt round-robin over the warps
-    const int nitems = nrb;
+    // items of consecutive stages dealt round-robin over the warps (2 * nrb
+    // need not be a multiple of NW)
+    const int nitems = 2 * nrb;
     const int first = (int)((warp + NW - (int)(((uint64_t)it * nitems) % NW)) % NW);
     for (int item = first; item < nitems; item += NW) {
-      const int rb = item;
+      const int c = item & 1, rb = item >> 1;
       const bool q_on = rb * 32 + lane < rows;
       const int q = min(rb * 32 + lane, rows - 1);
+      const int col = seg * 2 + c;
+      const bool col_on = col < ncol;  // an odd last column pair
       const int r1 = q & (G.r1 - 1), r2 = q >> G.lg_r1;
       const float f1 = fmaf((float)(xb1 + r1), s1, t1);
       const float f2 = fmaf((float)(xb2 + r2), s2, t2);
@@ -212,85 +213,80 @@ __global__ void __launch_bounds__(NWARP * 32 + 32, 1)
           wo[co] = w * wfix[co >> 2];
         }
       }
-      static_for<0, 2>([&](auto ccol) {
-        constexpr int c = decltype(ccol)::value;
-        const int col = seg * 2 + c;
-        const bool col_on = col < ncol;  // an odd last column pair
-        // 32B-swizzled stage row (32 bytes): 16-byte chunk c of row q at c ^ ((q >> 2) & 1)
-        float4* slot4 = reinterpret_cast<float4*>(buf + q * 32 + ((c ^ ((q >> 2) & 1)) << 4));
-        const float4 v4 = *slot4;
-        const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
-        int di[4];
-        if (!ADAPT) {  // one bin per voxel: the global edge table
-          if (!patho) {
-            bins2_edge(pk2(vv[0], vv[1]), vv[0], vv[1], glc, thrS, KC, di[0], di[1]);
-            bins2_edge(pk2(vv[2], vv[3]), vv[2], vv[3], glc, thrS, KC, di[2], di[3]);
-          } else {
-  #pragma unroll
-            for (int i = 0; i < 4; ++i) di[i] = bin_search(vv[i], thrS, KC);
-          }
-        } else if (s_dmode) {  // affine cells: one LDS.64 per voxel
-          int cl[4];
-          cl[0] = dict_cell(vv[0], vv[1], s_dv0, s_dS, &cl[1]);
-          cl[2] = dict_cell(vv[2], vv[3], s_dv0, s_dS, &cl[3]);
-  #pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const uint2 e = dltS[cl[i]];
-            di[i] = e.x == __float_as_uint(vv[i]) ? (int)e.y : -1;
-          }
+      // 32B-swizzled stage row (32 bytes): 16-byte chunk c of row q at c ^ ((q >> 2) & 1)
+      float4* slot4 = reinterpret_cast<float4*>(buf + q * 32 + ((c ^ ((q >> 2) & 1)) << 4));
+      const float4 v4 = *slot4;
+      const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
+      int di[4];
+      if (!ADAPT) {  // one bin per voxel: the global edge table
+        if (!patho) {
+          bins2_edge(pk2(vv[0], vv[1]), vv[0], vv[1], glc, thrS, KC, di[0], di[1]);
+          bins2_edge(pk2(vv[2], vv[3]), vv[2], vv[3], glc, thrS, KC, di[2], di[3]);
         } else {
-  #pragma unroll
-          for (int i = 0; i < 4; ++i) di[i] = dict_lookup(dltS, __float_as_uint(vv[i]));
+#pragma unroll
+          for (int i = 0; i < 4; ++i) di[i] = bin_search(vv[i], thrS, KC);
         }
-        const char* A[4];
-        int miss = 0;
-  #pragma unroll
+      } else if (s_dmode) {  // affine cells: one LDS.64 per voxel
+        int cl[4];
+        cl[0] = dict_cell(vv[0], vv[1], s_dv0, s_dS, &cl[1]);
+        cl[2] = dict_cell(vv[2], vv[3], s_dv0, s_dS, &cl[3]);
+#pragma unroll
         for (int i = 0; i < 4; ++i) {
-          miss |= (di[i] < 0) << i;
-          A[i] = reinterpret_cast<const char*>(Ms + ((c * 4 + i) * NCO) * KC + (di[i] >= 0 ? di[i] : 0));
+          const uint2 e = dltS[cl[i]];
+          di[i] = e.x == __float_as_uint(vv[i]) ? (int)e.y : -1;
         }
-        float acc[4] = {0.f, 0.f, 0.f, 0.f};
-        static_for<0, NCO>([&](auto coc) {
-          constexpr int co = decltype(coc)::value;
-          float m[4];
-  #pragma unroll
-          for (int i = 0; i < 4; ++i) m[i] = *reinterpret_cast<const float*>(A[i] + co * KC * 4);
-  #pragma unroll
-          for (int i = 0; i < 4; ++i) acc[i] = fmaf(wo[co], m[i], acc[i]);
-        });
-        if (ADAPT && miss) {  // values the (sampled) dictionary lacks: from the workspace LUTs
-          const int colc = min(col, ncol - 1);
-          const int tt = colT[colc];
-          float a[4] = {0.f, 0.f, 0.f, 0.f};
-          static_for<0, NCO>([&](auto coc) {  // same order as the gathers above
-            constexpr int co = decltype(coc)::value;
-            const int t0 = ofS[co] + tt;
-  #pragma unroll
-            for (int i = 0; i < 4; ++i)
-              if ((miss >> i) & 1) {
-                const float2 tw = *reinterpret_cast<const float2*>(colW + (colc * 4 + i) * 2);
-                const float L0 = lut_value_global(W, n, t0, vv[i]);
-                const float L1 = lut_value_global(W, n, t0 + tstr1, vv[i]);
-                a[i] = fmaf(wo[co], fmaf(tw.y, L1, tw.x * L0), a[i]);
-              }
-          });
-  #pragma unroll
-          for (int i = 0; i < 4; ++i)
-            if ((miss >> i) & 1) acc[i] = a[i];
-        }
-        float4 r;
-        r.x = fminf(fmaxf(acc[0], 0.f), 1.f);
-        r.y = fminf(fmaxf(acc[1], 0.f), 1.f);
-        r.z = fminf(fmaxf(acc[2], 0.f), 1.f);
-        r.w = fminf(fmaxf(acc[3], 0.f), 1.f);
-        if (TSTORE) {
-          if (q_on) *slot4 = r;  // in place; the producer TMA-stores the box
-        } else if (q_on && col_on) {
-          __stcs(reinterpret_cast<float4*>(out + gbase + (int64_t)r2 * G.vstride[KO - 2] +
-                                           (int64_t)r1 * G.vstride[KO - 1] + col * 4),
-                 r);
-        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) di[i] = dict_lookup(dltS, __float_as_uint(vv[i]));
+      }
+      const char* A[4];
+      int miss = 0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        miss |= (di[i] < 0) << i;
+        A[i] = reinterpret_cast<const char*>(Ms + ((c * 4 + i) * NCO) * KC + (di[i] >= 0 ? di[i] : 0));
+      }
+      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+      static_for<0, NCO>([&](auto coc) {
+        constexpr int co = decltype(coc)::value;
+        float m[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) m[i] = *reinterpret_cast<const float*>(A[i] + co * KC * 4);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc[i] = fmaf(wo[co], m[i], acc[i]);
       });
+      if (ADAPT && miss) {  // values the (sampled) dictionary lacks: from the workspace LUTs
+        const int colc = min(col, ncol - 1);
+        const int tt = colT[colc];
+        float a[4] = {0.f, 0.f, 0.f, 0.f};
+        static_for<0, NCO>([&](auto coc) {  // same order as the gathers above
+          constexpr int co = decltype(coc)::value;
+          const int t0 = ofS[co] + tt;
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            if ((miss >> i) & 1) {
+              const float2 tw = *reinterpret_cast<const float2*>(colW + (colc * 4 + i) * 2);
+              const float L0 = lut_value_global(W, n, t0, vv[i]);
+              const float L1 = lut_value_global(W, n, t0 + tstr1, vv[i]);
+              a[i] = fmaf(wo[co], fmaf(tw.y, L1, tw.x * L0), a[i]);
+            }
+        });
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          if ((miss >> i) & 1) acc[i] = a[i];
+      }
+      float4 r;
+      r.x = fminf(fmaxf(acc[0], 0.f), 1.f);
+      r.y = fminf(fmaxf(acc[1], 0.f), 1.f);
+      r.z = fminf(fmaxf(acc[2], 0.f), 1.f);
+      r.w = fminf(fmaxf(acc[3], 0.f), 1.f);
+      if (TSTORE) {
+        if (q_on) *slot4 = r;  // in place; the producer TMA-stores the box
+      } else if (q_on && col_on) {
+        __stcs(reinterpret_cast<float4*>(out + gbase + (int64_t)r2 * G.vstride[KO - 2] +
+                                         (int64_t)r1 * G.vstride[KO - 1] + col * 4),
+               r);
+      }
     }
     if (TSTORE) fence_proxy_async_smem();
     __syncwarp();
