@@ -368,6 +368,22 @@ __device__ __forceinline__ int edge_bin(uint32_t th, int k, float v) {
   return b;
 }
 
+// Histogram word of the reference bin: k as edge_bin, the word at
+// h + 4 * bin (h = the tile's row), without materialising the bin.
+__device__ __forceinline__ uint32_t edge_hist_addr(uint32_t th, int k, float v, uint32_t h) {
+  uint32_t a;
+  asm volatile(
+      "{\n\t.reg .u32 t;\n\t.reg .f32 x;\n\t.reg .pred p;\n\t"
+      "mad.lo.u32 t, %1, 4, %2;\n\t"
+      "ld.shared.f32 x, [t];\n\t"
+      "mad.lo.u32 %0, %1, 4, %4;\n\t"
+      "setp.lt.f32 p, %3, x;\n\t"
+      "@p sub.u32 %0, %0, 4;\n\t}"
+      : "=r"(a)
+      : "r"(k), "r"(th), "f"(v), "r"(h));
+  return a;
+}
+
 // Shared-memory add of val at addr when flag != 0 (predicated, no branch).
 __device__ __forceinline__ void red_add_if(uint32_t addr, uint32_t val, uint32_t flag) {
   asm volatile(

@@ -232,13 +232,18 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
 // Unit switch helpers: the CTA's [gtr][n + 1] shared histogram added into the
 // workspace counts (no index division; nonzero bins only), and a row copy
 // with four loads in flight per thread.
+// skip (optional): per-tile {lo, c}; degenerate tiles' rows (counted by the
+// hot path, never used) are not flushed.
 __device__ __forceinline__ void hist_flush(const uint32_t* hist, uint32_t* dst, int gtr, int n,
-                                           int tid) {
-  for (int t = 0; t < gtr; ++t)
+                                           int tid, const float2* skip = nullptr) {
+  const float kDegC = degenerate_lc().y;
+  for (int t = 0; t < gtr; ++t) {
+    if (skip && skip[t].y == kDegC) continue;
     for (int b = tid; b < n; b += kConsumers) {
       const uint32_t c = hist[t * (n + 1) + b];
       if (c) atomicAdd(dst + (int64_t)t * n + b, c);
     }
+  }
 }
 
 __device__ __forceinline__ void copy_rows(float* dst, const float* __restrict__ src, int count,
@@ -324,7 +329,7 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
       consumers_sync();
       if (tid == 0) s_bad = 0;
       if (cur >= 0) {
-        hist_flush(hist, W.counts + cur * n, (int)G.gtr, n, tid);
+        hist_flush(hist, W.counts + cur * n, (int)G.gtr, n, tid, ADAPT ? lcS : nullptr);
       }
       consumers_sync();
       for (int64_t k = tid; k < G.gtr * (n + 1); k += kConsumers) hist[k] = 0;
@@ -357,12 +362,13 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
       // the edge table (edge_bin); equal neighbouring (tile, bin) runs merge
       // into one predicated shared-memory add each -- no branches.
       const uint32_t wf = (uint32_t)S.wfix;
-      uint32_t w[4], ha[4], ok[4];
+      // degenerate tiles count into their own rows too (never flushed): no
+      // per-voxel masking
+      uint32_t w[4], ha[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         w[i] = wf * (uint32_t)trw[i];
-        ok[i] = hb[i] >= 0;
-        ha[i] = hist_s + (uint32_t)(hb[i] >= 0 ? hb[i] : 0) * 4u;
+        ha[i] = hist_s + (uint32_t)(trt[i] * (n + 1)) * 4u;
       }
       const uint32_t th0 = (uint32_t)__cvta_generic_to_shared(thv(0));
       const uint32_t th2 = (uint32_t)__cvta_generic_to_shared(thv(2));
@@ -382,22 +388,20 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
         const float vv[4] = {v.x, v.y, v.z, v.w};
         uint32_t a[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {  // degenerate tiles: distinct dummy keys, never merged
-          a[i] = ha[i] + 4u * (uint32_t)edge_bin(i < 2 ? th0 : th2, clamp_bits_k(tf[i], n), vv[i]);
-          if (!ok[i]) a[i] = 0xFFFFFFF0u + i;
-        }
+        for (int i = 0; i < 4; ++i)  // histogram word of the voxel's (tile, bin)
+          a[i] = edge_hist_addr(i < 2 ? th0 : th2, clamp_bits_k(tf[i], n), vv[i], ha[i]);
         // runs of equal keys carry their sum on the first add; suppressed adds
-        // (run tails, degenerate tiles) go to the thread's dummy word: every
-        // add unconditional, no branches around the atomics
+        // (run tails) go to the thread's dummy word: every add unconditional,
+        // no branches around the atomics
         const bool e01 = a[0] == a[1], e12 = a[1] == a[2], e23 = a[2] == a[3];
         const uint32_t s3 = w[3];
         const uint32_t s2 = w[2] + (e23 ? s3 : 0u);
         const uint32_t s1 = w[1] + (e12 ? s2 : 0u);
         const uint32_t s0 = w[0] + (e01 ? s1 : 0u);
-        red_add(ok[0] ? a[0] : dummy_s, s0);
-        red_add(ok[1] && !e01 ? a[1] : dummy_s, s1);
-        red_add(ok[2] && !e12 ? a[2] : dummy_s, s2);
-        red_add(ok[3] && !e23 ? a[3] : dummy_s, s3);
+        red_add(a[0], s0);
+        red_add(e01 ? dummy_s : a[1], s1);
+        red_add(e12 ? dummy_s : a[2], s2);
+        red_add(e23 ? dummy_s : a[3], s3);
       }
     } else if (lane_on) {
       const bool wuni = S.wuni != 0;
@@ -459,7 +463,7 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
   }
   consumers_sync();
   if (cur >= 0) {
-    hist_flush(hist, W.counts + cur * n, (int)G.gtr, n, tid);
+    hist_flush(hist, W.counts + cur * n, (int)G.gtr, n, tid, ADAPT ? lcS : nullptr);
   }
 }
 
