@@ -103,6 +103,8 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
   for (int i = 0; i < 4; ++i) trailing_tile(G, e0 + i, &trt[i], &dummy);
   float mn[4], mx[4], mn2[4], mx2[4];
   int bad = 0;
+  u64 nf01 = 0, nf23 = 0;  // finiteness accumulators (see the row loop)
+  const u64 zero2 = 0;
   int64_t cur = -1;
   const int64_t stage_elems = G.stage_stride;
   const int P4 = (int)G.P;
@@ -169,9 +171,12 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
           const float a[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
           float* m0 = (j & 1) ? mn2 : mn;
           float* m1 = (j & 1) ? mx2 : mx;
+          // finiteness: 0 * x is 0 for finite x and NaN for +-inf / NaN, so a
+          // packed fma chain goes NaN iff some voxel is not finite
+          nf01 = fma2(pk2(a[0], a[1]), zero2, nf01);
+          nf23 = fma2(pk2(a[2], a[3]), zero2, nf23);
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
-            bad |= !isfinite(a[i]);
             m0[i] = fminf(m0[i], a[i]);
             m1[i] = fmaxf(m1[i], a[i]);
           }
@@ -204,6 +209,12 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
     ++it;
   }
   if (cur >= 0) flush();
+  {
+    float z0, z1, z2, z3;
+    upk2(nf01, z0, z1);
+    upk2(nf23, z2, z3);
+    bad |= isnan(z0) || isnan(z1) || isnan(z2) || isnan(z3);
+  }
   if (bad) atomicMax(reinterpret_cast<long long*>(&W.range[2]), 1LL);
   if (DICT) {  // merge the CTA's values into the workspace set
     consumers_sync();
