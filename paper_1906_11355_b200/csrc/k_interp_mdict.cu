@@ -101,6 +101,7 @@ __global__ void __launch_bounds__(NWARP * 32 + 32, 1)
   float ugs[KO], ugt[KO];
   int64_t cur = -1;
   int seg = 0;
+  int rot = 0;  // round-robin offset of the item deal
   uint32_t it = 0;
   while (true) {
     const int s = it % G.nst;
@@ -193,7 +194,9 @@ __global__ void __launch_bounds__(NWARP * 32 + 32, 1)
     // items of consecutive stages dealt round-robin over the warps (2 * nrb
     // need not be a multiple of NW)
     const int nitems = 2 * nrb;
-    const int first = (int)((warp + NW - (int)(((uint64_t)it * nitems) % NW)) % NW);
+    const int first = warp >= rot ? warp - rot : warp + NW - rot;
+    rot += nitems % NW;  // items dealt so far, mod NW
+    if (rot >= NW) rot -= NW;
     for (int item = first; item < nitems; item += NW) {
       const int c = item & 1, rb = item >> 1;
       const bool q_on = rb * 32 + lane < rows;
