@@ -259,28 +259,6 @@ __device__ __forceinline__ void lut2_edge(u64 V, float v0, float v1, float2 lc, 
   m1 = *reinterpret_cast<const float*>(Lb + b1);
 }
 
-// One edge test + LUT gather against a tile block in shared memory (the NB
-// blend layout, NbBlock): k in [0, n] (clamp_bits), a = base + 4 pad(k); the
-// reference bin is k if v >= th[k] (at a + TH) else k - 1 (at a - 4, pads
-// repeat the entry before); returns LUT[bin] (at . + L).  Inline
-// PTX so both loads keep their [reg + imm] form off one address register.
-template <int TH, int L>
-__device__ __forceinline__ float edge_gather(uint32_t base, int k, float v) {
-  float m;
-  asm volatile(
-      "{\n\t.reg .u32 a;\n\t.reg .f32 t;\n\t.reg .pred p;\n\t"
-      "shr.u32 a, %1, 5;\n\t"
-      "add.u32 a, a, %1;\n\t"
-      "mad.lo.u32 a, a, 4, %2;\n\t"
-      "ld.shared.f32 t, [a+%4];\n\t"
-      "setp.lt.f32 p, %3, t;\n\t"
-      "@p sub.u32 a, a, 4;\n\t"
-      "ld.shared.f32 %0, [a+%5];\n\t}"
-      : "=f"(m)
-      : "r"(k), "r"(base), "f"(v), "n"(TH), "n"(L));
-  return m;
-}
-
 // ---- bracketed floor (the NB blend's fast path) ----------------------------
 // With d = fl32(v - lo) and c = fl32(n / (hi - lo)), the exact product d * c
 // is within a factor (1 +- 2^-23 (1 + 2^-20)) of the reference's f64 value q
@@ -387,14 +365,6 @@ __device__ __forceinline__ uint32_t edge_hist_addr(uint32_t th, int k, float v, 
       : "=r"(a)
       : "r"(k), "r"(th), "f"(v), "r"(h));
   return a;
-}
-
-// Shared-memory add of val at addr when flag != 0 (predicated, no branch).
-__device__ __forceinline__ void red_add_if(uint32_t addr, uint32_t val, uint32_t flag) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p red.shared.add.u32 [%0], %1;\n\t}" ::"r"(addr),
-      "r"(val), "r"(flag)
-      : "memory");
 }
 
 // Unconditional shared-memory add.
