@@ -300,8 +300,19 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
   const TileParam<float>* tparams = reinterpret_cast<const TileParam<float>*>(W.tparams);
   const TileParam<float> g0 = tparams[0];
   if (!ADAPT && tp_degenerate(g0.lim)) return;  // constant image: every mapping is 0.5
+  // 4 * kMagicBits kept opaque to ptxas (one IMAD per histogram address)
+  __shared__ uint32_t s_mb4;
+  if (threadIdx.x == 0) s_mb4 = 4u * (uint32_t)kMagicBits;
   pipe_init(*P.pipe, G.nst);
   __syncthreads();
+  uint32_t mb4;
+  asm volatile("ld.volatile.shared.u32 %0, [%1];"
+               : "=r"(mb4)
+               : "r"((uint32_t)__cvta_generic_to_shared(&s_mb4)));
+  // per-warp binning mode: bracketed floors, or the edge table for every voxel
+  // once most rows needed it (quantised data on bin edges), re-probed every
+  // 64 stages; G.nb_edges forces either
+  int k2_edges = G.nb_edges == 1 ? 1 : 0, k2_probe = 0;
   const int u0 = cta_units[blockIdx.x], u1 = cta_units[blockIdx.x + 1];
   if (threadIdx.x >= kConsumers) {
     if (threadIdx.x == kConsumers) pipe_produce<KO, false>(G, &tmap, units, u0, u1, *P.pipe, P.bufs);
@@ -387,23 +398,10 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
       const u64 L2 = pk2(lc2.x, lc2.x), C2 = pk2(lc2.y, lc2.y);
       const float* rp = buf + slot * G.P + e0;
       const int64_t rstep = (int64_t)G.rpi * G.P;
-#pragma unroll 4
-      for (int k = 0; k < trips; ++k, rp += rstep) {
-        const float4 v = *reinterpret_cast<const float4*>(rp);
-        u64 t01, t23;
-        asm("add.rn.f32x2 %0, %1, %2;" : "=l"(t01) : "l"(mul2(sub2(pk2(v.x, v.y), L0), C0)), "l"(pk2(kMagic, kMagic)));
-        asm("add.rn.f32x2 %0, %1, %2;" : "=l"(t23) : "l"(mul2(sub2(pk2(v.z, v.w), L2), C2)), "l"(pk2(kMagic, kMagic)));
-        float tf[4];
-        upk2(t01, tf[0], tf[1]);
-        upk2(t23, tf[2], tf[3]);
-        const float vv[4] = {v.x, v.y, v.z, v.w};
-        uint32_t a[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i)  // histogram word of the voxel's (tile, bin)
-          a[i] = edge_hist_addr(i < 2 ? th0 : th2, clamp_bits_k(tf[i], n), vv[i], ha[i]);
-        // runs of equal keys carry their sum on the first add; suppressed adds
-        // (run tails) go to the thread's dummy word: every add unconditional,
-        // no branches around the atomics
+      // runs of equal keys carry their sum on the first add; suppressed adds
+      // (run tails) go to the thread's dummy word: every add unconditional,
+      // no branches around the atomics
+      auto commit = [&](const uint32_t (&a)[4]) {
         const bool e01 = a[0] == a[1], e12 = a[1] == a[2], e23 = a[2] == a[3];
         const uint32_t s3 = w[3];
         const uint32_t s2 = w[2] + (e23 ? s3 : 0u);
@@ -413,6 +411,71 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
         red_add(e01 ? dummy_s : a[1], s1);
         red_add(e12 ? dummy_s : a[2], s2);
         red_add(e23 ? dummy_s : a[3], s3);
+      };
+      // histogram words via the edge table (k = rint of the f32 estimate, th
+      // decides k or k - 1)
+      auto edge_addrs = [&](const float4& v, uint32_t (&a)[4]) {
+        u64 t01, t23;
+        asm("add.rn.f32x2 %0, %1, %2;" : "=l"(t01) : "l"(mul2(sub2(pk2(v.x, v.y), L0), C0)), "l"(pk2(kMagic, kMagic)));
+        asm("add.rn.f32x2 %0, %1, %2;" : "=l"(t23) : "l"(mul2(sub2(pk2(v.z, v.w), L2), C2)), "l"(pk2(kMagic, kMagic)));
+        float tf[4];
+        upk2(t01, tf[0], tf[1]);
+        upk2(t23, tf[2], tf[3]);
+        const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i)  // histogram word of the voxel's (tile, bin)
+          a[i] = edge_hist_addr(i < 2 ? th0 : th2, clamp_bits_k(tf[i], n), vv[i], ha[i]);
+      };
+      // adaptive mode keeps the edge table only: per-voxel tile constants leave
+      // no registers for the bracketed floors (spills: 4D 0.33 -> 0.45 ms)
+      if (ADAPT || k2_edges) {
+#pragma unroll 4
+        for (int k = 0; k < trips; ++k, rp += rstep) {
+          const float4 v = *reinterpret_cast<const float4*>(rp);
+          uint32_t a[4];
+          edge_addrs(v, a);
+          commit(a);
+        }
+        if (!ADAPT && G.nb_edges < 0 && ++k2_probe >= 64) k2_edges = k2_probe = 0;
+      } else if constexpr (!ADAPT) {
+        // bracketed floors (binning.cuh: bin_window): a voxel of the tile's
+        // own support has d = v - lo >= 0, so the clamped lower floor is the
+        // bin wherever both floors agree; a row where some lane's disagree is
+        // redone through the edge table
+        const float2 w0 = bin_window(lc0.y), w2 = bin_window(lc2.y);
+        const u64 CL0 = pk2(w0.x, w0.x), CH0 = pk2(w0.y, w0.y);
+        const u64 CL2 = pk2(w2.x, w2.x), CH2 = pk2(w2.y, w2.y);
+        const u64 M2 = pk2(kMagic, kMagic);
+        uint32_t hab[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) hab[i] = ha[i] - mb4;
+        int nslow = 0;
+#pragma unroll 4
+        for (int k = 0; k < trips; ++k, rp += rstep) {
+          const float4 v = *reinterpret_cast<const float4*>(rp);
+          const u64 d01 = sub2(pk2(v.x, v.y), L0), d23 = sub2(pk2(v.z, v.w), L2);
+          float fa[4], fb[4];
+          upk2(fma_rm2(d01, CL0, M2), fa[0], fa[1]);
+          upk2(fma_rm2(d23, CL2, M2), fa[2], fa[3]);
+          upk2(fma_rm2(d01, CH0, M2), fb[0], fb[1]);
+          upk2(fma_rm2(d23, CH2, M2), fb[2], fb[3]);
+          uint32_t amb = 0, a[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int ab = __float_as_int(fa[i]);
+            amb |= (uint32_t)(ab ^ __float_as_int(fb[i]));
+            a[i] = hab[i] + 4u * (uint32_t)min(max(ab, kMagicBits), kMagicBits + n - 1);
+          }
+          if (__any_sync(__activemask(), amb != 0)) {  // rare on continuous data
+            ++nslow;
+            edge_addrs(v, a);
+          }
+          commit(a);
+        }
+        if (G.nb_edges < 0 && 4 * nslow > trips) {  // edges decide most rows: edge mode
+          k2_edges = 1;
+          k2_probe = 0;
+        }
       }
     } else if (lane_on) {
       const bool wuni = S.wuni != 0;
