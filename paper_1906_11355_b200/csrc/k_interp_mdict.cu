@@ -22,6 +22,10 @@
 // both produce the same bits.
 #include "k_pencil.cuh"
 
+#ifndef MDICT_BUILD_BATCH
+#define MDICT_BUILD_BATCH 4
+#endif
+
 namespace mg {
 
 
@@ -40,6 +44,7 @@ __global__ void __launch_bounds__(NWARP * 32 + 32, 1)
   constexpr int kMdictConsumers = NWARP * 32;
   constexpr int NW = NWARP;
   constexpr int KC = TK;
+  constexpr int MB_ = MDICT_BUILD_BATCH;  // table-build tasks per thread per pass (loads in flight)
   if (W.range[2] != 0) return;  // non-finite input: write nothing
   if (ADAPT && W.dmeta[2] == 0) return;  // no usable dictionary: the edge-table blend runs
   extern __shared__ __align__(1024) unsigned char smem[];
@@ -127,10 +132,10 @@ __global__ void __launch_bounds__(NWARP * 32 + 32, 1)
       const int ntask = 2 * NCO * nv4;
       // a thread's tasks in batches of four: all eight L2 loads in flight first
 #pragma unroll 1
-      for (int k0 = tid; k0 < ntask; k0 += 4 * kMdictConsumers) {
-        float4 L0[4], L1[4];
+      for (int k0 = tid; k0 < ntask; k0 += MB_ * kMdictConsumers) {
+        float4 L0[MB_], L1[MB_];
 #pragma unroll
-        for (int b = 0; b < 4; ++b) {
+        for (int b = 0; b < MB_; ++b) {
           const int k = min(k0 + b * kMdictConsumers, ntask - 1);
           const int v4 = k % nv4, cc = k / nv4;  // cc = c * NCO + co
           const int c = cc / NCO, co = cc - c * NCO;
@@ -139,7 +144,7 @@ __global__ void __launch_bounds__(NWARP * 32 + 32, 1)
           L1[b] = __ldg(reinterpret_cast<const float4*>(lsrc + (t0 + tstr1) * KC) + v4);
         }
 #pragma unroll
-        for (int b = 0; b < 4; ++b) {
+        for (int b = 0; b < MB_; ++b) {
           const int k = k0 + b * kMdictConsumers;
           if (k >= ntask) break;
           const int v4 = k % nv4, cc = k / nv4;
