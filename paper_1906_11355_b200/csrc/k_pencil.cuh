@@ -10,6 +10,10 @@
 
 #include "common.cuh"
 
+#ifndef NB_SWITCH_KT2
+#define NB_SWITCH_KT2 1
+#endif
+
 namespace mg {
 
 struct PencilSmem {
@@ -597,6 +601,10 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
   constexpr int NW = kConsumersBlend / 32;
   constexpr bool DICT = NB < 0;
   constexpr bool MORD = KT == 1 && KO == 3;
+  // per-warp edge-table mode of the NB blend (see nb_edges); compiling it out
+  // of the KT == 2 kernel (NB_SWITCH_KT2=0) removes a 24-byte spill (5D blend
+  // 3.72 -> 3.70 ms) but leaves quantised KT == 2 data on the bracketed floors
+  constexpr bool NB_SWITCH = NB > 0 && (KT == 1 || NB_SWITCH_KT2);
   if (W.range[2] != 0) return;  // non-finite input: write nothing
   if (DICT) {
     if (W.dmeta[2] == 0) return;
@@ -1010,7 +1018,7 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
 #pragma unroll
           for (int j = 0; j < KT; ++j) sbase[j] = (uint32_t)__cvta_generic_to_shared(base[j]);
           const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
-          if (!patho && nb_edges) {  // edge-table test for every voxel-corner
+          if (NB_SWITCH && !patho && nb_edges) {  // edge-table test for every voxel-corner
             constexpr int SF = KO >= 2 ? 2 : 1;
             const float g2[2] = {1.0f - f2, f2};
             const u64 M2 = pk2(kMagic, kMagic);
@@ -1177,7 +1185,7 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
             }
           }
           if constexpr (NB > 0) {  // per-warp mode switch (see nb_edges)
-            if (G.nb_edges < 0) {
+            if (NB_SWITCH && G.nb_edges < 0) {
               if (nb_edges) {
                 if (++nb_probe >= 64) nb_edges = nb_probe = 0;
               } else {
