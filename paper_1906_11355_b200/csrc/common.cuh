@@ -125,8 +125,10 @@ __device__ __forceinline__ int dict_cell(float a, float b, float v0, float S, in
   asm("add.rn.f32x2 %0, %1, %2;" : "=l"(T) : "l"(Y), "l"(D));
   float t0, t1;
   asm("mov.b64 {%0, %1}, %2;" : "=f"(t0), "=f"(t1) : "l"(T));
+  // one unsigned min (VIADDMNMX): values below v0 wrap to huge and land on the
+  // last cell, which the caller's bit comparison rejects like any other miss
   auto cl = [](float t) {
-    return min(max(__float_as_int(t), 0x4B400000), 0x4B400000 + kDictHL - 1) - 0x4B400000;
+    return (int)min((uint32_t)__float_as_int(t) - 0x4B400000u, (uint32_t)(kDictHL - 1));
   };
   if (c1) *c1 = cl(t1);
   return cl(t0);
