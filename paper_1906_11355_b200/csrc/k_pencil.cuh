@@ -70,7 +70,9 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
   const int u0 = cta_units[blockIdx.x], u1 = cta_units[blockIdx.x + 1];
   if (threadIdx.x >= kConsumers) {
     if (threadIdx.x == kConsumers)
-      pipe_produce<KO, false, false>(G, &tmap, units, u0, u1, *P.pipe, P.bufs);
+      pipe_produce<KO, false, false>(
+          G, &tmap, units, G.dyn_units ? 0 : u0, G.dyn_units ? G.dyn_units : u1, *P.pipe, P.bufs,
+          nullptr, G.dyn_units ? reinterpret_cast<unsigned long long*>(&W.range[3]) : nullptr);
     return;
   }
   const int tid = threadIdx.x;
@@ -319,7 +321,10 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
   int k2_edges = G.nb_edges == 1 ? 1 : 0, k2_probe = 0;
   const int u0 = cta_units[blockIdx.x], u1 = cta_units[blockIdx.x + 1];
   if (threadIdx.x >= kConsumers) {
-    if (threadIdx.x == kConsumers) pipe_produce<KO, false>(G, &tmap, units, u0, u1, *P.pipe, P.bufs);
+    if (threadIdx.x == kConsumers)
+      pipe_produce<KO, false>(
+          G, &tmap, units, G.dyn_units ? 0 : u0, G.dyn_units ? G.dyn_units : u1, *P.pipe, P.bufs,
+          nullptr, G.dyn_units ? reinterpret_cast<unsigned long long*>(&W.range[3]) : nullptr);
     return;
   }
   const int tid = threadIdx.x;
