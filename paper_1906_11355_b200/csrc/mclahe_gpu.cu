@@ -521,7 +521,8 @@ void build_units(mclahe_plan_s& pl) {
       interp_unit > 0 ? interp_unit : (local >= (int64_t{1} << 26) ? int64_t{1} << 18 : target);
   // K2 units likewise (handed out by a counter on such volumes, k2_dynamic):
   // fewer per-unit histogram flushes
-  const int64_t hist_target = k2_dynamic(pl, local) ? int64_t{1} << 18 : target;
+  static const int64_t k2_unit = getenv("MCLAHE_K2_UNIT") ? atoll(getenv("MCLAHE_K2_UNIT")) : 0;
+  const int64_t hist_target = k2_unit > 0 ? k2_unit : (k2_dynamic(pl, local) ? int64_t{1} << 18 : target);
   for (int fam = 0; fam < 2; ++fam) {
     Pencil& pc = fam == 0 ? pl.hist : pl.interp;
     if (!pc.on) continue;
