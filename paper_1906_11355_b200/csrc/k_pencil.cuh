@@ -168,7 +168,7 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
     const float* buf = P.bufs + s * stage_elems;
     if (lane_on) {
       // rows in groups of four (four LDS.128 in flight, two min/max chains);
-      // every fourth row pass (warp-uniform, rotating with the stage) feeds the
+      // one row pass in 4 * K2A_SAMPLE_GROUPS (warp-uniform, rotating) feeds the
       // dictionary sample: values the sample misses are rare ones, which the
       // blend resolves from the workspace LUTs
       const float* rp = buf + slot * P4 + e0;

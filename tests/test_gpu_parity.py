@@ -403,7 +403,7 @@ def test_value_dictionary_blend(M, case):
     assert st["used"] == (case not in ("many", "levels")), st
     # folded pairs: rank 4, one trailing dim, power-of-two cells (>= 32-row stages)
     assert st["folded"] == (case in ("scaled4d", "uneven", "rare", "wide")), st
-    if case not in ("many", "levels"):  # K2a samples a quarter of the rows
+    if case not in ("many", "levels"):  # K2a samples one row in eight
         assert 0 < st["values"] <= len(np.unique(x.view(np.uint32))), st
         if case == "rare":
             assert st["values"] < len(np.unique(x.view(np.uint32))), st  # misses exercised
