@@ -103,6 +103,7 @@ __global__ void __launch_bounds__(NWARP * 32 + 32, 1)
   const int64_t stage_elems = G.stage_stride;
   const int rows = G.stage_rows;
   const int nrb = (rows + 31) >> 5;
+  const int r1mask = G.r1 - 1, lg_r1 = G.lg_r1;  // per-item row split, kept in registers
   float ugs[KO], ugt[KO];
   int64_t cur = -1;
   int seg = 0;
@@ -208,7 +209,7 @@ __global__ void __launch_bounds__(NWARP * 32 + 32, 1)
       const int q = min(rb * 32 + lane, rows - 1);
       const int col = seg * 2 + c;
       const bool col_on = col < ncol;  // an odd last column pair
-      const int r1 = q & (G.r1 - 1), r2 = q >> G.lg_r1;
+      const int r1 = q & r1mask, r2 = q >> lg_r1;
       const float f1 = fmaf((float)(xb1 + r1), s1, t1);
       const float f2 = fmaf((float)(xb2 + r2), s2, t2);
       float wo[NCO];
