@@ -205,8 +205,8 @@ __global__ void __launch_bounds__(NWARP * 32 + 32, 1)
     if (rot >= NW) rot -= NW;
     for (int item = first; item < nitems; item += NW) {
       const int c = item & 1, rb = item >> 1;
-      const bool q_on = rb * 32 + lane < rows;
-      const int q = min(rb * 32 + lane, rows - 1);
+      // stages hold a power of two >= 32 rows (plan_mdict): every lane has a row
+      const int q = rb * 32 + lane;
       const int col = seg * 2 + c;
       const bool col_on = col < ncol;  // an odd last column pair
       const int r1 = q & r1mask, r2 = q >> lg_r1;
@@ -290,8 +290,8 @@ __global__ void __launch_bounds__(NWARP * 32 + 32, 1)
       r.z = fminf(fmaxf(acc[2], 0.f), 1.f);
       r.w = fminf(fmaxf(acc[3], 0.f), 1.f);
       if (TSTORE) {
-        if (q_on) *slot4 = r;  // in place; the producer TMA-stores the box
-      } else if (q_on && col_on) {
+        *slot4 = r;  // in place; the producer TMA-stores the box
+      } else if (col_on) {
         __stcs(reinterpret_cast<float4*>(out + gbase + (int64_t)r2 * G.vstride[KO - 2] +
                                          (int64_t)r1 * G.vstride[KO - 1] + col * 4),
                r);

@@ -446,7 +446,7 @@ void plan_mdict(mclahe_plan_s* pl) {
   static const int nst_cap = getenv("MCLAHE_MDICT_NST") ? atoi(getenv("MCLAHE_MDICT_NST")) : 4;
   m.r2 = (int)pow2_divisor(g2, std::min<int64_t>(256, std::max(1, rows_cap / m.r1)));
   m.stage_rows = m.r1 * m.r2;
-  if (m.stage_rows < 32) return;
+  if (m.stage_rows < 32) return;  // a power of two >= 32: the kernel assumes whole warps of rows
   m.stage_stride = align_up(m.stage_rows * 32, 1024) / 4;
   const int64_t nco = int64_t{1} << c.ko;
   m.tail = 2 * 4 * nco * tk * 4 + kDictHL * 8 + nco * 4 + 16 + ((c.P / 4 + 3) & ~int64_t(3)) * 4 +
