@@ -114,7 +114,11 @@ typedef struct {
  * are HOST buffers of prod(shape) elements of `dtype`; validation
  * (src/pipeline.cpp:19-34) happens first, with the reference messages.
  * Pinned host buffers are copied asynchronously; pageable ones through the
- * driver's staging path.  timings may be NULL. */
+ * driver's staging path.  timings may be NULL.
+ * On MCLAHE_ERR_VALIDATION for non-finite input `out` holds no result: in
+ * global mode it is never written (the flag is read after the range pass,
+ * before any blend); in adaptive mode the streamed call has already copied
+ * early chunks back, so it fills `out` with NaN before returning. */
 int mclahe_gpu_run(const mclahe_params_t* params, const void* in, void* out,
                    mclahe_timings_t* timings);
 

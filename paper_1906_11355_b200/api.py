@@ -161,19 +161,31 @@ class Plan:
     def _ptr(self, t) -> int:
         return int(t.data_ptr())
 
+    @staticmethod
+    def _same_device(*ts):
+        """Buffers of one pass must live on one device (kernels and TMA maps
+        address that device's memory); returns a context making it current."""
+        import torch
+        devs = {t.device for t in ts if t is not None}
+        if len(devs) != 1 or next(iter(devs)).type != "cuda":
+            raise ValidationError(f"pass buffers must share one CUDA device, got {sorted(map(str, devs))}")
+        return torch.cuda.device(next(iter(devs)))
+
     def reset(self, ws, stream=None):
         N.check(N.lib().mclahe_pass_reset(self._h, self._ptr(ws), _stream_handle(stream)))
 
     def range(self, x, ws, stream=None):
-        N.check(N.lib().mclahe_pass_range(self._h, self._ptr(x), self._ptr(ws),
-                                          _stream_handle(stream)))
+        with self._same_device(x, ws):
+            N.check(N.lib().mclahe_pass_range(self._h, self._ptr(x), self._ptr(ws),
+                                              _stream_handle(stream)))
 
     def make_params(self, ws, stream=None):
         N.check(N.lib().mclahe_pass_params(self._h, self._ptr(ws), _stream_handle(stream)))
 
     def histograms(self, x, ws, stream=None):
-        N.check(N.lib().mclahe_pass_histograms(self._h, self._ptr(x), self._ptr(ws),
-                                               _stream_handle(stream)))
+        with self._same_device(x, ws):
+            N.check(N.lib().mclahe_pass_histograms(self._h, self._ptr(x), self._ptr(ws),
+                                                   _stream_handle(stream)))
 
     def mappings(self, ws, stream=None, debug: dict | None = None):
         dbg = None
@@ -187,12 +199,14 @@ class Plan:
                                              _stream_handle(stream)))
 
     def interpolate(self, x, out, ws, stream=None):
-        N.check(N.lib().mclahe_pass_interpolate(self._h, self._ptr(x), self._ptr(out),
-                                                self._ptr(ws), _stream_handle(stream)))
+        with self._same_device(x, out, ws):
+            N.check(N.lib().mclahe_pass_interpolate(self._h, self._ptr(x), self._ptr(out),
+                                                    self._ptr(ws), _stream_handle(stream)))
 
     def enqueue(self, x, out, ws, stream=None):
-        N.check(N.lib().mclahe_plan_enqueue(self._h, self._ptr(x), self._ptr(out), self._ptr(ws),
-                                            _stream_handle(stream)))
+        with self._same_device(x, out, ws):
+            N.check(N.lib().mclahe_plan_enqueue(self._h, self._ptr(x), self._ptr(out), self._ptr(ws),
+                                                _stream_handle(stream)))
 
     def check(self, ws, stream=None):
         N.check(N.lib().mclahe_plan_check(self._h, self._ptr(ws), _stream_handle(stream)))
@@ -287,11 +301,14 @@ def _mclahe_device(x, kernel, n_bins, clip, adaptive, timings=None):
     if x.dtype not in (torch.float32, torch.float64):
         x = x.to(torch.float64)
     x = x.contiguous()
-    plan = _cached_plan(x.shape, kernel, n_bins, clip, adaptive, _dtype_code(x.dtype))
-    ws = plan.new_workspace(x.device)
-    out = torch.empty_like(x)
-    plan.enqueue(x, out, ws)
-    plan.check(ws)
+    # plans, TMA maps and launches belong to the tensor's device, which need
+    # not be the current one
+    with torch.cuda.device(x.device):
+        plan = _cached_plan(x.shape, kernel, n_bins, clip, adaptive, _dtype_code(x.dtype))
+        ws = plan.new_workspace(x.device)
+        out = torch.empty_like(x)
+        plan.enqueue(x, out, ws)
+        plan.check(ws)
     return out
 
 

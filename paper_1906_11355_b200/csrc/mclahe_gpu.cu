@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <limits>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -446,7 +447,19 @@ void plan_mdict(mclahe_plan_s* pl) {
   static const int nst_cap = getenv("MCLAHE_MDICT_NST") ? atoi(getenv("MCLAHE_MDICT_NST")) : 4;
   m.r2 = (int)pow2_divisor(g2, std::min<int64_t>(256, std::max(1, rows_cap / m.r1)));
   m.stage_rows = m.r1 * m.r2;
-  if (m.stage_rows < 32) return;  // a power of two >= 32: the kernel assumes whole warps of rows
+  // the kernel has no per-lane row clamp: every box must be full, i.e. the
+  // stage is whole warps of rows (a power of two >= 32) and R1 / R2 divide
+  // every cell extent along dims KO-1 / KO-2 (else the TMA box would cross
+  // into the next cell and lanes would read / write past it)
+  if (m.stage_rows < 32 || (m.stage_rows & (m.stage_rows - 1)) != 0) return;
+  for (auto& p : ex)
+    if ((p.second - p.first) % m.r2 != 0) return;
+  {
+    std::vector<std::pair<int64_t, int64_t>> ex1;
+    extents(*pl, true, c.ko - 1, ex1);
+    for (auto& p : ex1)
+      if ((p.second - p.first) % m.r1 != 0) return;
+  }
   m.stage_stride = align_up(m.stage_rows * 32, 1024) / 4;
   const int64_t nco = int64_t{1} << c.ko;
   m.tail = 2 * 4 * nco * tk * 4 + kDictHL * 8 + nco * 4 + 16 + ((c.P / 4 + 3) & ~int64_t(3)) * 4 +
@@ -1221,6 +1234,15 @@ int run_streamed(Streamed& S, const mclahe_params_t* p, const void* in, void* ou
         params_rows = r;
       }
     } else if (ranged == C && !gparams) {
+      // global mode: every voxel has been through the range pass before any
+      // bin exists, so the non-finite flag is final here -- report it before
+      // any blend or D2H touches the caller's buffer (the reference throws
+      // before it writes anything, src/pipeline.cpp:33)
+      int64_t gflag = 0;
+      MG_CUDA(cudaMemcpyAsync(&gflag, static_cast<char*>(ws) + M->info.off_range + 16,
+                              sizeof gflag, cudaMemcpyDeviceToHost, s_comp));
+      MG_CUDA(cudaStreamSynchronize(s_comp));
+      if (gflag) return fail(MCLAHE_ERR_VALIDATION, "image contains non-finite values");
       if ((rc = do_params(M, ws, s_comp))) return rc;
       gparams = true;
     }
@@ -1263,7 +1285,17 @@ int run_streamed(Streamed& S, const mclahe_params_t* p, const void* in, void* ou
                           cudaMemcpyDeviceToHost, s_comp));
   MG_CUDA(cudaStreamSynchronize(s_comp));
   MG_CUDA(cudaStreamSynchronize(s_out));
-  if (flag) return fail(MCLAHE_ERR_VALIDATION, "image contains non-finite values");
+  if (flag) {
+    // adaptive mode: early chunks were blended and copied back while later
+    // chunks were still arriving; scrub the caller's buffer so no partial
+    // result survives the error (NaN is never a valid output)
+    const int64_t n = volume(p);
+    if (p->dtype == MCLAHE_F64)
+      std::fill_n(static_cast<double*>(out), n, std::numeric_limits<double>::quiet_NaN());
+    else
+      std::fill_n(static_cast<float*>(out), n, std::numeric_limits<float>::quiet_NaN());
+    return fail(MCLAHE_ERR_VALIDATION, "image contains non-finite values");
+  }
   if (timings) {
     float total = 0.f;
     MG_CUDA(cudaEventElapsedTime(&total, ev[2 * C], ev[2 * C + 1]));
@@ -1318,6 +1350,9 @@ mclahe_plan_s* cached_plan(OneShot& o, const mclahe_params_t* p, int* rc, int fr
   if (frame_axis >= 0) {  // per-frame global ranges: K2a and the dictionary stay off
     pl->frame_axis = frame_axis;
     pl->dict_cap = 0;
+    // the plan was described as adaptive, so plan_mdict may have armed the
+    // folded-pair dictionary blend; with no dictionary it has no tables
+    pl->mdict = false;
     pl->off_frange = align_up(pl->info.workspace_bytes, 256);
     pl->info.workspace_bytes = align_up(pl->off_frange + q.shape[frame_axis] * 16, 256);
   }

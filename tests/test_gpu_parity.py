@@ -339,6 +339,42 @@ def test_streamed_host_api_matches_device(M, name):
         M.enhance(xn, *args)
 
 
+@pytest.mark.parametrize("ad", [False, True])
+def test_streamed_error_leaves_no_partial_output(M, ad):
+    """a non-finite voxel in a late chunk must not leave a partial
+    result in the caller's buffer.  Global mode never writes it (the flag is
+    read after the range pass, before any blend / D2H); adaptive mode scrubs
+    it with NaN (early chunks were already copied back)."""
+    import ctypes as C
+    from paper_1906_11355_b200 import _native as N
+    from paper_1906_11355_b200 import datasets
+    c = dict(SCALED["4d"])
+    shape = (c["shape"][0] * 2,) + tuple(c["shape"][1:])
+    x = datasets.make("4d", seed=5, shape=shape).numpy().copy()
+    x[-1, 5, 4, 3] = np.inf
+    params = N.make_params(x.shape, c["kernel"], c["n_bins"], c["clip_limit"], ad, 0)
+    out = np.full_like(x, 7.0)
+    rc = N.lib().mclahe_gpu_run(C.byref(params), x.ctypes.data, out.ctypes.data, None)
+    assert rc == 1 and b"non-finite" in N.lib().mclahe_last_error()
+    if ad:
+        assert np.isnan(out).all()
+    else:
+        assert np.all(out == 7.0)
+
+
+def test_framewise_global_rank4_folded_geometry(M):
+    """a global framewise call whose per-frame geometry
+    would arm the folded-pair blend (one trailing dim, multiple of 32) must
+    not launch it -- the frame plan has no dictionary tables."""
+    rng = np.random.default_rng(81)
+    x = (rng.poisson(3.0, (8, 64, 64, 32)) / 11.0).astype(np.float32)
+    kernel = (16, 16, 4)
+    params = M.EnhanceParams(0.02, 64, M.RangeMode.Global)
+    out = M.mclahe_framewise(x, 0, M.KernelSpec(kernel), params)
+    want = _framewise_oracle(x, 0, kernel, 64, 0.02, False, False)
+    assert np.max(np.abs(out.astype(np.float64) - want)) <= OUT_TOL
+
+
 def _run_plan(M, x, kernel, nb, clip, ad, no_dict=False):
     old = os.environ.pop("MCLAHE_NO_DICT", None)
     if no_dict:
