@@ -69,6 +69,13 @@ def _lib(impl: str) -> C.CDLL:
         lib.ref_tile_stats.argtypes = [_f64p, C.c_int, _i64p, _i64p, C.c_int64, C.c_double,
                                        C.c_int, _f64p, _f64p, _f64p, _f64p, _f64p, _u8p,
                                        C.c_char_p, C.c_int]
+        lib.ref_tile_stats_window.argtypes = [
+            _f64p, C.c_int, _i64p, _i64p, C.c_int64, C.c_double, C.c_int, C.c_int, C.c_double,
+            C.c_double, C.c_int64, C.c_int64, C.c_uint, _f64p, _f64p, _f64p, _f64p, _f64p, _u8p,
+            C.c_char_p, C.c_int]
+        lib.ref_blend_rows.argtypes = [
+            _f64p, C.c_int, _i64p, _i64p, C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_int64,
+            _f64p, _f64p, _f64p, _u8p, C.c_uint, _f64p, C.c_char_p, C.c_int]
         lib.ref_bin_index.restype = C.c_int64
         lib.ref_bin_index.argtypes = [C.c_double, C.c_double, C.c_double, C.c_int64]
         lib.ref_clip_histogram.argtypes = [_f64p, C.c_int64, C.c_double, _f64p]
@@ -160,6 +167,86 @@ def tile_stats(data: np.ndarray, kernel, n_bins: int, clip_limit: float, adaptiv
         raise OracleValidationError("tile_stats rejected the request")
     return dict(lo=lo, hi=hi, counts=counts, clipped=clipped, lut=lut,
                 degenerate=degen.astype(bool), grid=tuple(int(g) for g in grid))
+
+
+def ref_tile_stats_window(data: np.ndarray, kernel, n_bins: int, clip_limit: float,
+                          adaptive: bool, tile_row0: int, tile_rows: int,
+                          global_range=None, threads: int = 0) -> dict:
+    """The compiled reference's per-tile intermediates for tile rows
+    [tile_row0, tile_row0 + tile_rows) along dim 0 of ``data`` (its own
+    symmetric_pad / kernelize / build_mappings, multi-threaded).  global_range
+    (lo, hi) overrides the Global-mode range -- for dim-0 crops of a larger
+    volume (see ref_shim.cpp)."""
+    x = np.ascontiguousarray(data, dtype=np.float64)
+    shape, ker = _i64(x.shape), _i64(kernel)
+    _, _, grid = geometry(x.shape, kernel)
+    T = int(tile_rows) * int(np.prod(grid[1:]))
+    lo, hi = np.zeros(T), np.zeros(T)
+    counts, clipped, lut = (np.zeros((T, n_bins)) for _ in range(3))
+    degen = np.zeros(T, dtype=np.uint8)
+    err = C.create_string_buffer(256)
+    g = global_range is not None
+    glo, ghi = (float(global_range[0]), float(global_range[1])) if g else (0.0, 0.0)
+    rc = _lib("ref").ref_tile_stats_window(
+        _p(x, _f64p), x.ndim, _p(shape, _i64p), _p(ker, _i64p), int(n_bins), float(clip_limit),
+        int(bool(adaptive)), int(g), glo, ghi, int(tile_row0), int(tile_rows), int(threads),
+        _p(lo, _f64p), _p(hi, _f64p), _p(counts, _f64p), _p(clipped, _f64p), _p(lut, _f64p),
+        _p(degen, _u8p), err, 256)
+    if rc:
+        raise RuntimeError(err.value.decode())
+    return dict(lo=lo, hi=hi, counts=counts, clipped=clipped, lut=lut,
+                degenerate=degen.astype(bool))
+
+
+def ref_tile_rows_by_crop(x: np.ndarray, kernel, n_bins: int, clip_limit: float,
+                          adaptive: bool, t0: int, t1: int, global_range, threads: int = 0):
+    """Reference intermediates of tile rows [t0, t1) of a volume too large for
+    the reference's padded + kernelized copies, from one dim-0 crop.
+
+    With shape[0] % b0 == 0 every crop whose length is a multiple of b0 gets
+    the full volume's dim-0 padding (compute_pad_plan, nd_image.cpp:97-99:
+    before = floor(b0/2)).  Crop [(t0-1)*b0, (t1)*b0) then holds the full
+    volume's tile t as its tile t - t0 + 1 (tile rows of the crop away from its
+    own mirrored ends); a crop starting at row 0 keeps tile 0, and one ending at
+    the last row keeps the last tile.  Global mode takes the full volume's
+    range.  Returns (stats, crop_row0)."""
+    s0, b0 = int(x.shape[0]), int(kernel[0])
+    assert s0 % b0 == 0, "crop windows need shape[0] % kernel[0] == 0"
+    g0 = s0 // b0 + 1
+    a = max(0, (t0 - 1) * b0)
+    e = min(s0, t1 * b0)
+    if t1 == g0:  # window reaching the last tile: the crop ends at the last row
+        e = s0
+    first = t0 - (a // b0)  # crop tile index of full tile t0
+    if a > 0:
+        first = 1
+    st = ref_tile_stats_window(x[a:e], kernel, n_bins, clip_limit, adaptive, first, t1 - t0,
+                               global_range=global_range, threads=threads)
+    return st, a
+
+
+def ref_blend_rows(rows: np.ndarray, full_shape, kernel, row0: int, n_bins: int,
+                   tile_row0: int, stats: dict, threads: int = 0) -> np.ndarray:
+    """The reference's per-voxel loop (pipeline.cpp:94-127) for original rows
+    [row0, row0 + len(rows)) of a volume of ``full_shape``, over the mappings of
+    ``stats`` (tile rows starting at tile_row0)."""
+    x = np.ascontiguousarray(rows, dtype=np.float64)
+    shape, ker = _i64(full_shape), _i64(kernel)
+    per_row = int(np.prod(geometry(full_shape, kernel)[2][1:]))
+    tile_rows = len(stats["lo"]) // per_row
+    out = np.empty_like(x)
+    err = C.create_string_buffer(256)
+    lut = np.ascontiguousarray(stats["lut"], dtype=np.float64)
+    degen = np.ascontiguousarray(stats["degenerate"], dtype=np.uint8)
+    lo = np.ascontiguousarray(stats["lo"], dtype=np.float64)
+    hi = np.ascontiguousarray(stats["hi"], dtype=np.float64)
+    rc = _lib("ref").ref_blend_rows(
+        _p(x, _f64p), len(full_shape), _p(shape, _i64p), _p(ker, _i64p), int(row0),
+        int(row0) + x.shape[0], int(n_bins), int(tile_row0), int(tile_rows), _p(lo, _f64p),
+        _p(hi, _f64p), _p(lut, _f64p), _p(degen, _u8p), int(threads), _p(out, _f64p), err, 256)
+    if rc:
+        raise RuntimeError(err.value.decode())
+    return out
 
 
 def bin_index(value: float, lo: float, hi: float, n_bins: int, impl: str = "c") -> int:

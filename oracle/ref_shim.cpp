@@ -9,7 +9,9 @@
 // (histogram.hpp:51-80), neighbor_kernels / interp_coefficients /
 // transform_pixel (interpolation.hpp:28-45), gaussian_filter / median_filter
 // (filters.hpp:24-32) and the contrast metrics (metrics.hpp:19-36).
+#include <array>
 #include <cstdint>
+#include <stdexcept>
 #include <cstring>
 #include <exception>
 #include <string>
@@ -20,6 +22,7 @@
 #include "mclahe/interpolation.hpp"
 #include "mclahe/metrics.hpp"
 #include "mclahe/npy.hpp"
+#include "mclahe/parallel.hpp"
 #include "mclahe/nd_image.hpp"
 #include "mclahe/pipeline.hpp"
 
@@ -110,6 +113,132 @@ int ref_tile_stats(const double* data, int rank, const int64_t* shape, const int
       if (counts) std::memcpy(counts + k * nb, c.data(), nb * sizeof(double));
       if (clipped) std::memcpy(clipped + k * nb, cl.data(), nb * sizeof(double));
     }
+    return 0;
+  } catch (const mclahe::ValidationError& e) {
+    put_err(err, err_len, e.what());
+    return 1;
+  } catch (const std::exception& e) {
+    put_err(err, err_len, e.what());
+    return 2;
+  }
+}
+
+// ref_tile_stats for a window of tile rows [tile_row0, tile_row0 + tile_rows)
+// along dim 0, multi-threaded through the reference's own parallel_for
+// (parallel.hpp:23-61; results do not depend on the worker count).  With
+// has_global the Global-mode range is (glo, hi) instead of the image's own
+// min/max: the full-size gate runs the reference on dim-0 crops of a volume
+// too large for its padded + kernelized copies, and a crop's interior tile
+// rows equal the full volume's once the full volume's range is used.
+int ref_tile_stats_window(const double* data, int rank, const int64_t* shape,
+                          const int64_t* kernel, int64_t n_bins, double clip_limit, int adaptive,
+                          int has_global, double glo, double ghi, int64_t tile_row0,
+                          int64_t tile_rows, unsigned threads, double* lo, double* hi,
+                          double* counts, double* clipped, double* lut, uint8_t* degenerate,
+                          char* err, int err_len) {
+  try {
+    const mclahe::NdImage image = make_image(data, rank, shape);
+    const mclahe::KernelSpec ks{std::vector<size_t>(kernel, kernel + rank)};
+    const mclahe::PadPlan plan = mclahe::compute_pad_plan(image.shape(), ks);
+    const mclahe::NdImage padded = mclahe::symmetric_pad(image, plan);
+    const mclahe::KernelGrid grid = mclahe::kernelize(padded, ks);
+    mclahe::EnhanceParams params;
+    params.clip_limit = clip_limit;
+    params.n_bins = static_cast<size_t>(n_bins);
+    params.range_mode = adaptive ? mclahe::RangeMode::Adaptive : mclahe::RangeMode::Global;
+    mclahe::IntensityRange global;
+    if (has_global) {
+      global.lo = glo;
+      global.hi = ghi;
+    } else {
+      image.min_max(global.lo, global.hi);
+    }
+    const mclahe::MappingGrid maps = mclahe::build_mappings(grid, params, global, threads);
+    const size_t per_row = grid.block_count() / grid.grid_shape[0];
+    const size_t k0 = static_cast<size_t>(tile_row0) * per_row;
+    const size_t nk = static_cast<size_t>(tile_rows) * per_row;
+    if (k0 + nk > grid.block_count()) throw std::runtime_error("tile-row window out of range");
+    const size_t nb = static_cast<size_t>(n_bins);
+    mclahe::parallel_for(nk, threads, [&](size_t begin, size_t end) {
+      for (size_t i = begin; i < end; ++i) {
+        const size_t k = k0 + i;
+        const mclahe::KernelMapping& m = maps.at(k);
+        lo[i] = m.range.lo;
+        hi[i] = m.range.hi;
+        degenerate[i] = m.degenerate ? 1 : 0;
+        std::memcpy(lut + i * nb, m.values.data(), nb * sizeof(double));
+        std::vector<double> c(nb, 0.0), cl(nb, 0.0);
+        if (!m.range.degenerate()) {
+          c = mclahe::compute_histogram(grid.block(k), m.range, nb);
+          cl = mclahe::clip_histogram(c, clip_limit);
+        }
+        std::memcpy(counts + i * nb, c.data(), nb * sizeof(double));
+        std::memcpy(clipped + i * nb, cl.data(), nb * sizeof(double));
+      }
+    });
+    return 0;
+  } catch (const mclahe::ValidationError& e) {
+    put_err(err, err_len, e.what());
+    return 1;
+  } catch (const std::exception& e) {
+    put_err(err, err_len, e.what());
+    return 2;
+  }
+}
+
+// The per-voxel loop of mclahe::mclahe (src/pipeline.cpp:94-127) for the
+// original rows [row0, row1) of a volume of shape `shape`, over mappings given
+// for the tile rows [tile_row0, tile_row0 + tile_rows) (lo / hi / lut /
+// degenerate as ref_tile_stats_window returns them).  `rows` holds only those
+// voxel rows.  Each voxel goes through the reference's neighbor_kernels,
+// interp_coefficients and transform_pixel; mappings outside the window throw.
+int ref_blend_rows(const double* rows, int rank, const int64_t* shape, const int64_t* kernel,
+                   int64_t row0, int64_t row1, int64_t n_bins, int64_t tile_row0,
+                   int64_t tile_rows, const double* lo, const double* hi, const double* lut,
+                   const uint8_t* degenerate, unsigned threads, double* out, char* err,
+                   int err_len) {
+  try {
+    const mclahe::Shape full(shape, shape + rank);
+    const mclahe::KernelSpec ks{std::vector<size_t>(kernel, kernel + rank)};
+    const mclahe::PadPlan plan = mclahe::compute_pad_plan(full, ks);
+    mclahe::Shape gshape(rank);
+    for (int j = 0; j < rank; ++j)
+      gshape[j] = (full[j] + plan.before[j] + plan.after[j]) / ks.sizes[j];
+    const auto gstrides = mclahe::row_major_strides(gshape);
+    const size_t per_row = gstrides[0];
+    const size_t nb = static_cast<size_t>(n_bins);
+    std::vector<mclahe::KernelMapping> maps(static_cast<size_t>(tile_rows) * per_row);
+    for (size_t i = 0; i < maps.size(); ++i) {
+      maps[i].range = {lo[i], hi[i]};
+      maps[i].values.assign(lut + i * nb, lut + (i + 1) * nb);
+      maps[i].degenerate = degenerate[i] != 0;
+    }
+    mclahe::Shape local = full;
+    local[0] = static_cast<size_t>(row1 - row0);
+    const size_t n = mclahe::shape_product(local);
+    const size_t corners = mclahe::corner_count(static_cast<size_t>(rank));
+    const size_t first = static_cast<size_t>(tile_row0) * per_row;
+    mclahe::parallel_for(n, threads, [&](size_t begin, size_t end) {
+      std::array<size_t, mclahe::kMaxRank> pixel{};
+      std::array<double, mclahe::kMaxCorners> coeffs;
+      std::array<const mclahe::KernelMapping*, mclahe::kMaxCorners> nmaps;
+      std::vector<size_t> coord(rank, 0);
+      mclahe::unflatten(begin, local, coord);
+      for (size_t flat = begin; flat < end; ++flat) {
+        for (int j = 0; j < rank; ++j) pixel[j] = coord[j] + plan.before[j];
+        pixel[0] += static_cast<size_t>(row0);
+        const mclahe::NeighborSet ns = mclahe::neighbor_kernels({pixel.data(), size_t(rank)}, ks, gshape);
+        mclahe::interp_coefficients(ns, ks, {coeffs.data(), corners});
+        for (size_t c = 0; c < corners; ++c) {
+          size_t g = 0;
+          for (int j = 0; j < rank; ++j) g += (ns.lower[j] + ((c >> (rank - 1 - j)) & 1u)) * gstrides[j];
+          if (g < first || g - first >= maps.size()) throw std::runtime_error("mapping outside the window");
+          nmaps[c] = &maps[g - first];
+        }
+        out[flat] = mclahe::transform_pixel(rows[flat], {nmaps.data(), corners}, {coeffs.data(), corners});
+        mclahe::next_coord(coord, local);
+      }
+    });
     return 0;
   } catch (const mclahe::ValidationError& e) {
     put_err(err, err_len, e.what());
