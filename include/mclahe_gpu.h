@@ -246,6 +246,29 @@ int mclahe_metrics_device(int32_t rank, const int64_t* shape, const double* a_de
                           const double* b_dev, int64_t n_bins, double peak,
                           mclahe_metrics_t* report, void* stream);
 
+/* ---- The reference's per-operation API on the device (csrc/ops.cu) -------
+ * For callers of include/mclahe/{histogram,nd_image}.hpp that use the
+ * building blocks instead of mclahe::mclahe.  Host buffers, float64.
+ *
+ * mclahe_block_mappings: build_mappings (src/histogram.cpp:72-106) over
+ *   n_blocks contiguous blocks of block_len values (KernelGrid::blocks):
+ *   adaptive = each block's own min/max (first of the minimal class, NaN
+ *   never wins unless it is the block's front element), else
+ *   [global_lo, global_hi]; lo / hi / counts (compute_histogram) / clipped
+ *   (clip_histogram) / lut (normalized_cdf values or 0.5) / degenerate per
+ *   block, bit-identical to the reference.  Any output may be NULL, except
+ *   that lut and degenerate go together; lut == NULL skips clip / CDF (the
+ *   compute_histogram form).
+ * mclahe_nd_gather: op 0 = symmetric_pad (a = before, b = after,
+ *   src/nd_image.cpp:104-144), op 1 = kernelize (a = kernel sizes, b unused,
+ *   :146-187), op 2 = crop (a = offset, b = out shape, :189-218). */
+int mclahe_block_mappings(const double* host_blocks, int64_t n_blocks, int64_t block_len,
+                          int64_t n_bins, double clip_limit, int32_t adaptive, double global_lo,
+                          double global_hi, double* lo, double* hi, double* counts,
+                          double* clipped, double* lut, uint8_t* degenerate);
+int mclahe_nd_gather(int32_t op, int32_t rank, const int64_t* in_shape, const int64_t* a,
+                     const int64_t* b, const double* host_in, double* host_out);
+
 /* Number of kernel launches the last pass call on this thread issued. */
 int64_t mclahe_launch_count(void);
 

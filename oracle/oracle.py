@@ -40,6 +40,12 @@ def _lib(impl: str) -> C.CDLL:
         path = os.path.join(HERE, "liboracle.so")
     elif impl == "ref":
         path = os.path.join(HERE, "_ref", "libmclahe_ref.so")
+    elif impl == "b200":
+        # oracle/ref_shim.cpp compiled UNMODIFIED against the B200 drop-in's
+        # headers (include/mclahe/*.hpp) and linked to libmclahe_cpp.so -- a
+        # reference caller re-linked to the GPU build (tests/test_dropin_cpp.py
+        # builds it); the same ctypes surface as "ref"
+        path = os.environ.get("MCLAHE_SHIM_B200", os.path.join(HERE, "_ref", "libshim_b200.so"))
     else:
         raise ValueError(f"unknown oracle impl {impl!r}")
     if not os.path.exists(path):
@@ -162,7 +168,7 @@ def tile_stats(data: np.ndarray, kernel, n_bins: int, clip_limit: float, adaptiv
         rc = _lib("c").orc_tile_stats(*args)
     else:
         err = C.create_string_buffer(256)
-        rc = _lib("ref").ref_tile_stats(*args, err, 256)
+        rc = _lib(impl).ref_tile_stats(*args, err, 256)
     if rc:
         raise OracleValidationError("tile_stats rejected the request")
     return dict(lo=lo, hi=hi, counts=counts, clipped=clipped, lut=lut,
@@ -171,7 +177,7 @@ def tile_stats(data: np.ndarray, kernel, n_bins: int, clip_limit: float, adaptiv
 
 def ref_tile_stats_window(data: np.ndarray, kernel, n_bins: int, clip_limit: float,
                           adaptive: bool, tile_row0: int, tile_rows: int,
-                          global_range=None, threads: int = 0) -> dict:
+                          global_range=None, threads: int = 0, impl: str = "ref") -> dict:
     """The compiled reference's per-tile intermediates for tile rows
     [tile_row0, tile_row0 + tile_rows) along dim 0 of ``data`` (its own
     symmetric_pad / kernelize / build_mappings, multi-threaded).  global_range
@@ -187,7 +193,7 @@ def ref_tile_stats_window(data: np.ndarray, kernel, n_bins: int, clip_limit: flo
     err = C.create_string_buffer(256)
     g = global_range is not None
     glo, ghi = (float(global_range[0]), float(global_range[1])) if g else (0.0, 0.0)
-    rc = _lib("ref").ref_tile_stats_window(
+    rc = _lib(impl).ref_tile_stats_window(
         _p(x, _f64p), x.ndim, _p(shape, _i64p), _p(ker, _i64p), int(n_bins), float(clip_limit),
         int(bool(adaptive)), int(g), glo, ghi, int(tile_row0), int(tile_rows), int(threads),
         _p(lo, _f64p), _p(hi, _f64p), _p(counts, _f64p), _p(clipped, _f64p), _p(lut, _f64p),
@@ -226,7 +232,7 @@ def ref_tile_rows_by_crop(x: np.ndarray, kernel, n_bins: int, clip_limit: float,
 
 
 def ref_blend_rows(rows: np.ndarray, full_shape, kernel, row0: int, n_bins: int,
-                   tile_row0: int, stats: dict, threads: int = 0) -> np.ndarray:
+                   tile_row0: int, stats: dict, threads: int = 0, impl: str = "ref") -> np.ndarray:
     """The reference's per-voxel loop (pipeline.cpp:94-127) for original rows
     [row0, row0 + len(rows)) of a volume of ``full_shape``, over the mappings of
     ``stats`` (tile rows starting at tile_row0)."""
@@ -240,7 +246,7 @@ def ref_blend_rows(rows: np.ndarray, full_shape, kernel, row0: int, n_bins: int,
     degen = np.ascontiguousarray(stats["degenerate"], dtype=np.uint8)
     lo = np.ascontiguousarray(stats["lo"], dtype=np.float64)
     hi = np.ascontiguousarray(stats["hi"], dtype=np.float64)
-    rc = _lib("ref").ref_blend_rows(
+    rc = _lib(impl).ref_blend_rows(
         _p(x, _f64p), len(full_shape), _p(shape, _i64p), _p(ker, _i64p), int(row0),
         int(row0) + x.shape[0], int(n_bins), int(tile_row0), int(tile_rows), _p(lo, _f64p),
         _p(hi, _f64p), _p(lut, _f64p), _p(degen, _u8p), int(threads), _p(out, _f64p), err, 256)
@@ -252,7 +258,7 @@ def ref_blend_rows(rows: np.ndarray, full_shape, kernel, row0: int, n_bins: int,
 def bin_index(value: float, lo: float, hi: float, n_bins: int, impl: str = "c") -> int:
     if impl == "c":
         return int(_lib("c").orc_bin_index(value, lo, hi, n_bins))
-    return int(_lib("ref").ref_bin_index(value, lo, hi, n_bins))
+    return int(_lib(impl).ref_bin_index(value, lo, hi, n_bins))
 
 
 def bin_index_array(values: np.ndarray, lo: float, hi: float, n_bins: int) -> np.ndarray:
@@ -302,7 +308,7 @@ def neighbors(pixel, kernel, grid, impl: str = "c"):
         lib.orc_interp_coefficients(rank, _p(dlo, _f64p), _p(dhi, _f64p), _p(ker, _i64p),
                                     _p(coeff, _f64p))
     else:
-        if _lib("ref").ref_neighbors(rank, _p(px, _i64p), _p(ker, _i64p), _p(gr, _i64p),
+        if _lib(impl).ref_neighbors(rank, _p(px, _i64p), _p(ker, _i64p), _p(gr, _i64p),
                                      _p(lower, _i64p), _p(dlo, _f64p), _p(dhi, _f64p),
                                      _p(coeff, _f64p)):
             raise OracleValidationError("pixel outside the valid interpolation region")
@@ -316,11 +322,11 @@ def blend(coeff, mapped) -> float:
     return float(_lib("c").orc_blend(c.size, _p(c, _f64p), _p(m, _f64p)))
 
 
-def transform_pixel_ref(value, luts, lo, hi, degenerate, coeff) -> float:
+def transform_pixel_ref(value, luts, lo, hi, degenerate, coeff, impl: str = "ref") -> float:
     luts = np.ascontiguousarray(luts, dtype=np.float64)
     lo, hi, coeff = (np.ascontiguousarray(a, dtype=np.float64) for a in (lo, hi, coeff))
     dg = np.ascontiguousarray(degenerate, dtype=np.uint8)
-    return float(_lib("ref").ref_transform_pixel(float(value), coeff.size, _p(luts, _f64p),
+    return float(_lib(impl).ref_transform_pixel(float(value), coeff.size, _p(luts, _f64p),
                                                  luts.shape[1], _p(lo, _f64p), _p(hi, _f64p),
                                                  _p(dg, _u8p), _p(coeff, _f64p)))
 
@@ -401,33 +407,35 @@ def metrics_np(a: np.ndarray, b: np.ndarray, n_bins: int = 256, peak: float = 1.
     return dict(mse=mse_, psnr_db=psnr_, std=std_, entropy_bits=float(ent))
 
 
-def gaussian_filter_ref(x: np.ndarray, sigmas, truncate: float = 4.0) -> np.ndarray:
+def gaussian_filter_ref(x: np.ndarray, sigmas, truncate: float = 4.0,
+                        impl: str = "ref") -> np.ndarray:
     x = np.ascontiguousarray(x, dtype=np.float64)
     sg = np.ascontiguousarray(np.asarray(sigmas, dtype=np.float64))
     shape, out, err = _i64(x.shape), np.empty_like(x), C.create_string_buffer(256)
-    rc = _lib("ref").ref_gaussian(_p(x, _f64p), x.ndim, _p(shape, _i64p), _p(sg, _f64p),
+    rc = _lib(impl).ref_gaussian(_p(x, _f64p), x.ndim, _p(shape, _i64p), _p(sg, _f64p),
                                   C.c_double(truncate), _p(out, _f64p), err, 256)
     if rc:
         raise OracleValidationError(err.value.decode())
     return out
 
 
-def median_filter_ref(x: np.ndarray, window) -> np.ndarray:
+def median_filter_ref(x: np.ndarray, window, impl: str = "ref") -> np.ndarray:
     x = np.ascontiguousarray(x, dtype=np.float64)
     shape, win = _i64(x.shape), _i64(window)
     out, err = np.empty_like(x), C.create_string_buffer(256)
-    rc = _lib("ref").ref_median(_p(x, _f64p), x.ndim, _p(shape, _i64p), _p(win, _i64p),
+    rc = _lib(impl).ref_median(_p(x, _f64p), x.ndim, _p(shape, _i64p), _p(win, _i64p),
                                 _p(out, _f64p), err, 256)
     if rc:
         raise OracleValidationError(err.value.decode())
     return out
 
 
-def metrics_ref(a: np.ndarray, b: np.ndarray, n_bins: int = 256, peak: float = 1.0) -> dict:
+def metrics_ref(a: np.ndarray, b: np.ndarray, n_bins: int = 256, peak: float = 1.0,
+                impl: str = "ref") -> dict:
     a = np.ascontiguousarray(a, dtype=np.float64)
     b = np.ascontiguousarray(b, dtype=np.float64)
     shape, out, err = _i64(a.shape), np.zeros(4), C.create_string_buffer(256)
-    rc = _lib("ref").ref_metrics(_p(a, _f64p), _p(b, _f64p), a.ndim, _p(shape, _i64p),
+    rc = _lib(impl).ref_metrics(_p(a, _f64p), _p(b, _f64p), a.ndim, _p(shape, _i64p),
                                  C.c_int64(n_bins), C.c_double(peak), _p(out, _f64p), err, 256)
     if rc:
         raise OracleValidationError(err.value.decode())

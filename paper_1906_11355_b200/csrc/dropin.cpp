@@ -1,7 +1,10 @@
-// dropin.cpp -- the C++ drop-in (include/mclahe_b200.hpp) over the C ABI.
+// dropin.cpp -- the C++ drop-in (include/mclahe/pipeline.hpp, filters.hpp,
+// metrics.hpp) over the C ABI.
 // Host-side only: validation messages, dtype selection, frame loop; all
 // compute goes through mclahe_gpu_run (include/mclahe_gpu.h).
-#include "../../include/mclahe_b200.hpp"
+#include "mclahe/filters.hpp"
+#include "mclahe/metrics.hpp"
+#include "mclahe/pipeline.hpp"
 
 #include <cmath>
 #include <cstring>
@@ -13,48 +16,19 @@ namespace mclahe {
 
 namespace {
 
-std::size_t product(const Shape& s) {
-  std::size_t p = 1;
-  for (std::size_t e : s) {
-    if (e == 0) throw ValidationError("shape extents must be positive");
-    if (e > std::numeric_limits<std::size_t>::max() / p)
-      throw ValidationError("shape product overflows size_t");
-    p *= e;
-  }
-  return p;
-}
-
 void raise(int rc) {
   const std::string msg = mclahe_last_error();
   if (rc == MCLAHE_ERR_VALIDATION) throw ValidationError(msg);
   throw std::runtime_error("mclahe GPU error " + std::to_string(rc) + ": " + msg);
 }
 
-bool all_f32_exact(const std::vector<double>& v) {
+bool all_f32_exact(std::span<const double> v) {
   for (double x : v)
     if (static_cast<double>(static_cast<float>(x)) != x) return false;
   return true;
 }
 
 }  // namespace
-
-NdImage::NdImage(Shape shape, std::vector<double> data)
-    : shape_(std::move(shape)), data_(std::move(data)) {
-  if (shape_.empty() || shape_.size() > kMaxRank)
-    throw ValidationError("rank must be in [1, " + std::to_string(kMaxRank) + "]");
-  if (product(shape_) != data_.size())
-    throw ValidationError("data length does not match shape product");
-}
-
-NdImage NdImage::zeros(Shape shape) {
-  const std::size_t n = product(shape);
-  return NdImage(std::move(shape), std::vector<double>(n, 0.0));
-}
-
-NdImage NdImage::constant(Shape shape, double value) {
-  const std::size_t n = product(shape);
-  return NdImage(std::move(shape), std::vector<double>(n, value));
-}
 
 NdImage mclahe(const McLaheRequest& request, PhaseTimings* timings) {
   const NdImage& img = request.image;
@@ -74,7 +48,7 @@ NdImage mclahe(const McLaheRequest& request, PhaseTimings* timings) {
   p.clip_limit = request.params.clip_limit;
   mclahe_timings_t t{0.0, 0.0, 0.0};
   std::vector<double> out(img.size());
-  const std::vector<double>& src = img.data();
+  const std::span<const double> src = img.values();
   int rc;
   if (all_f32_exact(src)) {  // float32 pencil kernels, bit-identical bins
     p.dtype = MCLAHE_F32;
@@ -111,7 +85,7 @@ NdImage mclahe_framewise(const NdImage& image, std::size_t frame_axis, const Ker
   for (std::size_t i = 0; i < frame_axis; ++i) outer *= sh[i];
   for (std::size_t i = frame_axis + 1; i < sh.size(); ++i) inner *= sh[i];
   const std::size_t frames = sh[frame_axis];
-  std::vector<double> src = image.data();
+  std::vector<double> src(image.values().begin(), image.values().end());
   if (renormalize_slices) {  // normalize_to_unit per slice, in place
     Shape slice_shape;
     for (std::size_t i = 0; i < sh.size(); ++i)
@@ -122,7 +96,7 @@ NdImage mclahe_framewise(const NdImage& image, std::size_t frame_axis, const Ker
         std::memcpy(&buf[o * inner], &src[(o * frames + f) * inner], inner * sizeof(double));
       const NdImage norm = normalize_to_unit(NdImage(slice_shape, std::move(buf)));
       for (std::size_t o = 0; o < outer; ++o)
-        std::memcpy(&src[(o * frames + f) * inner], &norm.data()[o * inner], inner * sizeof(double));
+        std::memcpy(&src[(o * frames + f) * inner], &norm.values()[o * inner], inner * sizeof(double));
     }
   }
   mclahe_params_t p;
@@ -158,17 +132,13 @@ NdImage mclahe_framewise(const NdImage& image, std::size_t frame_axis, const Ker
 
 NdImage normalize_to_unit(const NdImage& image) {
   // src/pipeline.cpp:155-165
-  for (double v : image.data())
-    if (!std::isfinite(v)) throw ValidationError("image contains non-finite values");
-  double lo = image.data().front(), hi = lo;
-  for (double v : image.data()) {
-    if (v < lo) lo = v;
-    if (v > hi) hi = v;
-  }
+  if (!image.all_finite()) throw ValidationError("image contains non-finite values");
+  double lo, hi;
+  image.min_max(lo, hi);
   if (!(hi > lo)) return NdImage::constant(image.shape(), 0.5);
   const double span = hi - lo;
   std::vector<double> d(image.size());
-  for (std::size_t i = 0; i < d.size(); ++i) d[i] = (image.data()[i] - lo) / span;
+  for (std::size_t i = 0; i < d.size(); ++i) d[i] = (image[i] - lo) / span;
   return NdImage(image.shape(), std::move(d));
 }
 
@@ -182,8 +152,8 @@ MetricsReport metrics_call(const NdImage& a, const NdImage* b, std::size_t n_bin
   if (b && a.shape() != b->shape()) throw ValidationError("mse operands differ in shape");
   const std::vector<int64_t> sh = shape64(a);
   mclahe_metrics_t r{};
-  const int rc = mclahe_metrics(static_cast<int32_t>(a.rank()), sh.data(), a.data().data(),
-                                b ? b->data().data() : nullptr, static_cast<int64_t>(n_bins),
+  const int rc = mclahe_metrics(static_cast<int32_t>(a.rank()), sh.data(), a.values().data(),
+                                b ? b->values().data() : nullptr, static_cast<int64_t>(n_bins),
                                 peak, &r);
   if (rc != MCLAHE_OK) raise(rc);
   MetricsReport m;
@@ -204,7 +174,7 @@ NdImage gaussian_filter(const NdImage& image, const GaussianSpec& spec, unsigned
   const std::vector<int64_t> sh = shape64(image);
   std::vector<double> out(image.size());
   const int rc = mclahe_gaussian_filter(static_cast<int32_t>(image.rank()), sh.data(),
-                                        spec.sigmas.data(), spec.truncate, image.data().data(),
+                                        spec.sigmas.data(), spec.truncate, image.values().data(),
                                         out.data());
   if (rc != MCLAHE_OK) raise(rc);
   return NdImage(image.shape(), std::move(out));
@@ -218,7 +188,7 @@ NdImage median_filter(const NdImage& image, const MedianSpec& spec, unsigned thr
   const std::vector<int64_t> win(spec.window.begin(), spec.window.end());
   std::vector<double> out(image.size());
   const int rc = mclahe_median_filter(static_cast<int32_t>(image.rank()), sh.data(), win.data(),
-                                      image.data().data(), out.data());
+                                      image.values().data(), out.data());
   if (rc != MCLAHE_OK) raise(rc);
   return NdImage(image.shape(), std::move(out));
 }

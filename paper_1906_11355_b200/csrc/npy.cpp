@@ -13,7 +13,7 @@
 #include <string>
 #include <vector>
 
-#include "../../include/mclahe_b200.hpp"
+#include "mclahe/npy.hpp"
 
 namespace mclahe {
 
@@ -153,8 +153,9 @@ Dtype dtype_from_name(const std::string& name) {
   throw NpyError(NpyErrc::unsupported_dtype, "unsupported dtype name " + name);
 }
 
-std::pair<NdImage, ArrayFileMeta> read_npy(const std::string& path) {
-  std::ifstream in(path, std::ios::binary);
+std::pair<NdImage, ArrayFileMeta> read_npy(const std::filesystem::path& file) {
+  const std::string path = file.string();
+  std::ifstream in(file, std::ios::binary);
   if (!in) throw NpyError(NpyErrc::io_failure, "cannot open " + path);
   unsigned char pre[8];
   in.read(reinterpret_cast<char*>(pre), 8);
@@ -208,7 +209,8 @@ std::pair<NdImage, ArrayFileMeta> read_npy(const std::string& path) {
   return {std::move(img), meta};
 }
 
-void write_npy(const std::string& path, const NdImage& image, Dtype dtype) {
+void write_npy(const std::filesystem::path& file, const NdImage& image, Dtype dtype) {
+  const std::string path = file.string();
   const DtypeInfo& d = info(dtype);
   std::ostringstream dict;
   dict << "{'descr': '" << d.descr << "', 'fortran_order': False, 'shape': (";
@@ -225,7 +227,7 @@ void write_npy(const std::string& path, const NdImage& image, Dtype dtype) {
   if (header_len > 0xFFFF) throw NpyError(NpyErrc::bad_header, "header too large for NPY v1.0");
   std::vector<unsigned char> payload(image.size() * d.size);
   for (std::size_t i = 0; i < image.size(); ++i) encode(d, image[i], payload.data() + i * d.size);
-  std::ofstream out(path, std::ios::binary | std::ios::trunc);
+  std::ofstream out(file, std::ios::binary | std::ios::trunc);
   if (!out) throw NpyError(NpyErrc::io_failure, "cannot open " + path + " for writing");
   unsigned char head[10];
   std::memcpy(head, kNpyMagic, 6);
@@ -238,9 +240,10 @@ void write_npy(const std::string& path, const NdImage& image, Dtype dtype) {
   if (!out) throw NpyError(NpyErrc::io_failure, "write to " + path + " failed");
 }
 
-NdImage read_raw(const std::string& path, const ArrayFileMeta& meta) {
+NdImage read_raw(const std::filesystem::path& file, const ArrayFileMeta& meta) {
+  const std::string path = file.string();
   if (meta.fortran_order) throw NpyError(NpyErrc::fortran_order, "raw input must be C-ordered");
-  std::ifstream in(path, std::ios::binary | std::ios::ate);
+  std::ifstream in(file, std::ios::binary | std::ios::ate);
   if (!in) throw NpyError(NpyErrc::io_failure, "cannot open " + path);
   std::size_t expected = dtype_item_size(meta.dtype);
   for (std::size_t e : meta.shape) expected *= e;

@@ -1,10 +1,13 @@
-// A caller of the reference API, unchanged except for the include: builds an
+// A caller of the reference API (the reference headers mclahe/*.hpp, rebuilt
+// under include/mclahe): builds an
 // image, runs mclahe::mclahe, prints a checksum (or exercises validation).
 #include <cstdio>
 #include <cstring>
 #include <vector>
 
-#include "mclahe_b200.hpp"
+#include "mclahe/pipeline.hpp"
+#include "mclahe/filters.hpp"
+#include "mclahe/metrics.hpp"
 
 int main(int argc, char** argv) {
   const bool validate_only = argc > 1 && std::strcmp(argv[1], "validate") == 0;

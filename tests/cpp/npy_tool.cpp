@@ -9,7 +9,7 @@
 #include <string>
 #include <vector>
 
-#include "mclahe_b200.hpp"
+#include "mclahe/npy.hpp"
 
 int main(int argc, char** argv) {
   try {

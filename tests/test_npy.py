@@ -23,7 +23,7 @@ def tool(tmp_path_factory):
     if not os.path.exists(os.path.join(LIB, "libmclahe_cpp.so")):
         _native.build()
     out = str(tmp_path_factory.mktemp("npy") / "npy_tool")
-    subprocess.run(["g++", "-O2", "-std=c++17", "-I", os.path.join(ROOT, "include"),
+    subprocess.run(["g++", "-O2", "-std=c++20", "-I", os.path.join(ROOT, "include"),
                     os.path.join(ROOT, "tests", "cpp", "npy_tool.cpp"), "-L", LIB,
                     "-lmclahe_cpp", "-lmclahe_gpu", f"-Wl,-rpath,{LIB}", "-o", out], check=True)
     return out
