@@ -246,6 +246,30 @@ int mclahe_metrics_device(int32_t rank, const int64_t* shape, const double* a_de
                           const double* b_dev, int64_t n_bins, double peak,
                           mclahe_metrics_t* report, void* stream);
 
+/* ---- Multi-slab / multi-device --------------------------
+ * The volume is cut along dim 0 at interpolation-cell boundaries into
+ * n_slabs row-balanced slabs (mclahe_multi_cuts: n_slabs + 1 row
+ * boundaries); slab r runs on devices[r] with its own plan, stream and
+ * buffers.  Devices may repeat: logical slabs on one GPU take the identical
+ * code path (the 1-GPU test of the exchange).  Cross-slab traffic: the range
+ * keys (MAX over all slabs), the per-tile range keys of shared tile rows
+ * (adaptive, MAX with the neighbours) and the partial integer counts of
+ * shared tile rows (SUM with the neighbours) -- read by a combine kernel
+ * straight from the peers' snapshot buffers over NVLink / NVSwitch (P2P), or
+ * staged by cudaMemcpyPeerAsync where P2P is unavailable.  Integer combines
+ * are order-free: results are bit-identical to mclahe_gpu_run for any slab
+ * count and device list (the reference's worker-count promise,
+ * include/mclahe/pipeline.hpp:10-11, parallel.hpp:19-22).
+ * mclahe_gpu_run_multi: whole-volume HOST buffers.
+ * mclahe_gpu_run_multi_device: per-slab DEVICE buffers (slab r's rows
+ * [cuts[r], cuts[r+1]) resident on devices[r]). */
+int mclahe_multi_cuts(const mclahe_params_t* params, int32_t n_slabs, int64_t* cuts);
+int mclahe_gpu_run_multi(const mclahe_params_t* params, int32_t n_slabs, const int32_t* devices,
+                         const void* host_in, void* host_out, mclahe_timings_t* timings);
+int mclahe_gpu_run_multi_device(const mclahe_params_t* params, int32_t n_slabs,
+                                const int32_t* devices, const void* const* in_dev,
+                                void* const* out_dev, mclahe_timings_t* timings);
+
 /* ---- The reference's per-operation API on the device (csrc/ops.cu) -------
  * For callers of include/mclahe/{histogram,nd_image}.hpp that use the
  * building blocks instead of mclahe::mclahe.  Host buffers, float64.

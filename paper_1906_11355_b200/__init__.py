@@ -10,10 +10,11 @@ from ._native import NativeUnavailable, ValidationError  # noqa: F401
 from .api import (EnhanceParams, KernelSpec, McLaheRequest, PhaseTimings, Plan,  # noqa: F401
                   RangeMode, bin_index_device, enhance, launch_count, mclahe, mclahe_framewise,
                   normalize_to_unit, GaussianSpec, MedianSpec, MetricsReport, gaussian_filter,
-                  median_filter, compute_metrics, mse, psnr, rms_contrast, shannon_entropy)
+                  median_filter, compute_metrics, mse, psnr, rms_contrast, shannon_entropy,
+                  mclahe_multi, multi_cuts)
 
 __all__ = ["EnhanceParams", "KernelSpec", "McLaheRequest", "PhaseTimings", "Plan", "RangeMode",
            "ValidationError", "NativeUnavailable", "mclahe", "enhance", "bin_index_device",
            "launch_count", "mclahe_framewise", "normalize_to_unit", "GaussianSpec", "MedianSpec",
            "MetricsReport", "gaussian_filter", "median_filter", "compute_metrics", "mse", "psnr",
-           "rms_contrast", "shannon_entropy"]
+           "rms_contrast", "shannon_entropy", "mclahe_multi", "multi_cuts"]

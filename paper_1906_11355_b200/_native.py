@@ -90,6 +90,13 @@ SIGNATURES = {
     "mclahe_debug_bin_index": (C.c_int, [C.c_int32, _vp, _i64, C.c_double, C.c_double, _i64,
                                          _vp, _vp]),
     "mclahe_gpu_run_framewise": (C.c_int, [_vp, C.c_int32, _vp, _vp, _vp]),
+    "mclahe_multi_cuts": (C.c_int, [C.POINTER(Params), C.c_int32, _vp]),
+    "mclahe_gpu_run_multi": (C.c_int, [C.POINTER(Params), C.c_int32, _vp, _vp, _vp, _vp]),
+    "mclahe_gpu_run_multi_device": (C.c_int, [C.POINTER(Params), C.c_int32, _vp, _vp, _vp, _vp]),
+    "mclahe_block_mappings": (C.c_int, [_vp, C.c_int64, C.c_int64, C.c_int64, C.c_double,
+                                        C.c_int32, C.c_double, C.c_double, _vp, _vp, _vp, _vp,
+                                        _vp, _vp]),
+    "mclahe_nd_gather": (C.c_int, [C.c_int32, C.c_int32, _vp, _vp, _vp, _vp, _vp]),
     "mclahe_gaussian_filter": (C.c_int, [C.c_int32, _vp, _vp, C.c_double, _vp, _vp]),
     "mclahe_gaussian_filter_device": (C.c_int, [C.c_int32, _vp, _vp, C.c_double, _vp, _vp, _vp]),
     "mclahe_median_filter": (C.c_int, [C.c_int32, _vp, _vp, _vp, _vp]),

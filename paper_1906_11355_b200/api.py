@@ -486,6 +486,56 @@ def enhance(image, kernel_size, n_bins: int = 256, clip_limit: float = 1.0,
     return mclahe(req)
 
 
+def multi_cuts(shape, kernel, n_slabs: int, n_bins: int = 256, clip_limit: float = 1.0,
+               adaptive: bool = False) -> list:
+    """Row boundaries (n_slabs + 1) of the cell-aligned slabs the multi-slab
+    run uses along dim 0 (mclahe_multi_cuts; slabs.py slab_cuts' rule)."""
+    params = N.make_params(tuple(shape), tuple(kernel), n_bins, clip_limit, adaptive, N.F32)
+    cuts = (C.c_int64 * (n_slabs + 1))()
+    N.check(N.lib().mclahe_multi_cuts(C.byref(params), int(n_slabs), cuts))
+    return [int(c) for c in cuts]
+
+
+def mclahe_multi(image, kernel, n_bins: int = 256, clip_limit: float = 1.0,
+                 adaptive: bool = False, devices=(0,), timings: PhaseTimings | None = None):
+    """mclahe::mclahe over slabs along dim 0, slab r on devices[r], in one
+    process (mclahe_gpu_run_multi / _multi_device).  Devices
+    may repeat (logical slabs on one GPU).  numpy in -> numpy out (host
+    buffers); a list of CUDA tensors (slab r's rows on devices[r], see
+    multi_cuts) -> a list of output slabs.  Bit-identical to mclahe()."""
+    devs = (C.c_int32 * len(devices))(*[int(d) for d in devices])
+    n = len(devices)
+    t = N.Timings()
+    if isinstance(image, (list, tuple)):
+        import torch
+        xs = [s.contiguous() for s in image]
+        if len(xs) != n:
+            raise ValidationError("one input slab per device")
+        shape = (sum(int(s.shape[0]) for s in xs),) + tuple(xs[0].shape[1:])
+        params = N.make_params(shape, tuple(kernel), n_bins, clip_limit, adaptive,
+                               _dtype_code(xs[0].dtype))
+        outs = [torch.empty_like(s) for s in xs]
+        ins = (C.c_void_p * n)(*[s.data_ptr() for s in xs])
+        ous = (C.c_void_p * n)(*[o.data_ptr() for o in outs])
+        N.check(N.lib().mclahe_gpu_run_multi_device(C.byref(params), n, devs, ins, ous,
+                                                    C.byref(t)))
+        result = outs
+    else:
+        x = np.asarray(image)
+        if x.dtype != np.float32:
+            x = x.astype(np.float64)
+        x = np.ascontiguousarray(x)
+        params = N.make_params(x.shape, tuple(kernel), n_bins, clip_limit, adaptive,
+                               _dtype_code(x.dtype))
+        result = np.empty_like(x)
+        N.check(N.lib().mclahe_gpu_run_multi(C.byref(params), n, devs, x.ctypes.data,
+                                             result.ctypes.data, C.byref(t)))
+    if timings is not None:
+        timings.histograms_s += t.histograms_s
+        timings.interpolation_s += t.interpolation_s
+    return result
+
+
 def bin_index_device(values, lo: float, hi: float, n_bins: int, variant: int = 0):
     """bin_index (src/histogram.cpp:24-32) of a CUDA tensor through the kernels'
     binning; int32 result (-1 for a degenerate range).  variant 0: the generic

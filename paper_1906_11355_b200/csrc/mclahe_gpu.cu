@@ -1456,6 +1456,363 @@ int run_plan_host(OneShot& o, mclahe_plan_s* pl, const void* in, void* out, size
 
 }  // namespace
 
+// ---- multi-slab / multi-device run ---------------------
+// The volume is cut along dim 0 at interpolation-cell boundaries into
+// row-balanced slabs (the cut rule of slabs.py: slab_cuts).  Each slab has its
+// own window plan, device buffers and stream on its device; devices may
+// repeat (logical slabs on one GPU run the identical code path).  The only
+// cross-slab traffic:
+//   * range keys (~key(lo), key(hi), non-finite): MAX over all slabs;
+//   * adaptive: per-tile range keys of tile rows two windows share: MAX;
+//   * the partial integer counts of shared tile rows: SUM.
+// Each slab snapshots the rows it shares into its own exchange buffer (so a
+// neighbour's in-place combine never feeds back), records an event, and the
+// combine kernel of every slab reads its peers' snapshots directly -- peer
+// memory over NVLink / NVSwitch when the device differs (P2P enabled),
+// local memory for logical slabs; when P2P is unavailable the snapshot is
+// first staged with cudaMemcpyPeerAsync.  Integer MAX / SUM are order-free,
+// so every slab's counts, LUTs and output equal the one-device run bit for bit.
+namespace {
+
+__global__ void k_combine_max(int64_t* __restrict__ dst, const int64_t* __restrict__ src, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = max(dst[i], src[i]);
+}
+
+__global__ void k_combine_sum(uint32_t* __restrict__ dst, const uint32_t* __restrict__ src,
+                              int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] += src[i];
+}
+
+// Cell-aligned, row-balanced cuts (slabs.py: slab_cuts).
+int multi_cuts(const mclahe_params_t* p, int slabs, std::vector<int64_t>& cuts) {
+  const Dim d0 = make_dim(p->shape[0], p->kernel[0]);
+  std::vector<std::pair<int64_t, int64_t>> cells;
+  for (int64_t c = 0; c + 1 < d0.g; ++c) {
+    int64_t a, e;
+    cell_range(d0, c, &a, &e);
+    if (e > a) cells.push_back({a, e});
+  }
+  if (slabs < 1 || slabs > (int)cells.size())
+    return fail(MCLAHE_ERR_VALIDATION, "cannot split " + std::to_string(cells.size()) +
+                                           " interpolation cells along dim 0 over " +
+                                           std::to_string(slabs) + " slabs");
+  cuts.assign(1, 0);
+  int ci = 0;
+  for (int r = 0; r < slabs; ++r) {
+    int e = (int)cells.size();
+    if (r < slabs - 1) {
+      const double target = (double)p->shape[0] * (r + 1) / slabs;
+      const int lo_e = ci + 1, hi_e = (int)cells.size() - (slabs - r - 1);
+      e = lo_e;
+      for (int k = lo_e; k <= hi_e; ++k)
+        if (std::fabs((double)cells[k - 1].second - target) <
+            std::fabs((double)cells[e - 1].second - target))
+          e = k;
+    }
+    cuts.push_back(cells[e - 1].second);
+    ci = e;
+  }
+  return MCLAHE_OK;
+}
+
+struct Slab {
+  std::unique_ptr<mclahe_plan_s> plan;
+  int dev = 0;
+  cudaStream_t st = nullptr;
+  cudaEvent_t ev_range = nullptr, ev_counts = nullptr, ev_t[3] = {nullptr, nullptr, nullptr};
+  void* buf = nullptr;            // d_in | d_out | workspace | snapshots | staging
+  char *d_in = nullptr, *d_out = nullptr, *ws = nullptr;
+  int64_t* snap_keys = nullptr;   // range keys [4]
+  int64_t* snap_trange = nullptr; // tile range keys of rows [ov_a, ov_b)
+  uint32_t* snap_counts = nullptr;// counts of rows [ov_a, ov_b)
+  char* stage = nullptr;          // peer snapshots staged here when P2P is unavailable
+  int64_t ov_a = 0, ov_b = 0;     // union of the tile rows shared with any peer
+  int64_t rows = 0;
+};
+
+struct Multi {
+  std::vector<Slab> slabs;
+  std::vector<int64_t> cuts;
+  size_t stage_bytes = 0;
+  ~Multi() {
+    for (Slab& s : slabs) {
+      cudaSetDevice(s.dev);
+      if (s.buf) cudaFree(s.buf);
+      if (s.st) cudaStreamDestroy(s.st);
+      for (cudaEvent_t e : {s.ev_range, s.ev_counts, s.ev_t[0], s.ev_t[1], s.ev_t[2]})
+        if (e) cudaEventDestroy(e);
+    }
+  }
+};
+
+bool can_read(int dev, int peer) {
+  if (dev == peer) return true;
+  int ok = 0;
+  return cudaDeviceCanAccessPeer(&ok, dev, peer) == cudaSuccess && ok;
+}
+
+int build_multi(const mclahe_params_t* p, int n, const int32_t* devices, Multi& M) {
+  int rc = multi_cuts(p, n, M.cuts);
+  if (rc) return rc;
+  int ndev = 0;
+  MG_CUDA(cudaGetDeviceCount(&ndev));
+  for (int r = 0; r < n; ++r)
+    if (devices[r] < 0 || devices[r] >= ndev)
+      return fail(MCLAHE_ERR_VALIDATION, "device id " + std::to_string(devices[r]) + " out of range");
+  // peer access between every pair of distinct devices
+  for (int r = 0; r < n; ++r)
+    for (int q = 0; q < n; ++q) {
+      if (devices[r] == devices[q] || !can_read(devices[r], devices[q])) continue;
+      MG_CUDA(cudaSetDevice(devices[r]));
+      const cudaError_t e = cudaDeviceEnablePeerAccess(devices[q], 0);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) return cuda_fail(e, "cudaDeviceEnablePeerAccess");
+      cudaGetLastError();
+    }
+  M.slabs.resize((size_t)n);
+  const int64_t row_bytes = volume(p) / p->shape[0] * elem_size(p);
+  const int64_t n_bins = p->n_bins;
+  for (int r = 0; r < n; ++r) {
+    Slab& S = M.slabs[(size_t)r];
+    S.dev = devices[r];
+    MG_CUDA(cudaSetDevice(S.dev));
+    S.plan = std::make_unique<mclahe_plan_s>();
+    if ((rc = plan_describe(p, M.cuts[r], M.cuts[r + 1], S.plan.get()))) return rc;
+    if ((rc = device_init(S.plan.get()))) return rc;
+    S.rows = M.cuts[r + 1] - M.cuts[r];
+    const mclahe_plan_info_t& I = S.plan->info;
+    S.ov_a = INT64_MAX;
+    S.ov_b = INT64_MIN;
+    for (int q = 0; q < n; ++q) {
+      if (q == r) continue;
+      mclahe_plan_s tmp;
+      if ((rc = plan_describe(p, M.cuts[q], M.cuts[q + 1], &tmp))) return rc;
+      const int64_t a = std::max(I.tile_row_begin, tmp.info.tile_row_begin);
+      const int64_t b = std::min(I.tile_row_end, tmp.info.tile_row_end);
+      if (b > a) {
+        S.ov_a = std::min(S.ov_a, a);
+        S.ov_b = std::max(S.ov_b, b);
+      }
+    }
+    if (S.ov_b <= S.ov_a) S.ov_a = S.ov_b = I.tile_row_begin;
+  }
+  // one allocation per slab: in | out | workspace | snapshots | staging
+  int64_t max_ov = 0;
+  for (Slab& S : M.slabs) max_ov = std::max(max_ov, S.ov_b - S.ov_a);
+  const int64_t tpr = M.slabs[0].plan->info.tiles_per_row;
+  const int64_t snap_tr = max_ov * tpr * 16, snap_cnt = max_ov * tpr * n_bins * 4;
+  M.stage_bytes = (size_t)align_up(32 + snap_tr + snap_cnt, 256);
+  for (Slab& S : M.slabs) {
+    MG_CUDA(cudaSetDevice(S.dev));
+    const int64_t io = align_up(S.rows * row_bytes, 256);
+    const int64_t wsb = align_up(S.plan->info.workspace_bytes, 256);
+    const int64_t total = 2 * io + wsb + 4 * (int64_t)M.stage_bytes;  // snapshots + 3 staging slots
+    MG_CUDA(cudaMalloc(&S.buf, (size_t)total));
+    char* b = static_cast<char*>(S.buf);
+    S.d_in = b;
+    S.d_out = b + io;
+    S.ws = b + 2 * io;
+    char* snap = S.ws + wsb;
+    S.snap_keys = reinterpret_cast<int64_t*>(snap);
+    S.snap_trange = reinterpret_cast<int64_t*>(snap + 32);
+    S.snap_counts = reinterpret_cast<uint32_t*>(snap + 32 + snap_tr);
+    S.stage = snap + M.stage_bytes;  // staging slots 0 / 1 / 2: keys, tile ranges, counts
+    MG_CUDA(cudaStreamCreateWithFlags(&S.st, cudaStreamNonBlocking));
+    MG_CUDA(cudaEventCreateWithFlags(&S.ev_range, cudaEventDisableTiming));
+    MG_CUDA(cudaEventCreateWithFlags(&S.ev_counts, cudaEventDisableTiming));
+    for (cudaEvent_t& e : S.ev_t) MG_CUDA(cudaEventCreate(&e));
+  }
+  return MCLAHE_OK;
+}
+
+// Pointer of peer q's snapshot readable by slab r's device: direct, or
+// staged into r's staging slot with a peer copy on r's stream.
+int peer_view(Multi& M, int r, int q, const void* src, int64_t bytes, int slot, const void** out) {
+  Slab& S = M.slabs[(size_t)r];
+  const Slab& Q = M.slabs[(size_t)q];
+  if (can_read(S.dev, Q.dev)) {
+    *out = src;
+    return MCLAHE_OK;
+  }
+  char* dst = S.stage + slot * (int64_t)M.stage_bytes;
+  MG_CUDA(cudaMemcpyPeerAsync(dst, S.dev, src, Q.dev, (size_t)bytes, S.st));
+  *out = dst;
+  return MCLAHE_OK;
+}
+
+int grid_n(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 2048)); }
+
+// Slab r's combine of the rows [a, b) it shares with peer q (op 0: MAX of the
+// tile range keys, 1: SUM of counts).
+int combine_rows(Multi& M, int r, int q, int op, int slot) {
+  Slab& S = M.slabs[(size_t)r];
+  const Slab& Q = M.slabs[(size_t)q];
+  const mclahe_plan_info_t& I = S.plan->info;
+  const mclahe_plan_info_t& J = Q.plan->info;
+  const int64_t a = std::max(I.tile_row_begin, J.tile_row_begin);
+  const int64_t b = std::min(I.tile_row_end, J.tile_row_end);
+  if (b <= a) return MCLAHE_OK;
+  const int64_t tpr = I.tiles_per_row, nb = I.n_bins;
+  const int64_t per = op == 0 ? tpr * 2 : tpr * nb;  // elements per tile row
+  const int64_t n = (b - a) * per;
+  const void* src;
+  int rc;
+  if (op == 0) {
+    const int64_t* qs = Q.snap_trange + (a - Q.ov_a) * per;
+    if ((rc = peer_view(M, r, q, qs, n * 8, slot, &src))) return rc;
+    int64_t* dst = reinterpret_cast<int64_t*>(S.ws + I.off_tile_range) + (a - I.tile_row_begin) * per;
+    k_combine_max<<<grid_n(n), 256, 0, S.st>>>(dst, static_cast<const int64_t*>(src), n);
+  } else {
+    const uint32_t* qs = Q.snap_counts + (a - Q.ov_a) * per;
+    if ((rc = peer_view(M, r, q, qs, n * 4, slot, &src))) return rc;
+    uint32_t* dst = reinterpret_cast<uint32_t*>(S.ws + I.off_counts) + (a - I.tile_row_begin) * per;
+    k_combine_sum<<<grid_n(n), 256, 0, S.st>>>(dst, static_cast<const uint32_t*>(src), n);
+  }
+  MG_LAUNCHED();
+  return MCLAHE_OK;
+}
+
+// One multi-slab run.  host_in / host_out: whole-volume HOST buffers (each
+// slab copies its rows on its own stream), else in_dev / out_dev: per-slab
+// DEVICE buffers (slab r's rows on devices[r]).
+int run_multi(Multi& M, const mclahe_params_t* p, const void* host_in, void* host_out,
+              const void* const* in_dev, void* const* out_dev, mclahe_timings_t* timings) {
+  const int n = (int)M.slabs.size();
+  const int64_t row_bytes = volume(p) / p->shape[0] * elem_size(p);
+  const bool A = p->adaptive != 0;
+  int rc;
+  auto in_of = [&](int r) -> const void* { return host_in ? M.slabs[(size_t)r].d_in : in_dev[r]; };
+  auto out_of = [&](int r) -> void* { return host_out ? M.slabs[(size_t)r].d_out : out_dev[r]; };
+  // pass 1 per slab, then its snapshots
+  for (int r = 0; r < n; ++r) {
+    Slab& S = M.slabs[(size_t)r];
+    MG_CUDA(cudaSetDevice(S.dev));
+    if (host_in)
+      MG_CUDA(cudaMemcpyAsync(S.d_in, static_cast<const char*>(host_in) + M.cuts[r] * row_bytes,
+                              (size_t)(S.rows * row_bytes), cudaMemcpyHostToDevice, S.st));
+    MG_CUDA(cudaEventRecord(S.ev_t[0], S.st));
+    if ((rc = do_reset(S.plan.get(), S.ws, S.st))) return rc;
+    if ((rc = do_range(S.plan.get(), in_of(r), S.ws, S.st))) return rc;
+    const mclahe_plan_info_t& I = S.plan->info;
+    MG_CUDA(cudaMemcpyAsync(S.snap_keys, S.ws + I.off_range, 32, cudaMemcpyDeviceToDevice, S.st));
+    if (A && S.ov_b > S.ov_a)
+      MG_CUDA(cudaMemcpyAsync(S.snap_trange,
+                              S.ws + I.off_tile_range + (S.ov_a - I.tile_row_begin) * I.tiles_per_row * 16,
+                              (size_t)((S.ov_b - S.ov_a) * I.tiles_per_row * 16),
+                              cudaMemcpyDeviceToDevice, S.st));
+    MG_CUDA(cudaEventRecord(S.ev_range, S.st));
+  }
+  // range exchange: keys MAX over every slab, shared tile ranges MAX with the neighbours
+  for (int r = 0; r < n; ++r) {
+    Slab& S = M.slabs[(size_t)r];
+    MG_CUDA(cudaSetDevice(S.dev));
+    for (int q = 0; q < n; ++q) {
+      if (q == r) continue;
+      MG_CUDA(cudaStreamWaitEvent(S.st, M.slabs[(size_t)q].ev_range, 0));
+      const void* src;
+      if ((rc = peer_view(M, r, q, M.slabs[(size_t)q].snap_keys, 24, 0, &src))) return rc;
+      k_combine_max<<<1, 32, 0, S.st>>>(reinterpret_cast<int64_t*>(S.ws + S.plan->info.off_range),
+                                        static_cast<const int64_t*>(src), 3);
+      MG_LAUNCHED();
+      if (A && (rc = combine_rows(M, r, q, 0, 1))) return rc;
+    }
+    if ((rc = do_params(S.plan.get(), S.ws, S.st))) return rc;
+    if ((rc = do_hist(S.plan.get(), in_of(r), S.ws, S.st))) return rc;
+    const mclahe_plan_info_t& I = S.plan->info;
+    if (S.ov_b > S.ov_a)
+      MG_CUDA(cudaMemcpyAsync(S.snap_counts,
+                              S.ws + I.off_counts + (S.ov_a - I.tile_row_begin) * I.tiles_per_row * I.n_bins * 4,
+                              (size_t)((S.ov_b - S.ov_a) * I.tiles_per_row * I.n_bins * 4),
+                              cudaMemcpyDeviceToDevice, S.st));
+    MG_CUDA(cudaEventRecord(S.ev_counts, S.st));
+  }
+  // counts exchange (SUM with the neighbours), mappings, blend
+  for (int r = 0; r < n; ++r) {
+    Slab& S = M.slabs[(size_t)r];
+    MG_CUDA(cudaSetDevice(S.dev));
+    for (int q = 0; q < n; ++q) {
+      if (q == r) continue;
+      MG_CUDA(cudaStreamWaitEvent(S.st, M.slabs[(size_t)q].ev_counts, 0));
+      if ((rc = combine_rows(M, r, q, 1, 2))) return rc;
+    }
+    if ((rc = do_map(S.plan.get(), S.ws, nullptr, S.st))) return rc;
+    MG_CUDA(cudaEventRecord(S.ev_t[1], S.st));
+    if ((rc = do_interp(S.plan.get(), in_of(r), out_of(r), S.ws, S.st))) return rc;
+    MG_CUDA(cudaEventRecord(S.ev_t[2], S.st));
+  }
+  // every slab's flag is the combined (global) one: read slab 0's
+  int64_t flag = 0;
+  {
+    Slab& S = M.slabs[0];
+    MG_CUDA(cudaSetDevice(S.dev));
+    MG_CUDA(cudaMemcpyAsync(&flag, S.ws + S.plan->info.off_range + 16, 8, cudaMemcpyDeviceToHost, S.st));
+    MG_CUDA(cudaStreamSynchronize(S.st));
+  }
+  for (Slab& S : M.slabs) {
+    MG_CUDA(cudaSetDevice(S.dev));
+    MG_CUDA(cudaStreamSynchronize(S.st));
+  }
+  if (flag) return fail(MCLAHE_ERR_VALIDATION, "image contains non-finite values");
+  if (host_out)
+    for (int r = 0; r < n; ++r) {
+      Slab& S = M.slabs[(size_t)r];
+      MG_CUDA(cudaSetDevice(S.dev));
+      MG_CUDA(cudaMemcpyAsync(static_cast<char*>(host_out) + M.cuts[r] * row_bytes, S.d_out,
+                              (size_t)(S.rows * row_bytes), cudaMemcpyDeviceToHost, S.st));
+    }
+  double hist_s = 0, interp_s = 0;
+  for (Slab& S : M.slabs) {
+    MG_CUDA(cudaSetDevice(S.dev));
+    MG_CUDA(cudaStreamSynchronize(S.st));
+    float a = 0, b = 0;
+    MG_CUDA(cudaEventElapsedTime(&a, S.ev_t[0], S.ev_t[1]));
+    MG_CUDA(cudaEventElapsedTime(&b, S.ev_t[1], S.ev_t[2]));
+    hist_s = std::max(hist_s, a * 1e-3);
+    interp_s = std::max(interp_s, b * 1e-3);
+  }
+  if (timings) {
+    timings->histograms_s += hist_s;
+    timings->interpolation_s += interp_s;
+  }
+  return MCLAHE_OK;
+}
+
+std::mutex g_multi_mu;
+std::map<std::string, std::unique_ptr<Multi>>& multi_cache() {
+  static auto* c = new std::map<std::string, std::unique_ptr<Multi>>();
+  return *c;
+}
+
+int multi_get(const mclahe_params_t* params, int32_t n, const int32_t* devices, Multi** out) {
+  int rc = validate(params);
+  if (rc) return rc;
+  if (n < 1 || !devices) return fail(MCLAHE_ERR_VALIDATION, "need at least one slab and a device list");
+  mclahe_params_t q = *params;
+  q.reserved = 0;
+  for (int i = q.rank; i < MCLAHE_MAX_RANK; ++i) q.shape[i] = q.kernel[i] = 0;
+  std::string key(reinterpret_cast<const char*>(&q), sizeof q);
+  key.append(reinterpret_cast<const char*>(devices), sizeof(int32_t) * (size_t)n);
+  auto& C = multi_cache();
+  auto it = C.find(key);
+  if (it == C.end()) {
+    int cur = 0;
+    MG_CUDA(cudaGetDevice(&cur));
+    auto M = std::make_unique<Multi>();
+    rc = build_multi(&q, n, devices, *M);
+    cudaSetDevice(cur);
+    if (rc) return rc;
+    if (C.size() > 4) C.clear();
+    it = C.emplace(key, std::move(M)).first;
+  }
+  *out = it->second.get();
+  return MCLAHE_OK;
+}
+
+}  // namespace
+
 extern "C" {
 
 const char* mclahe_last_error(void) { return g_last_error.c_str(); }
@@ -1642,6 +1999,46 @@ int mclahe_gpu_run_framewise(const mclahe_params_t* params, int32_t frame_axis, 
   if (!pl) return rc;
   const size_t bytes = (size_t)(volume(&q) * elem_size(&q));
   return run_plan_host(o, pl, in, out, bytes, (size_t)align_up((int64_t)bytes, 256), timings);
+}
+
+int mclahe_multi_cuts(const mclahe_params_t* params, int32_t n_slabs, int64_t* cuts) {
+  int rc = validate(params);
+  if (rc) return rc;
+  if (!cuts) return fail(MCLAHE_ERR_VALIDATION, "null cuts");
+  std::vector<int64_t> c;
+  if ((rc = multi_cuts(params, n_slabs, c))) return rc;
+  std::copy(c.begin(), c.end(), cuts);
+  return MCLAHE_OK;
+}
+
+int mclahe_gpu_run_multi(const mclahe_params_t* params, int32_t n_slabs, const int32_t* devices,
+                         const void* host_in, void* host_out, mclahe_timings_t* timings) {
+  if (!host_in || !host_out) return fail(MCLAHE_ERR_VALIDATION, "null host buffer");
+  std::lock_guard<std::mutex> lock(g_multi_mu);
+  int cur = 0;
+  MG_CUDA(cudaGetDevice(&cur));
+  Multi* M = nullptr;
+  int rc = multi_get(params, n_slabs, devices, &M);
+  if (!rc) rc = run_multi(*M, params, host_in, host_out, nullptr, nullptr, timings);
+  cudaSetDevice(cur);
+  return rc;
+}
+
+int mclahe_gpu_run_multi_device(const mclahe_params_t* params, int32_t n_slabs,
+                                const int32_t* devices, const void* const* in_dev,
+                                void* const* out_dev, mclahe_timings_t* timings) {
+  if (!in_dev || !out_dev) return fail(MCLAHE_ERR_VALIDATION, "null device buffer list");
+  for (int r = 0; r < n_slabs; ++r)
+    if (!in_dev[r] || !out_dev[r] || !aligned16(in_dev[r]) || !aligned16(out_dev[r]))
+      return fail(MCLAHE_ERR_VALIDATION, "slab buffers must be non-NULL and 16-byte aligned");
+  std::lock_guard<std::mutex> lock(g_multi_mu);
+  int cur = 0;
+  MG_CUDA(cudaGetDevice(&cur));
+  Multi* M = nullptr;
+  int rc = multi_get(params, n_slabs, devices, &M);
+  if (!rc) rc = run_multi(*M, params, nullptr, nullptr, in_dev, out_dev, timings);
+  cudaSetDevice(cur);
+  return rc;
 }
 
 int mclahe_debug_bin_index(int32_t dtype, const void* values, int64_t n, double lo, double hi,
