@@ -293,6 +293,13 @@ int mclahe_block_mappings(const double* host_blocks, int64_t n_blocks, int64_t b
 int mclahe_nd_gather(int32_t op, int32_t rank, const int64_t* in_shape, const int64_t* a,
                      const int64_t* b, const double* host_in, double* host_out);
 
+/* Page-locked host memory (cudaHostAlloc, portable): buffers from here make
+ * the host-buffer calls copy at full PCIe rate and overlap H2D / compute /
+ * D2H; the C++ drop-in stages its float64 <-> float32 conversions in them.
+ * NULL on failure (mclahe_last_error() says why). */
+void* mclahe_host_alloc(size_t bytes);
+void mclahe_host_free(void* p);
+
 /* Number of kernel launches the last pass call on this thread issued. */
 int64_t mclahe_launch_count(void);
 

@@ -6,9 +6,14 @@
 #include "mclahe/metrics.hpp"
 #include "mclahe/pipeline.hpp"
 
+#include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstring>
 #include <limits>
+#include <mutex>
+#include <thread>
+#include <vector>
 
 #include "../../include/mclahe_gpu.h"
 
@@ -22,10 +27,104 @@ void raise(int rc) {
   throw std::runtime_error("mclahe GPU error " + std::to_string(rc) + ": " + msg);
 }
 
-bool all_f32_exact(std::span<const double> v) {
-  for (double x : v)
-    if (static_cast<double>(static_cast<float>(x)) != x) return false;
-  return true;
+// ---- host staging -------------------------------------------------------
+// The reference API hands over float64 vectors.  The GPU path wants the
+// values in page-locked memory (full-rate, asynchronous PCIe copies that the
+// streamed call overlaps with the kernels), as float32 when every value is
+// float32-representable (then the bins are bit-identical: f32 -> f64 is
+// exact).  One pinned in / out pair per process, grown on demand, guarded by
+// a mutex (the GPU call itself is serialised by the library anyway); the
+// narrowing (with the exactness check) and widening loops run on all host
+// threads.
+struct Staging {
+  std::mutex mu;
+  void* in = nullptr;
+  void* out = nullptr;
+  size_t cap = 0;
+};
+
+Staging& staging() {
+  static Staging* s = new Staging();  // process lifetime
+  return *s;
+}
+
+void ensure_staging(Staging& S, size_t bytes) {
+  if (S.cap >= bytes) return;
+  mclahe_host_free(S.in);
+  mclahe_host_free(S.out);
+  S.in = mclahe_host_alloc(bytes);
+  S.out = mclahe_host_alloc(bytes);
+  S.cap = (S.in && S.out) ? bytes : 0;
+  if (!S.cap) raise(MCLAHE_ERR_OOM);
+}
+
+// fn(begin, end) over [0, n) on up to hardware_concurrency threads (chunks of
+// whole 64 KiB pages of doubles)
+template <typename Fn>
+void host_parallel(std::size_t n, Fn&& fn) {
+  const unsigned hw = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+  const std::size_t grain = std::size_t{1} << 16;
+  const std::size_t workers = std::min<std::size_t>(hw, (n + grain - 1) / grain);
+  if (workers <= 1) {
+    fn(std::size_t{0}, n);
+    return;
+  }
+  const std::size_t chunk = ((n + workers - 1) / workers + grain - 1) / grain * grain;
+  std::vector<std::thread> pool;
+  for (std::size_t w = 1; w < workers && w * chunk < n; ++w)
+    pool.emplace_back([&, w] { fn(w * chunk, std::min(n, (w + 1) * chunk)); });
+  fn(0, std::min(n, chunk));
+  for (auto& t : pool) t.join();
+}
+
+// Runs one request on the GPU from float64 host values: narrows into the
+// pinned float32 stage when exact (else copies the doubles), calls `gpu`
+// (mclahe_gpu_run or the framewise form) on the pinned buffers, and widens
+// the result into a fresh vector, whose allocation (page faults of a zeroed
+// multi-GB vector) overlaps the GPU call.
+template <typename Gpu>
+std::vector<double> run_staged(mclahe_params_t& p, std::span<const double> src, Gpu&& gpu) {
+  const std::size_t n = src.size();
+  Staging& S = staging();
+  std::lock_guard<std::mutex> lock(S.mu);
+  ensure_staging(S, n * sizeof(double));
+  std::atomic<bool> exact{true};
+  float* in32 = static_cast<float*>(S.in);
+  host_parallel(n, [&](std::size_t b, std::size_t e) {
+    for (std::size_t i = b; i < e; i += 4096) {
+      if (!exact.load(std::memory_order_relaxed)) return;
+      const std::size_t ie = std::min(e, i + 4096);
+      bool ok = true;
+      for (std::size_t k = i; k < ie; ++k) {
+        const float f = static_cast<float>(src[k]);
+        ok &= static_cast<double>(f) == src[k];
+        in32[k] = f;
+      }
+      if (!ok) exact.store(false, std::memory_order_relaxed);
+    }
+  });
+  const bool f32 = exact.load();
+  if (!f32)
+    host_parallel(n, [&](std::size_t b, std::size_t e) {
+      std::memcpy(static_cast<double*>(S.in) + b, src.data() + b, (e - b) * sizeof(double));
+    });
+  p.dtype = f32 ? MCLAHE_F32 : MCLAHE_F64;
+  std::vector<double> out;
+  std::thread alloc([&] { out = std::vector<double>(n); });
+  const int rc = gpu(S.in, S.out);
+  alloc.join();
+  if (rc != MCLAHE_OK) raise(rc);
+  if (f32) {
+    const float* o = static_cast<const float*>(S.out);
+    host_parallel(n, [&](std::size_t b, std::size_t e) {
+      for (std::size_t k = b; k < e; ++k) out[k] = static_cast<double>(o[k]);
+    });
+  } else {
+    host_parallel(n, [&](std::size_t b, std::size_t e) {
+      std::memcpy(out.data() + b, static_cast<const double*>(S.out) + b, (e - b) * sizeof(double));
+    });
+  }
+  return out;
 }
 
 }  // namespace
@@ -47,19 +146,9 @@ NdImage mclahe(const McLaheRequest& request, PhaseTimings* timings) {
   p.n_bins = static_cast<int64_t>(request.params.n_bins);
   p.clip_limit = request.params.clip_limit;
   mclahe_timings_t t{0.0, 0.0, 0.0};
-  std::vector<double> out(img.size());
-  const std::span<const double> src = img.values();
-  int rc;
-  if (all_f32_exact(src)) {  // float32 pencil kernels, bit-identical bins
-    p.dtype = MCLAHE_F32;
-    std::vector<float> in32(src.begin(), src.end()), out32(src.size());
-    rc = mclahe_gpu_run(&p, in32.data(), out32.data(), &t);
-    if (rc == MCLAHE_OK) out.assign(out32.begin(), out32.end());
-  } else {
-    p.dtype = MCLAHE_F64;
-    rc = mclahe_gpu_run(&p, src.data(), out.data(), &t);
-  }
-  if (rc != MCLAHE_OK) raise(rc);
+  std::vector<double> out = run_staged(p, img.values(), [&](const void* in, void* o) {
+    return mclahe_gpu_run(&p, in, o, &t);
+  });
   if (timings) {
     timings->pad_s += t.pad_s;
     timings->histograms_s += t.histograms_s;
@@ -109,19 +198,9 @@ NdImage mclahe_framewise(const NdImage& image, std::size_t frame_axis, const Ker
   p.n_bins = static_cast<int64_t>(params.n_bins);
   p.clip_limit = params.clip_limit;
   mclahe_timings_t t{0.0, 0.0, 0.0};
-  std::vector<double> out(src.size());
-  int rc;
-  if (all_f32_exact(src)) {
-    p.dtype = MCLAHE_F32;
-    std::vector<float> in32(src.begin(), src.end()), out32(src.size());
-    rc = mclahe_gpu_run_framewise(&p, static_cast<int32_t>(frame_axis), in32.data(), out32.data(),
-                                  &t);
-    if (rc == MCLAHE_OK) out.assign(out32.begin(), out32.end());
-  } else {
-    p.dtype = MCLAHE_F64;
-    rc = mclahe_gpu_run_framewise(&p, static_cast<int32_t>(frame_axis), src.data(), out.data(), &t);
-  }
-  if (rc != MCLAHE_OK) raise(rc);
+  std::vector<double> out = run_staged(p, src, [&](const void* in, void* o) {
+    return mclahe_gpu_run_framewise(&p, static_cast<int32_t>(frame_axis), in, o, &t);
+  });
   if (timings) {
     timings->pad_s += t.pad_s;
     timings->histograms_s += t.histograms_s;

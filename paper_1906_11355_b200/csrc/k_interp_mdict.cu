@@ -30,7 +30,9 @@ namespace mg {
 
 
 // TSTORE: results written in place into the stage and TMA-stored by the
-// producer (otherwise each lane stores its 16 bytes straight to global).
+// producer (otherwise a lane blends both 16-byte columns of its row and
+// stores the full 32-byte sector straight to global; stages are released
+// right after they are read).
 // NWARP consumer warps (+ one producer warp).  ADAPT: value-dictionary tables
 // (TK = kDictKC values per row); global mode (!ADAPT): one bin per voxel from
 // the global edge table, tables per bin (TK = n_bins).
@@ -197,34 +199,20 @@ __global__ void __launch_bounds__(NWARP * 32 + 32, 1)
     for (int j = 1; j < KO - 2; ++j) gbase += (int64_t)S.x[j] * G.vstride[j];
     gbase += (int64_t)xb2 * G.vstride[KO - 2] + (int64_t)xb1 * G.vstride[KO - 1];
     unsigned char* buf = reinterpret_cast<unsigned char*>(P.bufs + s * stage_elems);
-    // items of consecutive stages dealt round-robin over the warps (2 * nrb
-    // need not be a multiple of NW)
-    const int nitems = 2 * nrb;
+    // items of consecutive stages dealt round-robin over the warps (the item
+    // count need not be a multiple of NW).  TSTORE: an item is one 16-byte
+    // column of a 32-row block, results in place (TMA-stored by the
+    // producer).  Otherwise an item is a whole 32-row block: a lane blends
+    // both columns of its row (one full 32-byte sector) and stores them
+    // straight to global memory; the stage is released as soon as the warp's
+    // last item has been read, so the producer refills it during the math.
+    const int nitems = TSTORE ? 2 * nrb : nrb;
     const int first = warp >= rot ? warp - rot : warp + NW - rot;
     rot += nitems % NW;  // items dealt so far, mod NW
     if (rot >= NW) rot -= NW;
-    for (int item = first; item < nitems; item += NW) {
-      const int c = item & 1, rb = item >> 1;
-      // stages hold a power of two >= 32 rows (plan_mdict): every lane has a row
-      const int q = rb * 32 + lane;
+    // one column's 4 voxels (frames) of row q against its tables
+    auto blend_col = [&](const int c, const float4 v4, const float (&wo)[NCO]) -> float4 {
       const int col = seg * 2 + c;
-      const bool col_on = col < ncol;  // an odd last column pair
-      const int r1 = q & r1mask, r2 = q >> lg_r1;
-      const float f1 = fmaf((float)(xb1 + r1), s1, t1);
-      const float f2 = fmaf((float)(xb2 + r2), s2, t2);
-      float wo[NCO];
-      {
-        const float g1[2] = {1.0f - f1, f1};
-#pragma unroll
-        for (int co = 0; co < NCO; ++co) {
-          float w = g1[co & 1];
-          w *= ((co >> 1) & 1) ? f2 : 1.0f - f2;
-          wo[co] = w * wfix[co >> 2];
-        }
-      }
-      // 32B-swizzled stage row (32 bytes): 16-byte chunk c of row q at c ^ ((q >> 2) & 1)
-      float4* slot4 = reinterpret_cast<float4*>(buf + q * 32 + ((c ^ ((q >> 2) & 1)) << 4));
-      const float4 v4 = *slot4;
       const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
       int di[4];
       if (!ADAPT) {  // one bin per voxel: the global edge table
@@ -289,17 +277,54 @@ __global__ void __launch_bounds__(NWARP * 32 + 32, 1)
       r.y = fminf(fmaxf(acc[1], 0.f), 1.f);
       r.z = fminf(fmaxf(acc[2], 0.f), 1.f);
       r.w = fminf(fmaxf(acc[3], 0.f), 1.f);
-      if (TSTORE) {
-        *slot4 = r;  // in place; the producer TMA-stores the box
-      } else if (col_on) {
-        __stcs(reinterpret_cast<float4*>(out + gbase + (int64_t)r2 * G.vstride[KO - 2] +
-                                         (int64_t)r1 * G.vstride[KO - 1] + col * 4),
-               r);
+      return r;
+    };
+    if (!TSTORE && first >= nitems) {  // no item for this warp in this stage
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&P.pipe->empty[s]);
+    }
+    for (int item = first; item < nitems; item += NW) {
+      const int c = TSTORE ? (item & 1) : 0, rb = TSTORE ? item >> 1 : item;
+      // stages hold a power of two >= 32 rows (plan_mdict): every lane has a row
+      const int q = rb * 32 + lane;
+      const int r1 = q & r1mask, r2 = q >> lg_r1;
+      const float f1 = fmaf((float)(xb1 + r1), s1, t1);
+      const float f2 = fmaf((float)(xb2 + r2), s2, t2);
+      float wo[NCO];
+      {
+        const float g1[2] = {1.0f - f1, f1};
+#pragma unroll
+        for (int co = 0; co < NCO; ++co) {
+          float w = g1[co & 1];
+          w *= ((co >> 1) & 1) ? f2 : 1.0f - f2;
+          wo[co] = w * wfix[co >> 2];
+        }
+      }
+      // 32B-swizzled stage row (32 bytes): 16-byte chunk c of row q at c ^ ((q >> 2) & 1)
+      if constexpr (TSTORE) {
+        float4* slot4 = reinterpret_cast<float4*>(buf + q * 32 + ((c ^ ((q >> 2) & 1)) << 4));
+        *slot4 = blend_col(c, *slot4, wo);  // in place; the producer TMA-stores the box
+      } else {
+        const int sw = (q >> 2) & 1;
+        const float4 va = *reinterpret_cast<const float4*>(buf + q * 32 + (sw << 4));
+        const float4 vb = *reinterpret_cast<const float4*>(buf + q * 32 + ((1 ^ sw) << 4));
+        if (item + NW >= nitems) {  // the warp's last read of this stage
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&P.pipe->empty[s]);
+        }
+        const float4 ra = blend_col(0, va, wo);
+        const float4 rbv = blend_col(1, vb, wo);
+        float* o = out + gbase + (int64_t)r2 * G.vstride[KO - 2] + (int64_t)r1 * G.vstride[KO - 1] +
+                   seg * 8;
+        if (seg * 2 < ncol) __stcs(reinterpret_cast<float4*>(o), ra);
+        if (seg * 2 + 1 < ncol) __stcs(reinterpret_cast<float4*>(o) + 1, rbv);
       }
     }
-    if (TSTORE) fence_proxy_async_smem();
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&P.pipe->empty[s]);
+    if (TSTORE) {
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&P.pipe->empty[s]);
+    }
     ++it;
   }
 }

@@ -2001,6 +2001,20 @@ int mclahe_gpu_run_framewise(const mclahe_params_t* params, int32_t frame_axis, 
   return run_plan_host(o, pl, in, out, bytes, (size_t)align_up((int64_t)bytes, 256), timings);
 }
 
+void* mclahe_host_alloc(size_t bytes) {
+  void* p = nullptr;
+  const cudaError_t e = cudaHostAlloc(&p, bytes, cudaHostAllocPortable);
+  if (e != cudaSuccess) {
+    cuda_fail(e, "cudaHostAlloc");
+    return nullptr;
+  }
+  return p;
+}
+
+void mclahe_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
 int mclahe_multi_cuts(const mclahe_params_t* params, int32_t n_slabs, int64_t* cuts) {
   int rc = validate(params);
   if (rc) return rc;

@@ -177,7 +177,10 @@ class DistExchange:
         ops, recv = [], []
         staged = buf.is_cuda and self._host_staged()
         for r, a, b in peers:
-            send = buf[a - me.begin:b - me.begin].clone()
+            # rows are the outer dim: the shared rows are a contiguous view,
+            # sent as is (every send completes before the in-place combine
+            # below); gloo has no CUDA P2P, so it is staged through the host
+            send = buf[a - me.begin:b - me.begin]
             if staged:
                 send = send.cpu()
             rbuf = torch.empty_like(send)
