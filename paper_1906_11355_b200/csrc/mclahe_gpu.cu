@@ -21,6 +21,13 @@
 #include "k_misc.cuh"
 #include "k_pencil.cuh"
 
+namespace mg {
+// k_tile.cu
+void launch_tile_major(int dtype_f64, int mode, int grid, cudaStream_t st, const KGeom& G,
+                       const void* in, WS W, int accum);
+cudaError_t tile_major_smem_cap(int max_smem);
+}  // namespace mg
+
 namespace {
 
 using namespace mg;
@@ -141,6 +148,11 @@ struct mclahe_plan_s {
   int hist_grid = 0, interp_grid = 0, range_grid = 0, map_grid = 0, map_block = 128;
   int hist_dyn_grid = 0;  // K2 grid when units are handed out dynamically (occupancy x SMs)
   int64_t map_smem = 0;
+  // tile-major K2 (k_tile.cu) for the non-pencil paths: fused range + counts
+  // in one kernel for single-slab adaptive plans; shared_ws: a chunk plan of
+  // the streamed call (workspace shared with the other chunks: combine, not store)
+  bool fused_k2 = false, shared_ws = false;
+  int tile_grid = 0;
   // batched framewise, global mode: tiles take their frame's range (-1: off)
   int frame_axis = -1;
   int64_t off_frange = 0;
@@ -751,6 +763,9 @@ int plan_describe(const mclahe_params_t* params, int64_t row_begin, int64_t row_
   // so a dictionary numbered per chunk would not be stable: edge tables only
   if (!full_window) plan_dict(pl);
   if (!full_window) plan_mdict(pl);
+  pl->shared_ws = full_window && (row_begin != 0 || row_end != params->shape[0]);
+  pl->fused_k2 = !pl->hist.on && params->adaptive && !pl->f32() && !pl->shared_ws &&
+                 row_begin == 0 && row_end == params->shape[0];
   return MCLAHE_OK;
 }
 
@@ -865,6 +880,10 @@ int device_init(mclahe_plan_s* pl) {
   host.resize(total, 0);
   MG_CUDA(cudaMemcpy(pl->d_tables, host.data(), total * sizeof(int32_t), cudaMemcpyHostToDevice));
   pl->range_grid = pl->sms * 4;
+  if (!pl->hist.on) {
+    MG_CUDA(tile_major_smem_cap(max_smem));
+    pl->tile_grid = (int)std::max<int64_t>(1, std::min<int64_t>(pl->G.win_tiles, (int64_t)pl->sms * 8));
+  }
   // mappings: one warp per tile, f64 scratch of n_bins per warp
   const int64_t n = pl->p.n_bins;
   int warps = (int)std::max<int64_t>(1, std::min<int64_t>(4, (96 * 1024) / (n * 8)));
@@ -949,11 +968,9 @@ int do_range(mclahe_plan_s* pl, const void* in, void* ws, cudaStream_t st) {
     }
     return MCLAHE_OK;
   }
-  const int grid = generic_grid(pl);
-  if (pl->f32())
-    k_tiles_generic<float, 0, true><<<grid, 256, 0, st>>>(pl->G, static_cast<const float*>(in), W);
-  else
-    k_tiles_generic<double, 0, true><<<grid, 256, 0, st>>>(pl->G, static_cast<const double*>(in), W);
+  // tile-major range (+ counts when fused: single-slab float64 plans)
+  launch_tile_major(pl->f32() ? 0 : 1, pl->fused_k2 ? 2 : 0, pl->tile_grid, st, pl->G, in, W,
+                    pl->shared_ws ? 1 : 0);
   MG_LAUNCHED();
   return MCLAHE_OK;
 }
@@ -994,14 +1011,9 @@ int do_hist(mclahe_plan_s* pl, const void* in, void* ws, cudaStream_t st) {
     MG_LAUNCHED();
     return MCLAHE_OK;
   }
-  const int grid = generic_grid(pl);
-  if (pl->f32()) {
-    if (A) k_tiles_generic<float, 1, true><<<grid, 256, 0, st>>>(pl->G, static_cast<const float*>(in), W);
-    else k_tiles_generic<float, 1, false><<<grid, 256, 0, st>>>(pl->G, static_cast<const float*>(in), W);
-  } else {
-    if (A) k_tiles_generic<double, 1, true><<<grid, 256, 0, st>>>(pl->G, static_cast<const double*>(in), W);
-    else k_tiles_generic<double, 1, false><<<grid, 256, 0, st>>>(pl->G, static_cast<const double*>(in), W);
-  }
+  if (pl->fused_k2) return MCLAHE_OK;  // counted by the range pass
+  (void)A;
+  launch_tile_major(pl->f32() ? 0 : 1, 1, pl->tile_grid, st, pl->G, in, W, pl->shared_ws ? 1 : 0);
   MG_LAUNCHED();
   return MCLAHE_OK;
 }
