@@ -293,6 +293,11 @@ int mclahe_block_mappings(const double* host_blocks, int64_t n_blocks, int64_t b
 int mclahe_nd_gather(int32_t op, int32_t rank, const int64_t* in_shape, const int64_t* a,
                      const int64_t* b, const double* host_in, double* host_out);
 
+/* The request checks of validate_request (src/pipeline.cpp:19-33, minus the
+ * finiteness scan that runs on the device), on the host only: no CUDA call,
+ * so a caller can reject a bad request before staging any data. */
+int mclahe_validate(const mclahe_params_t* params);
+
 /* Page-locked host memory (cudaHostAlloc, portable): buffers from here make
  * the host-buffer calls copy at full PCIe rate and overlap H2D / compute /
  * D2H; the C++ drop-in stages its float64 <-> float32 conversions in them.

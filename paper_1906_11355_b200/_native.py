@@ -97,6 +97,9 @@ SIGNATURES = {
                                         C.c_int32, C.c_double, C.c_double, _vp, _vp, _vp, _vp,
                                         _vp, _vp]),
     "mclahe_nd_gather": (C.c_int, [C.c_int32, C.c_int32, _vp, _vp, _vp, _vp, _vp]),
+    "mclahe_validate": (C.c_int, [C.POINTER(Params)]),
+    "mclahe_host_alloc": (C.c_void_p, [C.c_size_t]),
+    "mclahe_host_free": (None, [C.c_void_p]),
     "mclahe_gaussian_filter": (C.c_int, [C.c_int32, _vp, _vp, C.c_double, _vp, _vp]),
     "mclahe_gaussian_filter_device": (C.c_int, [C.c_int32, _vp, _vp, C.c_double, _vp, _vp, _vp]),
     "mclahe_median_filter": (C.c_int, [C.c_int32, _vp, _vp, _vp, _vp]),

@@ -145,6 +145,7 @@ NdImage mclahe(const McLaheRequest& request, PhaseTimings* timings) {
   }
   p.n_bins = static_cast<int64_t>(request.params.n_bins);
   p.clip_limit = request.params.clip_limit;
+  if (const int rc = mclahe_validate(&p)) raise(rc);  // before any staging, as the reference
   mclahe_timings_t t{0.0, 0.0, 0.0};
   std::vector<double> out = run_staged(p, img.values(), [&](const void* in, void* o) {
     return mclahe_gpu_run(&p, in, o, &t);
@@ -197,6 +198,14 @@ NdImage mclahe_framewise(const NdImage& image, std::size_t frame_axis, const Ker
     p.kernel[i] = static_cast<int64_t>(kernel.sizes[i]);
   p.n_bins = static_cast<int64_t>(params.n_bins);
   p.clip_limit = params.clip_limit;
+  {  // the slice request, checked before any staging (messages as per slice)
+    mclahe_params_t sl = p;
+    sl.rank = p.rank - 1;
+    for (int j = 0, k = 0; j < p.rank; ++j)
+      if (j != static_cast<int>(frame_axis)) sl.shape[k++] = p.shape[j];
+    for (int j = sl.rank; j < MCLAHE_MAX_RANK; ++j) sl.shape[j] = sl.kernel[j] = 0;
+    if (const int rc = mclahe_validate(&sl)) raise(rc);
+  }
   mclahe_timings_t t{0.0, 0.0, 0.0};
   std::vector<double> out = run_staged(p, src, [&](const void* in, void* o) {
     return mclahe_gpu_run_framewise(&p, static_cast<int32_t>(frame_axis), in, o, &t);

@@ -2013,6 +2013,8 @@ int mclahe_gpu_run_framewise(const mclahe_params_t* params, int32_t frame_axis, 
   return run_plan_host(o, pl, in, out, bytes, (size_t)align_up((int64_t)bytes, 256), timings);
 }
 
+int mclahe_validate(const mclahe_params_t* params) { return validate(params); }
+
 void* mclahe_host_alloc(size_t bytes) {
   void* p = nullptr;
   const cudaError_t e = cudaHostAlloc(&p, bytes, cudaHostAllocPortable);
