@@ -6,8 +6,13 @@
 #include "mclahe/metrics.hpp"
 #include "mclahe/pipeline.hpp"
 
+#include <sys/mman.h>
+
 #include <algorithm>
 #include <atomic>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <limits>
@@ -82,12 +87,46 @@ void host_parallel(std::size_t n, Fn&& fn) {
 // (mclahe_gpu_run or the framewise form) on the pinned buffers, and widens
 // the result into a fresh vector, whose allocation (page faults of a zeroed
 // multi-GB vector) overlaps the GPU call.
+using Clock = std::chrono::steady_clock;
+double secs(Clock::time_point a, Clock::time_point b) {
+  return std::chrono::duration<double>(b - a).count();
+}
+bool trace() {
+  static const bool on = std::getenv("MCLAHE_DROPIN_TRACE") != nullptr;
+  return on;
+}
+
 template <typename Gpu>
 std::vector<double> run_staged(mclahe_params_t& p, std::span<const double> src, Gpu&& gpu) {
+  const auto t0 = Clock::now();
   const std::size_t n = src.size();
+  // The result vector, allocated while the input is staged and the GPU runs:
+  // zeroing a fresh multi-GB vector is page-fault bound, so its (untouched)
+  // buffer first gets transparent huge pages and is faulted in by all host
+  // threads (one byte per page of the raw storage); the vector's own zero
+  // fill then runs on mapped memory.
+  std::vector<double> out;
+  std::thread alloc([&] {
+    out.reserve(n);
+    char* raw = reinterpret_cast<char*>(out.data());
+    const std::size_t bytes = n * sizeof(double);
+    const uintptr_t huge = uintptr_t{2} << 20;
+    const uintptr_t a = (reinterpret_cast<uintptr_t>(raw) + huge - 1) & ~(huge - 1);
+    const uintptr_t e = (reinterpret_cast<uintptr_t>(raw) + bytes) & ~(huge - 1);
+    if (e > a) madvise(reinterpret_cast<void*>(a), e - a, MADV_HUGEPAGE);
+    host_parallel(bytes / 4096, [&](std::size_t b, std::size_t en) {
+      for (std::size_t pg = b; pg < en; ++pg) reinterpret_cast<volatile char*>(raw)[pg * 4096] = 0;
+    });
+    out.resize(n);
+  });
   Staging& S = staging();
   std::lock_guard<std::mutex> lock(S.mu);
-  ensure_staging(S, n * sizeof(double));
+  try {
+    ensure_staging(S, n * sizeof(double));
+  } catch (...) {
+    alloc.join();
+    throw;
+  }
   std::atomic<bool> exact{true};
   float* in32 = static_cast<float*>(S.in);
   host_parallel(n, [&](std::size_t b, std::size_t e) {
@@ -109,10 +148,11 @@ std::vector<double> run_staged(mclahe_params_t& p, std::span<const double> src, 
       std::memcpy(static_cast<double*>(S.in) + b, src.data() + b, (e - b) * sizeof(double));
     });
   p.dtype = f32 ? MCLAHE_F32 : MCLAHE_F64;
-  std::vector<double> out;
-  std::thread alloc([&] { out = std::vector<double>(n); });
+  const auto t1 = Clock::now();
   const int rc = gpu(S.in, S.out);
+  const auto t2 = Clock::now();
   alloc.join();
+  const auto t3 = Clock::now();
   if (rc != MCLAHE_OK) raise(rc);
   if (f32) {
     const float* o = static_cast<const float*>(S.out);
@@ -124,6 +164,10 @@ std::vector<double> run_staged(mclahe_params_t& p, std::span<const double> src, 
       std::memcpy(out.data() + b, static_cast<const double*>(S.out) + b, (e - b) * sizeof(double));
     });
   }
+  if (trace())
+    std::fprintf(stderr, "[mclahe drop-in] %zu values (%s): stage-in %.3f s, gpu %.3f s, "
+                 "out-alloc wait %.3f s, stage-out %.3f s\n", n, f32 ? "f32" : "f64",
+                 secs(t0, t1), secs(t1, t2), secs(t2, t3), secs(t3, Clock::now()));
   return out;
 }
 

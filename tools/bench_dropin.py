@@ -53,7 +53,9 @@ for name in sys.argv[1:] or ["4d"]:
         np.save(path, x)
         argv = [path, kern, str(cfg["n_bins"]), str(cfg["clip_limit"]), str(int(cfg["adaptive"]))]
         line = {"config": name, "input": kind, "voxels": int(x.size)}
-        r = subprocess.run([exe_b200] + argv + ["4", "0"], capture_output=True, text=True, check=True)
+        r = subprocess.run([exe_b200] + argv + ["4", "0"], capture_output=True, text=True, check=True,
+                           env=dict(os.environ, MCLAHE_DROPIN_TRACE="1"))
+        sys.stderr.write(r.stderr)
         b = json.loads(r.stdout)
         line.update(b200_best_s=b["best_s"], b200_mean_s=b["mean_s"], b200_checksum=b["checksum"])
         if have_ref and os.environ.get("WITH_REF"):
