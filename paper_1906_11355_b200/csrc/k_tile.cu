@@ -164,7 +164,114 @@ __global__ void __launch_bounds__(kTileThreads)
   if (MODE != 1 && bad) atomicMax(reinterpret_cast<long long*>(&W.range[2]), 1LL);
 }
 
+// ------------------------------------------------------------- K4 -----
+// Cell-major blend for the same shapes / dtypes: one CTA per interpolation
+// cell (the box of original voxels sharing one set of 2^D neighbour tiles,
+// src/interpolation.cpp:24-35).  The 2^D corner LUTs and binning parameters
+// are staged in shared memory once per cell; voxels are walked last dim
+// fastest (coalesced), with 32-bit index arithmetic inside the box.  Per
+// voxel: the per-dim factors d_lo / b (exact half-integer numerators), 2^D
+// bins (bin_of: the reference rule) and the f64 sum of w * LUT, clamped.
+struct CellBox {
+  int64_t a[kMaxRank];
+  int32_t ext[kMaxRank];
+  int64_t cc[kMaxRank];
+  int64_t n;
+};
+
+template <typename T, bool ADAPT>
+__global__ void __launch_bounds__(kTileThreads)
+    k_interp_cell(const KGeom G, const T* __restrict__ in, T* __restrict__ out, WS W,
+                  int64_t cell0, int64_t ncells) {
+  extern __shared__ __align__(16) float lutS[];  // [2^D][n]
+  __shared__ TileParam<T> tpS[1 << kMaxRank];
+  __shared__ int32_t tileS[1 << kMaxRank];
+  __shared__ CellBox B;
+  if (W.range[2] != 0) return;  // non-finite input: write nothing
+  const int D = G.rank, NC = 1 << D, n = G.n_bins;
+  const T nm05 = (T)n - (T)0.5;
+  const TileParam<T>* tparams = reinterpret_cast<const TileParam<T>*>(W.tparams);
+  const int64_t row_end = G.row0 + G.local_voxels / G.vstride[0];
+  for (int64_t c = blockIdx.x; c < ncells; c += gridDim.x) {
+    if (threadIdx.x == 0) {
+      int64_t r = c;
+      for (int j = D - 1; j >= 0; --j) {
+        const int64_t nc = j == 0 ? ncells : G.d[j].g - 1;
+        B.cc[j] = j == 0 ? cell0 + r : r % nc;
+        if (j > 0) r /= nc;
+      }
+      B.n = 1;
+      for (int j = 0; j < D; ++j) {
+        int64_t a, e;
+        cell_range(G.d[j], B.cc[j], &a, &e);
+        if (j == 0) {
+          a = a > G.row0 ? a : G.row0;
+          e = e < row_end ? e : row_end;
+        }
+        B.a[j] = a;
+        B.ext[j] = (int32_t)(e > a ? e - a : 0);
+        B.n *= B.ext[j];
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x < NC) {  // corner co: tile cc + bits (dimension 0 the MSB)
+      int64_t f = (B.cc[0] + ((threadIdx.x >> (D - 1)) & 1) - G.trow0) * G.tstride[0];
+      for (int j = 1; j < D; ++j) f += (B.cc[j] + ((threadIdx.x >> (D - 1 - j)) & 1)) * G.tstride[j];
+      tileS[threadIdx.x] = (int32_t)f;
+      tpS[threadIdx.x] = tparams[ADAPT ? f : 0];
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < NC * n; k += kTileThreads) {
+      const int co = k / n;
+      lutS[k] = W.lut[(int64_t)tileS[co] * n + (k - co * n)];
+    }
+    __syncthreads();
+    const int64_t nv = B.n;
+    for (int64_t k = threadIdx.x; k < nv; k += kTileThreads) {
+      int64_t off = 0;
+      double fl[kMaxRank];
+      int64_t q = k;
+      for (int j = D - 1; j >= 0; --j) {
+        const int32_t e = B.ext[j];
+        const int32_t i = (int32_t)(q % e);
+        q /= e;
+        const int64_t x = B.a[j] + i;
+        off += (j == 0 ? x - G.row0 : x) * G.vstride[j];
+        fl[j] = (double)twice_dlo(G.d[j], x, B.cc[j]) / (double)(2 * G.d[j].b);
+      }
+      const T v = in[off];
+      const int bg = ADAPT ? 0 : bin_of(v, tpS[0], edge_row<T>(W, 0, n), n, nm05);
+      double acc = 0.0;
+      for (int co = 0; co < NC; ++co) {
+        double w = 1.0;
+        for (int j = 0; j < D; ++j) w *= ((co >> (D - 1 - j)) & 1) ? fl[j] : 1.0 - fl[j];
+        const int b = ADAPT ? bin_of(v, tpS[co], edge_row<T>(W, tileS[co], n), n, nm05) : bg;
+        acc += w * (double)lutS[co * n + b];
+      }
+      out[off] = (T)fmin(fmax(acc, 0.0), 1.0);
+    }
+    __syncthreads();
+  }
+}
+
 }  // namespace
+
+// Cell-major blend launch (k_interp_cell); shared memory 2^D * n_bins floats.
+void launch_interp_cell(int dtype_f64, int adaptive, int grid, cudaStream_t st, const KGeom& G,
+                        const void* in, void* out, WS W, int64_t cell0, int64_t ncells) {
+  const size_t smem = ((size_t)1 << G.rank) * (size_t)G.n_bins * 4;
+  if (dtype_f64) {
+    const double* x = static_cast<const double*>(in);
+    double* y = static_cast<double*>(out);
+    if (adaptive) k_interp_cell<double, true><<<grid, kTileThreads, smem, st>>>(G, x, y, W, cell0, ncells);
+    else k_interp_cell<double, false><<<grid, kTileThreads, smem, st>>>(G, x, y, W, cell0, ncells);
+  } else {
+    const float* x = static_cast<const float*>(in);
+    float* y = static_cast<float*>(out);
+    if (adaptive) k_interp_cell<float, true><<<grid, kTileThreads, smem, st>>>(G, x, y, W, cell0, ncells);
+    else k_interp_cell<float, false><<<grid, kTileThreads, smem, st>>>(G, x, y, W, cell0, ncells);
+  }
+}
 
 // Host accessors (mclahe_gpu.cu): MODE 0 / 1 / 2 for float or double.
 void launch_tile_major(int dtype_f64, int mode, int grid, cudaStream_t st, const KGeom& G,
@@ -185,7 +292,11 @@ void launch_tile_major(int dtype_f64, int mode, int grid, cudaStream_t st, const
 cudaError_t tile_major_smem_cap(int max_smem) {
   const void* fns[] = {reinterpret_cast<const void*>(k_tile_major<double, 1>),
                        reinterpret_cast<const void*>(k_tile_major<double, 2>),
-                       reinterpret_cast<const void*>(k_tile_major<float, 1>)};
+                       reinterpret_cast<const void*>(k_tile_major<float, 1>),
+                       reinterpret_cast<const void*>(k_interp_cell<double, true>),
+                       reinterpret_cast<const void*>(k_interp_cell<double, false>),
+                       reinterpret_cast<const void*>(k_interp_cell<float, true>),
+                       reinterpret_cast<const void*>(k_interp_cell<float, false>)};
   for (const void* f : fns) {
     cudaFuncAttributes fa;
     cudaError_t e = cudaFuncGetAttributes(&fa, f);

@@ -26,6 +26,8 @@ namespace mg {
 void launch_tile_major(int dtype_f64, int mode, int grid, cudaStream_t st, const KGeom& G,
                        const void* in, WS W, int accum);
 cudaError_t tile_major_smem_cap(int max_smem);
+void launch_interp_cell(int dtype_f64, int adaptive, int grid, cudaStream_t st, const KGeom& G,
+                        const void* in, void* out, WS W, int64_t cell0, int64_t ncells);
 }  // namespace mg
 
 namespace {
@@ -880,7 +882,7 @@ int device_init(mclahe_plan_s* pl) {
   host.resize(total, 0);
   MG_CUDA(cudaMemcpy(pl->d_tables, host.data(), total * sizeof(int32_t), cudaMemcpyHostToDevice));
   pl->range_grid = pl->sms * 4;
-  if (!pl->hist.on) {
+  if (!pl->hist.on || !pl->interp.on) {
     MG_CUDA(tile_major_smem_cap(max_smem));
     pl->tile_grid = (int)std::max<int64_t>(1, std::min<int64_t>(pl->G.win_tiles, (int64_t)pl->sms * 8));
   }
@@ -1112,6 +1114,18 @@ int do_interp(mclahe_plan_s* pl, const void* in, void* out, void* ws, cudaStream
                                                      static_cast<float*>(out),
                                                      pl->d_tables + pl->off_interp_units,
                                                      pl->d_tables + pl->off_interp_cta, W);
+    MG_LAUNCHED();
+    return MCLAHE_OK;
+  }
+  // cell-major blend when the 2^D corner LUTs fit shared memory
+  if (((int64_t{1} << pl->p.rank) * pl->p.n_bins * 4) <= 200 * 1024 && !getenv("MCLAHE_GENERIC_BLEND")) {
+    const Dim& d0 = pl->d[0];
+    const int64_t c0 = cell_of(d0, pl->info.row_begin);
+    const int64_t c1 = cell_of(d0, pl->info.row_end - 1);
+    int64_t ncells = c1 - c0 + 1;
+    for (int j = 1; j < pl->p.rank; ++j) ncells *= pl->d[j].g - 1;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ncells, (int64_t)pl->sms * 8));
+    launch_interp_cell(pl->f32() ? 0 : 1, A ? 1 : 0, grid, st, pl->G, in, out, W, c0, c1 - c0 + 1);
     MG_LAUNCHED();
     return MCLAHE_OK;
   }
@@ -1365,6 +1379,9 @@ mclahe_plan_s* cached_plan(OneShot& o, const mclahe_params_t* p, int* rc, int fr
     // the plan was described as adaptive, so plan_mdict may have armed the
     // folded-pair dictionary blend; with no dictionary it has no tables
     pl->mdict = false;
+    // the frame range pass sets the tiles' ranges; the counts come from the
+    // histogram pass (no fused tile-major range + counts)
+    pl->fused_k2 = false;
     pl->off_frange = align_up(pl->info.workspace_bytes, 256);
     pl->info.workspace_bytes = align_up(pl->off_frange + q.shape[frame_axis] * 16, 256);
   }
