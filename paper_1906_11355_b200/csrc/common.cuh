@@ -368,7 +368,8 @@ __device__ __noinline__ void pipe_produce(const KGeom& G, const CUtensorMap* map
                                           const int32_t* __restrict__ units, int u0, int u1,
                                           Pipe& pp, float* bufs,
                                           const CUtensorMap* out_map = nullptr,
-                                          unsigned long long* dyn = nullptr) {
+                                          unsigned long long* dyn = nullptr,
+                                          const TileParam<float>* skip_tp = nullptr) {
   const int nst = G.nst;
   const int nseg = G.nseg;
   const bool segv = G.tma_rank - KO == 2;  // the TMA view has a segment coordinate
@@ -417,6 +418,15 @@ __device__ __noinline__ void pipe_produce(const KGeom& G, const CUtensorMap* map
       key = (U[0] - G.trow0) * G.tstride[0];
 #pragma unroll 1
       for (int j = 1; j < KO; ++j) key += (int64_t)U[j] * G.tstride[j];
+      // K2b, adaptive: a unit whose tiles are all degenerate is never binned
+      // (build_mappings skips collapsed ranges, src/histogram.cpp:95-98), so
+      // its boxes are not even loaded
+      if (skip_tp) {
+        bool all = true;
+#pragma unroll 1
+        for (int t = 0; t < G.gtr && all; ++t) all = tp_degenerate(skip_tp[key + t].lim);
+        if (all) continue;
+      }
     }
     // boxes: dims < KO-2 one coordinate each, dim KO-2 in steps of R2, dim KO-1 of R1
     int64_t nfix = 1;

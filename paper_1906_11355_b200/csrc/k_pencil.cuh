@@ -332,7 +332,8 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
     if (threadIdx.x == kConsumers)
       pipe_produce<KO, false>(
           G, &tmap, units, G.dyn_units ? 0 : u0, G.dyn_units ? G.dyn_units : u1, *P.pipe, P.bufs,
-          nullptr, G.dyn_units ? reinterpret_cast<unsigned long long*>(&W.range[3]) : nullptr);
+          nullptr, G.dyn_units ? reinterpret_cast<unsigned long long*>(&W.range[3]) : nullptr,
+          ADAPT ? tparams : nullptr);
     return;
   }
   const int tid = threadIdx.x;

@@ -182,7 +182,7 @@ struct CellBox {
 template <typename T, bool ADAPT>
 __global__ void __launch_bounds__(kTileThreads)
     k_interp_cell(const KGeom G, const T* __restrict__ in, T* __restrict__ out, WS W,
-                  int64_t cell0, int64_t ncells) {
+                  int64_t cell0, int64_t ncells0) {
   extern __shared__ __align__(16) float lutS[];  // [2^D][n]
   __shared__ TileParam<T> tpS[1 << kMaxRank];
   __shared__ int32_t tileS[1 << kMaxRank];
@@ -192,14 +192,16 @@ __global__ void __launch_bounds__(kTileThreads)
   const T nm05 = (T)n - (T)0.5;
   const TileParam<T>* tparams = reinterpret_cast<const TileParam<T>*>(W.tparams);
   const int64_t row_end = G.row0 + G.local_voxels / G.vstride[0];
+  int64_t ncells = ncells0;  // the slab's dim-0 cells x every cell of the other dims
+  for (int j = 1; j < D; ++j) ncells *= G.d[j].g - 1;
   for (int64_t c = blockIdx.x; c < ncells; c += gridDim.x) {
     if (threadIdx.x == 0) {
       int64_t r = c;
-      for (int j = D - 1; j >= 0; --j) {
-        const int64_t nc = j == 0 ? ncells : G.d[j].g - 1;
-        B.cc[j] = j == 0 ? cell0 + r : r % nc;
-        if (j > 0) r /= nc;
+      for (int j = D - 1; j > 0; --j) {
+        B.cc[j] = r % (G.d[j].g - 1);
+        r /= G.d[j].g - 1;
       }
+      B.cc[0] = cell0 + r;
       B.n = 1;
       for (int j = 0; j < D; ++j) {
         int64_t a, e;
@@ -258,18 +260,18 @@ __global__ void __launch_bounds__(kTileThreads)
 
 // Cell-major blend launch (k_interp_cell); shared memory 2^D * n_bins floats.
 void launch_interp_cell(int dtype_f64, int adaptive, int grid, cudaStream_t st, const KGeom& G,
-                        const void* in, void* out, WS W, int64_t cell0, int64_t ncells) {
+                        const void* in, void* out, WS W, int64_t cell0, int64_t ncells0) {
   const size_t smem = ((size_t)1 << G.rank) * (size_t)G.n_bins * 4;
   if (dtype_f64) {
     const double* x = static_cast<const double*>(in);
     double* y = static_cast<double*>(out);
-    if (adaptive) k_interp_cell<double, true><<<grid, kTileThreads, smem, st>>>(G, x, y, W, cell0, ncells);
-    else k_interp_cell<double, false><<<grid, kTileThreads, smem, st>>>(G, x, y, W, cell0, ncells);
+    if (adaptive) k_interp_cell<double, true><<<grid, kTileThreads, smem, st>>>(G, x, y, W, cell0, ncells0);
+    else k_interp_cell<double, false><<<grid, kTileThreads, smem, st>>>(G, x, y, W, cell0, ncells0);
   } else {
     const float* x = static_cast<const float*>(in);
     float* y = static_cast<float*>(out);
-    if (adaptive) k_interp_cell<float, true><<<grid, kTileThreads, smem, st>>>(G, x, y, W, cell0, ncells);
-    else k_interp_cell<float, false><<<grid, kTileThreads, smem, st>>>(G, x, y, W, cell0, ncells);
+    if (adaptive) k_interp_cell<float, true><<<grid, kTileThreads, smem, st>>>(G, x, y, W, cell0, ncells0);
+    else k_interp_cell<float, false><<<grid, kTileThreads, smem, st>>>(G, x, y, W, cell0, ncells0);
   }
 }
 
