@@ -294,6 +294,23 @@ __device__ __forceinline__ float lut_at(uint32_t lbase, int bits) {
   return m;
 }
 
+// Same entry from the floor bits with one VIADDMNMX.RELU: k = clamp(bits -
+// kMagicBits, 0, nm1) at shared byte address base + 4 * k + OFF.  Exact only
+// while bits - kMagicBits cannot wrap (t > 0: the caller checks the range).
+template <int OFF>
+__device__ __forceinline__ float lut_at_relu(uint32_t base, int bits, int nm1) {
+  float m;
+  asm volatile(
+      "{\n\t.reg .s32 k;\n\t.reg .u32 a;\n\t"
+      "add.s32 k, %1, %3;\n\t"
+      "min.relu.s32 k, k, %4;\n\t"
+      "mad.lo.u32 a, k, 4, %2;\n\t"
+      "ld.shared.f32 %0, [a+%5];\n\t}"
+      : "=f"(m)
+      : "r"(bits), "r"(base), "r"(-kMagicBits), "r"(nm1), "n"(OFF));
+  return m;
+}
+
 // Bins of two voxels by the bracketed floors, as the NB blend computes them
 // (fast answer clamp(floor(d c_lo)); where the clamped floors disagree, the
 // edge table th (unpadded here) decides between them).  w = bin_window(c).

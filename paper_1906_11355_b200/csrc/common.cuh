@@ -192,16 +192,30 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
-// Busy-poll variant (no suspend-time hint): for consumers whose stage is
-// normally already full, where the sleep/wake round trip costs issue slots.
-__device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
+// Polling variant (no suspend-time hint): for the blend producer, whose slot
+// frees in well under a microsecond, where the suspend / wake round trip of
+// the hinted wait is on the critical path.  MG_SPIN_NS > 0 backs off that many
+// nanoseconds between polls: a bare spin issues ~3 instructions per poll on
+// the SM sub-partition it shares with four consumer warps (5D blend: 6 % of
+// all instructions issued).
+#ifndef MG_SPIN_NS
+#define MG_SPIN_NS 32
+#endif
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
   asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "MG_SPIN_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra MG_SPIN_%=;\n}" ::"r"(smem_u32(bar)),
-      "r"(parity)
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
       : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) {
+    if (MG_SPIN_NS > 0) __nanosleep(MG_SPIN_NS);
+  }
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
                                          uint64_t* bar) {

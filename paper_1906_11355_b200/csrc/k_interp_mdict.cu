@@ -111,9 +111,11 @@ __global__ void __launch_bounds__(NWARP * 32 + 32, 1)
   int seg = 0;
   int rot = 0;  // round-robin offset of the item deal
   uint32_t it = 0;
+  int cs_slot = 0;
+  uint32_t cs_phase = 0;
   while (true) {
-    const int s = it % G.nst;
-    mbar_wait(&P.pipe->full[s], (it / G.nst) & 1);
+    const int s = cs_slot;  // it % nst, (it / nst) & 1 as counters: no division
+    mbar_wait(&P.pipe->full[s], cs_phase);
     const Stage& S = P.pipe->st[s];
     if (S.unit < 0) break;
     const int64_t key = S.key * G.nseg + S.seg;
@@ -243,15 +245,21 @@ __global__ void __launch_bounds__(NWARP * 32 + 32, 1)
         miss |= (di[i] < 0) << i;
         A[i] = reinterpret_cast<const char*>(Ms + ((c * 4 + i) * NCO) * KC + (di[i] >= 0 ? di[i] : 0));
       }
-      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+      // two voxels per packed FFMA2 (same per-voxel order and rounding as
+      // fmaf: acc = fma(wo[co], M, acc), co ascending)
+      u64 acc01 = 0, acc23 = 0;
       static_for<0, NCO>([&](auto coc) {
         constexpr int co = decltype(coc)::value;
         float m[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) m[i] = *reinterpret_cast<const float*>(A[i] + co * KC * 4);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) acc[i] = fmaf(wo[co], m[i], acc[i]);
+        const u64 w2 = pk2(wo[co], wo[co]);
+        acc01 = fma2(pk2(m[0], m[1]), w2, acc01);
+        acc23 = fma2(pk2(m[2], m[3]), w2, acc23);
       });
+      float acc[4];
+      upk2(acc01, acc[0], acc[1]);
+      upk2(acc23, acc[2], acc[3]);
       if (ADAPT && miss) {  // values the (sampled) dictionary lacks: from the workspace LUTs
         const int colc = min(col, ncol - 1);
         const int tt = colT[colc];
@@ -326,6 +334,10 @@ __global__ void __launch_bounds__(NWARP * 32 + 32, 1)
       if (lane == 0) mbar_arrive(&P.pipe->empty[s]);
     }
     ++it;
+    if (++cs_slot == G.nst) {
+      cs_slot = 0;
+      cs_phase ^= 1;
+    }
   }
 }
 

@@ -330,12 +330,23 @@ template <typename T>
 __global__ void k_params(const KGeom G, WS W, int64_t t0, int64_t nt) {
   TileParam<T>* tp = reinterpret_cast<TileParam<T>*>(W.tparams);
   const int64_t n = G.adaptive ? t0 + nt : 1;
+  // adaptive: the smallest tile minimum goes to W.range[0] (MAX of ~key, as
+  // the global range pass keeps it) -- a lower bound on every voxel of the
+  // window, which the n_bins-specialised blend uses to pick its clamp
+  long long mkey = LLONG_MIN;
   for (int64_t t = (G.adaptive ? t0 : 0) + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
        t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t* r = G.adaptive ? W.trange + 2 * t : W.range;
     const double lo = okey_decode(~r[0]);
     const double hi = okey_decode(r[1]);
     tp[t] = make_tile_param<T>(lo, hi, G.n_bins);
+    if (G.adaptive && r[0] != INT64_MIN) mkey = max(mkey, (long long)r[0]);
+  }
+  if (G.adaptive) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mkey = max(mkey, __shfl_xor_sync(0xffffffffu, mkey, o));
+    if ((threadIdx.x & 31) == 0 && mkey != LLONG_MIN)
+      atomicMax(reinterpret_cast<long long*>(&W.range[0]), mkey);
   }
 }
 

@@ -147,9 +147,11 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
   };
 
   uint32_t it = 0;
+  int cs_slot = 0;
+  uint32_t cs_phase = 0;
   while (true) {
-    const int s = it % G.nst;
-    mbar_wait(&P.pipe->full[s], (it / G.nst) & 1);
+    const int s = cs_slot;  // it % nst, (it / nst) & 1 as counters: no division
+    mbar_wait(&P.pipe->full[s], cs_phase);
     const Stage& S = P.pipe->st[s];
     if (S.unit < 0) break;
     const int64_t key = S.key;
@@ -221,6 +223,10 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
     __syncwarp();
     if ((tid & 31) == 0) mbar_arrive(&P.pipe->empty[s]);
     ++it;
+    if (++cs_slot == G.nst) {
+      cs_slot = 0;
+      cs_phase ^= 1;
+    }
   }
   if (cur >= 0) flush();
   {
@@ -359,9 +365,11 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
   const int trips = slot < G.stage_rows ? (G.stage_rows - slot + G.rpi - 1) / G.rpi : 0;
 
   uint32_t it = 0;
+  int cs_slot = 0;
+  uint32_t cs_phase = 0;
   while (true) {
-    const int s = it % G.nst;
-    mbar_wait(&P.pipe->full[s], (it / G.nst) & 1);
+    const int s = cs_slot;  // it % nst, (it / nst) & 1 as counters: no division
+    mbar_wait(&P.pipe->full[s], cs_phase);
     const Stage& S = P.pipe->st[s];
     if (S.unit < 0) break;
     const int64_t key = S.key;
@@ -552,6 +560,10 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
     __syncwarp();
     if ((tid & 31) == 0) mbar_arrive(&P.pipe->empty[s]);
     ++it;
+    if (++cs_slot == G.nst) {
+      cs_slot = 0;
+      cs_phase ^= 1;
+    }
   }
   consumers_sync();
   if (cur >= 0) {
@@ -653,6 +665,7 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
   colT = reinterpret_cast<int*>((reinterpret_cast<uintptr_t>(colT) + 15) & ~uintptr_t(15));
   float* colW = reinterpret_cast<float*>(colT + ncol);  // [ncol][4][NCT], 16-byte aligned
   __shared__ int s_bad;
+  __shared__ int s_wrap;   // NB: a staged tile could see t <= 0 (no RELU clamp)
   __shared__ int s_dmode;  // DICT: 1 = affine lookup
   __shared__ float s_dv0, s_dS;
   // 4 * kMagicBits through shared memory: kept opaque to ptxas so the NB fast
@@ -683,6 +696,11 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
   // and re-probes the bracketed path every 64 items.  G.nb_edges forces either.
   int nb_edges = G.nb_edges == 1 ? 1 : 0;  // warp-uniform
   int nb_probe = 0, nb_slow = 0;
+  bool wrap_safe = false;
+  // NB: the volume's minimum (k_params, adaptive) bounds every voxel a unit
+  // blends from below; -inf when unknown (every unit takes the two-op clamp)
+  float vmin = -INFINITY;
+  if (NB > 0 && W.range[0] != INT64_MIN) vmin = __double2float_rd(okey_decode(~W.range[0]));
 
   // column table (independent of the unit): cells are shared by the column's
   // 4 voxels (the plan checks cell boundaries along the last dim are x4)
@@ -732,9 +750,11 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
   float ugs[KO], ugt[KO];  // unit geometry (see the stage geometry below)
   int64_t cur = -1;
   uint32_t it = 0;
+  int cs_slot = 0;
+  uint32_t cs_phase = 0;
   while (true) {
-    const int s = it % G.nst;
-    mbar_wait(&P.pipe->full[s], (it / G.nst) & 1);
+    const int s = cs_slot;  // it % nst, (it / nst) & 1 as counters: no division
+    mbar_wait(&P.pipe->full[s], cs_phase);
     const Stage& S = P.pipe->st[s];
     if (S.unit < 0) break;
     // NB with several segments stages one segment's trailing tiles at a time
@@ -742,6 +762,11 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
     const int64_t key = SEGW && G.nseg > 1 ? S.key * G.nseg + S.seg : S.key;
     if (key != cur) {
       consumers_sync<kConsumersBlend>();
+      if (tid == 0) {
+        s_bad = 0;
+        s_wrap = 0;
+      }
+      consumers_sync<kConsumersBlend>();  // flags reset before any staging thread sets them
       if (SEGW) {  // tile window of this segment: its columns' first tiles + far corner
         seg_lo = 0;
         seg_cnt = (int)gtr;
@@ -756,7 +781,6 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
           seg_cnt = min((int)gtr - mn, mx + ctoff[NCT - 1] - mn + 1);
         }
       }
-      if (tid == 0) s_bad = 0;
       if (!ADAPT && cur < 0)
         for (int k = tid; k < n1; k += kConsumersBlend) thrS[k] = W.thr[k];
       if (DICT && cur < 0) {
@@ -819,6 +843,9 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
             if (!(wn.y < INFINITY)) lc.y = __int_as_float(0x7fc00000);  // c_hi overflows: exact path
             *reinterpret_cast<float4*>(blk + (t * NCO + c2) * TBW) = make_float4(lc.x, wn.x, wn.y, lc.y);
             if (isnan(lc.y)) s_bad = 1;
+            // t = fl(fl(v - lo) * c_hi + 1.5 * 2^23) > 0 for every v >= vmin
+            // unless (lo - vmin) * c_hi reaches ~1.5 * 2^23 (margin: 2^22)
+            if (!((lc.x - vmin) * wn.y < 4194304.0f)) s_wrap = 1;
           }
           continue;
         }
@@ -859,6 +886,7 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
       }
       consumers_sync<kConsumersBlend>();
       if (ADAPT) patho = s_bad != 0;
+      wrap_safe = s_wrap == 0;
       cur = key;
 #pragma unroll
       for (int jd = 0; jd < KO; ++jd) {
@@ -1083,83 +1111,117 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
               });
             }
           } else if (!patho) {  // hot path: bracketed floors, one LUT gather per corner
-            // LUT byte address straight from the clamped floor bits:
-            // lbase + 4 * bits  (lbase = base - 4 * kMagicBits, mod 2^32)
+            const u64 M2 = pk2(kMagic, kMagic);
+            // outer corners in pairs (runtime loop: the unrolled body is one
+            // pair's 2 x NCT corners -- code size); weights as wo[] above.
+            // Trailing corners in pairs share one warp vote.  Voxel pairs
+            // accumulate with packed FFMA2 (per voxel the same fma order and
+            // rounding as the scalar paths).
+            // RELU: clamp the floor with one VIADDMNMX.RELU (min(bits - magic,
+            // NB - 1), then max 0); exact unless bits - magic wraps, i.e.
+            // t = fl(y + 1.5 * 2^23) <= 0, which needs y <= -1.5 * 2^23: the
+            // unit's staged tiles were checked against the volume's minimum
+            // (s_wrap).  Otherwise the signed-bits clamp (two ops).
+            constexpr int SF = KO >= 2 ? 2 : 1;
+            const float g2[2] = {1.0f - f2, f2};
+            // LUT byte address straight from the clamped floor bits (signed-bits
+            // clamp): lbase + 4 * bits  (lbase = base - 4 * kMagicBits, mod 2^32)
             uint32_t lbase[KT];
 #pragma unroll
             for (int j = 0; j < KT; ++j) lbase[j] = sbase[j] - mb4;
-            const u64 M2 = pk2(kMagic, kMagic);
-            // outer corners in pairs (runtime loop: the unrolled body is one
-            // pair's 2 x NCT corners -- code size); weights as wo[] above
-            constexpr int SF = KO >= 2 ? 2 : 1;
-            const float g2[2] = {1.0f - f2, f2};
+            u64 a2[NCT][2];
+#pragma unroll
+            for (int ct = 0; ct < NCT; ++ct) a2[ct][0] = a2[ct][1] = 0;
+            auto run = [&](auto relu_c) {
+              constexpr bool RELU = decltype(relu_c)::value;
 #pragma unroll 1
-            for (int cp = 0; cp < NCO / 2; ++cp) {
-              const float wf = pick(wfix, cp >> (SF - 1));
-              const float wg2 = KO >= 2 ? pick(g2, cp & 1) : 1.0f;
-              const uint32_t po = (uint32_t)(2 * cp * TB);
-              static_for<0, 2>([&](auto bc) {
-                constexpr int b1 = decltype(bc)::value;
-                float w = b1 ? f1 : 1.0f - f1;
-                if (KO >= 2) w *= wg2;
-                w *= wf;
-                float m0[4];  // MORD: trailing corner 0's gathers
-                (void)m0;
-                static_for<0, NCT>([&](auto ctc) {
-                  constexpr int ct = decltype(ctc)::value;
-                  constexpr int OFF = ((ct & 1) * NCO + b1) * TB;
-                  const char* B = base[ct >> 1] + po + OFF;
-                  const float4 hd = *reinterpret_cast<const float4*>(B);
-                  u64 ta[2], tb[2];
+              for (int cp = 0; cp < NCO / 2; ++cp) {
+                const float wf = pick(wfix, cp >> (SF - 1));
+                const float wg2 = KO >= 2 ? pick(g2, cp & 1) : 1.0f;
+                const uint32_t po = (uint32_t)(2 * cp * TB);
+                static_for<0, 2>([&](auto bc) {
+                  constexpr int b1 = decltype(bc)::value;
+                  float w = b1 ? f1 : 1.0f - f1;
+                  if (KO >= 2) w *= wg2;
+                  w *= wf;
+                  const u64 w2 = pk2(w, w);
+                  static_for<0, NCT / 2>([&](auto hc) {
+                    constexpr int hp = decltype(hc)::value;
+                    float m[2][4];
+                    uint32_t amb = 0;  // any lane-voxel whose two floors disagree
+                    static_for<0, 2>([&](auto ec) {
+                      constexpr int ct = 2 * hp + decltype(ec)::value;
+                      constexpr int OFF = ((ct & 1) * NCO + b1) * TB;
+                      const float4 hd = *reinterpret_cast<const float4*>(base[ct >> 1] + po + OFF);
+                      u64 ta[2], tb[2];
 #pragma unroll
-                  for (int h = 0; h < 2; ++h) {
-                    const u64 d = sub2(h ? V23 : V01, pk2(hd.x, hd.x));
-                    ta[h] = fma_rm2(d, pk2(hd.y, hd.y), M2);
-                    tb[h] = fma_rm2(d, pk2(hd.z, hd.z), M2);
-                  }
-                  float fa[4], fb[4];
-                  upk2(ta[0], fa[0], fa[1]);
-                  upk2(ta[1], fa[2], fa[3]);
-                  upk2(tb[0], fb[0], fb[1]);
-                  upk2(tb[1], fb[2], fb[3]);
-                  uint32_t amb = 0;  // any lane-voxel whose two floors disagree
-                  float m[4];
+                      for (int h = 0; h < 2; ++h) {
+                        const u64 d = sub2(h ? V23 : V01, pk2(hd.x, hd.x));
+                        ta[h] = fma_rm2(d, pk2(hd.y, hd.y), M2);
+                        tb[h] = fma_rm2(d, pk2(hd.z, hd.z), M2);
+                      }
+                      float fa[4], fb[4];
+                      upk2(ta[0], fa[0], fa[1]);
+                      upk2(ta[1], fa[2], fa[3]);
+                      upk2(tb[0], fb[0], fb[1]);
+                      upk2(tb[1], fb[2], fb[3]);
 #pragma unroll
-                  for (int i = 0; i < 4; ++i) {
-                    const int ab = __float_as_int(fa[i]);
-                    amb |= (uint32_t)(ab ^ __float_as_int(fb[i]));
-                    m[i] = lut_at<OFF + NbBlock::lut_off(NB) * 4>(
-                        lbase[ct >> 1] + po, min(max(ab, kMagicBits), kMagicBits + NB - 1));
-                  }
-                  if (__any_sync(0xffffffffu, amb != 0)) {
-                    // rare (q within ~5e-7 |q| of a bin edge): the clamped floors
-                    // are k - 1 and k and the edge table picks one
-                    ++nb_slow;
-                    const float* th = reinterpret_cast<const float*>(B) + NbBlock::th_off(NB);
-                    const float* L = reinterpret_cast<const float*>(B) + NbBlock::lut_off(NB);
+                      for (int i = 0; i < 4; ++i) {
+                        const int ab = __float_as_int(fa[i]);
+                        amb |= (uint32_t)(ab ^ __float_as_int(fb[i]));
+                        if constexpr (RELU)
+                          m[ct & 1][i] = lut_at_relu<OFF + NbBlock::lut_off(NB) * 4>(sbase[ct >> 1] + po, ab, NB - 1);
+                        else
+                          m[ct & 1][i] = lut_at<OFF + NbBlock::lut_off(NB) * 4>(
+                              lbase[ct >> 1] + po, min(max(ab, kMagicBits), kMagicBits + NB - 1));
+                      }
+                    });
+                    if (__any_sync(0xffffffffu, amb != 0)) {
+                      // rare (q within ~5e-7 |q| of a bin edge): the clamped floors
+                      // are k - 1 and k and the edge table picks one
+                      ++nb_slow;
+                      static_for<0, 2>([&](auto ec) {
+                        constexpr int ct = 2 * hp + decltype(ec)::value;
+                        constexpr int OFF = ((ct & 1) * NCO + b1) * TB;
+                        const char* B = base[ct >> 1] + po + OFF;
+                        const float4 hd = *reinterpret_cast<const float4*>(B);
+                        const float* th = reinterpret_cast<const float*>(B) + NbBlock::th_off(NB);
+                        const float* L = reinterpret_cast<const float*>(B) + NbBlock::lut_off(NB);
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) {  // recomputed: fa / fb are not kept live
-                      const float dd = __fsub_rn(vv[i], hd.x);
-                      const int ka = clamp_bits(__fmaf_rd(dd, hd.y, kMagic), NB - 1);
-                      const int kb = clamp_bits(__fmaf_rd(dd, hd.z, kMagic), NB - 1);
-                      if (ka != kb && vv[i] >= th[NbBlock::pad(kb)]) m[i] = L[kb];
+                        for (int i = 0; i < 4; ++i) {  // recomputed: fa / fb are not kept live
+                          const float dd = __fsub_rn(vv[i], hd.x);
+                          const int ka = clamp_bits(__fmaf_rd(dd, hd.y, kMagic), NB - 1);
+                          const int kb = clamp_bits(__fmaf_rd(dd, hd.z, kMagic), NB - 1);
+                          if (ka != kb && vv[i] >= th[NbBlock::pad(kb)]) m[ct & 1][i] = L[kb];
+                        }
+                      });
                     }
-                  }
-                  if constexpr (MORD) {  // fold the trailing pair, then one FMA per voxel
-                    if constexpr (ct == 0) {
+                    if constexpr (MORD) {  // fold the trailing pair, then one FMA per voxel
 #pragma unroll
-                      for (int i = 0; i < 4; ++i) m0[i] = m[i];
+                      for (int h = 0; h < 2; ++h) {
+                        const u64 in2 = fma2(pk2(m[1][2 * h], m[1][2 * h + 1]),
+                                             pk2(tw[2 * h][1 % NCT], tw[2 * h + 1][1 % NCT]),
+                                             mul2(pk2(tw[2 * h][0], tw[2 * h + 1][0]),
+                                                  pk2(m[0][2 * h], m[0][2 * h + 1])));
+                        a2[0][h] = fma2(in2, w2, a2[0][h]);
+                      }
                     } else {
 #pragma unroll
-                      for (int i = 0; i < 4; ++i)
-                        act[0][i] = fmaf(w, fmaf(tw[i][1], m[i], tw[i][0] * m0[i]), act[0][i]);
-                    }
-                  } else {
+                      for (int e = 0; e < 2; ++e)
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) act[ct][i] = fmaf(w, m[i], act[ct][i]);
-                  }
+                        for (int h = 0; h < 2; ++h)
+                          a2[2 * hp + e][h] = fma2(pk2(m[e][2 * h], m[e][2 * h + 1]), w2, a2[2 * hp + e][h]);
+                    }
+                  });
                 });
-              });
+              }
+            };
+            if (wrap_safe) run(std::integral_constant<bool, true>{});
+            else run(std::integral_constant<bool, false>{});
+#pragma unroll
+            for (int ct = 0; ct < NCT; ++ct) {
+              upk2(a2[ct][0], act[ct][0], act[ct][1]);
+              upk2(a2[ct][1], act[ct][2], act[ct][3]);
             }
           } else {  // a pathological range in the pencil: exact search where needed
 #pragma unroll
@@ -1295,6 +1357,10 @@ __global__ void __launch_bounds__(kBlendThreads, 1)
     __syncwarp();
     if (lane == 0) mbar_arrive(&P.pipe->empty[s]);
     ++it;
+    if (++cs_slot == G.nst) {
+      cs_slot = 0;
+      cs_phase ^= 1;
+    }
   }
 }
 

@@ -525,14 +525,18 @@ void push_unit(std::vector<int32_t>& units, std::vector<int64_t>& vox, const int
   }
 }
 
-// K2 histogram units handed out by an atomic counter (W.range[3], reset before
-// the pass) with 2^18-voxel units, global mode on volumes of >= 2^26 voxels
-// (Large 4D hist 2.18 -> 1.93 ms; adaptive 4D / 5D measured slower: 0.324 ->
-// 0.340 / 0.373 -> 0.385 ms, they keep the static voxel-balanced split);
+// K2 units (range and histogram passes) handed out by an atomic counter
+// (W.range[3], reset before each pass) on volumes of >= 2^26 voxels: 2^18-voxel
+// units in global mode (Large 4D hist 2.18 -> 1.93 ms), 2^17 in adaptive mode
+// (4D range + hist 0.564 -> 0.539 ms, 5D 0.601 -> 0.588; 2^16 / 2^18 slower:
+// more flushes / a longer tail).  The static voxel-balanced split left SMs
+// idle 18 % of the 4D histogram pass (ncu: active vs elapsed cycles) because
+// CTAs with the same voxel count finish at data-dependent times.
 // MCLAHE_STATIC_UNITS keeps the static split everywhere.
 bool k2_dynamic(const mclahe_plan_s& pl, int64_t local_voxels) {
   static const bool static_units = getenv("MCLAHE_STATIC_UNITS") != nullptr;
-  return !static_units && !pl.p.adaptive && local_voxels >= (int64_t{1} << 26);
+  (void)pl;
+  return !static_units && local_voxels >= (int64_t{1} << 26);
 }
 
 void build_units(mclahe_plan_s& pl) {
@@ -549,7 +553,9 @@ void build_units(mclahe_plan_s& pl) {
   // K2 units likewise (handed out by a counter on such volumes, k2_dynamic):
   // fewer per-unit histogram flushes
   static const int64_t k2_unit = getenv("MCLAHE_K2_UNIT") ? atoll(getenv("MCLAHE_K2_UNIT")) : 0;
-  const int64_t hist_target = k2_unit > 0 ? k2_unit : (k2_dynamic(pl, local) ? int64_t{1} << 18 : target);
+  const int64_t hist_target =
+      k2_unit > 0 ? k2_unit
+                  : (k2_dynamic(pl, local) ? (pl.p.adaptive ? int64_t{1} << 17 : int64_t{1} << 18) : target);
   for (int fam = 0; fam < 2; ++fam) {
     Pencil& pc = fam == 0 ? pl.hist : pl.interp;
     if (!pc.on) continue;
