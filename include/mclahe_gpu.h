@@ -193,6 +193,12 @@ int mclahe_debug_bin_index(int32_t dtype, const void* values_dev, int64_t n, dou
 int mclahe_plan_dict_state(mclahe_plan_t plan, const void* workspace, int32_t* state,
                            void* stream);
 
+/* Which kernels a plan runs (bit mask, after the plan's first pass on a
+ * device): 1 = fused pencil K2 (tile ranges and counts in one kernel, one read
+ * of the input from HBM; k_fused.cu), 2 = pencil histogram kernel, 4 = pencil
+ * blend, 8 = value dictionary armed, 16 = folded-pair blend armed. */
+int32_t mclahe_plan_flags(mclahe_plan_t plan);
+
 /* The pencil kernels' packed f32x2 binning on n device float32 values (pairs
  * of consecutive values): variant 1 = the histogram routine, 2 = the blend
  * gather (through an identity LUT), 3 = the bracketed floors of the

@@ -107,6 +107,7 @@ SIGNATURES = {
     "mclahe_metrics": (C.c_int, [C.c_int32, _vp, _vp, _vp, _i64, C.c_double, _vp]),
     "mclahe_metrics_device": (C.c_int, [C.c_int32, _vp, _vp, _vp, _i64, C.c_double, _vp, _vp]),
     "mclahe_plan_dict_state": (C.c_int, [_vp, _vp, C.POINTER(C.c_int32), _vp]),
+    "mclahe_plan_flags": (C.c_int32, [_vp]),
     "mclahe_debug_bin_index_packed": (C.c_int, [_vp, _i64, C.c_double, C.c_double, _i64,
                                                 C.c_int32, _vp, _vp]),
     "mclahe_launch_count": (C.c_int64, []),

@@ -211,6 +211,15 @@ class Plan:
     def check(self, ws, stream=None):
         N.check(N.lib().mclahe_plan_check(self._h, self._ptr(ws), _stream_handle(stream)))
 
+    @property
+    def flags(self) -> dict:
+        """Kernels the plan runs (valid once a pass has run on a device):
+        ``fused_k2`` (ranges + counts in one kernel, one HBM read), ``pencil_hist``,
+        ``pencil_blend``, ``dict`` (value dictionary armed), ``folded`` (folded-pair blend)."""
+        f = int(N.lib().mclahe_plan_flags(self._h))
+        return dict(fused_k2=bool(f & 1), pencil_hist=bool(f & 2), pencil_blend=bool(f & 4),
+                    dict=bool(f & 8), folded=bool(f & 16))
+
     def dict_state(self, ws, stream=None) -> dict:
         """Value-dictionary state after a run on ``ws``: ``used`` (the blend took
         the dictionary path), ``folded`` (through the folded-pair kernel

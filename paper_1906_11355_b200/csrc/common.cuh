@@ -149,6 +149,8 @@ struct WS {
   float* dvals;         // [kDictHG / 2] values by index
   uint2* dlt;           // [kDictHL] cuckoo lookup {bits, index}
   float* lutd;          // [win_tiles][kDictKC] LUT[bin(value)] per value
+  int32_t* k2g;         // fused K2: [groups] arrivals, then [groups] published flags
+  float* k2tab;         // fused K2: [groups] aligned table blocks (k_fused.cu ftab_bytes)
 };
 
 struct Debug {
@@ -244,6 +246,8 @@ struct Stage {
   int32_t cell[kMaxOuterDims];  // K4: cells of the unit (K2: tiles)
   TileParts p1, p2;             // K2: tile parts along dims KO-1 and KO-2
   int32_t tc[6];                // TMA box coordinates of the stage (K4 reuses them to store)
+  int32_t ph;                   // fused K2: 0 = range pass over the unit, 1 = counting pass
+  int32_t last;                 // fused K2: last box of the unit's pass
 };
 
 // Producer-private per-unit box (kept in shared memory, not registers, so
@@ -312,6 +316,44 @@ __device__ __forceinline__ void tma_load(void* dst, const CUtensorMap* map, int 
   }
 }
 
+// Same with an L2 cache-policy hint (createpolicy): the fused K2 keeps the
+// boxes of its range walk in L2 (evict_last) for the counting walk that
+// re-reads them, which then marks them evict_first.
+__device__ __forceinline__ void tma_load_hint(void* dst, const CUtensorMap* map, int rank,
+                                              const int* c, uint64_t* bar, uint64_t pol) {
+  const uint64_t m = reinterpret_cast<uint64_t>(map);
+  const uint32_t d = smem_u32(dst), b = smem_u32(bar);
+  switch (rank) {
+    case 2:
+      asm volatile(
+          "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+          " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(d), "l"(m), "r"(c[0]), "r"(c[1]), "r"(b), "l"(pol)
+          : "memory");
+      break;
+    case 3:
+      asm volatile(
+          "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+          " [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(d), "l"(m), "r"(c[0]), "r"(c[1]), "r"(c[2]),
+          "r"(b), "l"(pol)
+          : "memory");
+      break;
+    case 4:
+      asm volatile(
+          "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+          " [%0], [%1, {%2, %3, %4, %5}], [%6], %7;" ::"r"(d), "l"(m), "r"(c[0]), "r"(c[1]),
+          "r"(c[2]), "r"(c[3]), "r"(b), "l"(pol)
+          : "memory");
+      break;
+    default:
+      asm volatile(
+          "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+          " [%0], [%1, {%2, %3, %4, %5, %6}], [%7], %8;" ::"r"(d), "l"(m), "r"(c[0]), "r"(c[1]),
+          "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(b), "l"(pol)
+          : "memory");
+      break;
+  }
+}
+
 // TMA tensor store of one box from shared memory (bulk-group completion).
 __device__ __forceinline__ void tma_store(const CUtensorMap* map, int rank, const int* c,
                                           const void* src) {
@@ -352,6 +394,12 @@ __device__ __forceinline__ void tma_store_wait_all() {
 // Makes this thread's generic-proxy shared-memory writes visible to the TMA.
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ int ld_acquire_gpu(const int32_t* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
 }
 
 // Producer (one thread): walks the CTA's units box by box (the plan makes

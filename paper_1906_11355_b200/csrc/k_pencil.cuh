@@ -1372,6 +1372,11 @@ using PencilInterpFn = void (*)(const KGeom, const CUtensorMap, const CUtensorMa
                                 float*, const int32_t*, const int32_t*, WS);
 PencilRangeFn get_range_pencil(int ko, bool dict);
 PencilHistFn get_hist_pencil(int ko, bool adaptive);
+// fused adaptive K2 (k_fused.cu): ranges + counts in one kernel, one DRAM read
+PencilRangeFn get_k2_fused(int ko, bool dict);
+int k2_fused_threads();
+int64_t k2_fused_tail_bytes(int64_t gtr, int64_t n_bins, bool dict);
+int64_t k2_fused_tab_bytes(int64_t gtr, int64_t n_bins);
 PencilInterpFn get_interp_pencil(int ko, int kt, bool adaptive, int n_bins);
 PencilInterpFn get_interp_pencil_dict(int ko, int kt);
 // folded-pair blend; nullptr: none for this (ko, mode, n_bins)

@@ -154,6 +154,11 @@ struct mclahe_plan_s {
   // in one kernel for single-slab adaptive plans; shared_ws: a chunk plan of
   // the streamed call (workspace shared with the other chunks: combine, not store)
   bool fused_k2 = false, shared_ws = false;
+  // fused pencil K2 (k_fused.cu): single-slab float32 adaptive pencil plans;
+  // workspace [groups] arrival counters + [groups] published flags at off_k2g
+  bool fused_pencil = false, fused_try = false;
+  int64_t off_k2g = 0, off_k2tab = 0, k2_groups = 0, fused_smem = 0;
+  int fused_grid = 0, k2_group_units = 0;
   int tile_grid = 0;
   // batched framewise, global mode: tiles take their frame's range (-1: off)
   int frame_axis = -1;
@@ -553,8 +558,13 @@ void build_units(mclahe_plan_s& pl) {
   // K2 units likewise (handed out by a counter on such volumes, k2_dynamic):
   // fewer per-unit histogram flushes
   static const int64_t k2_unit = getenv("MCLAHE_K2_UNIT") ? atoll(getenv("MCLAHE_K2_UNIT")) : 0;
+  // fused K2: 2^14-voxel units (the bytes read between a box's two walks,
+  // ~2 units per CTA over every CTA, must stay in L2: 2^15 re-read 30 % from
+  // HBM, 2^16 and up nearly all of it)
+  static const int64_t fk2_unit = getenv("MCLAHE_FK2_UNIT") ? atoll(getenv("MCLAHE_FK2_UNIT")) : 0;
   const int64_t hist_target =
-      k2_unit > 0 ? k2_unit
+      pl.fused_try ? (fk2_unit > 0 ? fk2_unit : std::min<int64_t>(target, int64_t{1} << 14))
+      : k2_unit > 0 ? k2_unit
                   : (k2_dynamic(pl, local) ? (pl.p.adaptive ? int64_t{1} << 17 : int64_t{1} << 18) : target);
   for (int fam = 0; fam < 2; ++fam) {
     Pencil& pc = fam == 0 ? pl.hist : pl.interp;
@@ -691,6 +701,8 @@ int tensor_map(mclahe_plan_s* pl, int fam, const void* in) {
 // full_window: the workspace holds every tile row (chunks of a streamed
 // single-GPU run share one workspace); otherwise only the rows the slab
 // counts into or blends from.
+void plan_fused_pencil(mclahe_plan_s* pl, bool full_window);
+
 int plan_describe(const mclahe_params_t* params, int64_t row_begin, int64_t row_end,
                   mclahe_plan_s* pl, bool full_window = false) {
   int rc = validate(params);
@@ -764,6 +776,11 @@ int plan_describe(const mclahe_params_t* params, int64_t row_begin, int64_t row_
   I.fast_hist = pl->hist.on;
   I.fast_interp = pl->interp.on;
   I.trailing_dims = pl->interp.on ? pl->interp.kt : pl->hist.kt;
+  {  // the fused pencil K2 (plan_fused_pencil; opt-in, see k_fused.cu) wants small units
+    static const bool on = getenv("MCLAHE_FUSED_K2") != nullptr && atoi(getenv("MCLAHE_FUSED_K2")) != 0;
+    pl->fused_try = on && pl->hist.on && params->adaptive && pl->f32() && !full_window &&
+                    row_begin == 0 && row_end == params->shape[0];
+  }
   build_units(*pl);
   I.hist_units = (int64_t)pl->hist_vox.size();
   I.interp_units = (int64_t)pl->interp_vox.size();
@@ -772,9 +789,58 @@ int plan_describe(const mclahe_params_t* params, int64_t row_begin, int64_t row_
   if (!full_window) plan_dict(pl);
   if (!full_window) plan_mdict(pl);
   pl->shared_ws = full_window && (row_begin != 0 || row_end != params->shape[0]);
+  plan_fused_pencil(pl, full_window);
   pl->fused_k2 = !pl->hist.on && params->adaptive && !pl->f32() && !pl->shared_ws &&
                  row_begin == 0 && row_end == params->shape[0];
   return MCLAHE_OK;
+}
+
+// Arms the fused pencil K2 (k_fused.cu) for single-slab float32 adaptive plans:
+// numbers the tile groups (units sharing a key: one KO-outer tile, every
+// trailing tile) in the unit records ([6] group, [7] units in the group) and
+// appends the group counters to the workspace.  Every window tile must belong
+// to a group with at least one unit (the kernel writes every tile's binning
+// parameters).  Opt-in (MCLAHE_FUSED_K2=1): it halves the HBM reads of the
+// range + count passes but measured slower than the two passes (k_fused.cu).
+void plan_fused_pencil(mclahe_plan_s* pl, bool full_window) {
+  pl->fused_pencil = false;
+  if (!pl->fused_try) return;
+  (void)full_window;
+  const Pencil& c = pl->hist;
+  const int64_t groups = pl->G.win_tiles / c.gtr;
+  if (groups * c.gtr != pl->G.win_tiles || groups <= 0) return;
+  std::vector<int32_t>& U = pl->hist_units;
+  const int64_t nu = (int64_t)U.size() / kUnitInts;
+  std::vector<int32_t> per(groups, 0);
+  std::vector<int64_t> gid(nu);
+  for (int64_t u = 0; u < nu; ++u) {
+    const int32_t* r = &U[u * kUnitInts];
+    int64_t key = (r[0] - pl->G.trow0) * pl->G.tstride[0];
+    for (int j = 1; j < c.ko; ++j) key += (int64_t)r[j] * pl->G.tstride[j];
+    if (key % c.gtr != 0 || key / c.gtr >= groups || key < 0) return;
+    gid[u] = key / c.gtr;
+    if (u > 0 && gid[u] != gid[u - 1] && per[gid[u]] > 0) return;  // units of a group consecutive
+    ++per[gid[u]];
+  }
+  int mx = 0;
+  for (int64_t g = 0; g < groups; ++g) {
+    if (per[g] == 0) return;
+    mx = std::max(mx, per[g]);
+  }
+  if (c.ko > 5) return;  // record slots 6 / 7 hold the group
+  for (int64_t u = 0; u < nu; ++u) {
+    U[u * kUnitInts + 6] = (int32_t)gid[u];
+    U[u * kUnitInts + 7] = per[gid[u]];
+  }
+  pl->k2_groups = groups;
+  pl->k2_group_units = mx;
+  pl->off_k2g = align_up(pl->info.workspace_bytes, 256);
+  pl->off_k2tab = align_up(pl->off_k2g + 2 * groups * 4, 256);
+  pl->info.workspace_bytes =
+      align_up(pl->off_k2tab + groups * k2_fused_tab_bytes(c.gtr, pl->p.n_bins), 256);
+  pl->fused_smem = kPipeBytes + c.nst * c.stage_stride * 4 +
+                   k2_fused_tail_bytes(c.gtr, pl->p.n_bins, pl->dict_cap > 0);
+  pl->fused_pencil = true;
 }
 
 using RangeFn = PencilRangeFn;
@@ -801,6 +867,8 @@ WS ws_view(const mclahe_plan_s* pl, void* ws) {
   W.dvals = nullptr;
   W.dlt = nullptr;
   W.lutd = nullptr;
+  W.k2g = pl->fused_pencil ? reinterpret_cast<int32_t*>(b + pl->off_k2g) : nullptr;
+  W.k2tab = pl->fused_pencil ? reinterpret_cast<float*>(b + pl->off_k2tab) : nullptr;
   if (pl->dict_cap) {
     char* d = b + pl->off_dict;
     W.dmeta = reinterpret_cast<int32_t*>(d);
@@ -855,6 +923,15 @@ int device_init(mclahe_plan_s* pl) {
         1, std::min<int64_t>((int64_t)pl->hist_vox.size(), (int64_t)std::max(occ, 1) * pl->sms));
     pl->hist_dyn_grid = pl->hist_grid;
     hist_cta = balance(pl->hist_vox, pl->hist_grid);
+    if (pl->fused_pencil) {
+      RangeFn fk = get_k2_fused(pl->hist.ko, pl->dict_cap > 0);
+      int focc = 0;
+      MG_CUDA(raise_smem_cap(fk, max_smem));
+      MG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&focc, fk, k2_fused_threads(), pl->fused_smem));
+      pl->fused_grid = (int)std::min<int64_t>((int64_t)pl->hist_vox.size(), (int64_t)focc * pl->sms);
+      // a group's units wait for each other: they must all be able to run
+      if (focc < 1 || pl->fused_grid < pl->k2_group_units) pl->fused_pencil = false;
+    }
   }
   if (pl->interp.on) {
     int occ = 0;
@@ -959,6 +1036,23 @@ int do_range(mclahe_plan_s* pl, const void* in, void* ws, cudaStream_t st) {
     MG_LAUNCHED();
     return MCLAHE_OK;
   }
+  if (pl->fused_pencil) {  // ranges + counts, one DRAM read (k_fused.cu)
+    KGeom G = pencil_geom(*pl, pl->hist);
+    G.dyn_units = (int)pl->hist_vox.size();
+    MG_CUDA(cudaMemsetAsync(W.range + 3, 0, sizeof(int64_t), st));
+    MG_CUDA(cudaMemsetAsync(W.k2g, 0, (size_t)pl->k2_groups * 8, st));
+    int rc = tensor_map(pl, 0, in);
+    if (rc) return rc;
+    get_k2_fused(pl->hist.ko, pl->dict_cap > 0)<<<pl->fused_grid, k2_fused_threads(), pl->fused_smem, st>>>(
+        G, pl->map[0], static_cast<const float*>(in), pl->d_tables + pl->off_hist_units,
+        pl->d_tables + pl->off_hist_cta, W);
+    MG_LAUNCHED();
+    if (pl->dict_cap) {
+      k_dict_finalize<<<1, 1024, 0, st>>>(W, pl->dict_cap);
+      MG_LAUNCHED();
+    }
+    return MCLAHE_OK;
+  }
   if (pl->hist.on) {
     KGeom G = pencil_geom(*pl, pl->hist);
     G.dyn_units = k2_dynamic(*pl, pl->G.local_voxels) ? (int)pl->hist_vox.size() : 0;
@@ -987,6 +1081,7 @@ int do_range(mclahe_plan_s* pl, const void* in, void* ws, cudaStream_t st) {
 // nt < 0: the whole window) or the global range.
 int do_params(mclahe_plan_s* pl, void* ws, cudaStream_t st, int64_t t0 = 0, int64_t nt = -1) {
   WS W = ws_view(pl, ws);
+  if (pl->fused_pencil) return MCLAHE_OK;  // built by the fused K2 kernel
   if (nt < 0) nt = pl->G.win_tiles - t0;
   if (pl->p.adaptive && nt <= 0) return MCLAHE_OK;
   const int64_t n = pl->p.adaptive ? nt : 1;
@@ -1006,6 +1101,7 @@ int do_params(mclahe_plan_s* pl, void* ws, cudaStream_t st, int64_t t0 = 0, int6
 int do_hist(mclahe_plan_s* pl, const void* in, void* ws, cudaStream_t st) {
   WS W = ws_view(pl, ws);
   const bool A = pl->p.adaptive != 0;
+  if (pl->fused_pencil) return MCLAHE_OK;  // counted by the fused range pass
   if (pl->hist.on) {
     KGeom G = pencil_geom(*pl, pl->hist);
     G.dyn_units = k2_dynamic(*pl, pl->G.local_voxels) ? (int)pl->hist_vox.size() : 0;
@@ -1388,6 +1484,7 @@ mclahe_plan_s* cached_plan(OneShot& o, const mclahe_params_t* p, int* rc, int fr
     // the frame range pass sets the tiles' ranges; the counts come from the
     // histogram pass (no fused tile-major range + counts)
     pl->fused_k2 = false;
+    pl->fused_pencil = false;
     pl->off_frange = align_up(pl->info.workspace_bytes, 256);
     pl->info.workspace_bytes = align_up(pl->off_frange + q.shape[frame_axis] * 16, 256);
   }
@@ -2113,6 +2210,12 @@ int mclahe_debug_bin_index(int32_t dtype, const void* values, int64_t n, double 
     MG_LAUNCHED();
   }
   return MCLAHE_OK;
+}
+
+int32_t mclahe_plan_flags(mclahe_plan_t plan) {
+  if (!plan) return 0;
+  return (plan->fused_pencil ? 1 : 0) | (plan->hist.on ? 2 : 0) | (plan->interp.on ? 4 : 0) |
+         (plan->dict_cap ? 8 : 0) | (plan->mdict ? 16 : 0);
 }
 
 int mclahe_plan_dict_state(mclahe_plan_t plan, const void* workspace, int32_t* state,

@@ -113,6 +113,9 @@ def test_scaled_configs_vs_oracle(M, name):
     args = (c["kernel"], c["n_bins"], c["clip_limit"], c["adaptive"])
     st, plan = gpu_stats(M, x, *args)
     assert plan.info.fast_hist and plan.info.fast_interp, "pencil kernels expected"
+    # adaptive float32 single-slab plans count from the fused K2 kernel (k_fused.cu)
+    # when it is switched on (opt-in: tests/test_fused_k2.py runs this file so)
+    assert plan.flags["fused_k2"] == (c["adaptive"] and os.environ.get("MCLAHE_FUSED_K2") == "1")
     assert_stats_equal(st, O.tile_stats(x, *args, "c"), name)
     out = M.enhance(x, *args)
     want = O.mclahe(x, *args, "c")

@@ -21,7 +21,7 @@ def N():
 
 def test_exports_every_declared_symbol(N):
     hdr = open(os.path.join(ROOT, "include", "mclahe_gpu.h")).read()
-    declared = set(re.findall(r"^\s*(?:int|int64_t|const char\*|void\*|void)\s+(mclahe_\w+)\(",
+    declared = set(re.findall(r"^\s*(?:int|int32_t|int64_t|const char\*|void\*|void)\s+(mclahe_\w+)\(",
                               hdr, re.M))
     assert len(declared) >= 15
     L = N.lib()
