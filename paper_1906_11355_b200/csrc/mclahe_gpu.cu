@@ -2,6 +2,7 @@
 // validation, slab planning (tile windows, pencil units, CTA balancing),
 // pass launches and the one-shot drop-in.  Kernels live in kernels.cuh.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <atomic>
@@ -62,6 +63,16 @@ int cuda_fail(cudaError_t e, const char* where) {
 #define MG_LAUNCHED() MG_LAUNCHED_AT(__func__)
 
 int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+// NVTX range over one host-side pass / call (header-only NVTX v3: free unless
+// a profiler is attached), so an nsys / ncu timeline shows which pass a
+// kernel launch belongs to (mclahe.range, mclahe.histograms, ...).
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 }  // namespace
 
@@ -990,6 +1001,7 @@ int generic_grid(const mclahe_plan_s* pl) {
 }
 
 int do_reset(mclahe_plan_s* pl, void* ws, cudaStream_t st) {
+  NvtxRange nvtx("mclahe.reset");
   WS W = ws_view(pl, ws);
   const int64_t ntr = pl->p.adaptive ? pl->G.win_tiles * 2 : 0;
   MG_CUDA(cudaMemsetAsync(W.counts, 0, (size_t)pl->G.win_tiles * pl->p.n_bins * 4, st));
@@ -1001,6 +1013,7 @@ int do_reset(mclahe_plan_s* pl, void* ws, cudaStream_t st) {
 }
 
 int do_range(mclahe_plan_s* pl, const void* in, void* ws, cudaStream_t st) {
+  NvtxRange nvtx("mclahe.range");
   WS W = ws_view(pl, ws);
   if (pl->frame_axis >= 0) {  // framewise global mode: per-frame ranges
     const int ax = pl->frame_axis;
@@ -1080,6 +1093,7 @@ int do_range(mclahe_plan_s* pl, const void* in, void* ws, cudaStream_t st) {
 // Binning parameters + edge tables for window tiles [t0, t0 + nt) (adaptive;
 // nt < 0: the whole window) or the global range.
 int do_params(mclahe_plan_s* pl, void* ws, cudaStream_t st, int64_t t0 = 0, int64_t nt = -1) {
+  NvtxRange nvtx("mclahe.params");
   WS W = ws_view(pl, ws);
   if (pl->fused_pencil) return MCLAHE_OK;  // built by the fused K2 kernel
   if (nt < 0) nt = pl->G.win_tiles - t0;
@@ -1099,6 +1113,7 @@ int do_params(mclahe_plan_s* pl, void* ws, cudaStream_t st, int64_t t0 = 0, int6
 }
 
 int do_hist(mclahe_plan_s* pl, const void* in, void* ws, cudaStream_t st) {
+  NvtxRange nvtx("mclahe.histograms");
   WS W = ws_view(pl, ws);
   const bool A = pl->p.adaptive != 0;
   if (pl->fused_pencil) return MCLAHE_OK;  // counted by the fused range pass
@@ -1125,6 +1140,7 @@ int do_hist(mclahe_plan_s* pl, const void* in, void* ws, cudaStream_t st) {
 // Mappings of window tiles [t0, t0 + nt) (nt < 0: the whole window).
 int do_map(mclahe_plan_s* pl, void* ws, const mclahe_debug_t* dbg, cudaStream_t st,
            int64_t t0 = 0, int64_t nt = -1) {
+  NvtxRange nvtx("mclahe.mappings");
   if (nt < 0) nt = pl->G.win_tiles - t0;
   if (nt <= 0) return MCLAHE_OK;
   WS W = ws_view(pl, ws);
@@ -1157,6 +1173,7 @@ int do_map(mclahe_plan_s* pl, void* ws, const mclahe_debug_t* dbg, cudaStream_t 
 }
 
 int do_interp(mclahe_plan_s* pl, const void* in, void* out, void* ws, cudaStream_t st) {
+  NvtxRange nvtx("mclahe.interpolate");
   if (getenv("MCLAHE_DEBUG"))
     fprintf(stderr, "[mclahe] do_interp pencil=%d pending=%s\n", (int)pl->interp.on,
             cudaGetErrorString(cudaPeekAtLastError()));
@@ -2039,6 +2056,7 @@ int mclahe_plan_check(mclahe_plan_t plan, const void* ws, void* stream) {
 
 int mclahe_gpu_run_device(const mclahe_params_t* params, const void* in, void* out, void* stream,
                           mclahe_timings_t* timings) {
+  NvtxRange nvtx("mclahe_gpu_run_device");
   int rc = validate(params);
   if (rc) return rc;
   OneShot& o = oneshot();
@@ -2063,6 +2081,7 @@ int mclahe_gpu_run_device(const mclahe_params_t* params, const void* in, void* o
 
 int mclahe_gpu_run(const mclahe_params_t* params, const void* in, void* out,
                    mclahe_timings_t* timings) {
+  NvtxRange nvtx("mclahe_gpu_run");
   int rc = validate(params);
   if (rc) return rc;
   if (!in || !out) return fail(MCLAHE_ERR_VALIDATION, "null host buffer");
@@ -2104,6 +2123,7 @@ int mclahe_gpu_run(const mclahe_params_t* params, const void* in, void* out,
 
 int mclahe_gpu_run_framewise(const mclahe_params_t* params, int32_t frame_axis, const void* in,
                              void* out, mclahe_timings_t* timings) {
+  NvtxRange nvtx("mclahe_gpu_run_framewise");
   if (!params) return fail(MCLAHE_ERR_VALIDATION, "null params");
   const int D = params->rank;
   if (D < 2) return fail(MCLAHE_ERR_VALIDATION, "framewise mode needs rank >= 2");
@@ -2161,6 +2181,7 @@ int mclahe_multi_cuts(const mclahe_params_t* params, int32_t n_slabs, int64_t* c
 
 int mclahe_gpu_run_multi(const mclahe_params_t* params, int32_t n_slabs, const int32_t* devices,
                          const void* host_in, void* host_out, mclahe_timings_t* timings) {
+  NvtxRange nvtx("mclahe_gpu_run_multi");
   if (!host_in || !host_out) return fail(MCLAHE_ERR_VALIDATION, "null host buffer");
   std::lock_guard<std::mutex> lock(g_multi_mu);
   int cur = 0;
