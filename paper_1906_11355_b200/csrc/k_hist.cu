@@ -19,19 +19,20 @@ PencilRangeFn get_range_pencil(int ko, bool dict) {
   return dict ? range_t<true>(ko) : range_t<false>(ko);
 }
 
-template <bool A>
+template <bool A, bool MATCH>
 static PencilHistFn hist_t(int ko) {
   switch (ko) {
-    case 1: return k_hist_pencil<1, A>;
-    case 2: return k_hist_pencil<2, A>;
-    case 3: return k_hist_pencil<3, A>;
-    case 4: return k_hist_pencil<4, A>;
-    default: return k_hist_pencil<5, A>;
+    case 1: return k_hist_pencil<1, A, MATCH>;
+    case 2: return k_hist_pencil<2, A, MATCH>;
+    case 3: return k_hist_pencil<3, A, MATCH>;
+    case 4: return k_hist_pencil<4, A, MATCH>;
+    default: return k_hist_pencil<5, A, MATCH>;
   }
 }
 
-PencilHistFn get_hist_pencil(int ko, bool adaptive) {
-  return adaptive ? hist_t<true>(ko) : hist_t<false>(ko);
+PencilHistFn get_hist_pencil(int ko, bool adaptive, bool match) {
+  if (match) return adaptive ? hist_t<true, true>(ko) : hist_t<false, true>(ko);
+  return adaptive ? hist_t<true, false>(ko) : hist_t<false, false>(ko);
 }
 
 }  // namespace mg

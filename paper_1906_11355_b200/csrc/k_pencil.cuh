@@ -296,7 +296,11 @@ __device__ __forceinline__ void copy_rows(float* dst, const float* __restrict__ 
 // kernelize + compute_histogram while reading each input byte once.  A
 // thread's equal neighbouring (tile, bin) keys merge: one shared add carries
 // the whole run.
-template <int KO, bool ADAPT>
+// MATCH: warp-aggregated shared atomics (north_star's __match_any_sync): the
+// lanes holding the same histogram word elect one lane that adds the group's
+// sum (MATCH.ANY + REDUX per voxel slot) -- an A/B against the plain run-merged
+// adds (MCLAHE_K2_MATCH=1).
+template <int KO, bool ADAPT, bool MATCH>
 __global__ void __launch_bounds__(kPencilThreads, 3)
     k_hist_pencil(const __grid_constant__ KGeom G, const __grid_constant__ CUtensorMap tmap,
                   const float* __restrict__ in, const int32_t* __restrict__ units,
@@ -433,10 +437,24 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
         const uint32_t s2 = w[2] + (e23 ? s3 : 0u);
         const uint32_t s1 = w[1] + (e12 ? s2 : 0u);
         const uint32_t s0 = w[0] + (e01 ? s1 : 0u);
-        red_add(a[0], s0);
-        red_add(e01 ? dummy_s : a[1], s1);
-        red_add(e12 ? dummy_s : a[2], s2);
-        red_add(e23 ? dummy_s : a[3], s3);
+        if constexpr (MATCH) {
+          const uint32_t ad[4] = {a[0], e01 ? dummy_s : a[1], e12 ? dummy_s : a[2],
+                                  e23 ? dummy_s : a[3]};
+          const uint32_t sv[4] = {s0, s1, s2, s3};
+          const unsigned act = __activemask();
+          const int lane = threadIdx.x & 31;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const unsigned grp = __match_any_sync(act, ad[i]);
+            const uint32_t tot = __reduce_add_sync(grp, sv[i]);
+            if (__ffs(grp) - 1 == lane) red_add(ad[i], tot);
+          }
+        } else {
+          red_add(a[0], s0);
+          red_add(e01 ? dummy_s : a[1], s1);
+          red_add(e12 ? dummy_s : a[2], s2);
+          red_add(e23 ? dummy_s : a[3], s3);
+        }
       };
       // histogram words via the edge table (k = rint of the f32 estimate, th
       // decides k or k - 1)
@@ -1371,7 +1389,7 @@ using PencilHistFn = PencilRangeFn;
 using PencilInterpFn = void (*)(const KGeom, const CUtensorMap, const CUtensorMap, const float*,
                                 float*, const int32_t*, const int32_t*, WS);
 PencilRangeFn get_range_pencil(int ko, bool dict);
-PencilHistFn get_hist_pencil(int ko, bool adaptive);
+PencilHistFn get_hist_pencil(int ko, bool adaptive, bool match = false);
 // fused adaptive K2 (k_fused.cu): ranges + counts in one kernel, one DRAM read
 PencilRangeFn get_k2_fused(int ko, bool dict);
 int k2_fused_threads();

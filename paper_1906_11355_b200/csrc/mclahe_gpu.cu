@@ -858,7 +858,11 @@ using RangeFn = PencilRangeFn;
 using HistFn = PencilHistFn;
 using InterpFn = PencilInterpFn;
 RangeFn range_fn(int ko, bool dict) { return get_range_pencil(ko, dict); }
-HistFn hist_fn(int ko, bool a) { return get_hist_pencil(ko, a); }
+// MCLAHE_K2_MATCH=1: the warp-aggregated (__match_any_sync) histogram adds (A/B).
+HistFn hist_fn(int ko, bool a) {
+  static const bool match = getenv("MCLAHE_K2_MATCH") && atoi(getenv("MCLAHE_K2_MATCH")) != 0;
+  return get_hist_pencil(ko, a, match);
+}
 // MCLAHE_NO_NB=1 forces the runtime-n_bins blend kernel (A/B measurements).
 InterpFn interp_fn(int ko, int kt, bool a, int64_t n_bins) {
   return get_interp_pencil(ko, kt, a, nb_specialised(n_bins) ? (int)n_bins : 0);

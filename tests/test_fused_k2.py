@@ -69,3 +69,14 @@ def test_full_size_4d_bit_identical_to_two_pass(tmp_path):
     b = _run(tmp_path, False, 1)
     for k in ("lo", "hi", "counts", "clipped", "lut", "degenerate", "out"):
         assert np.array_equal(a[k], b[k]), k
+
+
+def test_parity_with_match_any_histograms():
+    """The __match_any_sync warp-aggregated K2b (MCLAHE_K2_MATCH=1, an A/B kept
+    for the record: 17x slower) counts exactly like the run-merged adds."""
+    env = dict(os.environ)
+    env["MCLAHE_K2_MATCH"] = "1"
+    r = subprocess.run([sys.executable, "-m", "pytest", "tests/test_gpu_parity.py", "-m", "gpu", "-x", "-q",
+                        "-k", "golden or random or scaled"],
+                       cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]

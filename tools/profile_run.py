@@ -13,13 +13,16 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="4d")
     ap.add_argument("--iters", type=int, default=2)
+    ap.add_argument("--f64", action="store_true", help="float64 volume (the f64 kernels)")
     a = ap.parse_args()
     import torch
     import paper_1906_11355_b200 as M
     from paper_1906_11355_b200 import datasets
     c = datasets.CONFIGS[a.config]
     x = datasets.make(a.config, seed=0, device="cuda")
-    plan = M.Plan(x.shape, c["kernel"], c["n_bins"], c["clip_limit"], c["adaptive"])
+    if a.f64:
+        x = x.double()
+    plan = M.Plan(x.shape, c["kernel"], c["n_bins"], c["clip_limit"], c["adaptive"], 1 if a.f64 else 0)
     ws = plan.new_workspace()
     out = torch.empty_like(x)
     for _ in range(a.iters):
