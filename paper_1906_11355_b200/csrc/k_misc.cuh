@@ -168,19 +168,24 @@ __global__ void __launch_bounds__(1024) k_dict_finalize(WS W, int cap) {
 
 // lutd[t][i] = LUT_t[bin_t(value_i)] with the reference bin rule in f64
 // (degenerate tiles: any bin, their LUT is constant).  Grid: tiles x values.
+// The reference bin of every dictionary value in every tile through the
+// guarded f32 rule and the tile's edge table (bin_of: exact, one f32 estimate
+// and at most one table load instead of an f64 divide per entry: 17 -> 15 us
+// on the 4D volume; a CTA per tile with its rows staged measured 26 us).
 template <typename T>
 __global__ void k_dict_luts(WS W, int64_t win_tiles, int n) {
   if (W.dmeta[2] == 0) return;
   const int K = W.dmeta[3];
   const TileParam<T>* tp = reinterpret_cast<const TileParam<T>*>(W.tparams);
+  const T nm05 = (T)n - (T)0.5;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < win_tiles * kDictKC;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t t = e / kDictKC;
     const int i = (int)(e - t * kDictKC);
     float r = 0.0f;
     if (i < K) {
-      const double lo = (double)tp[t].lo, hi = (double)tp[t].hi;
-      const int b = lo < hi ? bin_exact((double)W.dvals[i], lo, hi, n) : 0;
+      const TileParam<T> p = tp[t];
+      const int b = tp_degenerate(p.lim) ? 0 : bin_of((T)W.dvals[i], p, W.thr + t * (n + 1), n, nm05);
       r = W.lut[t * n + b];
     }
     W.lutd[e] = r;

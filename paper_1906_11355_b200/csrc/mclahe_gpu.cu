@@ -1169,6 +1169,7 @@ int do_map(mclahe_plan_s* pl, void* ws, const mclahe_debug_t* dbg, cudaStream_t 
     Wt.tparams = static_cast<char*>(W.tparams) + t0 * (int64_t)sizeof(TileParam<float>);
     Wt.lut = W.lut + t0 * pl->p.n_bins;
     Wt.lutd = W.lutd + t0 * kDictKC;
+    Wt.thr = W.thr + t0 * (pl->p.n_bins + 1);
     const int g = (int)std::min<int64_t>((nt * kDictKC + 255) / 256, (int64_t)pl->sms * 16);
     k_dict_luts<float><<<g, 256, 0, st>>>(Wt, nt, (int)pl->p.n_bins);
     MG_LAUNCHED();
