@@ -19,20 +19,21 @@ PencilRangeFn get_range_pencil(int ko, bool dict) {
   return dict ? range_t<true>(ko) : range_t<false>(ko);
 }
 
-template <bool A, bool MATCH>
+template <bool A, bool MATCH, bool CARRY>
 static PencilHistFn hist_t(int ko) {
   switch (ko) {
-    case 1: return k_hist_pencil<1, A, MATCH>;
-    case 2: return k_hist_pencil<2, A, MATCH>;
-    case 3: return k_hist_pencil<3, A, MATCH>;
-    case 4: return k_hist_pencil<4, A, MATCH>;
-    default: return k_hist_pencil<5, A, MATCH>;
+    case 1: return k_hist_pencil<1, A, MATCH, CARRY>;
+    case 2: return k_hist_pencil<2, A, MATCH, CARRY>;
+    case 3: return k_hist_pencil<3, A, MATCH, CARRY>;
+    case 4: return k_hist_pencil<4, A, MATCH, CARRY>;
+    default: return k_hist_pencil<5, A, MATCH, CARRY>;
   }
 }
 
-PencilHistFn get_hist_pencil(int ko, bool adaptive, bool match) {
-  if (match) return adaptive ? hist_t<true, true>(ko) : hist_t<false, true>(ko);
-  return adaptive ? hist_t<true, false>(ko) : hist_t<false, false>(ko);
+PencilHistFn get_hist_pencil(int ko, bool adaptive, int variant) {
+  if (variant == 1) return adaptive ? hist_t<true, true, false>(ko) : hist_t<false, true, false>(ko);
+  if (variant == 2) return adaptive ? hist_t<true, false, true>(ko) : hist_t<false, false, true>(ko);
+  return adaptive ? hist_t<true, false, false>(ko) : hist_t<false, false, false>(ko);
 }
 
 }  // namespace mg

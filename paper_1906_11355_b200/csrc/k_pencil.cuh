@@ -300,7 +300,11 @@ __device__ __forceinline__ void copy_rows(float* dst, const float* __restrict__ 
 // lanes holding the same histogram word elect one lane that adds the group's
 // sum (MATCH.ANY + REDUX per voxel slot) -- an A/B against the plain run-merged
 // adds (MCLAHE_K2_MATCH=1).
-template <int KO, bool ADAPT, bool MATCH>
+// CARRY: the run a thread ends a row with is carried into its next row (the
+// rows of a thread are rpi apart; on flat data they keep landing in the same
+// bin), so a same-word add is only issued when the run breaks -- fewer
+// same-address shared atomics from the 4 rows a warp holds.
+template <int KO, bool ADAPT, bool MATCH, bool CARRY = false>
 __global__ void __launch_bounds__(kPencilThreads, 3)
     k_hist_pencil(const __grid_constant__ KGeom G, const __grid_constant__ CUtensorMap tmap,
                   const float* __restrict__ in, const int32_t* __restrict__ units,
@@ -472,14 +476,30 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
       };
       // adaptive mode keeps the edge table only: per-voxel tile constants leave
       // no registers for the bracketed floors (spills: 4D 0.33 -> 0.45 ms)
+      // carried run (CARRY): address and sum of the last run of the previous row
+      uint32_t ca = dummy_s, cs = 0;
+      auto commit_carry = [&](const uint32_t (&a)[4]) {
+        const bool c0 = a[0] == ca, e01 = a[1] == a[0], e12 = a[2] == a[1], e23 = a[3] == a[2];
+        red_add(c0 ? dummy_s : ca, cs);  // the carried run ends unless a[0] continues it
+        const uint32_t r0 = w[0] + (c0 ? cs : 0u);
+        red_add(e01 ? dummy_s : a[0], r0);
+        const uint32_t r1 = w[1] + (e01 ? r0 : 0u);
+        red_add(e12 ? dummy_s : a[1], r1);
+        const uint32_t r2 = w[2] + (e12 ? r1 : 0u);
+        red_add(e23 ? dummy_s : a[2], r2);
+        cs = w[3] + (e23 ? r2 : 0u);
+        ca = a[3];
+      };
       if (ADAPT || k2_edges) {
 #pragma unroll 4
         for (int k = 0; k < trips; ++k, rp += rstep) {
           const float4 v = *reinterpret_cast<const float4*>(rp);
           uint32_t a[4];
           edge_addrs(v, a);
-          commit(a);
+          if constexpr (CARRY) commit_carry(a);
+          else commit(a);
         }
+        if constexpr (CARRY) red_add(ca, cs);
         if (!ADAPT && G.nb_edges < 0 && ++k2_probe >= 64) k2_edges = k2_probe = 0;
       } else if constexpr (!ADAPT) {
         // bracketed floors (binning.cuh: bin_window): a voxel of the tile's
@@ -514,8 +534,10 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
             ++nslow;
             edge_addrs(v, a);
           }
-          commit(a);
+          if constexpr (CARRY) commit_carry(a);
+          else commit(a);
         }
+        if constexpr (CARRY) red_add(ca, cs);
         if (G.nb_edges < 0 && 4 * nslow > trips) {  // edges decide most rows: edge mode
           k2_edges = 1;
           k2_probe = 0;
@@ -1389,7 +1411,7 @@ using PencilHistFn = PencilRangeFn;
 using PencilInterpFn = void (*)(const KGeom, const CUtensorMap, const CUtensorMap, const float*,
                                 float*, const int32_t*, const int32_t*, WS);
 PencilRangeFn get_range_pencil(int ko, bool dict);
-PencilHistFn get_hist_pencil(int ko, bool adaptive, bool match = false);
+PencilHistFn get_hist_pencil(int ko, bool adaptive, int variant = 0);  // 1 match, 2 carry
 // fused adaptive K2 (k_fused.cu): ranges + counts in one kernel, one DRAM read
 PencilRangeFn get_k2_fused(int ko, bool dict);
 int k2_fused_threads();

@@ -859,9 +859,15 @@ using HistFn = PencilHistFn;
 using InterpFn = PencilInterpFn;
 RangeFn range_fn(int ko, bool dict) { return get_range_pencil(ko, dict); }
 // MCLAHE_K2_MATCH=1: the warp-aggregated (__match_any_sync) histogram adds (A/B).
+// Runs carried across a thread's rows (k_hist_pencil CARRY) in global mode:
+// Large 4D hist 1.93 -> 1.80 ms; adaptive 4D / 5D unchanged (0.307 / 0.311,
+// 0.375 / 0.377 ms), so they keep the per-row merge.  MCLAHE_K2_CARRY=0/1
+// forces either (A/B).
 HistFn hist_fn(int ko, bool a) {
   static const bool match = getenv("MCLAHE_K2_MATCH") && atoi(getenv("MCLAHE_K2_MATCH")) != 0;
-  return get_hist_pencil(ko, a, match);
+  static const int carry_env = getenv("MCLAHE_K2_CARRY") ? atoi(getenv("MCLAHE_K2_CARRY")) : -1;
+  const bool carry = carry_env < 0 ? !a : carry_env != 0;
+  return get_hist_pencil(ko, a, match ? 1 : carry ? 2 : 0);
 }
 // MCLAHE_NO_NB=1 forces the runtime-n_bins blend kernel (A/B measurements).
 InterpFn interp_fn(int ko, int kt, bool a, int64_t n_bins) {

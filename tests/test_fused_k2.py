@@ -80,3 +80,14 @@ def test_parity_with_match_any_histograms():
                         "-k", "golden or random or scaled"],
                        cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+def test_parity_with_carried_runs_in_adaptive_mode():
+    """The carried-run K2b (default in global mode) forced on in adaptive mode
+    too (MCLAHE_K2_CARRY=1) counts exactly like the per-row merge."""
+    env = dict(os.environ)
+    env["MCLAHE_K2_CARRY"] = "1"
+    r = subprocess.run([sys.executable, "-m", "pytest", "tests/test_gpu_parity.py", "-m", "gpu", "-x", "-q",
+                        "-k", "golden or random or scaled or adversarial"],
+                       cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
