@@ -224,11 +224,13 @@ class Plan:
         """Value-dictionary state after a run on ``ws``: ``used`` (the blend took
         the dictionary path), ``folded`` (through the folded-pair kernel
         k_interp_mdict), ``values`` (distinct values collected), ``capacity``
-        (0 when the plan never arms it), ``affine`` (direct-table lookup)."""
+        (0 when the plan never arms it), ``affine`` (affine-cell lookup), ``direct``
+        (the affine cell is the value's index: values numbered by cell)."""
         st = (C.c_int32 * 4)()
         N.check(N.lib().mclahe_plan_dict_state(self._h, self._ptr(ws), st, _stream_handle(stream)))
         return dict(used=st[0] == 1 or (st[0] == 2 and st[2] > 0), folded=st[0] == 2,
-                    values=int(st[1]), capacity=int(st[2]), affine=bool(st[3]))
+                    values=int(st[1]), capacity=int(st[2]), affine=bool(st[3]),
+                    direct=st[3] == 2)
 
     def tile_stats(self, x, stream=None) -> dict:
         """Runs passes 1-3 and returns the per-tile intermediates of the

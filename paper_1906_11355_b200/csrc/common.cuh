@@ -90,12 +90,13 @@ constexpr int kDictLgBS = 10;        // K2a per-CTA set: 1024 buckets (16 KB)
 constexpr int kDictHS = 4 << kDictLgBS;
 constexpr int kDictLgHL = 10;        // blend lookup: 1024 {bits, index} (affine direct table or cuckoo hash)
 constexpr int kDictHL = 1 << kDictLgHL;
-constexpr int kDictKC = 576;         // values per tile row in the blend (capacity)
+constexpr int kDictKC = 608;         // values (or direct cells) per tile row in the blend (capacity)
 constexpr uint32_t kDictEmpty = 0xFFFFFFFFu;  // a NaN pattern: never a finite input
 __host__ __device__ __forceinline__ uint32_t dict_hash(uint32_t b, int lg) {
   return (b * 0x9E3779B1u) >> (32 - lg);
 }
 // meta[0]: values inserted, [1]: overflow, [2]: dictionary usable, [3]: K
+// (index slots), [7]: distinct values numbered
 
 // Cuckoo lookup: a value sits at one of two slots (branch-free, two LDS.64);
 // -1 when absent.
@@ -110,10 +111,14 @@ __device__ __forceinline__ int dict_lookup(const uint2* t, uint32_t b) {
   return e1.x == b ? (int)e1.y : e2.x == b ? (int)e2.y : -1;
 }
 
-// meta[4]: 1 = affine lookup (meta[5] = bits of v0, meta[6] = bits of S), 0 = cuckoo.
+// meta[4]: 1 = affine lookup (meta[5] = bits of v0, meta[6] = bits of S), 0 = cuckoo,
+// 2 = direct cells: the affine cell IS the index (values numbered by cell,
+// holes hold kDictEmpty), so the folded-pair blend gathers by cell after one
+// 32-bit check of the value's bits instead of an LDS.64 {bits, index} lookup.
 // Affine cells of two values (packed, as the blend computes them), clamped to
-// the table; the second value's cell goes to *c1 when c1 != nullptr.
+// [0, LIM]; the second value's cell goes to *c1 when c1 != nullptr.
 #ifdef __CUDACC__
+template <uint32_t LIM = kDictHL - 1>
 __device__ __forceinline__ int dict_cell(float a, float b, float v0, float S, int* c1) {
   unsigned long long V, D, Y, T;
   asm("mov.b64 %0, {%1, %2};" : "=l"(V) : "f"(a), "f"(b));
@@ -128,7 +133,7 @@ __device__ __forceinline__ int dict_cell(float a, float b, float v0, float S, in
   // one unsigned min (VIADDMNMX): values below v0 wrap to huge and land on the
   // last cell, which the caller's bit comparison rejects like any other miss
   auto cl = [](float t) {
-    return (int)min((uint32_t)__float_as_int(t) - 0x4B400000u, (uint32_t)(kDictHL - 1));
+    return (int)min((uint32_t)__float_as_int(t) - 0x4B400000u, LIM);
   };
   if (c1) *c1 = cl(t1);
   return cl(t0);

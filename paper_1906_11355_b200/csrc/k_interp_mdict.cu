@@ -86,7 +86,13 @@ __global__ void __launch_bounds__(NWARP * 32 + 32, 1)
     }
   }
   if (ADAPT) {
-    for (int k = tid; k < kDictHL; k += kMdictConsumers) dltS[k] = W.dlt[k];
+    if (W.dmeta[4] == 2) {  // direct cells: the values' bits by cell (holes never match)
+      uint32_t* bitsS = reinterpret_cast<uint32_t*>(dltS);
+      for (int k = tid; k < KC; k += kMdictConsumers)
+        bitsS[k] = k < W.dmeta[3] ? __float_as_uint(W.dvals[k]) : kDictEmpty;
+    } else {
+      for (int k = tid; k < kDictHL; k += kMdictConsumers) dltS[k] = W.dlt[k];
+    }
     if (tid == 0) {
       s_dmode = W.dmeta[4];
       s_dv0 = __int_as_float(W.dmeta[5]);
@@ -97,6 +103,10 @@ __global__ void __launch_bounds__(NWARP * 32 + 32, 1)
     for (int k = tid; k <= KC; k += kMdictConsumers) thrS[k] = W.thr[k];
     if (tid == 0) s_nv = KC;
   }
+  consumers_sync<kMdictConsumers>();
+  // dictionary constants in registers (not re-read from shared memory per item)
+  const int dmode = ADAPT ? s_dmode : 0;
+  const float dv0 = ADAPT ? s_dv0 : 0.0f, dS = ADAPT ? s_dS : 0.0f;
   const TileParam<float> g0 = reinterpret_cast<const TileParam<float>*>(W.tparams)[0];
   const float2 glc = tile_lc(g0);
   const bool patho = !ADAPT && isnan(glc.y);  // a range the float guard does not cover
@@ -106,6 +116,13 @@ __global__ void __launch_bounds__(NWARP * 32 + 32, 1)
   const int rows = G.stage_rows;
   const int nrb = (rows + 31) >> 5;
   const int r1mask = G.r1 - 1, lg_r1 = G.lg_r1;  // per-item row split, kept in registers
+  // a warp's 32 rows: 8 along dim KO-1 x 4 along dim KO-2 when the box has
+  // them (neighbouring voxels along dim KO-2 share values more often than
+  // those 16-32 rows apart along KO-1: ~8 % fewer gather wavefronts on the 4D
+  // volume); 8 consecutive rows per 8 lanes keep the 32-byte swizzled stage
+  // accesses conflict-free
+  const bool l84 = lg_r1 >= 3 && (rows >> lg_r1) >= 4;
+  const int h84 = lg_r1 - 3;
   float ugs[KO], ugt[KO];
   int64_t cur = -1;
   int seg = 0;
@@ -225,10 +242,17 @@ __global__ void __launch_bounds__(NWARP * 32 + 32, 1)
 #pragma unroll
           for (int i = 0; i < 4; ++i) di[i] = bin_search(vv[i], thrS, KC);
         }
-      } else if (s_dmode) {  // affine cells: one LDS.64 per voxel
+      } else if (dmode == 2) {  // direct cells: one 32-bit check per voxel, gathers by cell
         int cl[4];
-        cl[0] = dict_cell(vv[0], vv[1], s_dv0, s_dS, &cl[1]);
-        cl[2] = dict_cell(vv[2], vv[3], s_dv0, s_dS, &cl[3]);
+        cl[0] = dict_cell<KC - 1>(vv[0], vv[1], dv0, dS, &cl[1]);
+        cl[2] = dict_cell<KC - 1>(vv[2], vv[3], dv0, dS, &cl[3]);
+        const uint32_t* bitsS = reinterpret_cast<const uint32_t*>(dltS);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) di[i] = bitsS[cl[i]] == __float_as_uint(vv[i]) ? cl[i] : -1;
+      } else if (dmode) {  // affine cells: one LDS.64 per voxel
+        int cl[4];
+        cl[0] = dict_cell(vv[0], vv[1], dv0, dS, &cl[1]);
+        cl[2] = dict_cell(vv[2], vv[3], dv0, dS, &cl[3]);
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const uint2 e = dltS[cl[i]];
@@ -294,8 +318,16 @@ __global__ void __launch_bounds__(NWARP * 32 + 32, 1)
     for (int item = first; item < nitems; item += NW) {
       const int c = TSTORE ? (item & 1) : 0, rb = TSTORE ? item >> 1 : item;
       // stages hold a power of two >= 32 rows (plan_mdict): every lane has a row
-      const int q = rb * 32 + lane;
-      const int r1 = q & r1mask, r2 = q >> lg_r1;
+      int q, r1, r2;
+      if (l84) {
+        r1 = ((rb & ((1 << h84) - 1)) << 3) | (lane & 7);
+        r2 = ((rb >> h84) << 2) | (lane >> 3);
+        q = (r2 << lg_r1) | r1;
+      } else {
+        q = rb * 32 + lane;
+        r1 = q & r1mask;
+        r2 = q >> lg_r1;
+      }
       const float f1 = fmaf((float)(xb1 + r1), s1, t1);
       const float f2 = fmaf((float)(xb2 + r2), s2, t2);
       float wo[NCO];

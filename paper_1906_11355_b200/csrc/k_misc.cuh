@@ -104,37 +104,53 @@ __global__ void __launch_bounds__(1024) k_dict_finalize(WS W, int cap) {
   for (int o = 16; o > 0; o >>= 1) gap = fmin(gap, __shfl_xor_sync(0xffffffffu, gap, o));
   if ((tid & 31) == 0) s_gap[tid >> 5] = gap;
   __syncthreads();
-  // Affine direct table when the values are evenly spread (quantised data):
-  // cell = rint((v - v0) * S) with S = 1.25 / (smallest gap), so distinct
-  // values land in distinct cells and the blend looks a value up with one
-  // LDS.64 (dict_cell, the same packed arithmetic as the blend).
-  __shared__ int s_aff;
+  // Affine tables when the values are evenly spread (quantised data):
+  // cell = rint((v - v0) * S), the same packed arithmetic as the blends
+  // (dict_cell).  First try S = 1 / (smallest gap) with the cell as the value's
+  // index (mode 2, "direct": the values renumbered by cell, holes empty; needs
+  // every cell below cap), then S = 1.25 / gap with a {bits, index} table
+  // (mode 1); both need distinct values in distinct cells.
+  __shared__ int s_aff, s_maxc;
   __shared__ float s_v0, s_S;
-  if (tid == 0) {
-    double g = INFINITY;
-    for (int w = 0; w < 32; ++w) g = fmin(g, s_gap[w]);
-    const float v0 = K > 0 ? key_val(s_key[0]) : 0.0f;
-    const float S = K > 1 ? (float)(1.25 / g) : 1.0f;
-    const double span = K > 1 ? ((double)key_val(s_key[K - 1]) - (double)v0) * (double)S : 0.0;
-    s_aff = (K > 0 && isfinite(S) && S > 0.0f && span < kDictHL - 4) ? 1 : 0;
-    s_v0 = v0;
-    s_S = S;
-  }
-  __syncthreads();
-  if (s_aff) {
+  for (int att = 0; att < 2; ++att) {
+    const bool direct = att == 0;
+    if (tid == 0) {
+      double g = INFINITY;
+      for (int w = 0; w < 32; ++w) g = fmin(g, s_gap[w]);
+      const float v0 = K > 0 ? key_val(s_key[0]) : 0.0f;
+      const float S = K > 1 ? (float)((direct ? 1.0 : 1.25) / g) : 1.0f;
+      const double span = K > 1 ? ((double)key_val(s_key[K - 1]) - (double)v0) * (double)S : 0.0;
+      s_aff = (K > 0 && isfinite(S) && S > 0.0f && span < (direct ? cap - 2 : kDictHL - 4)) ? 1 : 0;
+      s_v0 = v0;
+      s_S = S;
+      s_maxc = 0;
+    }
+    __syncthreads();
+    const int tried = s_aff;
+    __syncthreads();  // every thread has read s_aff before tid 0 may rewrite it
+    if (!tried) continue;
     for (int i = tid; i < K; i += 1024) {
       const float v = key_val(s_key[i]);
       const int cell = dict_cell(v, v, s_v0, s_S, nullptr);
-      if (atomicCAS(&W.dlt[cell].x, kDictEmpty, __float_as_uint(v)) != kDictEmpty) s_aff = 0;
-      else W.dlt[cell].y = (uint32_t)i;
+      if ((direct && cell >= cap) || atomicCAS(&W.dlt[cell].x, kDictEmpty, __float_as_uint(v)) != kDictEmpty)
+        s_aff = 0;
+      else {
+        W.dlt[cell].y = (uint32_t)(direct ? cell : i);
+        atomicMax(&s_maxc, cell);
+      }
     }
     __syncthreads();
     if (s_aff) {
+      if (direct) {  // renumber by cell: dvals[cell] = value, holes empty
+        for (int c = tid; c < cap; c += 1024)
+          W.dvals[c] = __uint_as_float(c <= s_maxc ? W.dlt[c].x : kDictEmpty);
+      }
       if (tid == 0) {
-        W.dmeta[4] = 1;
+        W.dmeta[4] = direct ? 2 : 1;
         W.dmeta[5] = __float_as_int(s_v0);
         W.dmeta[6] = __float_as_int(s_S);
-        W.dmeta[3] = K;
+        W.dmeta[3] = direct ? s_maxc + 1 : K;
+        W.dmeta[7] = K;
         W.dmeta[2] = 1;
       }
       return;
@@ -162,6 +178,7 @@ __global__ void __launch_bounds__(1024) k_dict_finalize(WS W, int cap) {
       }
     }
     W.dmeta[3] = K;
+    W.dmeta[7] = K;
     W.dmeta[2] = ok ? 1 : 0;
   }
 }
@@ -183,7 +200,7 @@ __global__ void k_dict_luts(WS W, int64_t win_tiles, int n) {
     const int64_t t = e / kDictKC;
     const int i = (int)(e - t * kDictKC);
     float r = 0.0f;
-    if (i < K) {
+    if (i < K && __float_as_uint(W.dvals[i]) != kDictEmpty) {  // direct cells: holes stay 0
       const TileParam<T> p = tp[t];
       const int b = tp_degenerate(p.lim) ? 0 : bin_of((T)W.dvals[i], p, W.thr + t * (n + 1), n, nm05);
       r = W.lut[t * n + b];

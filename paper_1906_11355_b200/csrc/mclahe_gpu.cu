@@ -2266,7 +2266,7 @@ int mclahe_plan_dict_state(mclahe_plan_t plan, const void* workspace, int32_t* s
                           cudaMemcpyDeviceToHost, st));
   MG_CUDA(cudaStreamSynchronize(st));
   state[0] = m[2] ? (plan->mdict ? 2 : 1) : 0;
-  state[1] = m[3];
+  state[1] = m[7];
   state[3] = m[2] ? m[4] : 0;
   return MCLAHE_OK;
 }

@@ -447,9 +447,32 @@ def test_value_dictionary_blend(M, case):
         if case == "rare":
             assert st["values"] < len(np.unique(x.view(np.uint32))), st  # misses exercised
         assert st["affine"] == (case not in ("uneven", "rare")), st  # evenly quantised: direct table
+        # counts over a common denominator: the affine cell is the index itself
+        assert st["direct"] == (case in ("poisson", "edges", "scaled4d", "wide")), st
     assert torch.equal(out, ref)
     want = O.mclahe(x, *args, "c")
     assert np.max(np.abs(out.cpu().numpy().astype(np.float64) - want)) <= OUT_TOL
+
+
+def test_value_dictionary_direct_cells_misses(M):
+    """Direct-cell dictionary (values numbered by their affine cell): voxels
+    whose value is off the lattice or beyond either end of it (cells clamped
+    to the last one, negative offsets wrapping) fail the 32-bit check and take
+    the workspace-LUT path; the result equals the edge-table blend bit for bit."""
+    rng = np.random.default_rng(61)
+    x = (rng.poisson(3.0, (32, 32, 16, 32)) / 11.0).astype(np.float32)
+    flat = x.reshape(-1)
+    pos = rng.choice(x.size, 3, replace=False)
+    flat[pos] = np.array([100.0, 0.5 / 11.0, -0.25], np.float32)
+    args = ((8, 8, 4, 4), 256, 0.02, True)
+    out, st = _run_plan(M, x, *args)
+    ref, _ = _run_plan(M, x, *args, no_dict=True)
+    assert st["used"] and st["folded"], st
+    assert torch.equal(out, ref)
+    want = O.mclahe(x, *args, "c")
+    assert np.max(np.abs(out.cpu().numpy().astype(np.float64) - want)) <= OUT_TOL
+    if st["values"] == len(np.unique(x)) - 3:  # none of the three was sampled
+        assert st["direct"], st
 
 
 @pytest.mark.parametrize("nb", [128, 256, 512])
