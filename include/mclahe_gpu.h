@@ -122,6 +122,21 @@ typedef struct {
 int mclahe_gpu_run(const mclahe_params_t* params, const void* in, void* out,
                    mclahe_timings_t* timings);
 
+/* Out of core (src/pipeline.cpp:73-129 has no size limit beyond host memory;
+ * PAPER.md:216 names larger-than-memory volumes as future work).  When the
+ * volume, its result and the workspace do not fit the device memory that is
+ * free (or MCLAHE_MAX_DEVICE_BYTES), mclahe_gpu_run streams float32 volumes
+ * through a ring of chunk slots along dim 0 instead of full-size device
+ * buffers: a chunk stays resident until the tile rows its voxels blend from are
+ * complete (about 1.5 interpolation cells of rows later), then its slot takes
+ * the next chunk.  Adaptive mode reads the host volume once; global mode
+ * twice (the range needs every voxel before any bin exists).  Results are
+ * bit-identical to the in-core call.  This entry point is the same call with an
+ * explicit device-memory cap (bytes, > 0); MCLAHE_ERR_OOM if even the smallest
+ * ring (about 2.5 cells of dim-0 rows plus the workspace) does not fit. */
+int mclahe_gpu_run_out_of_core(const mclahe_params_t* params, const void* in, void* out,
+                               int64_t max_device_bytes, mclahe_timings_t* timings);
+
 /* Same, with DEVICE buffers on `stream` (cudaStream_t; NULL = legacy).  The
  * library allocates (and caches) its workspace.  Synchronises `stream` before
  * returning so the non-finite check can be reported. */

@@ -75,6 +75,7 @@ class Debug(C.Structure):
 _vp, _i64 = C.c_void_p, C.c_int64
 SIGNATURES = {
     "mclahe_gpu_run": (C.c_int, [C.POINTER(Params), _vp, _vp, C.POINTER(Timings)]),
+    "mclahe_gpu_run_out_of_core": (C.c_int, [C.POINTER(Params), _vp, _vp, C.c_int64, C.POINTER(Timings)]),
     "mclahe_gpu_run_device": (C.c_int, [C.POINTER(Params), _vp, _vp, _vp, C.POINTER(Timings)]),
     "mclahe_plan_create": (C.c_int, [C.POINTER(Params), _i64, _i64, C.POINTER(_vp)]),
     "mclahe_plan_destroy": (C.c_int, [_vp]),

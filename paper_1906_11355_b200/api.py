@@ -279,13 +279,18 @@ def _request_parts(request: McLaheRequest):
             RangeMode(p.range_mode) == RangeMode.Adaptive)
 
 
-def mclahe(request: McLaheRequest, timings: PhaseTimings | None = None):
+def mclahe(request: McLaheRequest, timings: PhaseTimings | None = None,
+           max_device_bytes: int | None = None):
     """mclahe::mclahe (include/mclahe/pipeline.hpp:30, src/pipeline.cpp:73-129).
 
     numpy image -> numpy result (float32 for float32 input, float64 for every
     other real dtype, as the reference computes on doubles); CUDA torch
     tensor -> CUDA torch tensor on the current stream.  Raises
-    ValidationError with the reference's messages."""
+    ValidationError with the reference's messages.
+
+    Host volumes larger than the free device memory stream through a ring of
+    chunk slots (out of core, mclahe_gpu_run_out_of_core); ``max_device_bytes``
+    caps the device memory the call may use (numpy input only)."""
     kernel, n_bins, clip, adaptive = _request_parts(request)
     img = request.image
     if _is_torch(img):
@@ -297,7 +302,11 @@ def mclahe(request: McLaheRequest, timings: PhaseTimings | None = None):
     params = N.make_params(x.shape, kernel, n_bins, clip, adaptive, _dtype_code(x.dtype))
     out = np.empty_like(x)
     t = N.Timings()
-    N.check(N.lib().mclahe_gpu_run(C.byref(params), x.ctypes.data, out.ctypes.data, C.byref(t)))
+    if max_device_bytes is not None:
+        N.check(N.lib().mclahe_gpu_run_out_of_core(C.byref(params), x.ctypes.data, out.ctypes.data,
+                                                   int(max_device_bytes), C.byref(t)))
+    else:
+        N.check(N.lib().mclahe_gpu_run(C.byref(params), x.ctypes.data, out.ctypes.data, C.byref(t)))
     if timings is not None:
         timings.pad_s += t.pad_s
         timings.histograms_s += t.histograms_s
@@ -487,14 +496,14 @@ def shannon_entropy(a, n_bins: int = 256) -> float:
 
 
 def enhance(image, kernel_size, n_bins: int = 256, clip_limit: float = 1.0,
-            adaptive_hist_range: bool = False):
+            adaptive_hist_range: bool = False, max_device_bytes: int | None = None):
     """Convenience form with the paper's argument names (data, kernel_size,
     n_bins, clip_limit, adaptive_hist_range)."""
     req = McLaheRequest(image=image, kernel=KernelSpec(tuple(kernel_size)),
                         params=EnhanceParams(clip_limit, n_bins,
                                              RangeMode.Adaptive if adaptive_hist_range
                                              else RangeMode.Global))
-    return mclahe(req)
+    return mclahe(req, max_device_bytes=max_device_bytes)
 
 
 def multi_cuts(shape, kernel, n_slabs: int, n_bins: int = 256, clip_limit: float = 1.0,

@@ -1300,9 +1300,23 @@ struct Streamed {
   std::vector<int64_t> cuts;      // chunk row boundaries (C + 1)
   std::vector<int> last_chunk;    // per tile row: last chunk its support meets
   int64_t tiles_per_row = 0;
+  // Out-of-core ring (in_slots > 0): the device holds in_slots input and
+  // out_slots output chunk slots instead of the whole volume; chunk k's rows
+  // live in input slot k % in_slots until it has been blended, its results in
+  // output slot k % out_slots until they are back on the host.
+  int in_slots = 0, out_slots = 0;
+  int64_t slot_bytes = 0;
+  std::vector<cudaEvent_t> rev;   // ring events: [0,C) landed, [C,2C) slot free, [2C,3C) D2H done, 3C..3C+2
+  Streamed() = default;
+  Streamed(const Streamed&) = delete;
+  Streamed& operator=(const Streamed&) = delete;
+  ~Streamed() {
+    for (cudaEvent_t e : rev)
+      if (e) cudaEventDestroy(e);
+  }
 };
 
-int build_streamed(const mclahe_params_t* p, Streamed& S) {
+int build_streamed(const mclahe_params_t* p, Streamed& S, int want_chunks = 0) {
   const Dim d0 = make_dim(p->shape[0], p->kernel[0]);
   std::vector<std::pair<int64_t, int64_t>> cells;
   for (int64_t c = 0; c + 1 < d0.g; ++c) {
@@ -1321,6 +1335,7 @@ int build_streamed(const mclahe_params_t* p, Streamed& S) {
       2, std::min(kMaxChunks, getenv("MCLAHE_CHUNKS") ? atoi(getenv("MCLAHE_CHUNKS")) : 16));
   int C = (int)std::max<int64_t>(
       1, std::min<int64_t>({S0 / align, (int64_t)max_chunks, std::max<int64_t>(1, bytes / (8 << 20))}));
+  if (want_chunks > 0) C = (int)std::max<int64_t>(1, std::min<int64_t>(S0 / align, want_chunks));
   if (C < 2 || cells.size() < 2) return MCLAHE_ERR_UNSUPPORTED;
   S.cuts.assign(1, 0);
   for (int k = 1; k < C; ++k) {
@@ -1348,11 +1363,88 @@ int build_streamed(const mclahe_params_t* p, Streamed& S) {
   return MCLAHE_OK;
 }
 
+// The step (index of the chunk whose arrival triggers it) at which each chunk
+// is blended, by the rules run_streamed applies; `main_pass_global`: the
+// second pass of a global-mode ring run (ranges known, a chunk is counted when
+// it lands again).
+std::vector<int> blend_steps(const Streamed& S, bool adaptive) {
+  const int C = (int)S.chunks.size();
+  const int64_t g0 = (int64_t)S.last_chunk.size();
+  std::vector<int> step((size_t)C, -1);
+  int hist = 0, blended = 0;
+  int64_t params_rows = adaptive ? 0 : g0, mapped_rows = 0;
+  for (int k = 0; k < C; ++k) {
+    if (adaptive) {
+      while (params_rows < g0 && S.last_chunk[(size_t)params_rows] < k + 1) ++params_rows;
+      while (hist < C && S.chunks[(size_t)hist]->info.count_row_end <= params_rows) ++hist;
+    } else {
+      hist = k + 1;
+    }
+    while (mapped_rows < g0 && S.last_chunk[(size_t)mapped_rows] < hist) ++mapped_rows;
+    while (blended < C && S.chunks[(size_t)blended]->info.need_row_end <= mapped_rows)
+      step[(size_t)blended++] = k;
+  }
+  return step;
+}
+
+// Out-of-core plan: the finest chunking is tried last; the first chunk count
+// whose ring (the chunks a blend waits for, one more to keep H2D running, and
+// the output slots) fits `budget` bytes beside the workspace wins.
+int build_ring(const mclahe_params_t* p, int64_t budget, std::unique_ptr<Streamed>& out) {
+  const int64_t S0 = p->shape[0];
+  const int64_t row_bytes = volume(p) / S0 * elem_size(p);
+  int64_t best_need = INT64_MAX;
+  for (int want = 16; ; want *= 2) {
+    auto S = std::make_unique<Streamed>();
+    const int rc = build_streamed(p, *S, want);
+    if (rc != MCLAHE_OK && rc != MCLAHE_ERR_UNSUPPORTED) return rc;
+    if (rc == MCLAHE_ERR_UNSUPPORTED)
+      return fail(MCLAHE_ERR_OOM, "volume does not fit the device memory budget and cannot be chunked along dim 0");
+    const int C = (int)S->chunks.size();
+    const std::vector<int> step = blend_steps(*S, p->adaptive != 0);
+    int lag = 0;
+    for (int b = 0; b < C; ++b) {
+      if (step[(size_t)b] < 0) return fail(MCLAHE_ERR_CUDA, "streamed schedule does not complete");
+      lag = std::max(lag, step[(size_t)b] - b);
+    }
+    int64_t slot = 0;
+    for (int k = 0; k < C; ++k) slot = std::max(slot, (S->cuts[(size_t)k + 1] - S->cuts[(size_t)k]) * row_bytes);
+    slot = align_up(slot, 1024);
+    const int64_t wsb = align_up(S->chunks[0]->info.workspace_bytes, 256);
+    // preferred / minimal ring: lag + 2 in, 3 out / lag + 1 in, 2 out
+    for (int slack = 1; slack >= 0; --slack) {
+      const int ni = std::min(C, lag + 1 + slack), no = std::min(C, 2 + slack);
+      const int64_t need = (ni + no) * slot + wsb;
+      best_need = std::min(best_need, need);
+      if (need <= budget) {
+        S->in_slots = ni;
+        S->out_slots = no;
+        S->slot_bytes = slot;
+        out = std::move(S);
+        return MCLAHE_OK;
+      }
+    }
+    if (C < want || want >= 4096) break;  // no finer chunking exists
+  }
+  return fail(MCLAHE_ERR_OOM, "volume does not fit the device memory budget: the out-of-core ring needs at least " +
+                                  std::to_string(best_need) + " bytes (about 2.5 interpolation cells of dim-0 rows)");
+}
+
 int run_streamed(Streamed& S, const mclahe_params_t* p, const void* in, void* out, void* d_in,
                  void* d_out, void* ws, cudaStream_t s_in, cudaStream_t s_comp, cudaStream_t s_out,
-                 std::vector<cudaEvent_t>& ev, mclahe_timings_t* timings) {
+                 std::vector<cudaEvent_t>& ev_shared, mclahe_timings_t* timings) {
   const int C = (int)S.chunks.size();
-  if (ev.size() < (size_t)(2 * C + 2)) return fail(MCLAHE_ERR_CUDA, "streamed run: too few events");
+  const bool ring = S.in_slots > 0;
+  // events: [0, C) inputs landed, [C, 2C) chunk blended (its input slot is
+  // free), [2C, 3C) ring: output back on the host, 3C / 3C+1 timing, 3C+2 ring
+  // pass boundary
+  if (ring && S.rev.empty()) {
+    S.rev.assign((size_t)(3 * C + 3), nullptr);
+    for (auto& e : S.rev) MG_CUDA(cudaEventCreate(&e));
+  }
+  std::vector<cudaEvent_t>& ev = ring ? S.rev : ev_shared;
+  const int T0 = ring ? 3 * C : 2 * C;
+  if (ev.size() < (size_t)(T0 + 2)) return fail(MCLAHE_ERR_CUDA, "streamed run: too few events");
   const int64_t row_bytes = volume(p) / p->shape[0] * elem_size(p);
   const int64_t g0 = (int64_t)S.last_chunk.size();
   const int64_t tpr = S.tiles_per_row;
@@ -1361,25 +1453,70 @@ int run_streamed(Streamed& S, const mclahe_params_t* p, const void* in, void* ou
   int rc;
   for (auto& c : S.chunks)
     if ((rc = device_init(c.get()))) return rc;
-  // events: [0, C) inputs landed, [C, 2C) outputs ready, 2C / 2C+1 timing
-  for (int k = 0; k < C; ++k) {
-    const int64_t off = S.cuts[k] * row_bytes, len = (S.cuts[k + 1] - S.cuts[k]) * row_bytes;
-    MG_CUDA(cudaMemcpyAsync(static_cast<char*>(d_in) + off, static_cast<const char*>(in) + off,
-                            (size_t)len, cudaMemcpyHostToDevice, s_in));
-    MG_CUDA(cudaEventRecord(ev[k], s_in));
-  }
-  MG_CUDA(cudaEventRecord(ev[2 * C], s_comp));
+  auto host_off = [&](int k) { return S.cuts[(size_t)k] * row_bytes; };
+  auto chunk_len = [&](int k) { return (S.cuts[(size_t)k + 1] - S.cuts[(size_t)k]) * row_bytes; };
+  auto in_ptr = [&](int k) {
+    return static_cast<char*>(d_in) + (ring ? (k % S.in_slots) * S.slot_bytes : host_off(k));
+  };
+  auto out_ptr = [&](int k) {
+    return static_cast<char*>(d_out) + (ring ? (k % S.out_slots) * S.slot_bytes : host_off(k));
+  };
+  // ring: a wait is only enqueued on an event recorded earlier in THIS call
+  std::vector<char> freed((size_t)C, 0), back((size_t)C, 0), landed((size_t)C, 0);
+  auto load = [&](int k) -> int {
+    if (ring && k >= S.in_slots) {
+      if (!freed[(size_t)(k - S.in_slots)]) return fail(MCLAHE_ERR_CUDA, "ring schedule: input slot still in use");
+      MG_CUDA(cudaStreamWaitEvent(s_in, ev[(size_t)(C + k - S.in_slots)], 0));
+    }
+    MG_CUDA(cudaMemcpyAsync(in_ptr(k), static_cast<const char*>(in) + host_off(k), (size_t)chunk_len(k),
+                            cudaMemcpyHostToDevice, s_in));
+    MG_CUDA(cudaEventRecord(ev[(size_t)k], s_in));
+    landed[(size_t)k] = 1;
+    return MCLAHE_OK;
+  };
+  MG_CUDA(cudaEventRecord(ev[(size_t)T0], s_comp));
   if ((rc = do_reset(M, ws, s_comp))) return rc;
-  int ranged = 0, hist = 0, blended = 0;
-  int64_t params_rows = 0, mapped_rows = 0;
   bool gparams = false;
-  float interp_ms = 0.f;
+  if (ring && !A) {
+    // global mode out of core: the range needs every voxel before any bin
+    // exists, so the volume streams through the ring twice (range; counts + blend)
+    for (int k = 0; k < C; ++k) {
+      if ((rc = load(k))) return rc;
+      MG_CUDA(cudaStreamWaitEvent(s_comp, ev[(size_t)k], 0));
+      if ((rc = do_range(S.chunks[(size_t)k].get(), in_ptr(k), ws, s_comp))) return rc;
+      MG_CUDA(cudaEventRecord(ev[(size_t)(C + k)], s_comp));
+      freed[(size_t)k] = 1;
+    }
+    int64_t gflag = 0;
+    MG_CUDA(cudaMemcpyAsync(&gflag, static_cast<char*>(ws) + M->info.off_range + 16, sizeof gflag,
+                            cudaMemcpyDeviceToHost, s_comp));
+    MG_CUDA(cudaStreamSynchronize(s_comp));  // every slot is free again
+    if (gflag) return fail(MCLAHE_ERR_VALIDATION, "image contains non-finite values");
+    if ((rc = do_params(M, ws, s_comp))) return rc;
+    gparams = true;
+    std::fill(freed.begin(), freed.end(), 0);
+    std::fill(landed.begin(), landed.end(), 0);
+  }
+  if (!ring)
+    for (int k = 0; k < C; ++k)
+      if ((rc = load(k))) return rc;
+  int ranged = gparams ? C : 0, hist = 0, blended = 0;
+  int64_t params_rows = 0, mapped_rows = 0;
   for (int k = 0; k < C; ++k) {
-    MG_CUDA(cudaStreamWaitEvent(s_comp, ev[k], 0));
-    mclahe_plan_s* pk = S.chunks[k].get();
-    const char* xk = static_cast<const char*>(d_in) + S.cuts[k] * row_bytes;
-    if ((rc = do_range(pk, xk, ws, s_comp))) return rc;
-    ranged = k + 1;
+    if (ring) {
+      // first pass of a ring: in_slots chunks in flight; later chunks are
+      // loaded as the blends free their slots (enqueued below, in order)
+      if (k == 0)
+        for (int j = 0; j < std::min(C, S.in_slots); ++j)
+          if ((rc = load(j))) return rc;
+    }
+    if (ring && !landed[(size_t)k]) return fail(MCLAHE_ERR_CUDA, "ring schedule: chunk not loaded");
+    MG_CUDA(cudaStreamWaitEvent(s_comp, ev[(size_t)k], 0));
+    mclahe_plan_s* pk = S.chunks[(size_t)k].get();
+    if (!gparams || A) {
+      if ((rc = do_range(pk, in_ptr(k), ws, s_comp))) return rc;
+      ranged = k + 1;
+    }
     // binning parameters: tile rows whose support is fully ranged (adaptive),
     // or the global range once every chunk is in
     if (A) {
@@ -1402,13 +1539,13 @@ int run_streamed(Streamed& S, const mclahe_params_t* p, const void* in, void* ou
       if ((rc = do_params(M, ws, s_comp))) return rc;
       gparams = true;
     }
-    // histograms of chunks whose counted tile rows all have parameters
+    // histograms of chunks whose counted tile rows all have parameters (the
+    // second pass of a global-mode ring counts a chunk when it lands again)
     while (hist < C) {
-      mclahe_plan_s* ph = S.chunks[hist].get();
-      const bool ready = A ? ph->info.count_row_end <= params_rows : gparams;
+      mclahe_plan_s* ph = S.chunks[(size_t)hist].get();
+      const bool ready = A ? ph->info.count_row_end <= params_rows : (gparams && (!ring || hist <= k));
       if (!ready) break;
-      const char* xh = static_cast<const char*>(d_in) + S.cuts[hist] * row_bytes;
-      if ((rc = do_hist(ph, xh, ws, s_comp))) return rc;
+      if ((rc = do_hist(ph, in_ptr(hist), ws, s_comp))) return rc;
       ++hist;
     }
     // mappings of tile rows whose every counting chunk is done
@@ -1420,22 +1557,30 @@ int run_streamed(Streamed& S, const mclahe_params_t* p, const void* in, void* ou
       mapped_rows = r;
     }
     // blend + D2H of chunks whose tile rows are all mapped
-    while (blended < C && S.chunks[blended]->info.need_row_end <= mapped_rows) {
-      mclahe_plan_s* pb = S.chunks[blended].get();
-      const int64_t off = S.cuts[blended] * row_bytes;
-      const int64_t len = (S.cuts[blended + 1] - S.cuts[blended]) * row_bytes;
-      if ((rc = do_interp(pb, static_cast<const char*>(d_in) + off, static_cast<char*>(d_out) + off,
-                          ws, s_comp)))
-        return rc;
-      MG_CUDA(cudaEventRecord(ev[C + blended], s_comp));
-      MG_CUDA(cudaStreamWaitEvent(s_out, ev[C + blended], 0));
-      MG_CUDA(cudaMemcpyAsync(static_cast<char*>(out) + off, static_cast<char*>(d_out) + off,
-                              (size_t)len, cudaMemcpyDeviceToHost, s_out));
+    while (blended < C && S.chunks[(size_t)blended]->info.need_row_end <= mapped_rows) {
+      mclahe_plan_s* pb = S.chunks[(size_t)blended].get();
+      if (ring && blended >= S.out_slots) {
+        if (!back[(size_t)(blended - S.out_slots)]) return fail(MCLAHE_ERR_CUDA, "ring schedule: output slot still in use");
+        MG_CUDA(cudaStreamWaitEvent(s_comp, ev[(size_t)(2 * C + blended - S.out_slots)], 0));
+      }
+      if ((rc = do_interp(pb, in_ptr(blended), out_ptr(blended), ws, s_comp))) return rc;
+      MG_CUDA(cudaEventRecord(ev[(size_t)(C + blended)], s_comp));
+      freed[(size_t)blended] = 1;
+      MG_CUDA(cudaStreamWaitEvent(s_out, ev[(size_t)(C + blended)], 0));
+      MG_CUDA(cudaMemcpyAsync(static_cast<char*>(out) + host_off(blended), out_ptr(blended),
+                              (size_t)chunk_len(blended), cudaMemcpyDeviceToHost, s_out));
+      if (ring) {
+        MG_CUDA(cudaEventRecord(ev[(size_t)(2 * C + blended)], s_out));
+        back[(size_t)blended] = 1;
+        // the freed input slot takes the next chunk not yet on its way
+        const int nxt = blended + S.in_slots;
+        if (nxt < C && (rc = load(nxt))) return rc;
+      }
       ++blended;
     }
   }
   if (blended != C) return fail(MCLAHE_ERR_CUDA, "streamed schedule did not complete");
-  MG_CUDA(cudaEventRecord(ev[2 * C + 1], s_comp));
+  MG_CUDA(cudaEventRecord(ev[(size_t)(T0 + 1)], s_comp));
   int64_t flag = 0;
   MG_CUDA(cudaMemcpyAsync(&flag, static_cast<char*>(ws) + M->info.off_range + 16, sizeof flag,
                           cudaMemcpyDeviceToHost, s_comp));
@@ -1454,8 +1599,7 @@ int run_streamed(Streamed& S, const mclahe_params_t* p, const void* in, void* ou
   }
   if (timings) {
     float total = 0.f;
-    MG_CUDA(cudaEventElapsedTime(&total, ev[2 * C], ev[2 * C + 1]));
-    (void)interp_ms;
+    MG_CUDA(cudaEventElapsedTime(&total, ev[(size_t)T0], ev[(size_t)(T0 + 1)]));
     timings->histograms_s += total * 1e-3;  // interleaved passes: reported as one span
   }
   return MCLAHE_OK;
@@ -2090,9 +2234,24 @@ int mclahe_gpu_run_device(const mclahe_params_t* params, const void* in, void* o
   return MCLAHE_OK;
 }
 
-int mclahe_gpu_run(const mclahe_params_t* params, const void* in, void* out,
-                   mclahe_timings_t* timings) {
-  NvtxRange nvtx("mclahe_gpu_run");
+namespace {
+
+// Device bytes a one-shot call may use: `cap` when given, else what is free
+// now plus the cached one-shot buffer (it is reallocated to fit), less a margin
+// for the chunk plans' tables; MCLAHE_MAX_DEVICE_BYTES caps both.
+int device_budget(const OneShot& o, int64_t cap, int64_t* budget) {
+  size_t free_b = 0, total_b = 0;
+  MG_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  int64_t b = (int64_t)free_b + (int64_t)o.buf_bytes;
+  b -= std::min<int64_t>(b / 16, int64_t{1} << 30);
+  if (const char* e = getenv("MCLAHE_MAX_DEVICE_BYTES")) b = std::min<int64_t>(b, atoll(e));
+  if (cap > 0) b = std::min(b, cap);
+  *budget = b;
+  return MCLAHE_OK;
+}
+
+int run_host(const mclahe_params_t* params, const void* in, void* out, int64_t max_device_bytes,
+             mclahe_timings_t* timings) {
   int rc = validate(params);
   if (rc) return rc;
   if (!in || !out) return fail(MCLAHE_ERR_VALIDATION, "null host buffer");
@@ -2102,13 +2261,51 @@ int mclahe_gpu_run(const mclahe_params_t* params, const void* in, void* out,
   if (!pl) return rc;
   const size_t bytes = (size_t)(volume(params) * elem_size(params));
   const size_t io = (size_t)align_up((int64_t)bytes, 256);
+  int dev = 0;
+  MG_CUDA(cudaGetDevice(&dev));
+  mclahe_params_t q = *params;
+  q.reserved = 0;
+  for (int i = q.rank; i < MCLAHE_MAX_RANK; ++i) q.shape[i] = q.kernel[i] = 0;
+  int64_t budget = 0;
+  if ((rc = device_budget(o, max_device_bytes, &budget))) return rc;
+  if ((int64_t)(2 * io) + pl->info.workspace_bytes > budget) {
+    // out of core: the volume streams through a ring of chunk slots
+    if (!pl->f32())
+      return fail(MCLAHE_ERR_OOM, "float64 volume does not fit the device memory budget (the out-of-core ring takes float32 volumes)");
+    std::string key = plan_key(&q, dev);
+    key.append("ring");
+    auto it = o.streamed.find(key);
+    if (it != o.streamed.end() && it->second) {
+      const Streamed& S = *it->second;
+      const int64_t need = (S.in_slots + S.out_slots) * S.slot_bytes +
+                           align_up(S.chunks[0]->info.workspace_bytes, 256);
+      if (need > budget) {
+        o.streamed.erase(it);
+        it = o.streamed.end();
+      }
+    }
+    if (it == o.streamed.end()) {
+      std::unique_ptr<Streamed> S;
+      if ((rc = build_ring(params, budget, S))) return rc;
+      if (o.streamed.size() > 8) o.streamed.clear();
+      it = o.streamed.emplace(key, std::move(S)).first;
+    }
+    Streamed& S = *it->second;
+    const int64_t in_b = S.in_slots * S.slot_bytes, out_b = S.out_slots * S.slot_bytes;
+    const size_t wsb = (size_t)S.chunks[0]->info.workspace_bytes;
+    if (o.buf && (int64_t)o.buf_bytes > budget) {  // a larger cached buffer breaks the cap
+      cudaFree(o.buf);
+      o.buf = nullptr;
+      o.buf_bytes = 0;
+    }
+    if ((rc = ensure_buf(o, (size_t)(in_b + out_b) + wsb))) return rc;
+    if ((rc = ensure_stream(o))) return rc;
+    char* base = static_cast<char*>(o.buf);
+    return run_streamed(S, params, in, out, base, base + in_b, base + in_b + out_b, o.s_in, o.stream,
+                        o.s_out, o.sev, timings);
+  }
   // float32 volumes large enough to chunk: streamed H2D / compute / D2H
   if (pl->f32() && getenv("MCLAHE_NO_STREAM") == nullptr) {
-    int dev = 0;
-    MG_CUDA(cudaGetDevice(&dev));
-    mclahe_params_t q = *params;
-    q.reserved = 0;
-    for (int i = q.rank; i < MCLAHE_MAX_RANK; ++i) q.shape[i] = q.kernel[i] = 0;
     const std::string key = plan_key(&q, dev);
     auto it = o.streamed.find(key);
     if (it == o.streamed.end()) {
@@ -2130,6 +2327,21 @@ int mclahe_gpu_run(const mclahe_params_t* params, const void* in, void* out,
     }
   }
   return run_plan_host(o, pl, in, out, bytes, io, timings);
+}
+
+}  // namespace
+
+int mclahe_gpu_run(const mclahe_params_t* params, const void* in, void* out,
+                   mclahe_timings_t* timings) {
+  NvtxRange nvtx("mclahe_gpu_run");
+  return run_host(params, in, out, 0, timings);
+}
+
+int mclahe_gpu_run_out_of_core(const mclahe_params_t* params, const void* in, void* out,
+                               int64_t max_device_bytes, mclahe_timings_t* timings) {
+  NvtxRange nvtx("mclahe_gpu_run_out_of_core");
+  if (max_device_bytes <= 0) return fail(MCLAHE_ERR_VALIDATION, "max_device_bytes must be positive");
+  return run_host(params, in, out, max_device_bytes, timings);
 }
 
 int mclahe_gpu_run_framewise(const mclahe_params_t* params, int32_t frame_axis, const void* in,
