@@ -252,7 +252,12 @@ struct Stage {
   TileParts p1, p2;             // K2: tile parts along dims KO-1 and KO-2
   int32_t tc[6];                // TMA box coordinates of the stage (K4 reuses them to store)
   int32_t ph;                   // fused K2: 0 = range pass over the unit, 1 = counting pass
-  int32_t last;                 // fused K2: last box of the unit's pass
+  int32_t last;                 // fused K2: last box of the unit's pass; NEXT producers: last
+                                // box of the work item, the fields below name the next item
+  int32_t nunit;                // next work item (-1: none)
+  int32_t nseg;                 // its segment
+  int64_t nkey;                 // its cell key
+  int32_t ncell[kMaxOuterDims]; // its cells
 };
 
 // Producer-private per-unit box (kept in shared memory, not registers, so
@@ -430,7 +435,13 @@ __device__ __forceinline__ bool parts_uniform(const TileParts& p, int64_t x, int
 // consumer warps share its SM sub-partition): slot / phase counters instead
 // of divisions, the unit record and geometry in registers, TMA coordinates in
 // registers.
-template <int KO, bool CELLS, bool WEIGHTS = !CELLS, bool STORE = false, bool SEGOUT = STORE>
+// NEXT: the producer takes the following work item while it starts the
+// current one and names it in the record of the current item's last box
+// (Stage::last / nunit / nseg / nkey / ncell), so a consumer that rebuilds
+// per-item tables can do so as soon as it has finished the item -- while the
+// next item's first boxes are still in flight -- instead of after they land.
+template <int KO, bool CELLS, bool WEIGHTS = !CELLS, bool STORE = false, bool SEGOUT = STORE,
+          bool NEXT = false>
 __device__ __noinline__ void pipe_produce(const KGeom& G, const CUtensorMap* map,
                                           const int32_t* __restrict__ units, int u0, int u1,
                                           Pipe& pp, float* bufs,
@@ -453,14 +464,27 @@ __device__ __noinline__ void pipe_produce(const KGeom& G, const CUtensorMap* map
   // dyn != nullptr: units are handed out dynamically (one atomic per unit,
   // [u0, u1) is then the whole list); otherwise the CTA's static range
   int u = dyn ? u0 + (int)atomicAdd(dyn, 1ULL) : u0;
+  // NEXT: the item after u, taken when u has kNextAhead boxes left to issue --
+  // late enough that the handout order stays what it is without the look-ahead
+  // (sibling items still start together on different CTAs and share their L2
+  // lines; taking it at the start of u gave one CTA two siblings in a row:
+  // 4D folded-pair blend 0.64 -> 0.68 ms), early enough to hide the atomic and
+  // the record read
+  constexpr int kNextAhead = 6;
+  int un = 0;
 #pragma unroll 1
-  for (; u < u1; u = dyn ? u0 + (int)atomicAdd(dyn, 1ULL) : u + 1) {
+  for (; u < u1; u = NEXT ? un : (dyn ? u0 + (int)atomicAdd(dyn, 1ULL) : u + 1)) {
     // seg_items: work item u = (unit u / nseg, segment u % nseg)
     const int seg_w = seg_items ? u % nseg : 0;
     const int32_t* U = units + (int64_t)(seg_items ? u / nseg : u) * kUnitInts;
     int32_t cellr[KO];
 #pragma unroll
     for (int j = 0; j < KO; ++j) cellr[j] = U[j];
+    // NEXT: the following item's identity, for the record of this item's last box
+    int32_t ncellr[KO] = {0};
+    int64_t nkey = 0;
+    int nseg_w = 0;
+    bool have_next = false;
     int64_t key = 0;
     B.a[0] = U[8];
     B.ext[0] = U[9] - U[8];
@@ -507,6 +531,8 @@ __device__ __noinline__ void pipe_produce(const KGeom& G, const CUtensorMap* map
       p1 = B.parts[KO - 1];
       if (KO >= 2) p2 = B.parts[KO - 2];
     }
+    // boxes of this work item still to issue (NEXT: the last one carries the next item)
+    int64_t left = nfix * n1 * n2 * (SEGOUT ? (seg_items ? 1 : nseg) : nseg);
     // blend (SEGOUT): segments outermost, so a consumer staging per segment
     // restages rarely
 #pragma unroll 1
@@ -541,6 +567,30 @@ __device__ __noinline__ void pipe_produce(const KGeom& G, const CUtensorMap* map
           S.unit = u;
           S.seg = seg;
           S.key = key;
+          if (NEXT) {
+            if (!have_next && left <= kNextAhead) {
+              have_next = true;
+              un = dyn ? u0 + (int)atomicAdd(dyn, 1ULL) : u + 1;
+              if (un < u1) {
+                const int32_t* Un = units + (int64_t)(seg_items ? un / nseg : un) * kUnitInts;
+                nseg_w = seg_items ? un % nseg : 0;
+#pragma unroll
+                for (int j = 0; j < KO; ++j) {
+                  ncellr[j] = Un[j];
+                  nkey = nkey * G.d[j].g + Un[j];
+                }
+              }
+            }
+            const bool last = --left == 0;
+            S.last = last ? 1 : 0;
+            if (last) {
+              S.nunit = un < u1 ? un : -1;
+              S.nseg = nseg_w;
+              S.nkey = nkey;
+#pragma unroll
+              for (int j = 0; j < KO; ++j) S.ncell[j] = ncellr[j];
+            }
+          }
 #pragma unroll
           for (int j = 0; j < KO - 2; ++j) S.x[j] = xf[j];
           S.x[KO - 1] = x1;

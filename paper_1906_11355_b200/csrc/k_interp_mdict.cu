@@ -25,6 +25,15 @@
 #ifndef MDICT_BUILD_BATCH
 #define MDICT_BUILD_BATCH 4
 #endif
+// 1: the producer names the next work item in the last box of the current one
+// (pipe_produce NEXT) and the consumers rebuild their tables before its first
+// box lands.  Measured slower (4D blend 0.641 -> 0.651 ms, Large 4D 4.06 ->
+// 4.21 ms; taking the next item at the start of the current one: 0.683 / 4.24,
+// the siblings of a pencil then run back to back on one CTA and stop sharing
+// their L2 lines), so it stays off: -DMDICT_NEXT=1 for A/B.
+#ifndef MDICT_NEXT
+#define MDICT_NEXT 0
+#endif
 
 namespace mg {
 
@@ -60,14 +69,18 @@ __global__ void __launch_bounds__(NWARP * 32 + 32, 1)
   int* colT = reinterpret_cast<int*>(
       (reinterpret_cast<uintptr_t>(ofS + NCO) + 15) & ~uintptr_t(15));  // [ncol]
   float* colW = reinterpret_cast<float*>(colT + ((ncol + 3) & ~3));    // [ncol][4][2]
-  __shared__ int s_dmode;
-  __shared__ float s_dv0, s_dS;
-  __shared__ int s_nv;
+  // dictionary scalars in the dynamic tail: the kernel has no static shared
+  // memory (1024-aligned, it would cost 1 KB of the opt-in and the fourth stage)
+  int* scal = reinterpret_cast<int*>(colW + ncol * 8);
+  int& s_dmode = scal[0];
+  float& s_dv0 = reinterpret_cast<float*>(scal)[1];
+  float& s_dS = reinterpret_cast<float*>(scal)[2];
+  int& s_nv = scal[3];
   pipe_init(*P.pipe, G.nst, NW);
   __syncthreads();
   if (threadIdx.x >= kMdictConsumers) {
     if (threadIdx.x == kMdictConsumers)
-      pipe_produce<KO, true, false, TSTORE, true>(G, &tmap, units, 0, G.dyn_units, *P.pipe,
+      pipe_produce<KO, true, false, TSTORE, true, MDICT_NEXT != 0>(G, &tmap, units, 0, G.dyn_units, *P.pipe,
                                                   P.bufs, &omap,
                                                   reinterpret_cast<unsigned long long*>(&W.range[3]));
     return;
@@ -130,19 +143,40 @@ __global__ void __launch_bounds__(NWARP * 32 + 32, 1)
   uint32_t it = 0;
   int cs_slot = 0;
   uint32_t cs_phase = 0;
+  // the next work item, named by the record of the current item's last box
+  // (pipe_produce NEXT): its tables are rebuilt as soon as this item is done,
+  // while its first boxes are still in flight
+  bool pend = false;
+  int pend_seg = 0;
+  int64_t pend_key = 0;
+  int32_t pend_cell[KO] = {0};
   while (true) {
     const int s = cs_slot;  // it % nst, (it / nst) & 1 as counters: no division
-    mbar_wait(&P.pipe->full[s], cs_phase);
     const Stage& S = P.pipe->st[s];
-    if (S.unit < 0) break;
-    const int64_t key = S.key * G.nseg + S.seg;
-    if (key != cur) {  // new work item: fold the two columns' corner pairs into M
-      consumers_sync<kMdictConsumers>();
-      seg = S.seg;
-      // window tile of corner co's trailing row: of0 + sum_j bit_j(co) * tstride[j]
-      int64_t of0 = (S.cell[0] - G.trow0) * G.tstride[0];
+    bool build = pend;
+    int32_t icell[KO];
+    int iseg = pend_seg;
+    int64_t ikey = pend_key;
 #pragma unroll
-      for (int j = 1; j < KO; ++j) of0 += S.cell[j] * G.tstride[j];
+    for (int j = 0; j < KO; ++j) icell[j] = pend_cell[j];
+    if (!pend) {
+      mbar_wait(&P.pipe->full[s], cs_phase);
+      if (S.unit < 0) break;
+      ikey = S.key * G.nseg + S.seg;
+      if (ikey != cur) {  // first item (or an item whose predecessor did not name it)
+        build = true;
+        iseg = S.seg;
+#pragma unroll
+        for (int j = 0; j < KO; ++j) icell[j] = S.cell[j];
+      }
+    }
+    if (build) {  // new work item: fold the two columns' corner pairs into M
+      consumers_sync<kMdictConsumers>();
+      seg = iseg;
+      // window tile of corner co's trailing row: of0 + sum_j bit_j(co) * tstride[j]
+      int64_t of0 = (icell[0] - G.trow0) * G.tstride[0];
+#pragma unroll
+      for (int j = 1; j < KO; ++j) of0 += icell[j] * G.tstride[j];
       auto ofc = [&](int co) {
         int64_t of = of0;
 #pragma unroll
@@ -186,13 +220,26 @@ __global__ void __launch_bounds__(NWARP * 32 + 32, 1)
         }
       }
       consumers_sync<kMdictConsumers>();
-      cur = key;
+      cur = ikey;
 #pragma unroll
       for (int jd = 0; jd < KO; ++jd) {
         const Dim& d = G.d[jd];
         ugs[jd] = G.inv_b[jd];
-        ugt[jd] = (float)(2 * d.before - 2 * (int64_t)S.cell[jd] * d.b - d.b + 1) * G.inv_2b[jd];
+        ugt[jd] = (float)(2 * d.before - 2 * (int64_t)icell[jd] * d.b - d.b + 1) * G.inv_2b[jd];
       }
+    }
+    if (pend) {  // tables ready: now wait for the item's first box
+      pend = false;
+      mbar_wait(&P.pipe->full[s], cs_phase);
+      if (S.unit < 0) break;
+    }
+    // this item's last box names the next item (read before the stage is released)
+    if (MDICT_NEXT && S.last && S.nunit >= 0) {
+      pend = true;
+      pend_seg = S.nseg;
+      pend_key = S.nkey * G.nseg + S.nseg;
+#pragma unroll
+      for (int j = 0; j < KO; ++j) pend_cell[j] = S.ncell[j];
     }
     // outer weights exactly as k_interp_pencil computes them
     float wfix[NCO / 4];
@@ -263,12 +310,10 @@ __global__ void __launch_bounds__(NWARP * 32 + 32, 1)
         for (int i = 0; i < 4; ++i) di[i] = dict_lookup(dltS, __float_as_uint(vv[i]));
       }
       const char* A[4];
-      int miss = 0;
+      const char* Mc = reinterpret_cast<const char*>(Ms + (c * 4) * NCO * KC);
+      const bool any_miss = ADAPT && (di[0] | di[1] | di[2] | di[3]) < 0;  // a missing value is -1
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        miss |= (di[i] < 0) << i;
-        A[i] = reinterpret_cast<const char*>(Ms + ((c * 4 + i) * NCO) * KC + (di[i] >= 0 ? di[i] : 0));
-      }
+      for (int i = 0; i < 4; ++i) A[i] = Mc + (i * NCO * KC + max(di[i], 0)) * 4;
       // two voxels per packed FFMA2 (same per-voxel order and rounding as
       // fmaf: acc = fma(wo[co], M, acc), co ascending)
       u64 acc01 = 0, acc23 = 0;
@@ -284,7 +329,10 @@ __global__ void __launch_bounds__(NWARP * 32 + 32, 1)
       float acc[4];
       upk2(acc01, acc[0], acc[1]);
       upk2(acc23, acc[2], acc[3]);
-      if (ADAPT && miss) {  // values the (sampled) dictionary lacks: from the workspace LUTs
+      if (any_miss) {  // values the (sampled) dictionary lacks: from the workspace LUTs
+        int miss = 0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) miss |= (di[i] < 0) << i;
         const int colc = min(col, ncol - 1);
         const int tt = colT[colc];
         float a[4] = {0.f, 0.f, 0.f, 0.f};
@@ -315,8 +363,10 @@ __global__ void __launch_bounds__(NWARP * 32 + 32, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&P.pipe->empty[s]);
     }
+    static_assert(NW % 2 == 0, "a warp's items of a stage share their column parity");
+    const int c = TSTORE ? (first & 1) : 0;  // item & 1 for every item of this warp in this stage
     for (int item = first; item < nitems; item += NW) {
-      const int c = TSTORE ? (item & 1) : 0, rb = TSTORE ? item >> 1 : item;
+      const int rb = TSTORE ? item >> 1 : item;
       // stages hold a power of two >= 32 rows (plan_mdict): every lane has a row
       int q, r1, r2;
       if (l84) {
@@ -330,14 +380,18 @@ __global__ void __launch_bounds__(NWARP * 32 + 32, 1)
       }
       const float f1 = fmaf((float)(xb1 + r1), s1, t1);
       const float f2 = fmaf((float)(xb2 + r2), s2, t2);
+      // wo[co] = (g1[co & 1] * g2[(co >> 1) & 1]) * wfix[co >> 2], two corners per
+      // packed multiply (same products, same rounding)
       float wo[NCO];
       {
-        const float g1[2] = {1.0f - f1, f1};
+        const u64 g1p = pk2(1.0f - f1, f1);
+        const float g20 = 1.0f - f2;
+        const u64 wa = mul2(g1p, pk2(g20, g20)), wb = mul2(g1p, pk2(f2, f2));
 #pragma unroll
-        for (int co = 0; co < NCO; ++co) {
-          float w = g1[co & 1];
-          w *= ((co >> 1) & 1) ? f2 : 1.0f - f2;
-          wo[co] = w * wfix[co >> 2];
+        for (int cf = 0; cf < NCO / 4; ++cf) {
+          const u64 wf = pk2(wfix[cf], wfix[cf]);
+          upk2(mul2(wa, wf), wo[4 * cf + 0], wo[4 * cf + 1]);
+          upk2(mul2(wb, wf), wo[4 * cf + 2], wo[4 * cf + 3]);
         }
       }
       // 32B-swizzled stage row (32 bytes): 16-byte chunk c of row q at c ^ ((q >> 2) & 1)

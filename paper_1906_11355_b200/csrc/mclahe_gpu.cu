@@ -493,9 +493,11 @@ void plan_mdict(mclahe_plan_s* pl) {
   m.stage_stride = align_up(m.stage_rows * 32, 1024) / 4;
   const int64_t nco = int64_t{1} << c.ko;
   m.tail = 2 * 4 * nco * tk * 4 + kDictHL * 8 + nco * 4 + 16 + ((c.P / 4 + 3) & ~int64_t(3)) * 4 +
-           (c.P / 4) * 32 + 16;
+           (c.P / 4) * 32 + 16 + 16;  // ... | colW | dictionary scalars [4]
   const int64_t stage = m.stage_stride * 4;
-  const int64_t nst = std::min<int64_t>(std::min(nst_cap, kMaxStages), (226 * 1024 - kPipeBytes - m.tail) / stage);
+  // 227 KB opt-in less the kernel's few static words (the other pencils keep
+  // 1 KB of headroom: 226 KB); with kDictKC = 608 the fourth stage needs it
+  const int64_t nst = std::min<int64_t>(std::min(nst_cap, kMaxStages), (227 * 1024 - 128 - kPipeBytes - m.tail) / stage);
   if (nst < 2) return;
   m.nst = (int)nst;
   m.smem = kPipeBytes + nst * stage + m.tail;
