@@ -278,8 +278,12 @@ def main():
             S.run_rank(x, shape, kernel, nb, clip, ad, rank, world, out=out, plan=plan, ws=ws,
                        windows=windows)
             return
-        if evs is not None:
-            evs[0].record(stream)
+        if evs is None:
+            # the whole step through the public call (mclahe_plan_enqueue): every
+            # pass, the dictionary numbering on its side branch
+            plan.enqueue(x, out, ws)
+            return
+        evs[0].record(stream)
         plan.reset(ws)
         plan.range(x, ws)
         plan.make_params(ws)

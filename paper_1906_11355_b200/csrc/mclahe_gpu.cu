@@ -190,8 +190,15 @@ struct mclahe_plan_s {
   mclahe_plan_s() = default;
   mclahe_plan_s(const mclahe_plan_s&) = delete;
   mclahe_plan_s& operator=(const mclahe_plan_s&) = delete;
+  // side branch of a whole-step enqueue: the dictionary numbering runs beside
+  // params / edge tables / histograms (created on first use)
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   ~mclahe_plan_s() {
     if (d_tables) cudaFree(d_tables);
+    if (side) cudaStreamDestroy(side);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
   }
 };
 
@@ -932,6 +939,11 @@ int device_init(mclahe_plan_s* pl) {
   int max_smem = 0;
   MG_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
   const bool A = pl->p.adaptive != 0;
+  if (pl->dict_cap > 0 && !pl->side) {  // side branch of enqueue_all (made here: not under capture)
+    MG_CUDA(cudaStreamCreateWithFlags(&pl->side, cudaStreamNonBlocking));
+    MG_CUDA(cudaEventCreateWithFlags(&pl->ev_fork, cudaEventDisableTiming));
+    MG_CUDA(cudaEventCreateWithFlags(&pl->ev_join, cudaEventDisableTiming));
+  }
   std::vector<int32_t> hist_cta, interp_cta;
   if (pl->hist.on) {
     int occ = 0;
@@ -1024,7 +1036,10 @@ int do_reset(mclahe_plan_s* pl, void* ws, cudaStream_t st) {
   return MCLAHE_OK;
 }
 
-int do_range(mclahe_plan_s* pl, const void* in, void* ws, cudaStream_t st) {
+// fork: the dictionary numbering (k_dict_finalize, only read by k_dict_luts and
+// the blend) goes to the plan's side stream and ev_join is recorded there; the
+// caller must make `st` wait for ev_join before the mappings pass.
+int do_range(mclahe_plan_s* pl, const void* in, void* ws, cudaStream_t st, bool fork = false) {
   NvtxRange nvtx("mclahe.range");
   WS W = ws_view(pl, ws);
   if (pl->frame_axis >= 0) {  // framewise global mode: per-frame ranges
@@ -1090,8 +1105,15 @@ int do_range(mclahe_plan_s* pl, const void* in, void* ws, cudaStream_t st) {
                                                     pl->d_tables + pl->off_hist_cta, W);
     MG_LAUNCHED();
     if (pl->dict_cap) {  // number the collected values once the slab's range pass is in
-      k_dict_finalize<<<1, 1024, 0, st>>>(W, pl->dict_cap);
+      cudaStream_t fs = st;
+      if (fork) {
+        MG_CUDA(cudaEventRecord(pl->ev_fork, st));
+        MG_CUDA(cudaStreamWaitEvent(pl->side, pl->ev_fork, 0));
+        fs = pl->side;
+      }
+      k_dict_finalize<<<1, 1024, 0, fs>>>(W, pl->dict_cap);
       MG_LAUNCHED();
+      if (fork) MG_CUDA(cudaEventRecord(pl->ev_join, pl->side));
     }
     return MCLAHE_OK;
   }
@@ -1701,11 +1723,18 @@ int ensure_stream(OneShot& o) {
 int enqueue_all(mclahe_plan_s* pl, const void* in, void* out, void* ws, cudaStream_t st,
                 cudaEvent_t* ev) {
   int rc;
+  // the dictionary numbering (~14 us, one CTA) leaves the critical path: it
+  // runs on a side branch beside params / edge tables / histograms and joins
+  // before the mappings pass (MCLAHE_NO_FORK=1 keeps one stream)
+  static const bool no_fork = getenv("MCLAHE_NO_FORK") != nullptr;
+  const bool fork = !no_fork && pl->dict_cap > 0 && pl->hist.on && !pl->fused_pencil &&
+                    pl->frame_axis < 0 && pl->side != nullptr;
   if (ev) MG_CUDA(cudaEventRecord(ev[0], st));
   if ((rc = do_reset(pl, ws, st))) return rc;
-  if ((rc = do_range(pl, in, ws, st))) return rc;
+  if ((rc = do_range(pl, in, ws, st, fork))) return rc;
   if ((rc = do_params(pl, ws, st))) return rc;
   if ((rc = do_hist(pl, in, ws, st))) return rc;
+  if (fork) MG_CUDA(cudaStreamWaitEvent(st, pl->ev_join, 0));
   if ((rc = do_map(pl, ws, nullptr, st))) return rc;
   if (ev) MG_CUDA(cudaEventRecord(ev[1], st));
   if ((rc = do_interp(pl, in, out, ws, st))) return rc;
