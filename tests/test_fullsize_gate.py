@@ -15,9 +15,13 @@ configs at their full sizes, seed 0.
   [0, 32), [256, 288) and [480, 512) through the reference's own per-voxel
   loop (neighbor_kernels / interp_coefficients / transform_pixel) over those
   mappings, within 1e-5.  The Global range is the full volume's min/max.
+  MCLAHE_GATE_L4D_ALL=1 walks every tile row and every voxel the same way, one
+  interpolation cell of rows at a time (~5 min of reference time; recorded in
+  profiles/r02_fullsize_gate.txt).
 
 Prints one summary line per config (run with -s to see it).
 """
+import os
 import time
 
 import numpy as np
@@ -96,8 +100,12 @@ def test_fullsize_l4d_tile_row_windows_vs_reference(M):
     total_tiles = total_vox = 0
     worst = 0.0
     t0s = time.perf_counter()
-    for (ta, tb), (ra, rb) in [((0, 2), (0, b0 // 2)), ((4, 6), (4 * b0, 4 * b0 + b0 // 2)),
-                               ((7, 9), (shape[0] - b0 // 2, shape[0]))]:
+    windows = [((0, 2), (0, b0 // 2)), ((4, 6), (4 * b0, 4 * b0 + b0 // 2)),
+               ((7, 9), (shape[0] - b0 // 2, shape[0]))]
+    every = os.environ.get("MCLAHE_GATE_L4D_ALL") == "1"
+    if every:  # every tile row and every voxel, one interpolation cell of rows at a time
+        windows = [((t, t + 2), (t * b0, min(shape[0], (t + 1) * b0))) for t in range(shape[0] // b0)]
+    for (ta, tb), (ra, rb) in windows:
         ref, _ = O.ref_tile_rows_by_crop(x, kernel, nb, clip, ad, ta, tb, grange)
         _assert_tiles(st, ref, slice(ta * per_row, tb * per_row), f"{name} tile rows {ta}-{tb}")
         want = O.ref_blend_rows(x[ra:rb], shape, kernel, ra, nb, ta, ref)
@@ -107,6 +115,9 @@ def test_fullsize_l4d_tile_row_windows_vs_reference(M):
         worst = max(worst, err)
         total_tiles += len(ref["lo"])
         total_vox += want.size
-    print(f"[gate] l4d: tile rows 0-1, 4-5, 7-8 ({total_tiles} tiles) bit-exact, "
-          f"{total_vox} voxels (rows 0-31, 256-287, 480-511) max|out - ref| = {worst:.3e}; "
+    what = ("every tile row (windows " + ", ".join(f"{a}-{b - 1}" for (a, b), _ in windows) + ")"
+            if every else "tile rows 0-1, 4-5, 7-8")
+    rows = "every row" if every else "rows 0-31, 256-287, 480-511"
+    print(f"[gate] l4d: {what} ({total_tiles} tile checks) bit-exact, "
+          f"{total_vox} voxels ({rows}) max|out - ref| = {worst:.3e}; "
           f"reference {time.perf_counter() - t0s:.1f} s")
