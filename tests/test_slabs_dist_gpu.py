@@ -66,3 +66,48 @@ def test_run_rank_matches_single_gpu(name, world):
         _, a, b, o = r
         got[a:b] = o
     assert np.array_equal(got, want.numpy())
+
+
+def _nccl_worker(port, name, q):
+    try:
+        import torch.distributed as dist
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        torch.cuda.set_device(0)
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda:0"))
+        from paper_1906_11355_b200 import datasets, slabs as S
+        c = CASES[name]
+        x = datasets.make(name, seed=5, shape=c["shape"]).cuda()
+        out, _, _ = S.run_rank(x, c["shape"], c["kernel"], c["n_bins"], c["clip_limit"],
+                               c["adaptive"], 0, 1)
+        # the exchange object's own device all-reduce (int64 keys, MAX) over NCCL
+        t = torch.tensor([3, -7, 2 ** 40], dtype=torch.int64, device="cuda")
+        S.DistExchange([], 0).allreduce_max(t)
+        torch.cuda.synchronize()
+        q.put((out.cpu().numpy(), t.cpu().tolist(), dist.get_backend()))
+        dist.destroy_process_group()
+    except Exception as e:  # pragma: no cover
+        q.put((repr(e),))
+
+
+@pytest.mark.parametrize("name", ["4d", "l4d"])
+def test_run_rank_nccl_world1(name):
+    """The NCCL leg of run_rank on the box's one GPU: process group on the
+    device, the range all-reduce on device tensors (no host staging), output
+    identical to the plain single-GPU call.  (More than one NCCL rank needs
+    more than one GPU; the 2/3-rank cases above run over gloo.)"""
+    import paper_1906_11355_b200 as M
+    from paper_1906_11355_b200 import datasets
+    c = CASES[name]
+    x = datasets.make(name, seed=5, shape=c["shape"])
+    want = M.enhance(x.cuda(), c["kernel"], c["n_bins"], c["clip_limit"], c["adaptive"]).cpu()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_nccl_worker, args=(_port(), name, q))
+    p.start()
+    res = q.get(timeout=300)
+    p.join(timeout=60)
+    assert len(res) == 3, res
+    got, t, backend = res
+    assert backend == "nccl"
+    assert t == [3, -7, 2 ** 40]
+    assert np.array_equal(got, want.numpy())
