@@ -34,9 +34,36 @@
 #ifndef MDICT_NEXT
 #define MDICT_NEXT 0
 #endif
+// timing probes (results are WRONG; never shipped): 1 = tables built for a CTA's
+// first item only, 2 = every gather at index 0 (broadcast), 3 = gathers at
+// index = lane (conflict-free, no broadcast), 4 = 1 + 3, 5 = no blend at all (copy)
+// 1: an in-place (TSTORE) item is a whole 32-row block, both 16-byte columns per
+// lane (outer weights and row geometry once per 8 voxels instead of per 4)
+// (-1: in global mode only -- Large 4D blend 4.05 -> 3.89 ms; the adaptive 4D blend
+// measured 0.623 -> 0.631 ms with it)
+#ifndef MDICT_BOTH
+#define MDICT_BOTH -1
+#endif
+#ifndef MDICT_PROBE
+#define MDICT_PROBE 0
+#endif
 
 namespace mg {
 
+// LDS [reg + imm]: one shared word at a compile-time byte offset from a 32-bit
+// shared address
+template <int OFF>
+__device__ __forceinline__ float lds_f32(uint32_t a) {
+  float m;
+  asm volatile("ld.shared.f32 %0, [%1+%2];" : "=f"(m) : "r"(a), "n"(OFF));
+  return m;
+}
+template <int OFF>
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+  uint32_t w;
+  asm volatile("ld.shared.u32 %0, [%1+%2];" : "=r"(w) : "r"(a), "n"(OFF));
+  return w;
+}
 
 // TSTORE: results written in place into the stage and TMA-stored by the
 // producer (otherwise a lane blends both 16-byte columns of its row and
@@ -61,7 +88,7 @@ __global__ void __launch_bounds__(NWARP * 32 + 32, 1)
   extern __shared__ __align__(1024) unsigned char smem[];
   const PencilSmem P = pencil_smem(G, smem);
   const int n = G.n_bins;
-  float* Ms = reinterpret_cast<float*>(P.tail);                  // [2][4][NCO][KC]
+  float* Ms = reinterpret_cast<float*>(P.tail);                  // [4 frames][NCO][2 columns][KC]
   uint2* dltS = reinterpret_cast<uint2*>(Ms + 2 * 4 * NCO * KC);  // ADAPT: [kDictHL]
   float* thrS = reinterpret_cast<float*>(dltS);                    // global: edge table [n + 1]
   int* ofS = reinterpret_cast<int*>(dltS + kDictHL);              // [NCO]
@@ -100,9 +127,11 @@ __global__ void __launch_bounds__(NWARP * 32 + 32, 1)
   }
   if (ADAPT) {
     if (W.dmeta[4] == 2) {  // direct cells: the values' bits by cell (holes never match)
+      // one copy per column, so a voxel's bits sit at a fixed offset from its table address
       uint32_t* bitsS = reinterpret_cast<uint32_t*>(dltS);
+      static_assert(2 * KC * 4 <= kDictHL * 8, "two copies of the cell bits fit the lookup area");
       for (int k = tid; k < KC; k += kMdictConsumers)
-        bitsS[k] = k < W.dmeta[3] ? __float_as_uint(W.dvals[k]) : kDictEmpty;
+        bitsS[k] = bitsS[KC + k] = k < W.dmeta[3] ? __float_as_uint(W.dvals[k]) : kDictEmpty;
     } else {
       for (int k = tid; k < kDictHL; k += kMdictConsumers) dltS[k] = W.dlt[k];
     }
@@ -119,6 +148,7 @@ __global__ void __launch_bounds__(NWARP * 32 + 32, 1)
   consumers_sync<kMdictConsumers>();
   // dictionary constants in registers (not re-read from shared memory per item)
   const int dmode = ADAPT ? s_dmode : 0;
+  const uint32_t ms32 = (uint32_t)__cvta_generic_to_shared(Ms);
   const float dv0 = ADAPT ? s_dv0 : 0.0f, dS = ADAPT ? s_dS : 0.0f;
   const TileParam<float> g0 = reinterpret_cast<const TileParam<float>*>(W.tparams)[0];
   const float2 glc = tile_lc(g0);
@@ -136,6 +166,15 @@ __global__ void __launch_bounds__(NWARP * 32 + 32, 1)
   // accesses conflict-free
   const bool l84 = lg_r1 >= 3 && (rows >> lg_r1) >= 4;
   const int h84 = lg_r1 - 3;
+  // row of (row block rb, lane) = a warp-uniform part from rb plus a per-lane
+  // constant, for both lane layouts: r1 = ((rb << rs1) & r1mask) + r1L,
+  // r2 = ((rb >> rs2a) << rs2b) + r2L, q = (r2 << lg_r1) | r1
+  const int rs1 = l84 ? 3 : 5;
+  const int rs2a = l84 ? h84 : (lg_r1 >= 5 ? lg_r1 - 5 : 0);
+  const int rs2b = l84 ? 2 : (lg_r1 >= 5 ? 0 : 5 - lg_r1);
+  const int r1L = l84 ? (lane & 7) : (lane & r1mask);
+  const int r2L = l84 ? (lane >> 3) : (lane >> lg_r1);
+  const int qL = (r2L << lg_r1) | r1L;
   float ugs[KO], ugt[KO];
   int64_t cur = -1;
   int seg = 0;
@@ -185,7 +224,7 @@ __global__ void __launch_bounds__(NWARP * 32 + 32, 1)
       };
       if (tid < NCO) ofS[tid] = (int)ofc(tid);
       const int nv4 = (s_nv + 3) >> 2;
-      const int ntask = 2 * NCO * nv4;
+      const int ntask = ((MDICT_PROBE == 1 || MDICT_PROBE == 4) && cur >= 0) ? 0 : 2 * NCO * nv4;
       // a thread's tasks in batches of four: all eight L2 loads in flight first
 #pragma unroll 1
       for (int k0 = tid; k0 < ntask; k0 += MB_ * kMdictConsumers) {
@@ -214,7 +253,7 @@ __global__ void __launch_bounds__(NWARP * 32 + 32, 1)
             float r[4];
 #pragma unroll
             for (int e = 0; e < 4; ++e) r[e] = fmaf(tw.y, a1[e], tw.x * a0[e]);
-            reinterpret_cast<float4*>(Ms + ((c * 4 + i) * NCO + co) * KC)[v4] =
+            reinterpret_cast<float4*>(Ms + ((i * NCO + co) * 2 + c) * KC)[v4] =
                 make_float4(r[0], r[1], r[2], r[3]);
           }
         }
@@ -272,67 +311,98 @@ __global__ void __launch_bounds__(NWARP * 32 + 32, 1)
     // both columns of its row (one full 32-byte sector) and stores them
     // straight to global memory; the stage is released as soon as the warp's
     // last item has been read, so the producer refills it during the math.
-    const int nitems = TSTORE ? 2 * nrb : nrb;
+    constexpr bool BOTH = TSTORE && (MDICT_BOTH == 1 || (MDICT_BOTH < 0 && !ADAPT));
+    constexpr bool HALF = TSTORE && !BOTH;  // items are single columns
+    const int nitems = HALF ? 2 * nrb : nrb;
     const int first = warp >= rot ? warp - rot : warp + NW - rot;
     rot += nitems % NW;  // items dealt so far, mod NW
     if (rot >= NW) rot -= NW;
     // one column's 4 voxels (frames) of row q against its tables
     auto blend_col = [&](const int c, const float4 v4, const float (&wo)[NCO]) -> float4 {
+      if (MDICT_PROBE == 5) return v4;  // pipeline only: stage in, stage out
       const int col = seg * 2 + c;
       const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
-      int di[4];
-      if (!ADAPT) {  // one bin per voxel: the global edge table
-        if (!patho) {
-          bins2_edge(pk2(vv[0], vv[1]), vv[0], vv[1], glc, thrS, KC, di[0], di[1]);
-          bins2_edge(pk2(vv[2], vv[3]), vv[2], vv[3], glc, thrS, KC, di[2], di[3]);
-        } else {
-#pragma unroll
-          for (int i = 0; i < 4; ++i) di[i] = bin_search(vv[i], thrS, KC);
-        }
-      } else if (dmode == 2) {  // direct cells: one 32-bit check per voxel, gathers by cell
+      float acc[4];
+      int miss = 0;  // voxels the dictionary does not hold (bit i)
+      // ONE shared address per voxel, a = Ms + 4 * (c * KC + index): its 2^KO
+      // folded-pair entries (and, for direct cells, the cell's value bits) sit at
+      // compile-time offsets from it (LDS [reg + imm])
+      const uint32_t mcs = ms32 + (uint32_t)(c * KC * 4);
+      uint32_t a[4];
+      bool direct = false;
+      if constexpr (ADAPT) direct = dmode == 2;
+      if (direct) {
+        // direct cells: the cell's value bits (one copy per column) are checked
+        // against the voxel; a voxel whose bits differ still gathers (valid cell,
+        // wrong value) and is redone below
+        constexpr int kBitsOff = 2 * 4 * NCO * KC * 4;  // dltS - Ms in bytes
         int cl[4];
         cl[0] = dict_cell<KC - 1>(vv[0], vv[1], dv0, dS, &cl[1]);
         cl[2] = dict_cell<KC - 1>(vv[2], vv[3], dv0, dS, &cl[3]);
-        const uint32_t* bitsS = reinterpret_cast<const uint32_t*>(dltS);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) di[i] = bitsS[cl[i]] == __float_as_uint(vv[i]) ? cl[i] : -1;
-      } else if (dmode) {  // affine cells: one LDS.64 per voxel
-        int cl[4];
-        cl[0] = dict_cell(vv[0], vv[1], dv0, dS, &cl[1]);
-        cl[2] = dict_cell(vv[2], vv[3], dv0, dS, &cl[3]);
+        bool bad = false;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          const uint2 e = dltS[cl[i]];
-          di[i] = e.x == __float_as_uint(vv[i]) ? (int)e.y : -1;
+          a[i] = mcs + 4u * (uint32_t)cl[i];
+          bad |= lds_u32<kBitsOff>(a[i]) != __float_as_uint(vv[i]);
+        }
+        if (bad) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) miss |= (lds_u32<kBitsOff>(a[i]) != __float_as_uint(vv[i])) << i;
         }
       } else {
+        int di[4];
+        if (!ADAPT) {  // one bin per voxel: the global edge table
+          if (!patho) {
+            bins2_edge(pk2(vv[0], vv[1]), vv[0], vv[1], glc, thrS, KC, di[0], di[1]);
+            bins2_edge(pk2(vv[2], vv[3]), vv[2], vv[3], glc, thrS, KC, di[2], di[3]);
+          } else {
 #pragma unroll
-        for (int i = 0; i < 4; ++i) di[i] = dict_lookup(dltS, __float_as_uint(vv[i]));
+            for (int i = 0; i < 4; ++i) di[i] = bin_search(vv[i], thrS, KC);
+          }
+        } else if (dmode) {  // affine cells: one LDS.64 per voxel
+          int cl[4];
+          cl[0] = dict_cell(vv[0], vv[1], dv0, dS, &cl[1]);
+          cl[2] = dict_cell(vv[2], vv[3], dv0, dS, &cl[3]);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const uint2 e = dltS[cl[i]];
+            di[i] = e.x == __float_as_uint(vv[i]) ? (int)e.y : -1;
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) di[i] = dict_lookup(dltS, __float_as_uint(vv[i]));
+        }
+        if (ADAPT && (di[0] | di[1] | di[2] | di[3]) < 0) {  // a missing value is -1
+#pragma unroll
+          for (int i = 0; i < 4; ++i) miss |= (di[i] < 0) << i;
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) a[i] = mcs + 4u * (uint32_t)(ADAPT ? max(di[i], 0) : di[i]);
       }
-      const char* A[4];
-      const char* Mc = reinterpret_cast<const char*>(Ms + (c * 4) * NCO * KC);
-      const bool any_miss = ADAPT && (di[0] | di[1] | di[2] | di[3]) < 0;  // a missing value is -1
+      if (MDICT_PROBE == 2 || MDICT_PROBE >= 3) {
 #pragma unroll
-      for (int i = 0; i < 4; ++i) A[i] = Mc + (i * NCO * KC + max(di[i], 0)) * 4;
-      // two voxels per packed FFMA2 (same per-voxel order and rounding as
-      // fmaf: acc = fma(wo[co], M, acc), co ascending)
-      u64 acc01 = 0, acc23 = 0;
-      static_for<0, NCO>([&](auto coc) {
-        constexpr int co = decltype(coc)::value;
-        float m[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) m[i] = *reinterpret_cast<const float*>(A[i] + co * KC * 4);
-        const u64 w2 = pk2(wo[co], wo[co]);
-        acc01 = fma2(pk2(m[0], m[1]), w2, acc01);
-        acc23 = fma2(pk2(m[2], m[3]), w2, acc23);
-      });
-      float acc[4];
-      upk2(acc01, acc[0], acc[1]);
-      upk2(acc23, acc[2], acc[3]);
-      if (any_miss) {  // values the (sampled) dictionary lacks: from the workspace LUTs
-        int miss = 0;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) miss |= (di[i] < 0) << i;
+        for (int i = 0; i < 4; ++i) a[i] = mcs + (MDICT_PROBE == 2 ? (a[i] & 0) : ((a[i] & 0) + 4 * lane));
+      }
+      {
+        // two voxels per packed FFMA2 (same per-voxel order and rounding as
+        // fmaf: acc = fma(wo[co], M, acc), co ascending)
+        u64 acc01 = 0, acc23 = 0;
+        static_for<0, NCO>([&](auto coc) {
+          constexpr int co = decltype(coc)::value;
+          constexpr int kOff = co * 2 * KC * 4, kFrame = NCO * 2 * KC * 4;
+          float m[4];
+          m[0] = lds_f32<kOff>(a[0]);
+          m[1] = lds_f32<kOff + kFrame>(a[1]);
+          m[2] = lds_f32<kOff + 2 * kFrame>(a[2]);
+          m[3] = lds_f32<kOff + 3 * kFrame>(a[3]);
+          const u64 w2 = pk2(wo[co], wo[co]);
+          acc01 = fma2(pk2(m[0], m[1]), w2, acc01);
+          acc23 = fma2(pk2(m[2], m[3]), w2, acc23);
+        });
+        upk2(acc01, acc[0], acc[1]);
+        upk2(acc23, acc[2], acc[3]);
+      }
+      if (miss) {  // values the (sampled) dictionary lacks: from the workspace LUTs
         const int colc = min(col, ncol - 1);
         const int tt = colT[colc];
         float a[4] = {0.f, 0.f, 0.f, 0.f};
@@ -364,20 +434,13 @@ __global__ void __launch_bounds__(NWARP * 32 + 32, 1)
       if (lane == 0) mbar_arrive(&P.pipe->empty[s]);
     }
     static_assert(NW % 2 == 0, "a warp's items of a stage share their column parity");
-    const int c = TSTORE ? (first & 1) : 0;  // item & 1 for every item of this warp in this stage
+    const int c = HALF ? (first & 1) : 0;  // item & 1 for every item of this warp in this stage
     for (int item = first; item < nitems; item += NW) {
-      const int rb = TSTORE ? item >> 1 : item;
+      const int rb = HALF ? item >> 1 : item;
       // stages hold a power of two >= 32 rows (plan_mdict): every lane has a row
-      int q, r1, r2;
-      if (l84) {
-        r1 = ((rb & ((1 << h84) - 1)) << 3) | (lane & 7);
-        r2 = ((rb >> h84) << 2) | (lane >> 3);
-        q = (r2 << lg_r1) | r1;
-      } else {
-        q = rb * 32 + lane;
-        r1 = q & r1mask;
-        r2 = q >> lg_r1;
-      }
+      const int r1u = (rb << rs1) & r1mask, r2u = (rb >> rs2a) << rs2b;
+      const int r1 = r1u + r1L, r2 = r2u + r2L;
+      const int q = ((r2u << lg_r1) | r1u) + qL;
       const float f1 = fmaf((float)(xb1 + r1), s1, t1);
       const float f2 = fmaf((float)(xb2 + r2), s2, t2);
       // wo[co] = (g1[co & 1] * g2[(co >> 1) & 1]) * wfix[co >> 2], two corners per
@@ -395,9 +458,17 @@ __global__ void __launch_bounds__(NWARP * 32 + 32, 1)
         }
       }
       // 32B-swizzled stage row (32 bytes): 16-byte chunk c of row q at c ^ ((q >> 2) & 1)
-      if constexpr (TSTORE) {
+      if constexpr (BOTH) {
+        const int sw = (q >> 2) & 1;
+        float4* pa = reinterpret_cast<float4*>(buf + q * 32 + (sw << 4));
+        float4* pb = reinterpret_cast<float4*>(buf + q * 32 + ((1 ^ sw) << 4));
+        const float4 va = *pa, vb = *pb;
+        *pa = blend_col(0, va, wo);
+        *pb = blend_col(1, vb, wo);
+      } else if constexpr (TSTORE) {
         float4* slot4 = reinterpret_cast<float4*>(buf + q * 32 + ((c ^ ((q >> 2) & 1)) << 4));
-        *slot4 = blend_col(c, *slot4, wo);  // in place; the producer TMA-stores the box
+        // in place; the producer TMA-stores the box
+        *slot4 = blend_col(c, *slot4, wo);
       } else {
         const int sw = (q >> 2) & 1;
         const float4 va = *reinterpret_cast<const float4*>(buf + q * 32 + (sw << 4));
