@@ -42,7 +42,10 @@ constexpr int kMaxRuns = 16;       // runs gathered into one stage
 constexpr int kMaxStages = 6;
 constexpr int kConsumers = 256;    // 8 consumer warps (K2 kernels)
 constexpr int kPencilThreads = kConsumers + 32;  // + producer warp
-constexpr int kConsumersBlend = 512;  // 16 consumer warps (K4: one CTA per SM)
+#ifndef BLEND_CONSUMERS
+#define BLEND_CONSUMERS 512
+#endif
+constexpr int kConsumersBlend = BLEND_CONSUMERS;  // consumer warps x 32 (K4: one CTA per SM)
 constexpr int kBlendThreads = kConsumersBlend + 32;
 
 // Kernel-side geometry (passed by value).

@@ -44,6 +44,16 @@
 #ifndef MDICT_BOTH
 #define MDICT_BOTH -1
 #endif
+// consumer warps of the folded-pair blend (+ one producer warp): 19 warps are the
+// most that keep 96 registers (5 warps per SM sub-partition).  Adaptive 4D blend
+// 0.627 (16) / 0.621 (18) / 0.666 ms (20, 80 registers); Large 4D (global mode)
+// 3.88 / 3.91 / 3.97 ms
+#ifndef MDICT_NWARP_ADAPT
+#define MDICT_NWARP_ADAPT 18
+#endif
+#ifndef MDICT_NWARP_GLOBAL
+#define MDICT_NWARP_GLOBAL 16
+#endif
 #ifndef MDICT_PROBE
 #define MDICT_PROBE 0
 #endif
@@ -498,19 +508,21 @@ __global__ void __launch_bounds__(NWARP * 32 + 32, 1)
   }
 }
 
-// 16 consumer warps at 96 registers: 20 / 24 warps (80 / 72 registers) measured
-// 0.78 / 0.86 ms against 0.72 ms on the 4D config.
 PencilInterpFn get_interp_mdict(int ko, bool tma_store, bool adaptive, int n_bins) {
   if (ko != 3) return nullptr;
   if (adaptive)
-    return tma_store ? k_interp_mdict<3, true, 16, true, kDictKC>
-                     : k_interp_mdict<3, false, 16, true, kDictKC>;
+    return tma_store ? k_interp_mdict<3, true, MDICT_NWARP_ADAPT, true, kDictKC>
+                     : k_interp_mdict<3, false, MDICT_NWARP_ADAPT, true, kDictKC>;
   switch (n_bins) {
-    case 128: return tma_store ? k_interp_mdict<3, true, 16, false, 128> : k_interp_mdict<3, false, 16, false, 128>;
-    case 256: return tma_store ? k_interp_mdict<3, true, 16, false, 256> : k_interp_mdict<3, false, 16, false, 256>;
-    case 512: return tma_store ? k_interp_mdict<3, true, 16, false, 512> : k_interp_mdict<3, false, 16, false, 512>;
+    case 128: return tma_store ? k_interp_mdict<3, true, MDICT_NWARP_GLOBAL, false, 128> : k_interp_mdict<3, false, MDICT_NWARP_GLOBAL, false, 128>;
+    case 256: return tma_store ? k_interp_mdict<3, true, MDICT_NWARP_GLOBAL, false, 256> : k_interp_mdict<3, false, MDICT_NWARP_GLOBAL, false, 256>;
+    case 512: return tma_store ? k_interp_mdict<3, true, MDICT_NWARP_GLOBAL, false, 512> : k_interp_mdict<3, false, MDICT_NWARP_GLOBAL, false, 512>;
     default: return nullptr;
   }
+}
+
+int interp_mdict_threads(bool adaptive) {
+  return (adaptive ? MDICT_NWARP_ADAPT : MDICT_NWARP_GLOBAL) * 32 + 32;
 }
 
 }  // namespace mg

@@ -1421,5 +1421,6 @@ PencilInterpFn get_interp_pencil(int ko, int kt, bool adaptive, int n_bins);
 PencilInterpFn get_interp_pencil_dict(int ko, int kt);
 // folded-pair blend; nullptr: none for this (ko, mode, n_bins)
 PencilInterpFn get_interp_mdict(int ko, bool tma_store, bool adaptive, int n_bins);
+int interp_mdict_threads(bool adaptive);  // its block size (consumer warps + the producer warp)
 
 }  // namespace mg

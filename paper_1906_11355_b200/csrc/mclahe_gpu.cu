@@ -1249,7 +1249,7 @@ int do_interp(mclahe_plan_s* pl, const void* in, void* out, void* ws, cudaStream
       const int grid = (int)std::min<int64_t>(Gm.dyn_units, pl->sms);
       // in-place results + TMA store (MCLAHE_MDICT_STG=1: per-lane global stores, A/B)
       static const bool tstore = getenv("MCLAHE_MDICT_STG") == nullptr;
-      get_interp_mdict(pl->interp.ko, tstore, A, (int)pl->p.n_bins)<<<grid, kBlendThreads,
+      get_interp_mdict(pl->interp.ko, tstore, A, (int)pl->p.n_bins)<<<grid, interp_mdict_threads(A),
                                                                   pl->interp_m.smem, st>>>(
           Gm, pl->map[3], pl->map[4], static_cast<const float*>(in), static_cast<float*>(out),
           pl->d_tables + pl->off_mdict_units, pl->d_tables + pl->off_interp_cta, W);
