@@ -54,6 +54,13 @@
 #ifndef MDICT_NWARP_GLOBAL
 #define MDICT_NWARP_GLOBAL 16
 #endif
+// 1: a new item's first batch of table loads is issued before the item barrier (in
+// flight while the slower warps finish the previous item).  Measured much slower
+// (4D blend 0.623 -> 0.727 ms, Large 4D 3.88 -> 4.14 ms: the batch's 32 registers
+// live across the barrier spill into the blend loop), so it stays off.
+#ifndef MDICT_EARLY_LOAD
+#define MDICT_EARLY_LOAD 0
+#endif
 #ifndef MDICT_PROBE
 #define MDICT_PROBE 0
 #endif
@@ -220,7 +227,6 @@ __global__ void __launch_bounds__(NWARP * 32 + 32, 1)
       }
     }
     if (build) {  // new work item: fold the two columns' corner pairs into M
-      consumers_sync<kMdictConsumers>();
       seg = iseg;
       // window tile of corner co's trailing row: of0 + sum_j bit_j(co) * tstride[j]
       int64_t of0 = (icell[0] - G.trow0) * G.tstride[0];
@@ -232,13 +238,10 @@ __global__ void __launch_bounds__(NWARP * 32 + 32, 1)
         for (int j = 0; j < KO; ++j) of += ((co >> (KO - 1 - j)) & 1) * G.tstride[j];
         return of;
       };
-      if (tid < NCO) ofS[tid] = (int)ofc(tid);
       const int nv4 = (s_nv + 3) >> 2;
       const int ntask = ((MDICT_PROBE == 1 || MDICT_PROBE == 4) && cur >= 0) ? 0 : 2 * NCO * nv4;
-      // a thread's tasks in batches of four: all eight L2 loads in flight first
-#pragma unroll 1
-      for (int k0 = tid; k0 < ntask; k0 += MB_ * kMdictConsumers) {
-        float4 L0[MB_], L1[MB_];
+      // a thread's tasks in batches of MB_: all 2 * MB_ L2 loads in flight first
+      auto load = [&](int k0, float4 (&L0)[MB_], float4 (&L1)[MB_]) {
 #pragma unroll
         for (int b = 0; b < MB_; ++b) {
           const int k = min(k0 + b * kMdictConsumers, ntask - 1);
@@ -248,6 +251,8 @@ __global__ void __launch_bounds__(NWARP * 32 + 32, 1)
           L0[b] = __ldg(reinterpret_cast<const float4*>(lsrc + t0 * KC) + v4);
           L1[b] = __ldg(reinterpret_cast<const float4*>(lsrc + (t0 + tstr1) * KC) + v4);
         }
+      };
+      auto fold = [&](int k0, const float4 (&L0)[MB_], const float4 (&L1)[MB_]) {
 #pragma unroll
         for (int b = 0; b < MB_; ++b) {
           const int k = k0 + b * kMdictConsumers;
@@ -267,6 +272,20 @@ __global__ void __launch_bounds__(NWARP * 32 + 32, 1)
                 make_float4(r[0], r[1], r[2], r[3]);
           }
         }
+      };
+      // the first batch's loads are issued BEFORE the barrier: they fly while the
+      // slower warps finish the previous item (the tables are only written after it)
+      float4 F0[MB_], F1[MB_];
+      if (MDICT_EARLY_LOAD && tid < ntask) load(tid, F0, F1);
+      consumers_sync<kMdictConsumers>();
+      if (tid < NCO) ofS[tid] = (int)ofc(tid);
+      if (MDICT_EARLY_LOAD && tid < ntask) fold(tid, F0, F1);
+#pragma unroll 1
+      for (int k0 = tid + (MDICT_EARLY_LOAD ? MB_ * kMdictConsumers : 0); k0 < ntask;
+           k0 += MB_ * kMdictConsumers) {
+        float4 L0[MB_], L1[MB_];
+        load(k0, L0, L1);
+        fold(k0, L0, L1);
       }
       consumers_sync<kMdictConsumers>();
       cur = ikey;
