@@ -388,6 +388,14 @@ __device__ __forceinline__ uint32_t edge_hist_addr(uint32_t th, int k, float v, 
 __device__ __forceinline__ void red_add(uint32_t addr, uint32_t val) {
   asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(val) : "memory");
 }
+// the same add predicated off where skip is set (no branch; lanes that skip take
+// no part in the instruction's bank conflicts)
+__device__ __forceinline__ void red_add_unless(uint32_t addr, uint32_t val, bool skip) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.eq.u32 p, %2, 0;\n\t@p red.shared.add.u32 [%0], %1;\n\t}" ::"r"(addr),
+      "r"(val), "r"((uint32_t)skip)
+      : "memory");
+}
 
 // Exact bin from the edge table alone (binary search over thr[1..n-1]);
 // used for ranges the float guard does not cover.

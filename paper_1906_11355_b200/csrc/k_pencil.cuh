@@ -304,6 +304,16 @@ __device__ __forceinline__ void copy_rows(float* dst, const float* __restrict__ 
 // rows of a thread are rpi apart; on flat data they keep landing in the same
 // bin), so a same-word add is only issued when the run breaks -- fewer
 // same-address shared atomics from the 4 rows a warp holds.
+// K2_PRED_RED: run tails predicated off instead of redirected to the thread's dummy word
+// (lanes that skip take no part in the add's bank conflicts: 4D hist 0.309 -> 0.299 ms,
+// 5D 0.379 -> 0.371 ms)
+#ifndef K2_PRED_RED
+#define K2_PRED_RED 1
+#endif
+// the same in the carried-run variant (global mode): Large 4D hist 1.806 -> 1.874 ms, off
+#ifndef K2_PRED_RED_CARRY
+#define K2_PRED_RED_CARRY 0
+#endif
 template <int KO, bool ADAPT, bool MATCH, bool CARRY = false>
 __global__ void __launch_bounds__(kPencilThreads, 3)
     k_hist_pencil(const __grid_constant__ KGeom G, const __grid_constant__ CUtensorMap tmap,
@@ -455,9 +465,15 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
           }
         } else {
           red_add(a[0], s0);
+#if K2_PRED_RED
+          red_add_unless(a[1], s1, e01);
+          red_add_unless(a[2], s2, e12);
+          red_add_unless(a[3], s3, e23);
+#else
           red_add(e01 ? dummy_s : a[1], s1);
           red_add(e12 ? dummy_s : a[2], s2);
           red_add(e23 ? dummy_s : a[3], s3);
+#endif
         }
       };
       // histogram words via the edge table (k = rint of the f32 estimate, th
@@ -480,6 +496,15 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
       uint32_t ca = dummy_s, cs = 0;
       auto commit_carry = [&](const uint32_t (&a)[4]) {
         const bool c0 = a[0] == ca, e01 = a[1] == a[0], e12 = a[2] == a[1], e23 = a[3] == a[2];
+#if K2_PRED_RED_CARRY
+        red_add_unless(ca, cs, c0);  // the carried run ends unless a[0] continues it
+        const uint32_t r0 = w[0] + (c0 ? cs : 0u);
+        red_add_unless(a[0], r0, e01);
+        const uint32_t r1 = w[1] + (e01 ? r0 : 0u);
+        red_add_unless(a[1], r1, e12);
+        const uint32_t r2 = w[2] + (e12 ? r1 : 0u);
+        red_add_unless(a[2], r2, e23);
+#else
         red_add(c0 ? dummy_s : ca, cs);  // the carried run ends unless a[0] continues it
         const uint32_t r0 = w[0] + (c0 ? cs : 0u);
         red_add(e01 ? dummy_s : a[0], r0);
@@ -487,6 +512,7 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
         red_add(e12 ? dummy_s : a[1], r1);
         const uint32_t r2 = w[2] + (e12 ? r1 : 0u);
         red_add(e23 ? dummy_s : a[2], r2);
+#endif
         cs = w[3] + (e23 ? r2 : 0u);
         ca = a[3];
       };
