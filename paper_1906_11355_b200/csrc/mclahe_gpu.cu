@@ -1200,7 +1200,9 @@ int do_map(mclahe_plan_s* pl, void* ws, const mclahe_debug_t* dbg, cudaStream_t 
     Wt.lut = W.lut + t0 * pl->p.n_bins;
     Wt.lutd = W.lutd + t0 * kDictKC;
     Wt.thr = W.thr + t0 * (pl->p.n_bins + 1);
-    const int g = (int)std::min<int64_t>((nt * kDictKC + 255) / 256, (int64_t)pl->sms * 16);
+    // CTAs per SM for the per-value rows (a thread's entries are chains of dependent loads)
+    static const int dl_mult = getenv("MCLAHE_DLUT_GRID") ? std::max(1, atoi(getenv("MCLAHE_DLUT_GRID"))) : 16;
+    const int g = (int)std::min<int64_t>((nt * kDictKC + 255) / 256, (int64_t)pl->sms * dl_mult);
     k_dict_luts<float><<<g, 256, 0, st>>>(Wt, nt, (int)pl->p.n_bins);
     MG_LAUNCHED();
   }
