@@ -427,12 +427,23 @@ __global__ void __launch_bounds__(256) k_tiles_generic(const KGeom G, const T* _
 // is bin-parallel.  Output: f32 LUT (+ optional f64 debug arrays).
 template <typename T>
 __global__ void __launch_bounds__(128) k_mappings(const KGeom G, WS W, Debug Dbg, int64_t t0,
-                                                  int64_t nt) {
+                                                  int64_t nt, int dict_rows = 0) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int n = G.n_bins;
   const int warps = blockDim.x >> 5, wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double* cdf = reinterpret_cast<double*>(smem) + (int64_t)wid * n;
   const TileParam<T>* tparams = reinterpret_cast<const TileParam<T>*>(W.tparams);
+  // dict_rows (float32 plans with a value dictionary): the warp also writes its
+  // tile's per-value row lutd[tile][i] = LUT[bin(value i)] (what k_dict_luts does in
+  // a launch of its own), from the LUT it has just built
+  bool drows = false;
+  int dK = 0;
+  if constexpr (sizeof(T) == 4) {
+    drows = dict_rows != 0 && W.dmeta[2] != 0;
+    dK = drows ? W.dmeta[3] : 0;
+  }
+  float* lutf = reinterpret_cast<float*>(cdf);  // the warp's LUT as floats, once cdf is done
+  const T nm05 = (T)n - (T)0.5;
   for (int64_t tile = t0 + (int64_t)blockIdx.x * warps + wid; tile < t0 + nt;
        tile += (int64_t)gridDim.x * warps) {
     const TileParam<T> tp = tparams[G.adaptive ? tile : 0];
@@ -451,6 +462,12 @@ __global__ void __launch_bounds__(128) k_mappings(const KGeom G, WS W, Debug Dbg
         if (Dbg.lut) Dbg.lut[tile * n + b] = 0.5;
       }
       if (Dbg.degenerate && lane == 0) Dbg.degenerate[tile] = 1;
+      if constexpr (sizeof(T) == 4) {
+        if (drows)
+          for (int i = lane; i < kDictKC; i += 32)
+            W.lutd[tile * kDictKC + i] =
+                (i < dK && __float_as_uint(W.dvals[i]) != kDictEmpty) ? 0.5f : 0.0f;
+      }
       continue;
     }
     // total = sum of counts (integers: exact in any order)
@@ -506,6 +523,20 @@ __global__ void __launch_bounds__(128) k_mappings(const KGeom G, WS W, Debug Dbg
     }
     if (Dbg.degenerate && lane == 0) Dbg.degenerate[tile] = degen ? 1 : 0;
     __syncwarp();
+    if constexpr (sizeof(T) == 4) {
+      if (drows) {
+        for (int b = lane; b < n; b += 32) lutf[b] = lut[b];  // own writes, read back
+        __syncwarp();
+        const float* th = W.thr + tile * (n + 1);
+        for (int i = lane; i < kDictKC; i += 32) {
+          float r = 0.0f;
+          if (i < dK && __float_as_uint(W.dvals[i]) != kDictEmpty)  // direct cells: holes stay 0
+            r = lutf[bin_of((T)W.dvals[i], tp, th, n, nm05)];
+          W.lutd[tile * kDictKC + i] = r;
+        }
+        __syncwarp();
+      }
+    }
   }
 }
 

@@ -1191,10 +1191,15 @@ int do_map(mclahe_plan_s* pl, void* ws, const mclahe_debug_t* dbg, cudaStream_t 
   }
   const int warps = pl->map_block / 32;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((nt + warps - 1) / warps, pl->map_grid));
-  if (pl->f32()) k_mappings<float><<<grid, pl->map_block, pl->map_smem, st>>>(pl->G, W, D, t0, nt);
-  else k_mappings<double><<<grid, pl->map_block, pl->map_smem, st>>>(pl->G, W, D, t0, nt);
+  // per-value LUT rows of the mapped tiles: written by the mappings warps themselves
+  // (MCLAHE_SPLIT_DLUT=1: by k_dict_luts in a launch of its own, A/B)
+  static const bool split_dlut = getenv("MCLAHE_SPLIT_DLUT") != nullptr;
+  const int fused_rows = (pl->dict_cap && pl->f32() && !split_dlut) ? 1 : 0;
+  if (pl->f32())
+    k_mappings<float><<<grid, pl->map_block, pl->map_smem, st>>>(pl->G, W, D, t0, nt, fused_rows);
+  else k_mappings<double><<<grid, pl->map_block, pl->map_smem, st>>>(pl->G, W, D, t0, nt, 0);
   MG_LAUNCHED();
-  if (pl->dict_cap) {  // per-value LUT rows of the mapped tiles
+  if (pl->dict_cap && !fused_rows) {  // per-value LUT rows of the mapped tiles
     WS Wt = W;
     Wt.tparams = static_cast<char*>(W.tparams) + t0 * (int64_t)sizeof(TileParam<float>);
     Wt.lut = W.lut + t0 * pl->p.n_bins;
