@@ -80,6 +80,7 @@ struct KGeom {
   int dyn_units;           // blend: > 0 = units handed out dynamically (count), via W.range[3]
   int seg_items;           // blend: 1 = a work item is (unit, ONE segment): item / nseg, item % nseg
   int nb_edges;            // NB blend: -1 auto (from the K2a value sample), 0 bracketed floors, 1 edge tables
+  int cell_hist;           // K2b: 1 = k_hist_cells is launched beside k_hist_pencil (dictionary state selects)
 };
 
 // Value dictionary (adaptive mode, float32): when the volume holds few

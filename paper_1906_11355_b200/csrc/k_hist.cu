@@ -36,4 +36,14 @@ PencilHistFn get_hist_pencil(int ko, bool adaptive, int variant) {
   return adaptive ? hist_t<true, false, false>(ko) : hist_t<false, false, false>(ko);
 }
 
+PencilHistFn get_hist_cells(int ko) {
+  switch (ko) {
+    case 1: return k_hist_cells<1>;
+    case 2: return k_hist_cells<2>;
+    case 3: return k_hist_cells<3>;
+    case 4: return k_hist_cells<4>;
+    default: return k_hist_cells<5>;
+  }
+}
+
 }  // namespace mg

@@ -338,6 +338,8 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
   const TileParam<float>* tparams = reinterpret_cast<const TileParam<float>*>(W.tparams);
   const TileParam<float> g0 = tparams[0];
   if (!ADAPT && tp_degenerate(g0.lim)) return;  // constant image: every mapping is 0.5
+  // quantised volume with direct dictionary cells: k_hist_cells counts it
+  if (ADAPT && G.cell_hist && W.dmeta[2] != 0 && W.dmeta[4] == 2) return;
   // 4 * kMagicBits kept opaque to ptxas (one IMAD per histogram address)
   __shared__ uint32_t s_mb4;
   if (threadIdx.x == 0) s_mb4 = 4u * (uint32_t)kMagicBits;
@@ -635,6 +637,188 @@ __global__ void __launch_bounds__(kPencilThreads, 3)
   if (cur >= 0) {
     hist_flush(hist, W.counts + cur * n, (int)G.gtr, n, tid, ADAPT ? lcS : nullptr);
   }
+}
+
+// K2b for quantised volumes (adaptive mode, value dictionary with direct cells --
+// kDict*, dmeta[4] == 2): voxels are counted per (tile, dictionary CELL) instead
+// of per (tile, bin).  A voxel's cell is one packed FMA + clamp and one 32-bit
+// check of the cell's value bits; no range, no edge table, no binning in the hot
+// loop.  Every voxel of a tile with the same value falls in the same bin, so the
+// unit switch turns the cell counts into bin counts exactly: one reference-rule
+// binning per (tile, value) -- ~5 k per unit against ~500 k voxels.  A voxel
+// whose value the (sampled) dictionary lacks is binned on the spot against the
+// workspace edge table and added to the workspace counts directly.  Launched
+// beside k_hist_pencil; the dictionary state in the workspace selects which of
+// the two runs (the other exits at once).
+template <int KO>
+__global__ void __launch_bounds__(kPencilThreads, 3)
+    k_hist_cells(const __grid_constant__ KGeom G, const __grid_constant__ CUtensorMap tmap,
+                 const float* __restrict__ in, const int32_t* __restrict__ units,
+                 const int32_t* __restrict__ cta_units, WS W) {
+  if (W.dmeta[2] == 0 || W.dmeta[4] != 2) return;  // k_hist_pencil counts this volume
+  constexpr int KC1 = kDictKC + 1;  // row pad: equal cells of neighbouring tiles in different banks
+  extern __shared__ __align__(128) unsigned char smem[];
+  const PencilSmem P = pencil_smem(G, smem);
+  const int n = G.n_bins;
+  uint32_t* hist = reinterpret_cast<uint32_t*>(P.tail);  // [gtr][KC1]
+  uint32_t* bitsS = hist + ((G.gtr * KC1 + 3) & ~3LL);    // [kDictKC] value bits by cell
+  const TileParam<float>* tparams = reinterpret_cast<const TileParam<float>*>(W.tparams);
+  const int K = min(W.dmeta[3], kDictKC);
+  const float dv0 = __int_as_float(W.dmeta[5]), dS = __int_as_float(W.dmeta[6]);
+  const float nm05 = (float)n - 0.5f;
+  for (int k = threadIdx.x; k < kDictKC; k += blockDim.x)
+    bitsS[k] = k < K ? __float_as_uint(W.dvals[k]) : kDictEmpty;
+  pipe_init(*P.pipe, G.nst);
+  __syncthreads();
+  const int u0 = cta_units[blockIdx.x], u1 = cta_units[blockIdx.x + 1];
+  if (threadIdx.x >= kConsumers) {
+    if (threadIdx.x == kConsumers)
+      pipe_produce<KO, false>(
+          G, &tmap, units, G.dyn_units ? 0 : u0, G.dyn_units ? G.dyn_units : u1, *P.pipe, P.bufs,
+          nullptr, G.dyn_units ? reinterpret_cast<unsigned long long*>(&W.range[3]) : nullptr,
+          tparams);
+    return;
+  }
+  const int tid = threadIdx.x;
+  const int slot = tid / G.tpr;
+  const int64_t e0 = (int64_t)(tid % G.tpr) * 4;
+  const bool lane_on = slot < G.rpi;
+  int trt[4], trw[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) trailing_tile(G, e0 + i, &trt[i], &trw[i]);
+  const int64_t stage_elems = G.stage_stride;
+  const uint32_t hist_s = (uint32_t)__cvta_generic_to_shared(hist);
+  const uint32_t bits_s = (uint32_t)__cvta_generic_to_shared(bitsS);
+  uint32_t ha[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) ha[i] = hist_s + (uint32_t)(trt[i] * KC1) * 4u;
+  // cell counts of unit `key` -> bin counts (degenerate tiles build no histogram)
+  // (four entries per thread at a time: their tile parameter / edge-table loads are
+  // independent chains)
+  auto flush = [&](int64_t key) {
+    const int total = (int)G.gtr * K;
+#pragma unroll 1
+    for (int e0f = tid; e0f < total; e0f += 4 * kConsumers) {
+      uint32_t cnt[4];
+      int tt[4], cc[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int e = e0f + j * kConsumers;
+        tt[j] = e < total ? e / K : 0;
+        cc[j] = e < total ? e - tt[j] * K : 0;
+        cnt[j] = e < total ? hist[tt[j] * KC1 + cc[j]] : 0u;
+      }
+      TileParam<float> tp[4];
+      float dv[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        tp[j] = tparams[key + tt[j]];
+        dv[j] = W.dvals[cc[j]];
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (cnt[j] == 0 || tp_degenerate(tp[j].lim)) continue;
+        const int64_t tile = key + tt[j];
+        atomicAdd(W.counts + tile * n + bin_of(dv[j], tp[j], W.thr + tile * (n + 1), n, nm05), cnt[j]);
+      }
+    }
+  };
+  int64_t cur = -1;
+  uint32_t it = 0;
+  int cs_slot = 0;
+  uint32_t cs_phase = 0;
+  while (true) {
+    const int s = cs_slot;
+    mbar_wait(&P.pipe->full[s], cs_phase);
+    const Stage& S = P.pipe->st[s];
+    if (S.unit < 0) break;
+    const int64_t key = S.key;
+    if (key != cur) {
+      consumers_sync();
+      if (cur >= 0) flush(cur);
+      consumers_sync();
+      for (int64_t k = tid; k < G.gtr * KC1; k += kConsumers) hist[k] = 0;
+      consumers_sync();
+      cur = key;
+    }
+    if (lane_on) {
+      const int rows = G.stage_rows;
+      const float* buf = P.bufs + s * stage_elems;
+      const bool wuni = S.wuni != 0;
+      const int32_t wfix = S.wfix;
+      auto row_weight = [&](int q) {
+        if (wuni) return (uint32_t)wfix;
+        const int r1 = q & (G.r1 - 1), r2 = q >> G.lg_r1;
+        int32_t w = wfix * S.p1.weight(S.x[KO - 1] + r1);
+        if (KO >= 2) w *= S.p2.weight(S.x[KO >= 2 ? KO - 2 : 0] + r2);
+        return (uint32_t)w;
+      };
+      // hot loop, no branches: a voxel whose bits differ from its cell's adds nothing
+      // here (predicated off) and the stage is revisited for it below
+      bool bad = false;
+#pragma unroll 4
+      for (int q = slot; q < rows; q += G.rpi) {
+        const uint32_t wrow = row_weight(q);
+        const float4 v = *reinterpret_cast<const float4*>(buf + q * G.P + e0);
+        const float vv[4] = {v.x, v.y, v.z, v.w};
+        int cl[4];
+        cl[0] = dict_cell<kDictKC - 1>(v.x, v.y, dv0, dS, &cl[1]);
+        cl[2] = dict_cell<kDictKC - 1>(v.z, v.w, dv0, dS, &cl[3]);
+        uint32_t a[4], w[4];
+        bool ok[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          uint32_t bw;
+          asm volatile("ld.shared.u32 %0, [%1];" : "=r"(bw) : "r"(bits_s + 4u * (uint32_t)cl[i]));
+          ok[i] = bw == __float_as_uint(vv[i]);
+          bad |= !ok[i];
+          a[i] = ha[i] + 4u * (uint32_t)cl[i];
+          w[i] = ok[i] ? wrow * (uint32_t)trw[i] : 0u;
+        }
+        // runs of equal (tile, cell) carry their sum on the first add (a miss carries
+        // weight 0 and can only share an address with a voxel of another value: it
+        // never merges into a real run's cell wrongly, its cell IS that address)
+        const bool e01 = a[0] == a[1], e12 = a[1] == a[2], e23 = a[2] == a[3];
+        const uint32_t s3 = w[3];
+        const uint32_t s2 = w[2] + (e23 ? s3 : 0u);
+        const uint32_t s1 = w[1] + (e12 ? s2 : 0u);
+        const uint32_t s0 = w[0] + (e01 ? s1 : 0u);
+        red_add_unless(a[0], s0, s0 == 0u);
+        red_add_unless(a[1], s1, e01 || s1 == 0u);
+        red_add_unless(a[2], s2, e12 || s2 == 0u);
+        red_add_unless(a[3], s3, e23 || s3 == 0u);
+      }
+      if (bad) {  // values the dictionary lacks: straight into the workspace counts
+#pragma unroll 1
+        for (int q = slot; q < rows; q += G.rpi) {
+          const uint32_t wrow = row_weight(q);
+          const float4 v = *reinterpret_cast<const float4*>(buf + q * G.P + e0);
+          const float vv[4] = {v.x, v.y, v.z, v.w};
+          int cl[4];
+          cl[0] = dict_cell<kDictKC - 1>(v.x, v.y, dv0, dS, &cl[1]);
+          cl[2] = dict_cell<kDictKC - 1>(v.z, v.w, dv0, dS, &cl[3]);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            if (bitsS[cl[i]] == __float_as_uint(vv[i])) continue;
+            const int64_t tile = cur + trt[i];
+            const TileParam<float> tp = tparams[tile];
+            if (!tp_degenerate(tp.lim))
+              atomicAdd(W.counts + tile * n + bin_of(vv[i], tp, W.thr + tile * (n + 1), n, nm05),
+                        wrow * (uint32_t)trw[i]);
+          }
+        }
+      }
+    }
+    __syncwarp();
+    if ((tid & 31) == 0) mbar_arrive(&P.pipe->empty[s]);
+    ++it;
+    if (++cs_slot == G.nst) {
+      cs_slot = 0;
+      cs_phase ^= 1;
+    }
+  }
+  consumers_sync();
+  if (cur >= 0) flush(cur);
 }
 
 // LUT value of one voxel against one window tile straight from the workspace
@@ -1448,5 +1632,7 @@ PencilInterpFn get_interp_pencil_dict(int ko, int kt);
 // folded-pair blend; nullptr: none for this (ko, mode, n_bins)
 PencilInterpFn get_interp_mdict(int ko, bool tma_store, bool adaptive, int n_bins);
 int interp_mdict_threads(bool adaptive);  // its block size (consumer warps + the producer warp)
+// K2b by dictionary cell (k_hist_cells); nullptr: none for this ko
+PencilHistFn get_hist_cells(int ko);
 
 }  // namespace mg

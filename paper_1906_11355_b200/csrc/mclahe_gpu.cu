@@ -180,6 +180,8 @@ struct mclahe_plan_s {
   // folded-pair dictionary blend (k_interp_mdict): one 8-float segment per work item
   Pencil interp_m;
   bool mdict = false;
+  bool cell_hist = false;        // K2b by dictionary cell launched beside the edge-table K2b
+  int64_t cell_hist_smem = 0;
   std::vector<int32_t> mdict_units;  // whole cells (the interp units' dim-0 chunks merged)
   int64_t off_mdict_units = 0;
   // TMA views of the last input buffer (re-encoded when the pointer changes)
@@ -222,6 +224,7 @@ KGeom pencil_geom(const mclahe_plan_s& pl, const Pencil& pc) {
   G.nseg = pc.nseg;
   G.stage_stride = pc.stage_stride;
   G.dict = pl.dict_cap > 0 ? 1 : 0;
+  G.cell_hist = pl.cell_hist ? 1 : 0;
   static const int nb_edges = getenv("MCLAHE_NB_EDGES") ? atoi(getenv("MCLAHE_NB_EDGES")) : -1;
   G.nb_edges = nb_edges;
   G.stiles = (int)(pc.kt > 0 && !pc.hist_family ? nb_seg_tiles(pl, pc) : pc.gtr);
@@ -954,6 +957,26 @@ int device_init(mclahe_plan_s* pl) {
       RangeFn r = range_fn(pl->hist.ko, pl->dict_cap > 0);
       MG_CUDA(raise_smem_cap(r, max_smem));
     }
+    // K2b by dictionary cell (k_hist_cells), opt-in with MCLAHE_CELL_HIST=1: whole-volume
+    // adaptive float32 plans with the value dictionary armed, when its [gtr][kDictKC + 1]
+    // counters keep the CTAs per SM.  Exact (parity suites green with it) but slower than the
+    // edge-table K2b on the 4D volume (0.340 vs 0.299 ms): per-cell keys merge far fewer
+    // neighbouring voxels than per-bin keys, so more lanes take part in every shared add.
+    pl->cell_hist = false;
+    if (A && pl->dict_cap > 0 && pl->f32() && !pl->fused_pencil && pl->frame_axis < 0 &&
+        !pl->shared_ws && pl->info.row_begin == 0 && pl->info.row_end == pl->p.shape[0] &&
+        getenv("MCLAHE_CELL_HIST")) {
+      const int64_t tail = align_up(pl->hist.gtr * (kDictKC + 1) * 4, 16) + kDictKC * 4;
+      const int64_t smem = pl->hist.smem - pl->hist.tail + tail;
+      HistFn fc = get_hist_cells(pl->hist.ko);
+      int occ_c = 0;
+      if (smem <= max_smem && raise_smem_cap(fc, max_smem) == cudaSuccess &&
+          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_c, fc, kPencilThreads, smem) == cudaSuccess &&
+          occ_c >= occ) {
+        pl->cell_hist = true;
+        pl->cell_hist_smem = smem;
+      }
+    }
     pl->hist_grid = (int)std::max<int64_t>(
         1, std::min<int64_t>((int64_t)pl->hist_vox.size(), (int64_t)std::max(occ, 1) * pl->sms));
     pl->hist_dyn_grid = pl->hist_grid;
@@ -1162,6 +1185,13 @@ int do_hist(mclahe_plan_s* pl, const void* in, void* ws, cudaStream_t st) {
                                                  pl->d_tables + pl->off_hist_units,
                                                  pl->d_tables + pl->off_hist_cta, W);
     MG_LAUNCHED();
+    if (pl->cell_hist) {  // the dictionary state selects which of the two counts the volume
+      get_hist_cells(pl->hist.ko)<<<G.dyn_units ? pl->hist_dyn_grid : pl->hist_grid, kPencilThreads,
+                                    pl->cell_hist_smem, st>>>(
+          G, pl->map[0], static_cast<const float*>(in), pl->d_tables + pl->off_hist_units,
+          pl->d_tables + pl->off_hist_cta, W);
+      MG_LAUNCHED();
+    }
     return MCLAHE_OK;
   }
   if (pl->fused_k2) return MCLAHE_OK;  // counted by the range pass
@@ -1740,8 +1770,10 @@ int enqueue_all(mclahe_plan_s* pl, const void* in, void* out, void* ws, cudaStre
   if ((rc = do_reset(pl, ws, st))) return rc;
   if ((rc = do_range(pl, in, ws, st, fork))) return rc;
   if ((rc = do_params(pl, ws, st))) return rc;
+  // (the cell-counting K2b reads the numbered dictionary: it joins before the histograms)
+  if (fork && pl->cell_hist) MG_CUDA(cudaStreamWaitEvent(st, pl->ev_join, 0));
   if ((rc = do_hist(pl, in, ws, st))) return rc;
-  if (fork) MG_CUDA(cudaStreamWaitEvent(st, pl->ev_join, 0));
+  if (fork && !pl->cell_hist) MG_CUDA(cudaStreamWaitEvent(st, pl->ev_join, 0));
   if ((rc = do_map(pl, ws, nullptr, st))) return rc;
   if (ev) MG_CUDA(cudaEventRecord(ev[1], st));
   if ((rc = do_interp(pl, in, out, ws, st))) return rc;
