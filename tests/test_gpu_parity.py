@@ -378,22 +378,55 @@ def test_framewise_global_rank4_folded_geometry(M):
     assert np.max(np.abs(out.astype(np.float64) - want)) <= OUT_TOL
 
 
-def _run_plan(M, x, kernel, nb, clip, ad, no_dict=False):
+def _run_plan(M, x, kernel, nb, clip, ad, no_dict=False, cell_hist=False):
     old = os.environ.pop("MCLAHE_NO_DICT", None)
+    old_c = os.environ.pop("MCLAHE_CELL_HIST", None)
     if no_dict:
         os.environ["MCLAHE_NO_DICT"] = "1"
+    if cell_hist:
+        os.environ["MCLAHE_CELL_HIST"] = "1"
     try:
         plan = M.Plan(x.shape, kernel, nb, clip, ad)
     finally:
         os.environ.pop("MCLAHE_NO_DICT", None)
+        os.environ.pop("MCLAHE_CELL_HIST", None)
         if old is not None:
             os.environ["MCLAHE_NO_DICT"] = old
+        if old_c is not None:
+            os.environ["MCLAHE_CELL_HIST"] = old_c
     xt = x if isinstance(x, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(x)).cuda()
     ws = plan.new_workspace()
     out = torch.empty_like(xt)
     plan.enqueue(xt, out, ws)
     plan.check(ws)
     return out, plan.dict_state(ws)
+
+
+@pytest.mark.parametrize("case", ["poisson", "rare", "ragged"])
+def test_cell_histogram_variant(M, case):
+    """K2b by dictionary cell (k_hist_cells, MCLAHE_CELL_HIST=1): voxels counted per
+    (tile, value), cell counts turned into bin counts at the unit switch, values the
+    sampled dictionary lacks binned on the spot -- the result must equal the
+    edge-table K2b's bit for bit (same counts -> same LUTs -> same output)."""
+    rng = np.random.default_rng({"poisson": 11, "rare": 12, "ragged": 13}[case])
+    if case == "poisson":
+        x = (rng.poisson(3.0, (48, 40, 24, 32)) / 11.0).astype(np.float32)
+        args = ((12, 10, 6, 4), 256, 0.02, True)
+    elif case == "rare":
+        x = (rng.poisson(3.0, (32, 32, 16, 32)) / 11.0).astype(np.float32)
+        pos = rng.choice(x.size, 400, replace=False)
+        x.reshape(-1)[pos] = (0.3 + np.arange(400) * 1e-4).astype(np.float32)
+        args = ((8, 8, 4, 4), 256, 0.02, True)
+    else:  # mirrored padding in every outer dim: non-uniform row weights
+        x = (rng.poisson(5.0, (37, 29, 19, 32)) / 17.0).astype(np.float32)
+        x[:6] = 0.25  # degenerate tiles
+        args = ((8, 8, 4, 4), 128, 0.03, True)
+    a, da = _run_plan(M, x, *args)
+    b, db = _run_plan(M, x, *args, cell_hist=True)
+    assert da["used"] and db["used"]
+    assert torch.equal(a, b)
+    want = O.mclahe(x, *args, "c")
+    assert np.max(np.abs(b.cpu().numpy().astype(np.float64) - want)) <= OUT_TOL
 
 
 @pytest.mark.parametrize("case", ["poisson", "edges", "scaled4d", "many", "uneven", "rare", "wide",
